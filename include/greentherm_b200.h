@@ -1,0 +1,110 @@
+/* greentherm_b200.h — batched / device-resident extension of greentherm.h.
+ *
+ * The reference C ABI cannot take a caller-supplied variation map per sample
+ * (refresh_random, reference greens.cpp:448-454, is not exported) and runs one
+ * sample per thread (reference solver.cpp:376-387). These entry points keep
+ * the reference conventions (gt_status return, thread-local last error,
+ * caller-owned out objects, borrowed inputs) and add:
+ *   - a prepared, device-resident GreensSet (reference PreparedGreens,
+ *     solver.cpp:113-121, built once instead of on every call);
+ *   - the Monte-Carlo steady composition of the reference run_one
+ *     (solver.cpp:353-374) over a batch of (power map, variation map) pairs,
+ *     from host buffers (end-to-end) or device buffers (resident).
+ *
+ * Per-sample semantics (mode A, reference closed forms):
+ *   p_leak0 = leak_frac * p_dyn * var            (leakage_baseline with
+ *                                                 d_length = ln(var)/beta_L)
+ *   mu      = mean(p_leak0), p_var = p_leak0 - mu
+ *   T       = max(0, conv(F_det, p_dyn + p_leak0) + f_rand o p_var * sum * rand_scale)
+ * with F_det / f_rand from the closed forms at mu_used = mu (mu_per_sample=1)
+ * or the GreensSet mu (mu_per_sample=0, the reference monte_carlo choice).
+ */
+#ifndef GREENTHERM_B200_H
+#define GREENTHERM_B200_H
+
+#include <stddef.h>
+
+#include "greentherm.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { GT_FP32 = 0, GT_FP64 = 1 };
+
+/* Per-sample status bits reported by the batch solves. */
+enum {
+    GT_SAMPLE_BAD_POWER = 1,
+    GT_SAMPLE_BAD_VAR = 2,
+    GT_SAMPLE_RUNAWAY_DET = 4,
+    GT_SAMPLE_RUNAWAY_RAND = 8,
+    GT_SAMPLE_NONFINITE = 16,
+    GT_SAMPLE_NOCONVERGE = 32,
+    GT_SAMPLE_KIRCHHOFF = 64
+};
+
+/* Build a GreensSet from arrays (n x n row-major doubles) instead of a
+ * calibration directory; g_sp0 may be NULL (then f_sp0 + f_sp0(c,c) - kappa_inf,
+ * reference greens.cpp:170-175). f_det/f_rand/p_var may be NULL (zero maps). */
+gt_status gt_greens_from_arrays(int n, double pitch, const double* f_sp0, const double* g_sp0,
+                                double phi, double kappa_inf, double alpha, double beta,
+                                double mu, double capacitance, double rand_scale,
+                                const double* f_det, const double* f_rand, const double* p_var,
+                                gt_greens** out);
+
+typedef struct gt_device_greens gt_device_greens;
+
+/* Prepare the device tables (baseline kernel spectrum, alpha multiplier, ...)
+ * for `precision` (GT_FP32 / GT_FP64) on CUDA device `device`. */
+gt_status gt_greens_to_device(const gt_greens* g, int precision, int device,
+                              gt_device_greens** out);
+void gt_device_greens_free(gt_device_greens* d);
+int gt_device_greens_precision(const gt_device_greens* d);
+
+typedef struct gt_batch_opts {
+    double leak_frac;    /* p_leak0 = leak_frac * p_dyn * var (0.3 for the benchmark) */
+    int mu_per_sample;   /* 1: sample mean leakage in the closed forms; 0: GreensSet mu */
+    int with_rand;       /* 0 omits the shift-variant term                       */
+    int chunk;           /* samples in flight per pass (0 = automatic)          */
+    double exponent_cap; /* |ln var| guard, 0 = reference default 6.0            */
+} gt_batch_opts;
+
+void gt_batch_opts_default(gt_batch_opts* o);
+
+/* Per-sample results (device layout of gt_mc_batch_device's `stats`). */
+typedef struct gt_sample_stats {
+    double sum_leak, sum_applied, sum_rise, max_rise, mean_rise, mu;
+    unsigned long long max_bits;
+    int status;
+    int pad_;
+} gt_sample_stats;
+
+/* End-to-end batch from host memory: p_dyn, var are batch x n x n in the
+ * device precision (float* for GT_FP32, double* for GT_FP64; pinned memory is
+ * fastest). t_out (same type, may be NULL) receives the rise maps; max_out /
+ * mean_out / status_out (may be NULL) receive per-sample results. Copies are
+ * overlapped with compute in chunks. online_ms = wall time of the call. */
+gt_status gt_mc_batch(const gt_device_greens* d, const void* p_dyn, const void* var, int batch,
+                      const gt_batch_opts* opts, void* t_out, double* max_out, double* mean_out,
+                      int* status_out, double* online_ms);
+
+/* Device-resident batch: all pointers are device memory on the greens'
+ * device; stats is batch x gt_sample_stats. Enqueued on `stream` (a
+ * cudaStream_t, NULL = the library stream); returns without synchronising. */
+gt_status gt_mc_batch_device(const gt_device_greens* d, const void* p_dyn, const void* var,
+                             int batch, const gt_batch_opts* opts, void* t_out,
+                             gt_sample_stats* stats, void* stream);
+
+/* Bytes of device scratch a device-resident batch uses per in-flight sample,
+ * and the number of kernels it launches for (batch, chunk). */
+size_t gt_mc_scratch_bytes(int n, int precision);
+int gt_mc_kernel_launches(int batch, int chunk);
+
+/* Device count visible to the library (0 without a GPU). */
+int gt_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GREENTHERM_B200_H */

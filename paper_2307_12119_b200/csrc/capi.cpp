@@ -1,0 +1,671 @@
+// capi.cpp — the drop-in C ABI (include/greentherm.h) and its batched
+// extension (include/greentherm_b200.h). Host code is C++; every solve is
+// enqueued on the GPU through the internal POD interface of gt_device.h.
+// There is no CPU compute fallback: without a CUDA device the solve entries
+// fail with GT_ERR_INTERNAL (stage "device").
+//
+// Error plumbing mirrors the reference (capi.cpp:22-48): exceptions never
+// cross the ABI, message and stage are thread-local.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/greentherm.h"
+#include "../../include/greentherm_b200.h"
+#include "gt_device.h"
+#include "gt_ops.h"
+#include "host.hpp"
+
+using namespace gth;
+
+static_assert(sizeof(gt_sample_stats) == sizeof(gtd_sample_stats), "stats layout");
+
+namespace {
+
+thread_local std::string t_err;
+thread_local std::string t_stage;
+
+template <typename Fn>
+gt_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return GT_OK;
+    } catch (const Error& e) {
+        t_err = e.what();
+        t_stage = e.stage;
+        return static_cast<gt_status>(e.status);
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        t_stage = "internal";
+        return GT_ERR_INTERNAL;
+    }
+}
+
+using wall = std::chrono::steady_clock;
+double ms_since(wall::time_point t0) {
+    return std::chrono::duration<double, std::milli>(wall::now() - t0).count();
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ST_INTERNAL, "device", std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cuda_ok(int e, const char* what) { cuda_ok(static_cast<cudaError_t>(e), what); }
+
+void need_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1)
+        fail(ST_INTERNAL, "device", "no CUDA device available (this library has no CPU solve path)");
+}
+
+bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// RAII device buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cuda_ok(cudaMalloc(&p, b), "cudaMalloc");
+        bytes = b;
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------ handle types
+struct gt_field {
+    Field f;
+};
+struct gt_greens {
+    Greens g;
+};
+struct gt_result {
+    std::vector<Field> rise;
+    std::vector<double> times;
+};
+struct gt_trace {
+    double dt = 0.0;
+    std::vector<Field> frames;
+};
+
+struct gt_device_greens {
+    int device = 0;
+    int fp64 = 0;
+    gtd_greens d{};
+    Greens host;  // copy of the set the tables were built from
+    cudaStream_t stream = nullptr;
+    DBuf fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
+    // batch scratch (guarded by mu)
+    std::mutex mu;
+    DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
+    cudaStream_t slot_stream[2] = {nullptr, nullptr};
+    void* host_stats = nullptr;
+    size_t host_stats_bytes = 0;
+    ~gt_device_greens() {
+        if (host_stats) cudaFreeHost(host_stats);
+        for (auto& s : slot_stream)
+            if (s) cudaStreamDestroy(s);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+// Host-computed fp64 constant tables (analytic; no transform work).
+std::vector<double> twiddles(int m) {
+    std::vector<double> t(2 * static_cast<size_t>(m));
+    for (int k = 0; k < m; ++k) {
+        const double a = -2.0 * M_PI * static_cast<double>(k) / m;
+        t[2 * k] = std::cos(a);
+        t[2 * k + 1] = std::sin(a);
+    }
+    return t;
+}
+
+// k1[u] = sum_{x<n} exp(-2 pi i u (x - c) / m): spectrum of the centred die box.
+std::vector<double> box_spectrum(int n) {
+    const int m = 2 * n, c = n / 2;
+    std::vector<double> k(2 * static_cast<size_t>(m));
+    for (int u = 0; u < m; ++u) {
+        double re = 0.0, im = 0.0;
+        for (int x = 0; x < n; ++x) {
+            const long long e = (static_cast<long long>(u) * (x - c)) % m;
+            const double a = -2.0 * M_PI * static_cast<double>((e + m) % m) / m;
+            re += std::cos(a);
+            im += std::sin(a);
+        }
+        k[2 * u] = re;
+        k[2 * u + 1] = im;
+    }
+    return k;
+}
+
+template <typename T>
+std::vector<T> narrow(const std::vector<double>& v) {
+    return std::vector<T>(v.begin(), v.end());
+}
+
+void upload(DBuf& b, const void* src, size_t bytes, cudaStream_t st) {
+    b.ensure(bytes);
+    cuda_ok(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), "upload");
+}
+
+std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision, int device) {
+    need_device();
+    const int n = g.n;
+    if (!pow2(n) || n < 16 || n > 512)
+        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..512, got n=" + std::to_string(n));
+    if (precision != GT_FP32 && precision != GT_FP64) fail(ST_CONFIG, "device", "precision must be GT_FP32 or GT_FP64");
+    cuda_ok(cudaSetDevice(device), "cudaSetDevice");
+    auto d = std::make_unique<gt_device_greens>();
+    d->device = device;
+    d->fp64 = precision == GT_FP64;
+    d->host = g;
+    cuda_ok(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
+    const int m = 2 * n, hp = gtd_padded_width(n, d->fp64);
+    const size_t cb = d->fp64 ? 16 : 8, rb = d->fp64 ? 8 : 4;
+    cudaStream_t st = d->stream;
+
+    const std::vector<double> tw = twiddles(m), k1 = box_spectrum(n);
+    upload(d->tw64, tw.data(), tw.size() * 8, st);
+    if (d->fp64) {
+        upload(d->tw, tw.data(), tw.size() * 8, st);
+        upload(d->k1, k1.data(), k1.size() * 8, st);
+    } else {
+        auto twf = narrow<float>(tw), k1f = narrow<float>(k1);
+        upload(d->tw, twf.data(), twf.size() * 4, st);
+        upload(d->k1, k1f.data(), k1f.size() * 4, st);
+        cuda_ok(cudaStreamSynchronize(st), "sync");
+    }
+    upload(d->fsp0, g.f_sp0.v.data(), g.f_sp0.v.size() * 8, st);
+    upload(d->gsp0, g.g_sp0.v.data(), g.g_sp0.v.size() * 8, st);
+    d->work.ensure(static_cast<size_t>(m) * m * 16);
+    d->fk.ensure(static_cast<size_t>(m) * hp * cb);
+    d->gtab.ensure(static_cast<size_t>(n + 1) * (n + 1) * rb);
+    cuda_ok(gtd_greens_tables(static_cast<const double*>(d->fsp0.p), static_cast<const double*>(d->gsp0.p),
+                              g.phi, n, hp, d->fp64, d->tw64.p, d->work.p, d->fk.p, d->gtab.p, st),
+            "greens tables");
+    cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
+    d->d.n = n;
+    d->d.m = m;
+    d->d.h = n + 1;
+    d->d.hp = hp;
+    d->d.fp64 = d->fp64;
+    d->d.fk = d->fk.p;
+    d->d.gtab = d->gtab.p;
+    d->d.k1 = d->k1.p;
+    d->d.tw = d->tw.p;
+    d->d.alpha = g.alpha;
+    d->d.beta = g.beta;
+    d->d.rand_scale = g.rand_scale;
+    d->d.mu_fixed = g.mu;
+    return d;
+}
+
+gtd_mc_opts to_dev_opts(const gt_batch_opts* o) {
+    gtd_mc_opts r{};
+    r.mu_per_sample = o ? o->mu_per_sample : 1;
+    r.with_rand = o ? o->with_rand : 1;
+    r.exponent_cap = (o && o->exponent_cap > 0.0) ? o->exponent_cap : 6.0;
+    return r;
+}
+
+int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o) {
+    if (o && o->chunk > 0) return std::min(o->chunk, batch);
+    const size_t per = gtd_mc_scratch_bytes_per_sample(n, fp64);
+    const size_t budget = 48ull << 20;  // keep a chunk's intermediates L2-resident
+    int c = static_cast<int>(std::max<size_t>(1, budget / per));
+    return std::min(c, batch);
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------- status / errors
+const char* gt_status_name(gt_status s) {
+    switch (s) {
+        case GT_OK: return "ok";
+        case GT_ERR_CONFIG: return "config";
+        case GT_ERR_SOLVER: return "solver";
+        case GT_ERR_VALIDATION: return "validation";
+        case GT_ERR_INTERNAL: return "internal";
+    }
+    return "unknown";
+}
+const char* gt_last_error(void) { return t_err.c_str(); }
+const char* gt_last_error_stage(void) { return t_stage.c_str(); }
+
+// ------------------------------------------------------------------ fields
+gt_status gt_field_create(int n, double pitch, const char* unit, gt_field** out) {
+    return guarded([&] { *out = new gt_field{Field(n, pitch, parse_unit(unit ? unit : "watts"))}; });
+}
+gt_status gt_field_load(const char* path, gt_field** out) {
+    return guarded([&] { *out = new gt_field{read_field(path)}; });
+}
+gt_status gt_field_save(const gt_field* f, const char* path) {
+    return guarded([&] { write_field(f->f, path); });
+}
+void gt_field_free(gt_field* f) { delete f; }
+int gt_field_n(const gt_field* f) { return f->f.n; }
+double gt_field_pitch(const gt_field* f) { return f->f.pitch; }
+const char* gt_field_unit(const gt_field* f) { return unit_str(f->f.unit); }
+double gt_field_get(const gt_field* f, int i, int j) { return f->f.at(i, j); }
+void gt_field_set(gt_field* f, int i, int j, double value) { f->f.at(i, j) = value; }
+const double* gt_field_data(const gt_field* f) { return f->f.v.data(); }
+double gt_field_max(const gt_field* f) { return f->f.max(); }
+double gt_field_sum(const gt_field* f) { return f->f.sum(); }
+
+gt_status gt_field_render(const gt_field* f, const char* path, int cell_px) {
+    // P6 raster with the legend in header comments (reference heatmap.cpp:41-76).
+    return guarded([&] {
+        const Field& F = f->f;
+        F.check_finite("render_heatmap input");
+        const int px = cell_px < 1 ? 4 : cell_px;
+        const double lo = F.min(), hi = F.max(), span = hi - lo;
+        static const unsigned char stops[5][3] = {{0, 0, 96}, {0, 128, 255}, {0, 224, 128}, {255, 224, 0}, {224, 16, 16}};
+        std::ofstream os(path, std::ios::binary);
+        if (!os) fail(ST_CONFIG, "heatmap", std::string("cannot open '") + path + "' for writing");
+        char hdr[160];
+        const int w = F.n * px;
+        const int len = std::snprintf(hdr, sizeof hdr, "P6\n# legend_min %.12g K\n# legend_max %.12g K\n%d %d\n255\n",
+                                      lo, hi, w, w);
+        os.write(hdr, len);
+        std::string row(static_cast<size_t>(w) * 3, '\0');
+        for (int i = 0; i < F.n; ++i) {
+            for (int j = 0; j < F.n; ++j) {
+                const double t = span > 0.0 ? std::clamp((F.at(i, j) - lo) / span, 0.0, 1.0) : 0.0;
+                const double x = t * 4.0;
+                const int k = std::min(static_cast<int>(x), 3);
+                const double a = x - k;
+                unsigned char rgb[3];
+                for (int ch = 0; ch < 3; ++ch)
+                    rgb[ch] = static_cast<unsigned char>(stops[k][ch] + (stops[k + 1][ch] - stops[k][ch]) * a + 0.5);
+                for (int p = 0; p < px; ++p) std::memcpy(&row[(static_cast<size_t>(j) * px + p) * 3], rgb, 3);
+            }
+            for (int p = 0; p < px; ++p) os.write(row.data(), static_cast<std::streamsize>(row.size()));
+        }
+        if (!os) fail(ST_CONFIG, "heatmap", std::string("write failed for '") + path + "'");
+    });
+}
+
+gt_status gt_write_default_stack(const char* path) {
+    return guarded([&] { save_stack_file(Stack{}, path); });
+}
+gt_status gt_write_default_variation(const char* path) {
+    return guarded([&] { save_var_file(VarParams{}, path); });
+}
+
+// ------------------------------------------------------------------ greens
+gt_status gt_calibrate(const char* stack_path, const char* variation_path, const gt_field* nominal_leak,
+                       double leak_total, gt_greens** out, double* offline_ms) {
+    return guarded([&] {
+        auto t0 = wall::now();
+        Stack s = stack_path ? load_stack_file(stack_path) : Stack{};
+        VarParams v = variation_path ? load_var_file(variation_path) : VarParams{};
+        Greens g = gt_ops_calibrate_modal(s, v, nominal_leak ? &nominal_leak->f : nullptr, leak_total);
+        if (offline_ms) *offline_ms = ms_since(t0);
+        *out = new gt_greens{std::move(g)};
+    });
+}
+gt_status gt_greens_save(const gt_greens* g, const char* dir) {
+    return guarded([&] { save_greens_dir(g->g, dir); });
+}
+gt_status gt_greens_load(const char* dir, gt_greens** out) {
+    return guarded([&] { *out = new gt_greens{load_greens_dir(dir)}; });
+}
+void gt_greens_free(gt_greens* g) { delete g; }
+int gt_greens_n(const gt_greens* g) { return g->g.n; }
+double gt_greens_alpha(const gt_greens* g) { return g->g.alpha; }
+double gt_greens_beta(const gt_greens* g) { return g->g.beta; }
+double gt_greens_mu(const gt_greens* g) { return g->g.mu; }
+double gt_greens_capacitance(const gt_greens* g) { return g->g.capacitance; }
+double gt_greens_kappa_inf(const gt_greens* g) { return g->g.kappa_inf; }
+gt_status gt_greens_field(const gt_greens* g, const char* which, gt_field** out) {
+    return guarded([&] {
+        const std::string w = which ? which : "";
+        const Field* f = w == "f_sp0"    ? &g->g.f_sp0
+                         : w == "g_sp0"  ? &g->g.g_sp0
+                         : w == "f_det"  ? &g->g.f_det
+                         : w == "f_rand" ? &g->g.f_rand
+                         : w == "p_var"  ? &g->g.p_var
+                                         : nullptr;
+        if (!f) fail(ST_CONFIG, "capi", "unknown greens field '" + w + "'");
+        *out = new gt_field{*f};
+    });
+}
+
+// ------------------------------------------------------------------ results
+int gt_result_count(const gt_result* r) { return static_cast<int>(r->rise.size()); }
+double gt_result_time(const gt_result* r, int idx) {
+    return (idx < 0 || static_cast<size_t>(idx) >= r->times.size()) ? 0.0 : r->times[idx];
+}
+gt_status gt_result_map(const gt_result* r, int idx, gt_field** out) {
+    return guarded([&] {
+        if (idx < 0 || static_cast<size_t>(idx) >= r->rise.size()) fail(ST_CONFIG, "capi", "result index out of range");
+        *out = new gt_field{r->rise[idx]};
+    });
+}
+void gt_result_free(gt_result* r) { delete r; }
+
+// ------------------------------------------------------------------ solves
+gt_status gt_solve_steady(const gt_greens* g, const gt_field* p_dyn, int with_rand, gt_field** out,
+                          double* online_ms) {
+    return guarded([&] {
+        double ms = 0.0;
+        Field f = gt_ops_steady(g->g, p_dyn->f, with_rand != 0, &ms);
+        if (online_ms) *online_ms = ms;
+        *out = new gt_field{std::move(f)};
+    });
+}
+
+gt_status gt_solve_step(const gt_greens* g, const gt_field* p_dyn, const double* times, int n_times,
+                        int with_rand, gt_result** out, double* online_ms) {
+    return guarded([&] {
+        if (!times || n_times < 1) fail(ST_CONFIG, "capi", "step solve needs times");
+        double ms = 0.0;
+        std::vector<double> tv(times, times + n_times);
+        auto r = std::make_unique<gt_result>();
+        r->rise = gt_ops_step(g->g, p_dyn->f, tv, with_rand != 0, &ms);
+        r->times = tv;
+        if (online_ms) *online_ms = ms;
+        *out = r.release();
+    });
+}
+
+gt_status gt_trace_load(const char* dir, gt_trace** out) {
+    return guarded([&] {
+        const Kv kv = Kv::parse(std::string(dir) + "/trace.txt");
+        auto t = std::make_unique<gt_trace>();
+        t->dt = kv.num("dt");
+        const long long cnt = kv.integer("frames");
+        for (long long i = 0; i < cnt; ++i) {
+            char b[32];
+            std::snprintf(b, sizeof b, "frame_%04lld.map", i);
+            t->frames.push_back(read_field(std::string(dir) + "/" + b));
+        }
+        gt_ops_check_trace(t->dt, t->frames);
+        *out = t.release();
+    });
+}
+gt_status gt_trace_create(double dt, gt_trace** out) {
+    return guarded([&] {
+        if (!(dt > 0.0)) fail(ST_CONFIG, "capi", "trace dt must be positive");
+        auto t = std::make_unique<gt_trace>();
+        t->dt = dt;
+        *out = t.release();
+    });
+}
+gt_status gt_trace_push(gt_trace* t, const gt_field* frame) {
+    return guarded([&] { t->frames.push_back(frame->f); });
+}
+gt_status gt_trace_save(const gt_trace* t, const char* dir) {
+    return guarded([&] {
+        gt_ops_check_trace(t->dt, t->frames);
+        std::filesystem::create_directories(dir);
+        Kv kv;
+        kv.put_num("dt", t->dt);
+        kv.put_int("frames", static_cast<long long>(t->frames.size()));
+        kv.save(std::string(dir) + "/trace.txt");
+        for (size_t i = 0; i < t->frames.size(); ++i) {
+            char b[32];
+            std::snprintf(b, sizeof b, "frame_%04zu.map", i);
+            write_field(t->frames[i], std::string(dir) + "/" + b);
+        }
+    });
+}
+int gt_trace_frames(const gt_trace* t) { return static_cast<int>(t->frames.size()); }
+double gt_trace_dt(const gt_trace* t) { return t->dt; }
+void gt_trace_free(gt_trace* t) { delete t; }
+
+gt_status gt_solve_trace(const gt_greens* g, const gt_trace* trace, int window, int with_rand,
+                         gt_result** out, double* online_ms) {
+    return guarded([&] {
+        double ms = 0.0;
+        auto r = std::make_unique<gt_result>();
+        r->rise = gt_ops_trace(g->g, trace->dt, trace->frames, window, with_rand != 0, &r->times, &ms);
+        if (online_ms) *online_ms = ms;
+        *out = r.release();
+    });
+}
+
+// ---------------------------------------------------- FDM reference solver
+gt_status gt_oracle_steady(const char*, const char*, const gt_field*, const gt_field*, int, int, gt_field**,
+                           int*) {
+    return guarded([&] {
+        fail(ST_INTERNAL, "oracle",
+             "the finite-difference reference solver is not part of the device build (see DESIGN.md: out of scope)");
+    });
+}
+gt_status gt_oracle_transient(const char*, const char*, const gt_field*, const gt_field*, int, const double*,
+                              int, double, gt_result**) {
+    return guarded([&] {
+        fail(ST_INTERNAL, "oracle",
+             "the finite-difference reference solver is not part of the device build (see DESIGN.md: out of scope)");
+    });
+}
+
+gt_status gt_error_metrics(const gt_field* calc, const gt_field* ref, gt_error_report* out) {
+    // reference solver.cpp:289-312
+    return guarded([&] {
+        const Field& a = calc->f;
+        const Field& b = ref->f;
+        if (!a.same_shape(b)) fail(ST_CONFIG, "solver", "error_metrics: map shapes differ");
+        double sum = 0.0, mx = 0.0;
+        for (size_t k = 0; k < a.v.size(); ++k) {
+            const double e = std::abs(a.v[k] - b.v[k]);
+            sum += e;
+            mx = std::max(mx, e);
+        }
+        const double mae = sum / static_cast<double>(a.v.size());
+        const double rmax = b.max();
+        out->mae = mae;
+        out->max_err = mx;
+        out->pct_of_max_rise = rmax > 0.0 ? 100.0 * mae / rmax : 0.0;
+        out->max_pct_of_max_rise = rmax > 0.0 ? 100.0 * mx / rmax : 0.0;
+        const auto [ci, cj] = a.argmax();
+        const auto [ri, rj] = b.argmax();
+        out->hotspot_hit = std::max(std::abs(ci - ri), std::abs(cj - rj)) <= 1 ? 1 : 0;
+    });
+}
+
+gt_status gt_monte_carlo(const gt_greens* g, const char* variation_path, const gt_field* nominal_leak,
+                         double leak_total, const gt_field* p_dyn, const unsigned long long* seeds, int n_seeds,
+                         int jobs, const char* csv_path, double* mean_max, double* std_max) {
+    return guarded([&] {
+        if (!seeds || n_seeds < 1) fail(ST_CONFIG, "capi", "monte carlo needs seeds");
+        VarParams v = variation_path ? load_var_file(variation_path) : VarParams{};
+        const Greens& G = g->g;
+        Field leak = nominal_leak ? nominal_leak->f
+                                  : Field(G.n, G.pitch, Unit::Watts,
+                                          (leak_total > 0.0 ? leak_total : 15.0) / (static_cast<double>(G.n) * G.n));
+        std::vector<unsigned long long> sv(seeds, seeds + n_seeds);
+        gt_ops_monte_carlo(G, v, leak, p_dyn->f, sv, jobs, csv_path ? csv_path : "", mean_max, std_max);
+    });
+}
+
+gt_status gt_write_builtin_suite(const char*, const char*) {
+    return guarded([&] {
+        fail(ST_INTERNAL, "validate",
+             "the oracle-vs-Green validation suite needs the FDM solver, which is not part of the device build");
+    });
+}
+gt_status gt_validate_suite(const char*, const char*, int, int*, int*) {
+    return guarded([&] {
+        fail(ST_INTERNAL, "validate",
+             "the oracle-vs-Green validation suite needs the FDM solver, which is not part of the device build");
+    });
+}
+
+// ------------------------------------------------------ batched extension
+gt_status gt_greens_from_arrays(int n, double pitch, const double* f_sp0, const double* g_sp0, double phi,
+                                double kappa_inf, double alpha, double beta, double mu, double capacitance,
+                                double rand_scale, const double* f_det, const double* f_rand,
+                                const double* p_var, gt_greens** out) {
+    return guarded([&] {
+        if (!f_sp0) fail(ST_CONFIG, "greens", "f_sp0 is required");
+        Greens g;
+        g.n = n;
+        g.pitch = pitch;
+        const size_t nn = static_cast<size_t>(n) * n;
+        auto mk = [&](const double* src, Unit u) {
+            Field f(n, pitch, u);
+            if (src) std::copy(src, src + nn, f.v.begin());
+            return f;
+        };
+        g.f_sp0 = mk(f_sp0, Unit::KelvinPerWatt);
+        if (g_sp0) {
+            g.g_sp0 = mk(g_sp0, Unit::KelvinPerWatt);
+        } else {
+            g.g_sp0 = g.f_sp0;
+            const double shift = g.f_sp0.at(n / 2, n / 2) - kappa_inf;
+            for (double& x : g.g_sp0.v) x += shift;
+        }
+        g.f_det = mk(f_det, Unit::KelvinPerWatt);
+        g.f_rand = mk(f_rand, Unit::KelvinPerWatt);
+        g.p_var = mk(p_var, Unit::Watts);
+        g.phi = phi;
+        g.kappa_inf = kappa_inf;
+        g.alpha = alpha;
+        g.beta = beta;
+        g.mu = mu;
+        g.capacitance = capacitance;
+        g.rand_scale = rand_scale;
+        g.validate();
+        *out = new gt_greens{std::move(g)};
+    });
+}
+
+gt_status gt_greens_to_device(const gt_greens* g, int precision, int device, gt_device_greens** out) {
+    return guarded([&] { *out = prepare_device(g->g, precision, device).release(); });
+}
+void gt_device_greens_free(gt_device_greens* d) { delete d; }
+int gt_device_greens_precision(const gt_device_greens* d) { return d->fp64 ? GT_FP64 : GT_FP32; }
+
+void gt_batch_opts_default(gt_batch_opts* o) {
+    o->leak_frac = 0.3;
+    o->mu_per_sample = 1;
+    o->with_rand = 1;
+    o->chunk = 0;
+    o->exponent_cap = 6.0;
+}
+
+size_t gt_mc_scratch_bytes(int n, int precision) { return gtd_mc_scratch_bytes_per_sample(n, precision == GT_FP64); }
+int gt_mc_kernel_launches(int batch, int chunk) { return gtd_mc_launch_count(batch, chunk); }
+
+int gt_device_count(void) {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
+gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, const void* var, int batch,
+                             const gt_batch_opts* opts, void* t_out, gt_sample_stats* stats, void* stream) {
+    return guarded([&] {
+        if (batch < 1 || !p_dyn || !var || !stats) fail(ST_CONFIG, "capi", "batch needs inputs and a stats array");
+        auto* d = const_cast<gt_device_greens*>(dc);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        const int n = d->d.n;
+        const int chunk = auto_chunk(n, d->fp64, batch, opts);
+        d->scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * chunk);
+        gtd_mc_opts o = to_dev_opts(opts);
+        gtd_mc_in in{};
+        in.P = p_dyn;
+        in.N = p_dyn;
+        in.V = var;
+        in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
+        in.nom_scale = opts ? opts->leak_frac : 0.3;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        cuda_ok(gtd_mc_batch(&d->d, &in, batch, &o, t_out, reinterpret_cast<gtd_sample_stats*>(stats),
+                             d->scratch.p, chunk, st),
+                "mc batch launch");
+    });
+}
+
+gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void* var, int batch,
+                      const gt_batch_opts* opts, void* t_out, double* max_out, double* mean_out, int* status_out,
+                      double* online_ms) {
+    return guarded([&] {
+        if (batch < 1 || !p_dyn || !var) fail(ST_CONFIG, "capi", "batch needs inputs");
+        auto t0 = wall::now();
+        auto* d = const_cast<gt_device_greens*>(dc);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        const int n = d->d.n;
+        const size_t es = d->fp64 ? 8 : 4;
+        const size_t map = static_cast<size_t>(n) * n * es;
+        // Pipeline chunk: large enough to amortise launches, two slots in flight.
+        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 256);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr);
+        gtd_mc_opts o = to_dev_opts(opts);
+        for (int s = 0; s < 2; ++s) {
+            if (!d->slot_stream[s]) cuda_ok(cudaStreamCreateWithFlags(&d->slot_stream[s], cudaStreamNonBlocking), "stream");
+            d->slot_in[s].ensure(2 * map * chunk);
+            if (t_out) d->slot_out[s].ensure(map * chunk);
+            d->slot_scr[s].ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * inner);
+            d->slot_stats[s].ensure(sizeof(gtd_sample_stats) * chunk);
+        }
+        const size_t hs_bytes = sizeof(gtd_sample_stats) * static_cast<size_t>(batch);
+        if (d->host_stats_bytes < hs_bytes) {
+            if (d->host_stats) cudaFreeHost(d->host_stats);
+            d->host_stats = nullptr;
+            d->host_stats_bytes = 0;
+            cuda_ok(cudaMallocHost(&d->host_stats, hs_bytes), "cudaMallocHost");
+            d->host_stats_bytes = hs_bytes;
+        }
+        auto* hs = static_cast<gtd_sample_stats*>(d->host_stats);
+        const char* P = static_cast<const char*>(p_dyn);
+        const char* V = static_cast<const char*>(var);
+        for (int s0 = 0, k = 0; s0 < batch; s0 += chunk, ++k) {
+            const int cnt = std::min(chunk, batch - s0);
+            const int s = k & 1;
+            cudaStream_t st = d->slot_stream[s];
+            char* din = static_cast<char*>(d->slot_in[s].p);
+            cuda_ok(cudaMemcpyAsync(din, P + s0 * map, cnt * map, cudaMemcpyHostToDevice, st), "h2d p");
+            cuda_ok(cudaMemcpyAsync(din + chunk * map, V + s0 * map, cnt * map, cudaMemcpyHostToDevice, st), "h2d var");
+            gtd_mc_in in{};
+            in.P = din;
+            in.N = din;
+            in.V = din + chunk * map;
+            in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
+            in.nom_scale = opts ? opts->leak_frac : 0.3;
+            auto* dst = static_cast<gtd_sample_stats*>(d->slot_stats[s].p);
+            cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, t_out ? d->slot_out[s].p : nullptr, dst, d->slot_scr[s].p,
+                                 std::min(inner, cnt), st),
+                    "mc batch launch");
+            if (t_out)
+                cuda_ok(cudaMemcpyAsync(static_cast<char*>(t_out) + s0 * map, d->slot_out[s].p, cnt * map,
+                                        cudaMemcpyDeviceToHost, st),
+                        "d2h maps");
+            cuda_ok(cudaMemcpyAsync(hs + s0, dst, sizeof(gtd_sample_stats) * cnt, cudaMemcpyDeviceToHost, st), "d2h stats");
+        }
+        for (auto& st : d->slot_stream) cuda_ok(cudaStreamSynchronize(st), "batch sync");
+        for (int i = 0; i < batch; ++i) {
+            if (max_out) max_out[i] = hs[i].max_rise;
+            if (mean_out) mean_out[i] = hs[i].mean_rise;
+            if (status_out) status_out[i] = hs[i].status;
+        }
+        if (online_ms) *online_ms = ms_since(t0);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+// fft_tile.cuh — shared-memory tile FFT engine for sm_100a.
+//
+// A "tile" is a block of L independent complex lines of power-of-two length M
+// held in shared memory with the LINE index fastest: element j of line l lives
+// at tile[j * LP + l] (LP >= L is the padded pitch). Warp lanes are mapped
+// across lines, so every butterfly load/store of a warp touches 16 (fp32) or
+// 8 (fp64) consecutive complex values per row: exactly the minimum number of
+// shared-memory wavefronts whatever the Stockham index permutation, i.e. the
+// engine is bank-conflict free by construction.
+//
+// The transform is a Stockham autosort FFT (natural order in and out) with
+// radix-8 register butterflies and one trailing radix-2/4 stage when log2(M)
+// is not a multiple of 3. Twiddles come from a per-CTA shared table
+// tw[t] = exp(-2*pi*i*t/M) computed on the host in fp64.
+//
+// Convention (reference spectral.hpp:12-20): forward = unnormalised sum with
+// exp(-2*pi*i*k*j/M); inverse = exp(+...) WITHOUT the 1/M factor (callers fold
+// the 1/m^2 into their epilogue).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace gtb {
+
+template <typename T>
+struct V2;
+template <>
+struct V2<float> {
+    using type = float2;
+};
+template <>
+struct V2<double> {
+    using type = double2;
+};
+template <typename T>
+using cplx = typename V2<T>::type;
+
+template <typename T>
+__device__ __forceinline__ cplx<T> mk(T x, T y) {
+    cplx<T> r;
+    r.x = x;
+    r.y = y;
+    return r;
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> cadd(cplx<T> a, cplx<T> b) {
+    return mk<T>(a.x + b.x, a.y + b.y);
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> csub(cplx<T> a, cplx<T> b) {
+    return mk<T>(a.x - b.x, a.y - b.y);
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> cmul(cplx<T> a, cplx<T> b) {
+    return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> cconj(cplx<T> a) {
+    return mk<T>(a.x, -a.y);
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> cscale(cplx<T> a, T s) {
+    return mk<T>(a.x * s, a.y * s);
+}
+template <typename T>
+__device__ __forceinline__ T cabs2(cplx<T> a) {
+    return a.x * a.x + a.y * a.y;
+}
+// a / b for complex b
+template <typename T>
+__device__ __forceinline__ cplx<T> cdiv(cplx<T> a, cplx<T> b) {
+    T d = T(1) / cabs2<T>(b);
+    return mk<T>((a.x * b.x + a.y * b.y) * d, (a.y * b.x - a.x * b.y) * d);
+}
+// multiply by (SIGN * i): SIGN = -1 gives -i, +1 gives +i
+template <int SIGN, typename T>
+__device__ __forceinline__ cplx<T> mul_si(cplx<T> a) {
+    return SIGN < 0 ? mk<T>(a.y, -a.x) : mk<T>(-a.y, a.x);
+}
+
+constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+// ---------------------------------------------------------------- butterflies
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft2(cplx<T>* v) {
+    cplx<T> a = v[0], b = v[1];
+    v[0] = cadd<T>(a, b);
+    v[1] = csub<T>(a, b);
+}
+
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft4(cplx<T>* v) {
+    cplx<T> a0 = cadd<T>(v[0], v[2]), a1 = csub<T>(v[0], v[2]);
+    cplx<T> b0 = cadd<T>(v[1], v[3]), b1 = mul_si<SIGN, T>(csub<T>(v[1], v[3]));
+    v[0] = cadd<T>(a0, b0);
+    v[2] = csub<T>(a0, b0);
+    v[1] = cadd<T>(a1, b1);
+    v[3] = csub<T>(a1, b1);
+}
+
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft8(cplx<T>* v) {
+    const T r = T(0.70710678118654752440084436210485);
+    // radix-2 DIF layer with W8^k twiddles
+    cplx<T> a0 = cadd<T>(v[0], v[4]), a4 = csub<T>(v[0], v[4]);
+    cplx<T> a1 = cadd<T>(v[1], v[5]), a5 = csub<T>(v[1], v[5]);
+    cplx<T> a2 = cadd<T>(v[2], v[6]), a6 = csub<T>(v[2], v[6]);
+    cplx<T> a3 = cadd<T>(v[3], v[7]), a7 = csub<T>(v[3], v[7]);
+    // W8^1 = (1 + SIGN i)/sqrt2, W8^2 = SIGN i, W8^3 = (-1 + SIGN i)/sqrt2
+    a5 = SIGN < 0 ? mk<T>((a5.x + a5.y) * r, (a5.y - a5.x) * r)
+                  : mk<T>((a5.x - a5.y) * r, (a5.y + a5.x) * r);
+    a6 = mul_si<SIGN, T>(a6);
+    a7 = SIGN < 0 ? mk<T>((a7.y - a7.x) * r, -(a7.x + a7.y) * r)
+                  : mk<T>(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);
+    // two DFT4 on (a0..a3) -> even outputs, (a4..a7) -> odd outputs
+    cplx<T> e[4] = {a0, a1, a2, a3};
+    cplx<T> o[4] = {a4, a5, a6, a7};
+    dft4<SIGN, T>(e);
+    dft4<SIGN, T>(o);
+    v[0] = e[0];
+    v[2] = e[1];
+    v[4] = e[2];
+    v[6] = e[3];
+    v[1] = o[0];
+    v[3] = o[1];
+    v[5] = o[2];
+    v[7] = o[3];
+}
+
+template <int R, int SIGN, typename T>
+__device__ __forceinline__ void dftR(cplx<T>* v) {
+    if constexpr (R == 8)
+        dft8<SIGN, T>(v);
+    else if constexpr (R == 4)
+        dft4<SIGN, T>(v);
+    else if constexpr (R == 2)
+        dft2<SIGN, T>(v);
+}
+
+// ------------------------------------------------------------- tile geometry
+// Lines per tile: keep a tile near 64 KiB so 2-3 CTAs share an SM.
+template <typename T, int M>
+struct TileGeom {
+    static constexpr int CB = int(sizeof(cplx<T>));
+    static constexpr int Lraw = 65536 / (M * CB);
+    static constexpr int L = Lraw > 32 ? 32 : (Lraw < 4 ? 4 : Lraw);
+    static constexpr int LOG2M = ilog2(M);
+    static constexpr int N8 = LOG2M / 3;           // radix-8 stages
+    static constexpr int RLAST = 1 << (LOG2M % 3); // 1, 2 or 4
+    // threads: one radix-8 butterfly per thread per step of the widest stage
+    static constexpr int NBMIN = (M / 8) * L;
+    static constexpr int NT = NBMIN >= 256 ? 256 : NBMIN;
+};
+
+// One Stockham stage over a whole tile, in place (all loads, barrier, stores).
+template <typename T, int M, int L, int LP, int NT, int SIGN, int R, int NS>
+__device__ __forceinline__ void stockham_stage(cplx<T>* tile, const cplx<T>* tw) {
+    constexpr int NB = (M / R) * L;
+    static_assert(NB % NT == 0, "butterflies must divide evenly over threads");
+    constexpr int BPT = NB / NT;
+    cplx<T> v[BPT][R];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int l = id % L, j = id / L;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = tile[(j + r * (M / R)) * LP + l];
+        if constexpr (NS > 1) {
+            const int k = j % NS;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                cplx<T> w = tw[k * r * (M / (NS * R))];
+                if (SIGN > 0) w.y = -w.y;
+                v[b][r] = cmul<T>(v[b][r], w);
+            }
+        }
+        dftR<R, SIGN, T>(v[b]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int l = id % L, j = id / L;
+        const int k = j % NS;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) tile[(base + r * NS) * LP + l] = v[b][r];
+    }
+    __syncthreads();
+}
+
+template <typename T, int M, int L, int LP, int NT, int SIGN, int S>
+struct StageRunner {
+    using G = TileGeom<T, M>;
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* tw) {
+        if constexpr (S < G::N8) {
+            constexpr int NS = 1 << (3 * S);
+            stockham_stage<T, M, L, LP, NT, SIGN, 8, NS>(tile, tw);
+            StageRunner<T, M, L, LP, NT, SIGN, S + 1>::run(tile, tw);
+        } else if constexpr (G::RLAST > 1) {
+            constexpr int NS = 1 << (3 * G::N8);
+            stockham_stage<T, M, L, LP, NT, SIGN, G::RLAST, NS>(tile, tw);
+        }
+    }
+};
+
+// Full length-M transform of every line of the tile. Caller must
+// __syncthreads() after filling the tile; on return the tile holds the
+// natural-order spectrum and all threads are synchronised.
+template <typename T, int M, int L, int LP, int NT, int SIGN>
+__device__ __forceinline__ void tile_fft(cplx<T>* tile, const cplx<T>* tw) {
+    StageRunner<T, M, L, LP, NT, SIGN, 0>::run(tile, tw);
+}
+
+// Cooperative copy of the M-entry twiddle table into shared memory.
+template <typename T, int M, int NT>
+__device__ __forceinline__ void load_twiddles(cplx<T>* s_tw, const cplx<T>* g_tw) {
+    for (int t = threadIdx.x; t < M; t += NT) s_tw[t] = g_tw[t];
+}
+
+}  // namespace gtb

@@ -1,0 +1,97 @@
+// gt_device.h — internal thin C ABI between the C++ host layer (capi.cpp) and
+// the sm_100a kernels. Plain POD structs, device pointers, dims and a stream;
+// no torch or C++ types cross this boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Per-sample scalars accumulated by the fused passes (fp64 accumulation of
+ * the compensated sums of the reference, field.cpp:45-57). */
+typedef struct gtd_sample_stats {
+    double sum_leak;     /* sum of p_leak0 over the die (-> mu)      */
+    double sum_applied;  /* sum of p_dyn + p_leak0 (-> Hadamard scale) */
+    double sum_rise;     /* sum of the clamped rise map             */
+    double max_rise;     /* written by finalize                     */
+    double mean_rise;    /* written by finalize                     */
+    double mu;           /* mean leakage used for p_var             */
+    unsigned long long max_bits; /* double bits of max rise (rise >= 0) */
+    int status;          /* bit flags, GTD_ST_*                      */
+} gtd_sample_stats;
+
+enum {
+    GTD_ST_BAD_POWER = 1,     /* p_dyn < 0 or non-finite  -> ConfigError   */
+    GTD_ST_BAD_VAR = 2,       /* var <= 0 / non-finite / |ln var|>cap      */
+    GTD_ST_RUNAWAY_DET = 4,   /* |den| < 1e-6 in deterministic_spectrum    */
+    GTD_ST_RUNAWAY_RAND = 8,  /* |den| < 1e-6 in random_greens             */
+    GTD_ST_NONFINITE = 16,    /* non-finite rise                           */
+    GTD_ST_NOCONVERGE = 32,   /* fixed point hit max_iters                 */
+    GTD_ST_KIRCHHOFF = 64     /* Kirchhoff inverse left its validity range */
+};
+
+/* Device-resident prepared GreensSet (reference PreparedGreens,
+ * solver.cpp:113-121, plus the per-frequency tables the fused kernels read). */
+typedef struct gtd_greens {
+    int n, m, h, hp;      /* grid, padded grid 2n, R2C width n+1, padded pitch */
+    int fp64;             /* 1: tables are double, 0: float                    */
+    void* fk;             /* [m][hp] complex: baseline kernel spectrum (C7)    */
+    void* gtab;           /* [(n+1)][(n+1)] real: alpha multiplier g(du,dv) (C6)*/
+    void* k1;             /* [m] complex: 1-D spectrum of the centred die box  */
+    void* tw;             /* [m] complex: exp(-2 pi i t/m)                     */
+    double alpha, beta, rand_scale, mu_fixed;
+} gtd_greens;
+
+/* Inputs of a Monte-Carlo batch: p_leak0 = nom_scale * N * V, applied = P + p_leak0.
+ * Sample strides are in elements (0 broadcasts one map to every sample). */
+typedef struct gtd_mc_in {
+    const void* P;
+    const void* N;
+    const void* V;
+    long long sP, sN, sV;
+    double nom_scale;
+} gtd_mc_in;
+
+/* Options of the Monte-Carlo batch (mode A = reference run_one semantics). */
+typedef struct gtd_mc_opts {
+    int mu_per_sample;  /* 1: closed forms use the sample mean leakage; 0: gs.mu */
+    int with_rand;      /* 0 drops the shift-variant term (ablation)            */
+    double exponent_cap;/* |ln var| guard (variation.cpp:173-178)               */
+} gtd_mc_opts;
+
+/* Scratch bytes needed per in-flight sample by gtd_mc_batch. */
+size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64);
+
+/* Mode-A batch. Maps are [B][n][n] (float or double per g->fp64).
+ * out: [B][n][n] rise maps or NULL. stats: [B] device array. scratch holds
+ * `chunk` samples (gtd_mc_scratch_bytes_per_sample each). Returns a CUDA
+ * error code (0 = launched). */
+int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch,
+                 const gtd_mc_opts* opts, void* out, gtd_sample_stats* stats, void* scratch,
+                 int chunk, cudaStream_t stream);
+
+/* Number of kernel launches gtd_mc_batch issues for a given batch/chunk. */
+int gtd_mc_launch_count(int batch, int chunk);
+
+#ifdef __cplusplus
+}
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* Padded R2C width of the fused passes (n+1 rounded to the column tile). */
+int gtd_padded_width(int n, int fp64);
+/* Batched in-place 2-D complex FFT of [batch][m][m] (sign -1 forward,
+ * +1 inverse without 1/m^2); tw = m complex twiddles of the same precision. */
+int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, cudaStream_t st);
+/* GreensSet device tables from fp64 f_sp0 / g_sp0 (device n x n maps). */
+int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
+                      int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out,
+                      cudaStream_t st);
+#ifdef __cplusplus
+}
+#endif

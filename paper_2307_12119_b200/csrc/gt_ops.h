@@ -1,0 +1,20 @@
+// gt_ops.h — host orchestration of the reference-API solves (steady, step,
+// trace, Monte Carlo, calibration) over the device kernels.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+gth::Greens gt_ops_calibrate_modal(const gth::Stack& s, const gth::VarParams& v, const gth::Field* nominal_leak,
+                                   double leak_total);
+gth::Field gt_ops_steady(const gth::Greens& g, const gth::Field& p_dyn, bool with_rand, double* online_ms);
+std::vector<gth::Field> gt_ops_step(const gth::Greens& g, const gth::Field& p_dyn, const std::vector<double>& times,
+                                    bool with_rand, double* online_ms);
+void gt_ops_check_trace(double dt, const std::vector<gth::Field>& frames);
+std::vector<gth::Field> gt_ops_trace(const gth::Greens& g, double dt, const std::vector<gth::Field>& frames,
+                                     int window, bool with_rand, std::vector<double>* times, double* online_ms);
+void gt_ops_monte_carlo(const gth::Greens& g, const gth::VarParams& v, const gth::Field& nominal_leak,
+                        const gth::Field& p_dyn, const std::vector<unsigned long long>& seeds, int jobs,
+                        const std::string& csv_path, double* mean_max, double* std_max);

@@ -1,0 +1,503 @@
+// mc_modeA.cu — fused three-pass Monte-Carlo steady composition (mode A).
+//
+// One unit of work = the reference's monte_carlo run_one (solver.cpp:353-374)
+// on a (power map, variation map) pair:
+//   p_leak0 = leak_frac * p_dyn * var               (leakage_baseline, variation.cpp:162-195)
+//   mu = mean(p_leak0), p_var = p_leak0 - mu
+//   F_det  = fk / (1 - alpha g (1+F(mu)) - mu beta fk)           (greens.cpp:203-216)
+//   F_rand = F_det (beta fk q + alpha F(p_var) g) /
+//            (1 - alpha (1+F(mu)+F(p_var)) g - mu beta fk - beta fk q)  (greens.cpp:225-251)
+//   T = max(0, crop(IFFT(F_det . FFT(mirror(p_dyn+p_leak0))))
+//            + kernel_to_die(IFFT(F_rand)) o p_var * sum(applied) * rand_scale)
+//
+// All transforms are on the mirror-padded m = 2n torus. Instead of the
+// reference's four full m x m complex FFTs per sample, the path runs:
+//   pass 1 (rows)   : per die row x, ONE complex length-m FFT of
+//                     z = mirror(applied row) + i * centre-embedded(p_leak0 row),
+//                     split into the two half spectra A[x][v], B[x][v] (v < n+1),
+//                     plus the row-symmetrised p_leak0 S[x][dv] for q.
+//   pass 2 (columns): per column v, expand A (mirror) and B (centre embedding)
+//                     to length m, forward FFT, closed-form spectral algebra,
+//                     inverse FFT, keep only the n rows the die needs.
+//   pass 3 (rows)   : per die row, one complex length-m inverse FFT of
+//                     Y + i R (both Hermitian), crop / kernel_to_die gather,
+//                     Hadamard term, clamp, per-sample max / sum.
+// F(p_var) is formed in pass 2 as F(p_leak0) - mu * K1 with K1 = k1 (x) k1 the
+// analytic spectrum of the centred die box, so pass 1 never waits for mu.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "fft_tile.cuh"
+#include "gt_device.h"
+
+namespace gtb {
+
+template <typename T>
+struct Real;
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Sum of `v` over the CTA, result valid in thread 0. `red` >= 32 doubles.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (ln == 0) red[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = ln < (NT >> 5) ? red[ln] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* red) {
+    v = warp_max(v);
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (ln == 0) red[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = ln < (NT >> 5) ? red[ln] : 0.0;
+        r = warp_max(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ bool finite_(T v) {
+    return isfinite(v);
+}
+
+template <typename T>
+struct MCIn {
+    const T* P;
+    const T* N;
+    const T* V;
+    long long sP, sN, sV;
+    T nom_scale;
+    __device__ __forceinline__ const T* p(size_t s) const { return P + s * sP; }
+    __device__ __forceinline__ const T* nn(size_t s) const { return N + s * sN; }
+    __device__ __forceinline__ const T* v(size_t s) const { return V + s * sV; }
+};
+
+template <typename T, int M>
+struct MCGeom {
+    using G = TileGeom<T, M>;
+    static constexpr int n = M / 2;
+    static constexpr int c = n / 2;
+    static constexpr int h = n + 1;
+    static constexpr int L = G::L;
+    static constexpr int NT = G::NT;
+    static constexpr int W = L / 2;  // columns per pass-2 tile
+    static constexpr int hp = ((h + W - 1) / W) * W;
+    static constexpr int LP = L + 1;  // padded pitch for row tiles (transposing I/O)
+    static constexpr int SP = n + 1;  // padded pitch of the row staging arrays
+};
+
+// ------------------------------------------------------------------ pass 1
+template <typename T, int M>
+__global__ void __launch_bounds__(TileGeom<T, M>::NT)
+mc_pass1(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
+         cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
+         const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
+    using Gm = MCGeom<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
+    constexpr int hp = Gm::hp, SP = Gm::SP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + M * LP;
+    T* st_a = reinterpret_cast<T*>(s_tw + M);
+    T* st_l = st_a + L * SP;
+    double* red = reinterpret_cast<double*>(st_l + L * SP);
+
+    const int x0 = blockIdx.x * L;
+    const int s = blockIdx.y;
+    const size_t sg = static_cast<size_t>(sample0) + s;
+    const T* P = in.p(sg);
+    const T* Nm = in.nn(sg);
+    const T* V = in.v(sg);
+    const bool n_is_p = Nm == P;
+
+    load_twiddles<T, M, NT>(s_tw, g_tw);
+
+    double sum_l = 0.0, sum_a = 0.0;
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < L * n; idx += NT) {
+        const int l = idx / n, y = idx - l * n;
+        const int x = x0 + l;
+        T a = T(0), lk = T(0);
+        if (x < n) {
+            const T p = P[x * n + y];
+            const T nm = n_is_p ? p : Nm[x * n + y];
+            const T vr = V[x * n + y];
+            if (!(p >= T(0)) || !finite_(p) || !(nm >= T(0)) || !finite_(nm)) bad |= GTD_ST_BAD_POWER;
+            if (!(vr >= var_lo && vr <= var_hi)) bad |= GTD_ST_BAD_VAR;
+            lk = in.nom_scale * nm * vr;
+            a = p + lk;
+            sum_l += double(lk);
+            sum_a += double(a);
+        }
+        st_a[l * SP + y] = a;
+        st_l[l * SP + y] = lk;
+    }
+    // reductions (also act as the barrier for the staging arrays)
+    const double tl = block_sum<NT>(sum_l, red);
+    const double ta = block_sum<NT>(sum_a, red);
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        atomicAdd(&stats[sg].sum_leak, tl);
+        atomicAdd(&stats[sg].sum_applied, ta);
+        if (bad) atomicOr(&stats[sg].status, bad);
+    }
+
+    // Build the packed tile: re = mirror(applied), im = centre-embedded p_leak0.
+    for (int idx = threadIdx.x; idx < M * L; idx += NT) {
+        const int l = idx % L, j = idx / L;
+        const int ym = j < n ? j : M - 1 - j;
+        T re = st_a[l * SP + ym];
+        T im = T(0);
+        if (j < c)
+            im = st_l[l * SP + j + c];
+        else if (j >= M - c)
+            im = st_l[l * SP + j - M + c];
+        tile[j * LP + l] = mk<T>(re, im);
+    }
+    // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185).
+    for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+        const int l = idx / hp, dv = idx - l * hp;
+        const int x = x0 + l;
+        if (x >= n) continue;
+        T v = T(0);
+        if (dv < h) {
+            const int jp = min(c + dv, n - 1), jm = max(c - dv, 0);
+            v = st_l[l * SP + jp] + st_l[l * SP + jm];
+        }
+        Srow[(static_cast<size_t>(s) * n + x) * hp + dv] = v;
+    }
+    __syncthreads();
+    tile_fft<T, M, L, LP, NT, -1>(tile, s_tw);
+
+    // Split Z into the two real-input half spectra and store rows.
+    for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+        const int l = idx / hp, v = idx - l * hp;
+        const int x = x0 + l;
+        if (x >= n) continue;
+        cplx<T> A = mk<T>(T(0), T(0)), B = A;
+        if (v < h) {
+            const cplx<T> Z = tile[v * LP + l];
+            const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
+            A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
+            const T dx = Z.x - Zc.x, dy = Z.y - Zc.y;
+            B = mk<T>(T(0.5) * dy, T(-0.5) * dx);
+        }
+        const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+        Aspec[o] = A;
+        Bspec[o] = B;
+    }
+}
+
+// ------------------------------------------------------------------ pass 2
+template <typename T, int M>
+__global__ void __launch_bounds__(TileGeom<T, M>::NT)
+mc_pass2(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
+         cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
+         gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
+         const cplx<T>* __restrict__ fk, const T* __restrict__ gtab,
+         const cplx<T>* __restrict__ k1, T alpha, T beta, int mu_per_sample, T mu_fixed) {
+    using Gm = MCGeom<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT, W = Gm::W;
+    constexpr int hp = Gm::hp;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + M * L;
+    T* s_srow = reinterpret_cast<T*>(s_tw + M);
+
+    const int v0 = blockIdx.x * W;
+    const int s = blockIdx.y;
+    const size_t sg = static_cast<size_t>(sample0) + s;
+    const size_t sbase = static_cast<size_t>(s) * n * hp;
+
+    load_twiddles<T, M, NT>(s_tw, g_tw);
+    // Zero the rows of the B lines outside the centre embedding.
+    for (int idx = threadIdx.x; idx < (M - 2 * c) * W; idx += NT) {
+        const int w = idx % W, u = c + idx / W;
+        tile[u * L + W + w] = mk<T>(T(0), T(0));
+    }
+    for (int idx = threadIdx.x; idx < n * W; idx += NT) {
+        const int w = idx % W, x = idx / W;
+        const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
+        const cplx<T> a = Aspec[o];
+        tile[x * L + w] = a;
+        tile[(M - 1 - x) * L + w] = a;
+        const int rho = (x - c + M) & (M - 1);
+        tile[rho * L + W + w] = Bspec[o];
+        s_srow[x * W + w] = Srow[o];
+    }
+    // Per-sample scalars (pass 1 has completed: kernel boundary).
+    const double n2 = double(n) * double(n);
+    const double mu_s = stats[sg].sum_leak / n2;
+    const T mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
+    const T* Nm = in.nn(sg);
+    const T* V = in.v(sg);
+    const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
+    const T pl_00 = in.nom_scale * Nm[0] * V[0];
+    // q = sym(Q), Q = p_var + p_var(c,c) - p_var(0,0)  (greens.cpp:177-184)
+    const T qshift = T(double(pl_cc) - double(pl_00) - mu_s);
+    const T mus = T(mu_s);
+    __syncthreads();
+    tile_fft<T, M, L, L, NT, -1>(tile, s_tw);
+
+    int flags = 0;
+    for (int idx = threadIdx.x; idx < M * W; idx += NT) {
+        const int w = idx % W, u = idx / W;
+        const int v = v0 + w;
+        if (v >= h) continue;
+        const int du = u <= M - u ? u : M - u;
+        const cplx<T> Ah = tile[u * L + w];
+        const cplx<T> Bh = tile[u * L + W + w];
+        const cplx<T> K = cmul<T>(k1[u], k1[v]);
+        const cplx<T> Bp = mk<T>(Bh.x - mus * K.x, Bh.y - mus * K.y);  // F(p_var)
+        const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
+        const T g = gtab[du * (n + 1) + v];
+        const int ip = min(c + du, n - 1), im = max(c - du, 0);
+        const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
+        const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
+        // deterministic closed form
+        const T a1 = T(1) - alpha * g * (T(1) + fmu);
+        const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
+        if (cabs2<T>(den1) < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
+        const cplx<T> Fdet = cdiv<T>(f, den1);
+        const cplx<T> Y = cmul<T>(Fdet, Ah);
+        // random closed form
+        const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
+        const cplx<T> num = cmul<T>(Fdet, t1);
+        const cplx<T> den2 = mk<T>(a1 - alpha * g * Bp.x - mu_g * beta * f.x - beta * q * f.x,
+                                   -alpha * g * Bp.y - mu_g * beta * f.y - beta * q * f.y);
+        if (cabs2<T>(den2) < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
+        const cplx<T> R = cdiv<T>(num, den2);
+        tile[u * L + w] = Y;
+        tile[u * L + W + w] = R;
+    }
+    flags = __syncthreads_or(flags);
+    if (flags && threadIdx.x == 0) atomicOr(&stats[sg].status, flags);
+    tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
+
+    // Keep rows [0, n) of Y (crop) and rows rho(x) of R (kernel_to_die), in place.
+    for (int idx = threadIdx.x; idx < n * W; idx += NT) {
+        const int w = idx % W, x = idx / W;
+        const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
+        const int rho = (x - c + M) & (M - 1);
+        Aspec[o] = tile[x * L + w];
+        Bspec[o] = tile[rho * L + W + w];
+    }
+}
+
+// ------------------------------------------------------------------ pass 3
+template <typename T, int M>
+__global__ void __launch_bounds__(TileGeom<T, M>::NT)
+mc_pass3(const MCIn<T> in, int sample0, const cplx<T>* __restrict__ Aspec,
+         const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
+         const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
+    using Gm = MCGeom<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
+    constexpr int hp = Gm::hp;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + M * LP;
+    double* red = reinterpret_cast<double*>(s_tw + M);
+
+    const int x0 = blockIdx.x * L;
+    const int s = blockIdx.y;
+    const size_t sg = static_cast<size_t>(sample0) + s;
+    load_twiddles<T, M, NT>(s_tw, g_tw);
+
+    for (int idx = threadIdx.x; idx < L * h; idx += NT) {
+        const int l = idx / h, v = idx - l * h;
+        const int x = x0 + l;
+        cplx<T> y = mk<T>(T(0), T(0)), r = y;
+        if (x < n) {
+            const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+            y = Aspec[o];
+            r = Bspec[o];
+        }
+        if (v == 0 || v == n) {
+            tile[v * LP + l] = mk<T>(y.x, r.x);
+        } else {
+            tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
+            tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+        }
+    }
+    const double n2 = double(n) * double(n);
+    const double mu_s = stats[sg].sum_leak / n2;
+    const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+    const T inv = T(1.0 / (double(M) * double(M)));
+    const T* Nm = in.nn(sg);
+    const T* V = in.v(sg);
+    __syncthreads();
+    tile_fft<T, M, L, LP, NT, +1>(tile, s_tw);
+
+    double sum_t = 0.0;
+    double mx = 0.0;
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < L * n; idx += NT) {
+        const int l = idx / n, j = idx - l * n;
+        const int x = x0 + l;
+        if (x >= n) continue;
+        const T yv = tile[j * LP + l].x * inv;
+        const int jr = (j - c + M) & (M - 1);
+        const T rv = tile[jr * LP + l].y * inv;
+        const T pv = T(double(in.nom_scale * Nm[x * n + j] * V[x * n + j]) - mu_s);
+        T t = yv + rv * pv * scale;
+        if (!finite_(t)) bad = GTD_ST_NONFINITE;
+        t = t > T(0) ? t : T(0);
+        if (out) out[(sg * n + x) * n + j] = t;
+        sum_t += double(t);
+        mx = fmax(mx, double(t));
+    }
+    const double ts = block_sum<NT>(sum_t, red);
+    const double tm = block_max<NT>(mx, red);
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        atomicAdd(&stats[sg].sum_rise, ts);
+        atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
+        if (bad) atomicOr(&stats[sg].status, bad);
+        if (blockIdx.x == 0) stats[sg].mu = mu_s;
+    }
+}
+
+__global__ void mc_finalize(gtd_sample_stats* stats, int sample0, int count, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    gtd_sample_stats& st = stats[sample0 + i];
+    st.max_rise = __longlong_as_double(static_cast<long long>(st.max_bits));
+    st.mean_rise = st.sum_rise / (double(n) * double(n));
+}
+
+// ------------------------------------------------------------------ host side
+template <typename T, int M>
+struct MCLaunch {
+    using Gm = MCGeom<T, M>;
+    static size_t smem1() {
+        return sizeof(cplx<T>) * (M * Gm::LP + M) + sizeof(T) * 2 * Gm::L * Gm::SP + 64 * sizeof(double);
+    }
+    static size_t smem2() {
+        return sizeof(cplx<T>) * (M * Gm::L + M) + sizeof(T) * Gm::n * Gm::W;
+    }
+    static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
+
+    static int run(const gtd_greens* g, const MCIn<T>& in, int batch, const gtd_mc_opts* o,
+                   T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st) {
+        constexpr int n = Gm::n, hp = Gm::hp, L = Gm::L, NT = Gm::NT;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(mc_pass1<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem1()));
+            cudaFuncSetAttribute(mc_pass2<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
+            cudaFuncSetAttribute(mc_pass3<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem3()));
+            init = true;
+        }
+        const size_t per = static_cast<size_t>(n) * hp;
+        cplx<T>* A = reinterpret_cast<cplx<T>*>(scratch);
+        cplx<T>* B = A + per * chunk;
+        T* S = reinterpret_cast<T*>(B + per * chunk);
+        const cplx<T>* tw = reinterpret_cast<const cplx<T>*>(g->tw);
+        const cplx<T>* fk = reinterpret_cast<const cplx<T>*>(g->fk);
+        const T* gt = reinterpret_cast<const T*>(g->gtab);
+        const cplx<T>* k1 = reinterpret_cast<const cplx<T>*>(g->k1);
+        const T var_lo = T(exp(-o->exponent_cap)), var_hi = T(exp(o->exponent_cap));
+        cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
+        for (int s0 = 0; s0 < batch; s0 += chunk) {
+            const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
+            dim3 g1((n + L - 1) / L, cnt), g2(hp / Gm::W, cnt);
+            mc_pass1<T, M><<<g1, NT, smem1(), st>>>(in, s0, A, B, S, stats, tw, var_lo, var_hi);
+            mc_pass2<T, M><<<g2, NT, smem2(), st>>>(in, s0, A, B, S, stats, tw, fk, gt, k1,
+                                                   T(g->alpha), T(g->beta), o->mu_per_sample,
+                                                   T(g->mu_fixed));
+            mc_pass3<T, M><<<g1, NT, smem3(), st>>>(in, s0, A, B, stats, tw, out,
+                                                   T(g->rand_scale), o->with_rand);
+            mc_finalize<<<(cnt + 127) / 128, 128, 0, st>>>(stats, s0, cnt, n);
+        }
+        return static_cast<int>(cudaGetLastError());
+    }
+};
+
+}  // namespace gtb
+
+using namespace gtb;
+
+template <typename T>
+static int dispatch_mc(const gtd_greens* g, const gtd_mc_in* i, int batch, const gtd_mc_opts* o,
+                       void* out, gtd_sample_stats* stats, void* scratch, int chunk,
+                       cudaStream_t st) {
+    MCIn<T> in;
+    in.P = static_cast<const T*>(i->P);
+    in.N = static_cast<const T*>(i->N);
+    in.V = static_cast<const T*>(i->V);
+    in.sP = i->sP;
+    in.sN = i->sN;
+    in.sV = i->sV;
+    in.nom_scale = T(i->nom_scale);
+    T* O = static_cast<T*>(out);
+    switch (g->m) {
+        case 32: return MCLaunch<T, 32>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 64: return MCLaunch<T, 64>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 128: return MCLaunch<T, 128>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 256: return MCLaunch<T, 256>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 512: return MCLaunch<T, 512>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 1024: return MCLaunch<T, 1024>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
+template <typename T>
+static int geom_hp(int m) {
+    switch (m) {
+        case 32: return MCGeom<T, 32>::hp;
+        case 64: return MCGeom<T, 64>::hp;
+        case 128: return MCGeom<T, 128>::hp;
+        case 256: return MCGeom<T, 256>::hp;
+        case 512: return MCGeom<T, 512>::hp;
+        case 1024: return MCGeom<T, 1024>::hp;
+        default: return -1;
+    }
+}
+
+extern "C" {
+
+int gtd_padded_width(int n, int fp64) { return fp64 ? geom_hp<double>(2 * n) : geom_hp<float>(2 * n); }
+
+size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64) {
+    const int hp = gtd_padded_width(n, fp64);
+    if (hp < 0) return 0;
+    const size_t cb = fp64 ? 16 : 8, rb = fp64 ? 8 : 4;
+    return static_cast<size_t>(n) * hp * (2 * cb + rb);
+}
+
+int gtd_mc_launch_count(int batch, int chunk) {
+    const int chunks = (batch + chunk - 1) / chunk;
+    return 1 + chunks * 4;  // memset + (pass1, pass2, pass3, finalize) per chunk
+}
+
+int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_mc_opts* opts,
+                 void* out, gtd_sample_stats* stats, void* scratch, int chunk,
+                 cudaStream_t stream) {
+    if (!g || !in || batch < 1 || chunk < 1) return static_cast<int>(cudaErrorInvalidValue);
+    return g->fp64 ? dispatch_mc<double>(g, in, batch, opts, out, stats, scratch, chunk, stream)
+                   : dispatch_mc<float>(g, in, batch, opts, out, stats, scratch, chunk, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+"""Mode-A Monte-Carlo batch on the GPU vs the CPU oracle (the reference's own
+run_one arithmetic, solver.cpp:353-374) through the C ABI.
+
+Tolerances: fp64 device path vs fp64 reference: 1e-8 K absolute (FFT
+algorithm differences only). fp32 device path: the north-star bar of
+1e-3 K maximum absolute error (BASELINE.json).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FP64_ATOL = 1e-8
+FP32_ATOL = 1e-3
+
+
+def _dg(g, prec):
+    from paper_2307_12119_b200.api import DeviceGreens
+    return DeviceGreens(g, prec)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN / "mc_n64.npz")
+
+
+@pytest.fixture(scope="module")
+def g64(greens64, golden):
+    return dataclasses.replace(greens64, rand_scale=float(golden["rand_scale"]))
+
+
+@pytest.mark.parametrize("prec,atol", [(1, FP64_ATOL), (0, FP32_ATOL)])
+def test_mc_matches_golden(b200lib, g64, golden, prec, atol):
+    dg = _dg(g64, prec)
+    out, mx, mean, st, _ = dg.mc_batch_host(golden["p_dyn"], golden["var"], dg.opts(mu_per_sample=1))
+    assert (st == 0).all(), st
+    err = np.abs(out.astype(np.float64) - golden["t_mu_sample"]).max()
+    print(f"prec={prec} max|dT|={err:.3e} K on peak {golden['max_mu_sample'].max():.1f} K")
+    assert err <= atol
+    np.testing.assert_allclose(mx, golden["max_mu_sample"], rtol=0, atol=atol)
+    np.testing.assert_allclose(mean, golden["mean_mu_sample"], rtol=0, atol=atol)
+
+
+@pytest.mark.parametrize("prec,atol", [(1, FP64_ATOL), (0, FP32_ATOL)])
+def test_mc_greens_mu_mode(b200lib, g64, golden, prec, atol):
+    """mu_per_sample = 0: closed forms at the GreensSet mu (reference monte_carlo)."""
+    dg = _dg(g64, prec)
+    _, mx, mean, st, _ = dg.mc_batch_host(golden["p_dyn"], golden["var"], dg.opts(mu_per_sample=0),
+                                          want_maps=False)
+    assert (st == 0).all()
+    np.testing.assert_allclose(mx, golden["max_mu_greens"], rtol=0, atol=atol)
+    np.testing.assert_allclose(mean, golden["mean_mu_greens"], rtol=0, atol=atol)
+
+
+@pytest.mark.parametrize("n", [16, 32, 128])
+def test_mc_live_oracle_sizes(b200lib, oracle, n):
+    """Other grid sizes: reference calibrate() at n, fresh seeded inputs, live oracle."""
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import GreensArrays
+    d = oracle.calibrate(n, die_edge=0.016, beta=0.017, leak_total=84.0, fit_rand_scale=False)
+    g = GreensArrays(**{k: d[k] for k in ("n", "pitch", "f_sp0", "g_sp0", "phi", "kappa_inf", "alpha", "beta",
+                                           "mu")}, rand_scale=1.0)
+    cfg = dataclasses.replace(inputs.CONFIGS["cfg1"], n=n, blocks=min(32, n * n // 16), base_seed=77 + n)
+    B = 5
+    p = inputs.power_batch(cfg, 0, B, np.float64)
+    v = inputs.variation_batch(cfg, 0, B).numpy().astype(np.float64)
+    t_ref, mx_ref, _, st_ref, _ = oracle.mc_batch(g, p, v, jobs=4)
+    assert (st_ref == 0).all()
+    dg = _dg(g, 1)
+    out, mx, _, st, _ = dg.mc_batch_host(p, v, dg.opts())
+    assert (st == 0).all()
+    assert np.abs(out - t_ref).max() <= FP64_ATOL
+
+
+def test_mc_config1_grid_fp32(b200lib, oracle, greens256):
+    """The headline grid (n = 256, config-1 generator) in fp32 against the fp64 reference."""
+    from paper_2307_12119_b200 import inputs
+    cfg = inputs.CONFIGS["cfg1"]
+    B = 6
+    p = inputs.power_batch(cfg, 0, B, np.float32)
+    v = inputs.variation_batch(cfg, 0, B).numpy().astype(np.float32)
+    t_ref, mx_ref, _, st_ref, _ = oracle.mc_batch(greens256, p, v, jobs=8)
+    assert (st_ref == 0).all()
+    for prec, atol in ((0, FP32_ATOL), (1, FP64_ATOL)):
+        dg = _dg(greens256, prec)
+        out, mx, _, st, _ = dg.mc_batch_host(p, v, dg.opts())
+        assert (st == 0).all()
+        err = np.abs(out.astype(np.float64) - t_ref).max()
+        print(f"n=256 prec={prec} max|dT|={err:.3e} K (peak {t_ref.max():.1f} K)")
+        assert err <= atol
+
+
+def test_mc_sample_status_isolated(b200lib, g64, golden):
+    """A bad sample is flagged (check_power / exponent cap) without touching its neighbours."""
+    p = golden["p_dyn"].astype(np.float64).copy()
+    v = golden["var"].astype(np.float64).copy()
+    p[1, 3, 3] = -1.0        # ConfigError in the reference (solver.cpp:63-70)
+    v[2, 0, 0] = np.exp(7.0)  # |ln var| > 6: ValidationError (variation.cpp:173-178)
+    dg = _dg(g64, 1)
+    out, mx, _, st, _ = dg.mc_batch_host(p, v, dg.opts())
+    assert st[0] == 0 and st[3] == 0
+    assert st[1] & 1 and st[2] & 2
+    np.testing.assert_allclose(out[0], golden["t_mu_sample"][0], atol=FP64_ATOL)
+    np.testing.assert_allclose(out[3], golden["t_mu_sample"][3], atol=FP64_ATOL)
+
+
+def test_mc_runaway_flag(b200lib, oracle, g64, golden):
+    """Leakage gain at unity -> RunawayError in the reference (greens.cpp:32-39)."""
+    g = dataclasses.replace(g64, beta=5.0)
+    _, _, _, st_ref, _ = oracle.mc_batch(g, golden["p_dyn"][:2], golden["var"][:2], jobs=2, want_maps=False)
+    dg = _dg(g, 1)
+    _, _, _, st, _ = dg.mc_batch_host(golden["p_dyn"][:2], golden["var"][:2], dg.opts(), want_maps=False)
+    assert (st_ref == 3).all()
+    assert ((st & (4 | 8)) != 0).all()
+
+
+def test_mc_chunking_is_invisible(b200lib, g64, golden):
+    p = np.concatenate([golden["p_dyn"]] * 3).astype(np.float32)
+    v = np.concatenate([golden["var"]] * 3).astype(np.float32)
+    dg = _dg(g64, 0)
+    a = dg.mc_batch_host(p, v, dg.opts(chunk=5))
+    b = dg.mc_batch_host(p, v, dg.opts(chunk=12))
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_mc_device_resident_equals_host_path(b200lib, g64, golden):
+    import torch
+    from paper_2307_12119_b200.api import SAMPLE_STATS_DTYPE
+    dg = _dg(g64, 0)
+    p = torch.from_numpy(golden["p_dyn"]).cuda()
+    v = torch.from_numpy(golden["var"]).cuda()
+    out = torch.empty_like(p)
+    B = p.shape[0]
+    stats = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    dg.mc_batch_device(p.data_ptr(), v.data_ptr(), B, dg.opts(), out.data_ptr(), stats.data_ptr(),
+                       torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=SAMPLE_STATS_DTYPE)
+    h_out, h_mx, _, _, _ = dg.mc_batch_host(golden["p_dyn"], golden["var"], dg.opts())
+    np.testing.assert_array_equal(out.cpu().numpy(), h_out)
+    np.testing.assert_array_equal(st["max_rise"], h_mx)
