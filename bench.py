@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json headline: steady-state thermal solves/s on the
+256x256 Monte-Carlo batch (config 1) and its fraction of the B200 HBM roofline.
+
+One "step" = one pass of the hot path over the configured batch of
+(power map, variation map) pairs per GPU: the reference's monte_carlo run_one
+(solver.cpp:353-374) per pair — leakage baseline, deterministic and random
+closed-form Green's functions, mirror-padded convolution, shift-variant
+Hadamard term, clamp, max/mean — through libgreentherm_b200.so.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun, one rank per GPU): samples are sharded, no collective on
+the data path ("scaling": "weak": every rank solves its own batch of distinct
+seeded pairs); timing = CUDA events on the launching stream, max over ranks.
+--impl reference times the reference's own CPU implementation (the unchanged
+reference core compiled by oracle/Makefile) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "steady-state thermal solves/sec @256x256 MC batch; % of HBM roofline"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--batch", type=int, default=0, help="pairs per GPU (0 = config batch)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def greens_cfg1():
+    """GreensSet for the config-1 grid: the reference's own calibrate() at n=256
+    (FDM impulse response + alpha fit), committed as data in tests/golden."""
+    from paper_2307_12119_b200.api import GreensArrays
+    z = np.load(ROOT / "tests" / "golden" / "greens_n256.npz")
+    f = z["f_sp0"]
+    n = int(z["n"])
+    c = n // 2
+    return GreensArrays(n=n, pitch=float(z["pitch"]), f_sp0=f, g_sp0=f + (f[c, c] - float(z["kappa_inf"])),
+                        phi=float(z["phi"]), kappa_inf=float(z["kappa_inf"]), alpha=float(z["alpha"]),
+                        beta=float(z["beta"]), mu=float(z["mu"]), capacitance=float(z["capacitance"]),
+                        rand_scale=float(z["rand_scale"]))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        self.t_on = None
+
+    def mark_load(self):
+        self.t_on = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower().startswith("active")})
+        loaded = [r[0] for r in rows if r[0] > 0.5 * r[1]] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def bytes_per_sample(n: int, es: int) -> list[float]:
+    """Algorithmic HBM bytes per (power map, variation map) pair for each fused
+    pass: h = n+1 half-spectrum columns."""
+    h = n + 1
+    cb = 2 * es
+    p1 = 2 * es * n * n + 2 * cb * n * h + es * n * h      # P,var in; A,B half spectra + S out
+    p2 = (2 * cb + es) * n * h + 2 * cb * n * h             # A,B,S in; Y',R' out
+    p3 = 2 * cb * n * h + 2 * es * n * n + es * n * n       # Y',R' + P,var in; T out
+    return [p1, p2, p3]
+
+
+def survey_bytes_per_solve(n: int, es: int) -> float:
+    """SURVEY.md §8(d) mode-A unit: B_A = 5 p n^2 + 16 p n h."""
+    return 5 * es * n * n + 16 * es * n * (n + 1)
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_reference_rate(cfg, seconds: float, threads: int, start: int = 0):
+    """The reference's own CPU path (oracle/_ref) on a bounded sample."""
+    from oracle import refpy
+    from paper_2307_12119_b200 import inputs
+    if not refpy.build_if_possible():
+        return None
+    g = greens_cfg1()
+    # probe: one sample per thread, then size the sample to ~`seconds`
+    k = max(1, threads)
+    p = inputs.power_batch(cfg, start, k, np.float32)
+    v = inputs.variation_batch(cfg, start, k).numpy().astype(np.float32)
+    t = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+    S = int(max(k, min(4096, k * max(1.0, seconds / max(t, 1e-3)))))
+    S = max(k, (S // k) * k)
+    p = inputs.power_batch(cfg, start, S, np.float32)
+    v = inputs.variation_batch(cfg, start, S).numpy().astype(np.float32)
+    _, _, _, st, secs = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)
+    return {"value": S / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{S} cfg1 pairs (n=256) through the unchanged reference core "
+                      f"(oracle/_ref, FFTW/Eigen shims), {threads} std::threads as in solver.cpp:376-387; "
+                      f"{secs:.1f} s", "failed": int((st != 0).sum())}
+
+
+def run_reference_arm(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    per_step = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    from oracle import refpy
+    from paper_2307_12119_b200 import inputs
+    if not refpy.build_if_possible():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built and /root/reference absent"}))
+        return
+    g = greens_cfg1()
+    k = threads
+    p = inputs.power_batch(cfg, 0, k, np.float32)
+    v = inputs.variation_batch(cfg, 0, k).numpy().astype(np.float32)
+    t = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+    S = max(k, int(k * per_step / max(t, 1e-3)) // k * k)
+    p = inputs.power_batch(cfg, 0, S, np.float32)
+    v = inputs.variation_batch(cfg, 0, S).numpy().astype(np.float32)
+    for _ in range(args.warmup):
+        refpy.mc_batch(g, p[:k], v[:k], jobs=threads, want_maps=False)
+    secs = 0.0
+    for _ in range(args.steps):
+        secs += refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+    value = S * args.steps / secs
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "cfg1 mode A: reference run_one on 256x256 (power, variation) pairs",
+                       "n": 256, "pairs_per_step": S},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{S} cfg1 pairs per step, unchanged reference core (oracle/_ref)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import GT_FP32, GT_FP64, SAMPLE_STATS_DTYPE, DeviceGreens
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prec = GT_FP64 if args.precision == "fp64" else GT_FP32
+    tdt = torch.float64 if prec == GT_FP64 else torch.float32
+    es = 8 if prec == GT_FP64 else 4
+    B = args.batch or cfg.batch
+    n = cfg.n
+
+    dg = DeviceGreens(greens_cfg1(), prec, device=local)
+    opts = dg.opts(leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=args.chunk)
+    P, V = inputs.mc_inputs(cfg, rank * B, B, device=str(dev), torch_dtype=tdt)
+    out = torch.empty_like(P)
+    stats = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        dg.mc_batch_device(P.data_ptr(), V.data_ptr(), B, opts, out.data_ptr(), stats.data_ptr(),
+                           stream.cuda_stream)
+
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks.mark_load()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dg.profile_begin()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pass_ms, kernels, calls = dg.profile_end()
+    if ws > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = ws * B / (ms / 1e3)
+
+    st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=SAMPLE_STATS_DTYPE)
+    failed = int((st["status"] != 0).sum())
+
+    # fp64 residual check on a subset (BASELINE cfg1: "fp32 with fp64 residual check")
+    resid = None
+    if prec == GT_FP32:
+        k = min(32, B)
+        dg64 = DeviceGreens(greens_cfg1(), GT_FP64, device=local)
+        P64, V64 = P[:k].double().contiguous(), V[:k].double().contiguous()
+        o64 = torch.empty_like(P64)
+        s64 = torch.zeros(k * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        dg64.mc_batch_device(P64.data_ptr(), V64.data_ptr(), k, dg64.opts(), o64.data_ptr(), s64.data_ptr(),
+                             stream.cuda_stream)
+        torch.cuda.synchronize()
+        resid = {"samples": k, "max_abs_K": float((out[:k].double() - o64).abs().max().item()),
+                 "peak_K": float(o64.max().item())}
+        dg64.close()
+
+    # roofline of the dominant pass (CUDA events around each pass on the launching stream)
+    bps = bytes_per_sample(n, es)
+    dom = int(np.argmax(pass_ms[:3]))
+    achieved = bps[dom] * B * args.steps / (pass_ms[dom] / 1e3) / 1e9
+    peak, peak_src = peaks()
+    whole = survey_bytes_per_solve(n, es) * B / (ms / 1e3) / 1e9  # per GPU
+
+    # end to end through the public host API: pinned host inputs, H2D + compute + D2H of per-pair results
+    e2e = None
+    if not args.no_e2e:
+        Ph = P.cpu().pin_memory()
+        Vh = V.cpu().pin_memory()
+        import ctypes as C
+        from paper_2307_12119_b200.api import check, lib
+        L = lib()
+        mx = np.empty(B)
+        mean = np.empty(B)
+        sts = np.empty(B, dtype=np.int32)
+        msc = C.c_double()
+
+        def e2e_step():
+            check(L, L.gt_mc_batch(dg.handle, C.c_void_p(Ph.data_ptr()), C.c_void_p(Vh.data_ptr()), B,
+                                   C.byref(opts), None, mx.ctypes.data_as(C.POINTER(C.c_double)),
+                                   mean.ctypes.data_as(C.POINTER(C.c_double)),
+                                   sts.ctypes.data_as(C.POINTER(C.c_int)), C.byref(msc)))
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        el = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev, dtype=torch.float64)
+        if ws > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * B / float(el.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * B * n * n * es, "d2h_bytes_per_step": B * SAMPLE_STATS_DTYPE.itemsize,
+               "ms_per_step": 1e3 * float(el.item()),
+               "path": "gt_mc_batch (host API): pinned p_dyn/var -> H2D, fused passes, D2H of per-pair max/mean/status"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_rate(cfg, args.cpu_seconds, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if prec == GT_FP32 else "f64", "data": "synthetic",
+            "config": {"workload": "cfg1 mode A: reference run_one (solver.cpp:353-374) per (power map, variation "
+                                   "map) pair, 256x256 grid, per-sample mean leakage, shift-variant term on",
+                       "n": n, "pairs_per_gpu": B, "precision": args.precision, "chunk": args.chunk or "auto",
+                       "greens": "reference calibrate() at n=256 (tests/golden/greens_n256.npz), rand_scale 1.0",
+                       "l2": "no flush: 2 x pairs x 256 KiB inputs per step (>> 126 MB L2)",
+                       "parallelism": f"dp{ws} (independent pairs per GPU, no collective)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": ["mc_pass1 (rows)", "mc_pass2 (columns)", "mc_pass3 (rows)"][dom],
+                         "pass_ms_per_step": [x / args.steps for x in pass_ms[:3]],
+                         "bytes_per_pair_per_pass": bps, "peak_source": peak_src,
+                         "whole_solve_GBps_survey_model": whole,
+                         "whole_solve_frac_survey_model": whole / peak},
+            "gpu_launches": int(kernels), "batch_calls": int(calls), "failed_pairs": failed,
+            "fp64_residual_check": resid, "clocks": clk,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    dg.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_2307_12119_b200 import inputs
+    cfg = inputs.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

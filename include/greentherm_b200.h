@@ -90,7 +90,8 @@ gt_status gt_mc_batch(const gt_device_greens* d, const void* p_dyn, const void* 
 
 /* Device-resident batch: all pointers are device memory on the greens'
  * device; stats is batch x gt_sample_stats. Enqueued on `stream` (a
- * cudaStream_t, NULL = the library stream); returns without synchronising. */
+ * cudaStream_t; NULL = the library's own stream, pass cudaStreamLegacy for the
+ * legacy default stream); returns without synchronising. */
 gt_status gt_mc_batch_device(const gt_device_greens* d, const void* p_dyn, const void* var,
                              int batch, const gt_batch_opts* opts, void* t_out,
                              gt_sample_stats* stats, void* stream);
@@ -99,6 +100,16 @@ gt_status gt_mc_batch_device(const gt_device_greens* d, const void* p_dyn, const
  * and the number of kernels it launches for (batch, chunk). */
 size_t gt_mc_scratch_bytes(int n, int precision);
 int gt_mc_kernel_launches(int batch, int chunk);
+
+/* Per-pass profiling of device batches: between begin and end every batch
+ * call records CUDA events on its stream around the three fused passes;
+ * end() synchronises and returns the summed milliseconds per pass
+ * (pass_ms[0..2] = row / column / row pass, pass_ms[3] = their sum), the
+ * kernels launched and the batch calls made since begin. */
+gt_status gt_profile_begin(gt_device_greens* d);
+gt_status gt_profile_end(gt_device_greens* d, double* pass_ms, long long* kernels, long long* calls);
+/* Kernels launched by this prepared set since the last gt_profile_begin. */
+long long gt_kernel_launches(const gt_device_greens* d);
 
 /* Device count visible to the library (0 without a GPU). */
 int gt_device_count(void);

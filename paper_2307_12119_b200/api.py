@@ -107,6 +107,9 @@ _EXT = [
     ("gt_mc_scratch_bytes", C.c_size_t, [cint, cint]),
     ("gt_mc_kernel_launches", cint, [cint, cint]),
     ("gt_device_count", cint, []),
+    ("gt_profile_begin", cint, [vp]),
+    ("gt_profile_end", cint, [vp, pdbl, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    ("gt_kernel_launches", C.c_longlong, [vp]),
 ]
 EXT_SYMBOLS = [n for n, _, _ in _EXT]
 
@@ -256,6 +259,17 @@ class DeviceGreens:
                         stats_ptr: int, stream: int | None = None) -> None:
         """Device-resident batch on raw device pointers (e.g. torch .data_ptr())."""
         L = lib()
+        # stream None -> library stream; 0 (torch's legacy default stream) -> cudaStreamLegacy (0x1)
+        sp = None if stream is None else C.c_void_p(stream if stream else 1)
         check(L, L.gt_mc_batch_device(self._d, C.c_void_p(p_ptr), C.c_void_p(v_ptr), batch, C.byref(opts),
-                                      C.c_void_p(out_ptr) if out_ptr else None, C.c_void_p(stats_ptr),
-                                      C.c_void_p(stream) if stream else None))
+                                      C.c_void_p(out_ptr) if out_ptr else None, C.c_void_p(stats_ptr), sp))
+
+    def profile_begin(self) -> None:
+        check(lib(), lib().gt_profile_begin(self._d))
+
+    def profile_end(self):
+        """-> (pass_ms[4], kernels, calls)"""
+        ms = (C.c_double * 4)()
+        k, c = C.c_longlong(), C.c_longlong()
+        check(lib(), lib().gt_profile_end(self._d, ms, C.byref(k), C.byref(c)))
+        return list(ms), k.value, c.value

@@ -120,7 +120,25 @@ struct gt_device_greens {
     cudaStream_t slot_stream[2] = {nullptr, nullptr};
     void* host_stats = nullptr;
     size_t host_stats_bytes = 0;
+    // profiling (gt_profile_begin/end): events recorded between pass launches
+    bool profiling = false;
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    std::vector<cudaEvent_t> event_pool;
+    size_t pool_used = 0;
+    long long kernels = 0, calls = 0;
+    static void mark(void* ctx, int point, cudaStream_t st) {
+        auto* self = static_cast<gt_device_greens*>(ctx);
+        if (self->pool_used == self->event_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            self->event_pool.push_back(e);
+        }
+        cudaEvent_t e = self->event_pool[self->pool_used++];
+        cudaEventRecord(e, st);
+        self->marks.emplace_back(point, e);
+    }
     ~gt_device_greens() {
+        for (auto e : event_pool) cudaEventDestroy(e);
         if (host_stats) cudaFreeHost(host_stats);
         for (auto& s : slot_stream)
             if (s) cudaStreamDestroy(s);
@@ -596,8 +614,10 @@ gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, cons
         in.nom_scale = opts ? opts->leak_frac : 0.3;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
         cuda_ok(gtd_mc_batch(&d->d, &in, batch, &o, t_out, reinterpret_cast<gtd_sample_stats*>(stats),
-                             d->scratch.p, chunk, st),
+                             d->scratch.p, chunk, st, d->profiling ? &gt_device_greens::mark : nullptr, d),
                 "mc batch launch");
+        d->kernels += gtd_mc_launch_count(batch, chunk);
+        d->calls += 1;
     });
 }
 
@@ -650,8 +670,9 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
             in.nom_scale = opts ? opts->leak_frac : 0.3;
             auto* dst = static_cast<gtd_sample_stats*>(d->slot_stats[s].p);
             cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, t_out ? d->slot_out[s].p : nullptr, dst, d->slot_scr[s].p,
-                                 std::min(inner, cnt), st),
+                                 std::min(inner, cnt), st, nullptr, nullptr),
                     "mc batch launch");
+            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt));
             if (t_out)
                 cuda_ok(cudaMemcpyAsync(static_cast<char*>(t_out) + s0 * map, d->slot_out[s].p, cnt * map,
                                         cudaMemcpyDeviceToHost, st),
@@ -667,5 +688,44 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         if (online_ms) *online_ms = ms_since(t0);
     });
 }
+
+gt_status gt_profile_begin(gt_device_greens* d) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(d->mu);
+        d->profiling = true;
+        d->marks.clear();
+        d->pool_used = 0;
+        d->kernels = 0;
+        d->calls = 0;
+    });
+}
+
+gt_status gt_profile_end(gt_device_greens* d, double* pass_ms, long long* kernels, long long* calls) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        double acc[4] = {0, 0, 0, 0};
+        for (size_t i = 0; i + 3 < d->marks.size(); i += 4) {
+            for (int k = 0; k < 3; ++k) {
+                if (d->marks[i + k].first != k || d->marks[i + k + 1].first != k + 1)
+                    fail(ST_INTERNAL, "profile", "unbalanced profiling marks");
+                cuda_ok(cudaEventSynchronize(d->marks[i + k + 1].second), "event sync");
+                float ms = 0.f;
+                cuda_ok(cudaEventElapsedTime(&ms, d->marks[i + k].second, d->marks[i + k + 1].second), "elapsed");
+                acc[k] += ms;
+            }
+        }
+        acc[3] = acc[0] + acc[1] + acc[2];
+        if (pass_ms)
+            for (int k = 0; k < 4; ++k) pass_ms[k] = acc[k];
+        if (kernels) *kernels = d->kernels;
+        if (calls) *calls = d->calls;
+        d->profiling = false;
+        d->marks.clear();
+        d->pool_used = 0;
+    });
+}
+
+long long gt_kernel_launches(const gt_device_greens* d) { return d->kernels; }
 
 }  // extern "C"

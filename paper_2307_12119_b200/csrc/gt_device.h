@@ -62,6 +62,11 @@ typedef struct gtd_mc_opts {
     double exponent_cap;/* |ln var| guard (variation.cpp:173-178)               */
 } gtd_mc_opts;
 
+/* Optional profiling hook: called on the host between launches with the
+ * point index (0 before pass 1, 1 after pass 1, 2 after pass 2, 3 after pass 3)
+ * so the caller can record CUDA events on the same stream. */
+typedef void (*gtd_mark_fn)(void* ctx, int point, cudaStream_t st);
+
 /* Scratch bytes needed per in-flight sample by gtd_mc_batch. */
 size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64);
 
@@ -71,7 +76,7 @@ size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64);
  * error code (0 = launched). */
 int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch,
                  const gtd_mc_opts* opts, void* out, gtd_sample_stats* stats, void* scratch,
-                 int chunk, cudaStream_t stream);
+                 int chunk, cudaStream_t stream, gtd_mark_fn mark, void* ctx);
 
 /* Number of kernel launches gtd_mc_batch issues for a given batch/chunk. */
 int gtd_mc_launch_count(int batch, int chunk);

@@ -78,6 +78,12 @@ __device__ __forceinline__ double block_max(double v, double* red) {
     return r;
 }
 
+// Bitwise OR of per-thread status flags into the sample's status word.
+__device__ __forceinline__ void or_flags(int* dst, int flags) {
+    const int w = __reduce_or_sync(0xffffffffu, flags);
+    if ((threadIdx.x & 31) == 0 && w) atomicOr(dst, w);
+}
+
 template <typename T>
 __device__ __forceinline__ bool finite_(T v) {
     return isfinite(v);
@@ -156,13 +162,12 @@ mc_pass1(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
         st_l[l * SP + y] = lk;
     }
     // reductions (also act as the barrier for the staging arrays)
+    or_flags(&stats[sg].status, bad);
     const double tl = block_sum<NT>(sum_l, red);
     const double ta = block_sum<NT>(sum_a, red);
-    bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
         atomicAdd(&stats[sg].sum_leak, tl);
         atomicAdd(&stats[sg].sum_applied, ta);
-        if (bad) atomicOr(&stats[sg].status, bad);
     }
 
     // Build the packed tile: re = mirror(applied), im = centre-embedded p_leak0.
@@ -293,8 +298,8 @@ mc_pass2(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
         tile[u * L + w] = Y;
         tile[u * L + W + w] = R;
     }
-    flags = __syncthreads_or(flags);
-    if (flags && threadIdx.x == 0) atomicOr(&stats[sg].status, flags);
+    or_flags(&stats[sg].status, flags);
+    __syncthreads();
     tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
 
     // Keep rows [0, n) of Y (crop) and rows rho(x) of R (kernel_to_die), in place.
@@ -369,13 +374,12 @@ mc_pass3(const MCIn<T> in, int sample0, const cplx<T>* __restrict__ Aspec,
         sum_t += double(t);
         mx = fmax(mx, double(t));
     }
+    or_flags(&stats[sg].status, bad);
     const double ts = block_sum<NT>(sum_t, red);
     const double tm = block_max<NT>(mx, red);
-    bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
         atomicAdd(&stats[sg].sum_rise, ts);
         atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
-        if (bad) atomicOr(&stats[sg].status, bad);
         if (blockIdx.x == 0) stats[sg].mu = mu_s;
     }
 }
@@ -401,7 +405,8 @@ struct MCLaunch {
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
 
     static int run(const gtd_greens* g, const MCIn<T>& in, int batch, const gtd_mc_opts* o,
-                   T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st) {
+                   T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st,
+                   gtd_mark_fn mark, void* ctx) {
         constexpr int n = Gm::n, hp = Gm::hp, L = Gm::L, NT = Gm::NT;
         static bool init = false;
         if (!init) {
@@ -423,12 +428,16 @@ struct MCLaunch {
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
             dim3 g1((n + L - 1) / L, cnt), g2(hp / Gm::W, cnt);
+            if (mark) mark(ctx, 0, st);
             mc_pass1<T, M><<<g1, NT, smem1(), st>>>(in, s0, A, B, S, stats, tw, var_lo, var_hi);
+            if (mark) mark(ctx, 1, st);
             mc_pass2<T, M><<<g2, NT, smem2(), st>>>(in, s0, A, B, S, stats, tw, fk, gt, k1,
                                                    T(g->alpha), T(g->beta), o->mu_per_sample,
                                                    T(g->mu_fixed));
+            if (mark) mark(ctx, 2, st);
             mc_pass3<T, M><<<g1, NT, smem3(), st>>>(in, s0, A, B, stats, tw, out,
                                                    T(g->rand_scale), o->with_rand);
+            if (mark) mark(ctx, 3, st);
             mc_finalize<<<(cnt + 127) / 128, 128, 0, st>>>(stats, s0, cnt, n);
         }
         return static_cast<int>(cudaGetLastError());
@@ -442,7 +451,7 @@ using namespace gtb;
 template <typename T>
 static int dispatch_mc(const gtd_greens* g, const gtd_mc_in* i, int batch, const gtd_mc_opts* o,
                        void* out, gtd_sample_stats* stats, void* scratch, int chunk,
-                       cudaStream_t st) {
+                       cudaStream_t st, gtd_mark_fn mark, void* ctx) {
     MCIn<T> in;
     in.P = static_cast<const T*>(i->P);
     in.N = static_cast<const T*>(i->N);
@@ -453,12 +462,12 @@ static int dispatch_mc(const gtd_greens* g, const gtd_mc_in* i, int batch, const
     in.nom_scale = T(i->nom_scale);
     T* O = static_cast<T*>(out);
     switch (g->m) {
-        case 32: return MCLaunch<T, 32>::run(g, in, batch, o, O, stats, scratch, chunk, st);
-        case 64: return MCLaunch<T, 64>::run(g, in, batch, o, O, stats, scratch, chunk, st);
-        case 128: return MCLaunch<T, 128>::run(g, in, batch, o, O, stats, scratch, chunk, st);
-        case 256: return MCLaunch<T, 256>::run(g, in, batch, o, O, stats, scratch, chunk, st);
-        case 512: return MCLaunch<T, 512>::run(g, in, batch, o, O, stats, scratch, chunk, st);
-        case 1024: return MCLaunch<T, 1024>::run(g, in, batch, o, O, stats, scratch, chunk, st);
+        case 32: return MCLaunch<T, 32>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 64: return MCLaunch<T, 64>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 128: return MCLaunch<T, 128>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 256: return MCLaunch<T, 256>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 512: return MCLaunch<T, 512>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 1024: return MCLaunch<T, 1024>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -489,15 +498,15 @@ size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64) {
 
 int gtd_mc_launch_count(int batch, int chunk) {
     const int chunks = (batch + chunk - 1) / chunk;
-    return 1 + chunks * 4;  // memset + (pass1, pass2, pass3, finalize) per chunk
+    return chunks * 4;  // kernels: pass1, pass2, pass3, finalize per chunk (plus one memset node)
 }
 
 int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_mc_opts* opts,
                  void* out, gtd_sample_stats* stats, void* scratch, int chunk,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, gtd_mark_fn mark, void* ctx) {
     if (!g || !in || batch < 1 || chunk < 1) return static_cast<int>(cudaErrorInvalidValue);
-    return g->fp64 ? dispatch_mc<double>(g, in, batch, opts, out, stats, scratch, chunk, stream)
-                   : dispatch_mc<float>(g, in, batch, opts, out, stats, scratch, chunk, stream);
+    return g->fp64 ? dispatch_mc<double>(g, in, batch, opts, out, stats, scratch, chunk, stream, mark, ctx)
+                   : dispatch_mc<float>(g, in, batch, opts, out, stats, scratch, chunk, stream, mark, ctx);
 }
 
 }  // extern "C"
