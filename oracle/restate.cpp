@@ -104,7 +104,15 @@ double ref_mc_batch(const ref_greens* g, const double* p_dyn, const double* var,
     const size_t nn = static_cast<size_t>(n) * n;
     // Seed-invariant spectrum, as monte_carlo hoists it (solver.cpp:350-351).
     std::vector<cplx> fdet_fixed;
-    if (!mu_per_sample) fdet_fixed = deterministic_spectrum(gs.f_sp0, gs.phi, gs.g_sp0, gs.alpha, gs.beta, gs.mu);
+    if (!mu_per_sample) {
+        try {
+            fdet_fixed = deterministic_spectrum(gs.f_sp0, gs.phi, gs.g_sp0, gs.alpha, gs.beta, gs.mu);
+        } catch (const Error& e) {  // the whole reference call fails (solver.cpp:350-351)
+            for (int i = 0; i < batch; ++i)
+                if (status_out) status_out[i] = status_class(e);
+            return 0.0;
+        }
+    }
     const FieldMap zero(n, gs.pitch, Unit::Dimensionless);
     pool(batch, jobs, [&](int i) {
         int st = 0;

@@ -109,13 +109,17 @@ def test_mc_sample_status_isolated(b200lib, g64, golden):
 
 
 def test_mc_runaway_flag(b200lib, oracle, g64, golden):
-    """Leakage gain at unity -> RunawayError in the reference (greens.cpp:32-39)."""
-    g = dataclasses.replace(g64, beta=5.0)
-    _, _, _, st_ref, _ = oracle.mc_batch(g, golden["p_dyn"][:2], golden["var"][:2], jobs=2, want_maps=False)
-    dg = _dg(g, 1)
-    _, _, _, st, _ = dg.mc_batch_host(golden["p_dyn"][:2], golden["var"][:2], dg.opts(), want_maps=False)
+    """Leakage feedback gain exactly at unity at DC -> the deterministic denominator
+    1 - mu beta F(f_sp0) collapses: RunawayError in the reference (greens.cpp:32-39)."""
+    fk0 = float(np.sum(g64.f_sp0))  # fk[0,0] = sum(f_sp0 - phi) + phi m^2/4 (greens.cpp:194-201)
+    g = dataclasses.replace(g64, beta=1.0 / (g64.mu * fk0))
+    p, v = golden["p_dyn"][:2], golden["var"][:2]
+    _, _, _, st_ref, _ = oracle.mc_batch(g, p, v, mu_per_sample=0, jobs=2, want_maps=False)
     assert (st_ref == 3).all()
-    assert ((st & (4 | 8)) != 0).all()
+    for prec in (0, 1):
+        dg = _dg(g, prec)
+        _, _, _, st, _ = dg.mc_batch_host(p, v, dg.opts(mu_per_sample=0), want_maps=False)
+        assert ((st & 4) != 0).all(), st
 
 
 def test_mc_chunking_is_invisible(b200lib, g64, golden):
