@@ -218,7 +218,7 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     upload(d->gsp0, g.g_sp0.v.data(), g.g_sp0.v.size() * 8, st);
     d->work.ensure(static_cast<size_t>(m) * m * 16);
     d->fk.ensure(static_cast<size_t>(m) * hp * cb);
-    d->gtab.ensure(static_cast<size_t>(n + 1) * (n + 1) * rb);
+    d->gtab.ensure(static_cast<size_t>(n + 1) * hp * rb);
     cuda_ok(gtd_greens_tables(static_cast<const double*>(d->fsp0.p), static_cast<const double*>(d->gsp0.p),
                               g.phi, n, hp, d->fp64, d->tw64.p, d->work.p, d->fk.p, d->gtab.p, st),
             "greens tables");

@@ -129,16 +129,16 @@ __global__ void k_fk_half(const double2* __restrict__ K, int m, int hp, double d
     fk[static_cast<size_t>(u) * hp + v] = mk<T>(T(z.x), T(z.y));
 }
 
-// g(du,dv) = g_sp0(c,c) - 1/4 sum_{+-,+-} g_sp0(clamp(c+-du), clamp(c+-dv)).
+// g(du,dv) = g_sp0(c,c) - 1/4 sum_{+-,+-} g_sp0(clamp(c+-du), clamp(c+-dv)); row pitch hp.
 template <typename T>
-__global__ void k_gtab(const double* __restrict__ g_sp0, int n, T* __restrict__ gt) {
+__global__ void k_gtab(const double* __restrict__ g_sp0, int n, int hp, T* __restrict__ gt) {
     const int du = blockIdx.y, dv = blockIdx.x * blockDim.x + threadIdx.x;
     if (dv > n) return;
     const int c = n / 2;
     auto cl = [n](int i) { return i < 0 ? 0 : (i > n - 1 ? n - 1 : i); };
     const int ip = cl(c + du), im = cl(c - du), jp = cl(c + dv), jm = cl(c - dv);
     const double s = g_sp0[ip * n + jp] + g_sp0[ip * n + jm] + g_sp0[im * n + jp] + g_sp0[im * n + jm];
-    gt[du * (n + 1) + dv] = T(g_sp0[c * n + c] - 0.25 * s);
+    gt[du * hp + dv] = T(g_sp0[c * n + c] - 0.25 * s);
 }
 
 }  // namespace gtb
@@ -166,12 +166,12 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
     if (fp64) {
         k_fk_half<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp, dc_add,
                                                                       static_cast<double2*>(fk_out));
-        k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n,
+        k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                           static_cast<double*>(gtab_out));
     } else {
         k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp, dc_add,
                                                                      static_cast<float2*>(fk_out));
-        k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n,
+        k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                          static_cast<float*>(gtab_out));
     }
     return static_cast<int>(cudaGetLastError());

@@ -150,7 +150,9 @@ struct TileGeom {
     static constexpr int RLAST = 1 << (LOG2M % 3); // 1, 2 or 4
     // threads: one radix-8 butterfly per thread per step of the widest stage
     static constexpr int NBMIN = (M / 8) * L;
-    static constexpr int NT = NBMIN >= 256 ? 256 : NBMIN;
+    static constexpr int NT = NBMIN >= 512 ? 512 : NBMIN;
+    // resident CTAs the register budget must allow (<= 64 regs/thread at 1024 threads/SM)
+    static constexpr int MINB = 1024 / NT;
 };
 
 // One Stockham stage over a whole tile, in place (all loads, barrier, stores).

@@ -39,7 +39,7 @@ typedef struct gtd_greens {
     int n, m, h, hp;      /* grid, padded grid 2n, R2C width n+1, padded pitch */
     int fp64;             /* 1: tables are double, 0: float                    */
     void* fk;             /* [m][hp] complex: baseline kernel spectrum (C7)    */
-    void* gtab;           /* [(n+1)][(n+1)] real: alpha multiplier g(du,dv) (C6)*/
+    void* gtab;           /* [(n+1)][hp] real: alpha multiplier g(du,dv) (C6)   */
     void* k1;             /* [m] complex: 1-D spectrum of the centred die box  */
     void* tw;             /* [m] complex: exp(-2 pi i t/m)                     */
     double alpha, beta, rand_scale, mu_fixed;

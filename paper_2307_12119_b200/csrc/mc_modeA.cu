@@ -116,110 +116,121 @@ struct MCGeom {
 };
 
 // ------------------------------------------------------------------ pass 1
+// Persistent over (sample, block of L die rows). Each die row x becomes one
+// complex line z = mirror(applied row) + i * centre-embedded(p_leak0 row).
 template <typename T, int M>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT)
-mc_pass1(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
          const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
     using Gm = MCGeom<T, M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
-    constexpr int hp = Gm::hp, SP = Gm::SP;
+    constexpr int hp = Gm::hp;
+    constexpr int RB = (n + L - 1) / L;
+    constexpr int EPT = (L * n + NT - 1) / NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* tileT = reinterpret_cast<T*>(tile);
     cplx<T>* s_tw = tile + M * LP;
-    T* st_a = reinterpret_cast<T*>(s_tw + M);
-    T* st_l = st_a + L * SP;
-    double* red = reinterpret_cast<double*>(st_l + L * SP);
-
-    const int x0 = blockIdx.x * L;
-    const int s = blockIdx.y;
-    const size_t sg = static_cast<size_t>(sample0) + s;
-    const T* P = in.p(sg);
-    const T* Nm = in.nn(sg);
-    const T* V = in.v(sg);
-    const bool n_is_p = Nm == P;
+    double* red = reinterpret_cast<double*>(s_tw + M);
 
     load_twiddles<T, M, NT>(s_tw, g_tw);
+    for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
+        const int s = item / RB;
+        const int x0 = (item - s * RB) * L;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const T* P = in.p(sg);
+        const T* Nm = in.nn(sg);
+        const T* V = in.v(sg);
+        const bool n_is_p = Nm == P;
 
-    double sum_l = 0.0, sum_a = 0.0;
-    int bad = 0;
-    for (int idx = threadIdx.x; idx < L * n; idx += NT) {
-        const int l = idx / n, y = idx - l * n;
-        const int x = x0 + l;
-        T a = T(0), lk = T(0);
-        if (x < n) {
-            const T p = P[x * n + y];
-            const T nm = n_is_p ? p : Nm[x * n + y];
-            const T vr = V[x * n + y];
+        // imaginary part outside the centre embedding is zero
+        for (int idx = threadIdx.x; idx < (M - 2 * c) * L; idx += NT) {
+            const int l = idx % L, j = c + idx / L;
+            tileT[2 * (j * LP + l) + 1] = T(0);
+        }
+        T pv[EPT], nv[EPT], vv[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, y = idx - l * n, x = x0 + l;
+            pv[k] = nv[k] = T(0);
+            vv[k] = T(1);
+            if (idx < L * n && x < n) {
+                pv[k] = P[x * n + y];
+                nv[k] = n_is_p ? pv[k] : Nm[x * n + y];
+                vv[k] = V[x * n + y];
+            }
+        }
+        double sum_l = 0.0, sum_a = 0.0;
+        int bad = 0;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= L * n) break;
+            const int l = idx / n, y = idx - l * n;
+            const T p = pv[k], nm = nv[k], vr = vv[k];
             if (!(p >= T(0)) || !finite_(p) || !(nm >= T(0)) || !finite_(nm)) bad |= GTD_ST_BAD_POWER;
             if (!(vr >= var_lo && vr <= var_hi)) bad |= GTD_ST_BAD_VAR;
-            lk = in.nom_scale * nm * vr;
-            a = p + lk;
+            const T lk = in.nom_scale * nm * vr;
+            const T a = p + lk;
             sum_l += double(lk);
             sum_a += double(a);
+            tileT[2 * (y * LP + l)] = a;
+            tileT[2 * ((M - 1 - y) * LP + l)] = a;
+            tileT[2 * (((y - c) & (M - 1)) * LP + l) + 1] = lk;
         }
-        st_a[l * SP + y] = a;
-        st_l[l * SP + y] = lk;
-    }
-    // reductions (also act as the barrier for the staging arrays)
-    or_flags(&stats[sg].status, bad);
-    const double tl = block_sum<NT>(sum_l, red);
-    const double ta = block_sum<NT>(sum_a, red);
-    if (threadIdx.x == 0) {
-        atomicAdd(&stats[sg].sum_leak, tl);
-        atomicAdd(&stats[sg].sum_applied, ta);
-    }
+        or_flags(&stats[sg].status, bad);
+        const double tl = block_sum<NT>(sum_l, red);  // (contains the barrier for the tile)
+        const double ta = block_sum<NT>(sum_a, red);
+        if (threadIdx.x == 0) {
+            atomicAdd(&stats[sg].sum_leak, tl);
+            atomicAdd(&stats[sg].sum_applied, ta);
+        }
+        // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185),
+        // read back from the embedded imaginary part: p_leak0(l, y) at j = (y - c) mod M.
+        for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+            const int l = idx / hp, dv = idx - l * hp;
+            const int x = x0 + l;
+            if (x >= n) continue;
+            T v = T(0);
+            if (dv < h) {
+                const int jp = min(c + dv, n - 1), jm = max(c - dv, 0);
+                v = tileT[2 * (((jp - c) & (M - 1)) * LP + l) + 1] + tileT[2 * (((jm - c) & (M - 1)) * LP + l) + 1];
+            }
+            Srow[(static_cast<size_t>(s) * n + x) * hp + dv] = v;
+        }
+        __syncthreads();
+        tile_fft<T, M, L, LP, NT, -1>(tile, s_tw);
 
-    // Build the packed tile: re = mirror(applied), im = centre-embedded p_leak0.
-    for (int idx = threadIdx.x; idx < M * L; idx += NT) {
-        const int l = idx % L, j = idx / L;
-        const int ym = j < n ? j : M - 1 - j;
-        T re = st_a[l * SP + ym];
-        T im = T(0);
-        if (j < c)
-            im = st_l[l * SP + j + c];
-        else if (j >= M - c)
-            im = st_l[l * SP + j - M + c];
-        tile[j * LP + l] = mk<T>(re, im);
-    }
-    // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185).
-    for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
-        const int l = idx / hp, dv = idx - l * hp;
-        const int x = x0 + l;
-        if (x >= n) continue;
-        T v = T(0);
-        if (dv < h) {
-            const int jp = min(c + dv, n - 1), jm = max(c - dv, 0);
-            v = st_l[l * SP + jp] + st_l[l * SP + jm];
+        // Split Z into the two real-input half spectra and store rows.
+        for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+            const int l = idx / hp, v = idx - l * hp;
+            const int x = x0 + l;
+            if (x >= n) continue;
+            cplx<T> A = mk<T>(T(0), T(0)), B = A;
+            if (v < h) {
+                const cplx<T> Z = tile[v * LP + l];
+                const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
+                A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
+                const T dx = Z.x - Zc.x, dy = Z.y - Zc.y;
+                B = mk<T>(T(0.5) * dy, T(-0.5) * dx);
+            }
+            const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+            Aspec[o] = A;
+            Bspec[o] = B;
         }
-        Srow[(static_cast<size_t>(s) * n + x) * hp + dv] = v;
-    }
-    __syncthreads();
-    tile_fft<T, M, L, LP, NT, -1>(tile, s_tw);
-
-    // Split Z into the two real-input half spectra and store rows.
-    for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
-        const int l = idx / hp, v = idx - l * hp;
-        const int x = x0 + l;
-        if (x >= n) continue;
-        cplx<T> A = mk<T>(T(0), T(0)), B = A;
-        if (v < h) {
-            const cplx<T> Z = tile[v * LP + l];
-            const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
-            A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
-            const T dx = Z.x - Zc.x, dy = Z.y - Zc.y;
-            B = mk<T>(T(0.5) * dy, T(-0.5) * dx);
-        }
-        const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
-        Aspec[o] = A;
-        Bspec[o] = B;
+        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ pass 2
+// Persistent over (sample, tile of W half-spectrum columns). Tile line 2w holds
+// the A column v0+w (mirror-expanded), line 2w+1 the B column (centre-embedded),
+// so one thread reads both operands of a frequency with one vector access.
 template <typename T, int M>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT)
-mc_pass2(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
          gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
          const cplx<T>* __restrict__ fk, const T* __restrict__ gtab,
@@ -227,160 +238,204 @@ mc_pass2(const MCIn<T> in, int sample0, cplx<T>* __restrict__ Aspec,
     using Gm = MCGeom<T, M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT, W = Gm::W;
     constexpr int hp = Gm::hp;
+    constexpr int CT = hp / W;
+    constexpr int EPT = (n * W + NT - 1) / NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + M * L;
     T* s_srow = reinterpret_cast<T*>(s_tw + M);
 
-    const int v0 = blockIdx.x * W;
-    const int s = blockIdx.y;
-    const size_t sg = static_cast<size_t>(sample0) + s;
-    const size_t sbase = static_cast<size_t>(s) * n * hp;
-
     load_twiddles<T, M, NT>(s_tw, g_tw);
-    // Zero the rows of the B lines outside the centre embedding.
-    for (int idx = threadIdx.x; idx < (M - 2 * c) * W; idx += NT) {
-        const int w = idx % W, u = c + idx / W;
-        tile[u * L + W + w] = mk<T>(T(0), T(0));
-    }
-    for (int idx = threadIdx.x; idx < n * W; idx += NT) {
-        const int w = idx % W, x = idx / W;
-        const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
-        const cplx<T> a = Aspec[o];
-        tile[x * L + w] = a;
-        tile[(M - 1 - x) * L + w] = a;
-        const int rho = (x - c + M) & (M - 1);
-        tile[rho * L + W + w] = Bspec[o];
-        s_srow[x * W + w] = Srow[o];
-    }
-    // Per-sample scalars (pass 1 has completed: kernel boundary).
-    const double n2 = double(n) * double(n);
-    const double mu_s = stats[sg].sum_leak / n2;
-    const T mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
-    const T* Nm = in.nn(sg);
-    const T* V = in.v(sg);
-    const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
-    const T pl_00 = in.nom_scale * Nm[0] * V[0];
-    // q = sym(Q), Q = p_var + p_var(c,c) - p_var(0,0)  (greens.cpp:177-184)
-    const T qshift = T(double(pl_cc) - double(pl_00) - mu_s);
-    const T mus = T(mu_s);
-    __syncthreads();
-    tile_fft<T, M, L, L, NT, -1>(tile, s_tw);
+    for (int item = blockIdx.x; item < count * CT; item += gridDim.x) {
+        const int s = item / CT;
+        const int v0 = (item - s * CT) * W;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const size_t sbase = static_cast<size_t>(s) * n * hp;
 
-    int flags = 0;
-    for (int idx = threadIdx.x; idx < M * W; idx += NT) {
-        const int w = idx % W, u = idx / W;
-        const int v = v0 + w;
-        if (v >= h) continue;
-        const int du = u <= M - u ? u : M - u;
-        const cplx<T> Ah = tile[u * L + w];
-        const cplx<T> Bh = tile[u * L + W + w];
-        const cplx<T> K = cmul<T>(k1[u], k1[v]);
-        const cplx<T> Bp = mk<T>(Bh.x - mus * K.x, Bh.y - mus * K.y);  // F(p_var)
-        const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
-        const T g = gtab[du * (n + 1) + v];
-        const int ip = min(c + du, n - 1), im = max(c - du, 0);
-        const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
-        const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
-        // deterministic closed form
-        const T a1 = T(1) - alpha * g * (T(1) + fmu);
-        const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
-        if (cabs2<T>(den1) < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
-        const cplx<T> Fdet = cdiv<T>(f, den1);
-        const cplx<T> Y = cmul<T>(Fdet, Ah);
-        // random closed form
-        const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
-        const cplx<T> num = cmul<T>(Fdet, t1);
-        const cplx<T> den2 = mk<T>(a1 - alpha * g * Bp.x - mu_g * beta * f.x - beta * q * f.x,
-                                   -alpha * g * Bp.y - mu_g * beta * f.y - beta * q * f.y);
-        if (cabs2<T>(den2) < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
-        const cplx<T> R = cdiv<T>(num, den2);
-        tile[u * L + w] = Y;
-        tile[u * L + W + w] = R;
-    }
-    or_flags(&stats[sg].status, flags);
-    __syncthreads();
-    tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
+        for (int idx = threadIdx.x; idx < (M - 2 * c) * W; idx += NT) {
+            const int w = idx % W, u = c + idx / W;
+            tile[u * L + 2 * w + 1] = mk<T>(T(0), T(0));
+        }
+        cplx<T> av[EPT], bv[EPT];
+        T sv[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx < n * W) {
+                const int w = idx % W, x = idx / W;
+                const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
+                av[k] = Aspec[o];
+                bv[k] = Bspec[o];
+                sv[k] = Srow[o];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx < n * W) {
+                const int w = idx % W, x = idx / W;
+                tile[x * L + 2 * w] = av[k];
+                tile[(M - 1 - x) * L + 2 * w] = av[k];
+                tile[((x - c) & (M - 1)) * L + 2 * w + 1] = bv[k];
+                s_srow[x * W + w] = sv[k];
+            }
+        }
+        // Per-sample scalars (pass 1 has completed: kernel boundary).
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        const T mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
+        const T* Nm = in.nn(sg);
+        const T* V = in.v(sg);
+        const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
+        const T pl_00 = in.nom_scale * Nm[0] * V[0];
+        // q = sym(Q), Q = p_var + p_var(c,c) - p_var(0,0)  (greens.cpp:177-184)
+        const T qshift = T(double(pl_cc) - double(pl_00) - mu_s);
+        const T mus = T(mu_s);
+        __syncthreads();
+        tile_fft<T, M, L, L, NT, -1>(tile, s_tw);
 
-    // Keep rows [0, n) of Y (crop) and rows rho(x) of R (kernel_to_die), in place.
-    for (int idx = threadIdx.x; idx < n * W; idx += NT) {
-        const int w = idx % W, x = idx / W;
-        const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
-        const int rho = (x - c + M) & (M - 1);
-        Aspec[o] = tile[x * L + w];
-        Bspec[o] = tile[rho * L + W + w];
+        int flags = 0;
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < M * W; idx += NT) {
+            const int w = idx % W, u = idx / W;
+            const int v = v0 + w;
+            if (v >= h) continue;
+            const int du = u <= M - u ? u : M - u;
+            const cplx<T> Ah = tile[u * L + 2 * w];
+            const cplx<T> Bh = tile[u * L + 2 * w + 1];
+            const cplx<T> K = cmul<T>(k1[u], k1[v]);
+            const cplx<T> Bp = mk<T>(Bh.x - mus * K.x, Bh.y - mus * K.y);  // F(p_var)
+            const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
+            const T g = gtab[du * hp + v];
+            const int ip = min(c + du, n - 1), im = max(c - du, 0);
+            const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
+            const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
+            // deterministic closed form (greens.cpp:203-216)
+            const T a1 = T(1) - alpha * g * (T(1) + fmu);
+            const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
+            if (cabs2<T>(den1) < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
+            const cplx<T> Fdet = cdiv<T>(f, den1);
+            const cplx<T> Y = cmul<T>(Fdet, Ah);
+            // random closed form (greens.cpp:225-251)
+            const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
+            const cplx<T> num = cmul<T>(Fdet, t1);
+            const cplx<T> den2 = mk<T>(a1 - alpha * g * Bp.x - mu_g * beta * f.x - beta * q * f.x,
+                                       -alpha * g * Bp.y - mu_g * beta * f.y - beta * q * f.y);
+            if (cabs2<T>(den2) < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
+            const cplx<T> R = cdiv<T>(num, den2);
+            tile[u * L + 2 * w] = Y;
+            tile[u * L + 2 * w + 1] = R;
+        }
+        or_flags(&stats[sg].status, flags);
+        __syncthreads();
+        tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
+
+        // Keep rows [0, n) of Y (crop) and rows rho(x) of R (kernel_to_die), in place.
+        for (int idx = threadIdx.x; idx < n * W; idx += NT) {
+            const int w = idx % W, x = idx / W;
+            const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
+            Aspec[o] = tile[x * L + 2 * w];
+            Bspec[o] = tile[((x - c) & (M - 1)) * L + 2 * w + 1];
+        }
+        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ pass 3
 template <typename T, int M>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT)
-mc_pass3(const MCIn<T> in, int sample0, const cplx<T>* __restrict__ Aspec,
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
          const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
          const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
     using Gm = MCGeom<T, M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
     constexpr int hp = Gm::hp;
+    constexpr int RB = (n + L - 1) / L;
+    constexpr int EPT = (L * h + NT - 1) / NT;
+    constexpr int EPO = (L * n + NT - 1) / NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + M * LP;
     double* red = reinterpret_cast<double*>(s_tw + M);
 
-    const int x0 = blockIdx.x * L;
-    const int s = blockIdx.y;
-    const size_t sg = static_cast<size_t>(sample0) + s;
     load_twiddles<T, M, NT>(s_tw, g_tw);
+    for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
+        const int s = item / RB;
+        const int x0 = (item - s * RB) * L;
+        const size_t sg = static_cast<size_t>(sample0) + s;
 
-    for (int idx = threadIdx.x; idx < L * h; idx += NT) {
-        const int l = idx / h, v = idx - l * h;
-        const int x = x0 + l;
-        cplx<T> y = mk<T>(T(0), T(0)), r = y;
-        if (x < n) {
-            const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
-            y = Aspec[o];
-            r = Bspec[o];
+        cplx<T> yv[EPT], rv[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / h, v = idx - l * h, x = x0 + l;
+            yv[k] = rv[k] = mk<T>(T(0), T(0));
+            if (idx < L * h && x < n) {
+                const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+                yv[k] = Aspec[o];
+                rv[k] = Bspec[o];
+            }
         }
-        if (v == 0 || v == n) {
-            tile[v * LP + l] = mk<T>(y.x, r.x);
-        } else {
-            tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
-            tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= L * h) break;
+            const int l = idx / h, v = idx - l * h;
+            const cplx<T> y = yv[k], r = rv[k];
+            if (v == 0 || v == n) {
+                tile[v * LP + l] = mk<T>(y.x, r.x);
+            } else {
+                tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
+                tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+            }
         }
-    }
-    const double n2 = double(n) * double(n);
-    const double mu_s = stats[sg].sum_leak / n2;
-    const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
-    const T inv = T(1.0 / (double(M) * double(M)));
-    const T* Nm = in.nn(sg);
-    const T* V = in.v(sg);
-    __syncthreads();
-    tile_fft<T, M, L, LP, NT, +1>(tile, s_tw);
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T inv = T(1.0 / (double(M) * double(M)));
+        const T* Nm = in.nn(sg);
+        const T* V = in.v(sg);
+        __syncthreads();
+        tile_fft<T, M, L, LP, NT, +1>(tile, s_tw);
+        T nv[EPO], vv[EPO];
+#pragma unroll
+        for (int k = 0; k < EPO; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, j = idx - l * n, x = x0 + l;
+            nv[k] = vv[k] = T(0);
+            if (idx < L * n && x < n) {
+                nv[k] = Nm[x * n + j];
+                vv[k] = V[x * n + j];
+            }
+        }
 
-    double sum_t = 0.0;
-    double mx = 0.0;
-    int bad = 0;
-    for (int idx = threadIdx.x; idx < L * n; idx += NT) {
-        const int l = idx / n, j = idx - l * n;
-        const int x = x0 + l;
-        if (x >= n) continue;
-        const T yv = tile[j * LP + l].x * inv;
-        const int jr = (j - c + M) & (M - 1);
-        const T rv = tile[jr * LP + l].y * inv;
-        const T pv = T(double(in.nom_scale * Nm[x * n + j] * V[x * n + j]) - mu_s);
-        T t = yv + rv * pv * scale;
-        if (!finite_(t)) bad = GTD_ST_NONFINITE;
-        t = t > T(0) ? t : T(0);
-        if (out) out[(sg * n + x) * n + j] = t;
-        sum_t += double(t);
-        mx = fmax(mx, double(t));
-    }
-    or_flags(&stats[sg].status, bad);
-    const double ts = block_sum<NT>(sum_t, red);
-    const double tm = block_max<NT>(mx, red);
-    if (threadIdx.x == 0) {
-        atomicAdd(&stats[sg].sum_rise, ts);
-        atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
-        if (blockIdx.x == 0) stats[sg].mu = mu_s;
+        double sum_t = 0.0;
+        double mx = 0.0;
+        int bad = 0;
+#pragma unroll
+        for (int k = 0; k < EPO; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, j = idx - l * n, x = x0 + l;
+            if (idx >= L * n || x >= n) continue;
+            const T yd = tile[j * LP + l].x * inv;
+            const int jr = (j - c) & (M - 1);
+            const T rd = tile[jr * LP + l].y * inv;
+            const T pvar = T(double(in.nom_scale * nv[k] * vv[k]) - mu_s);
+            T t = yd + rd * pvar * scale;
+            if (!finite_(t)) bad = GTD_ST_NONFINITE;
+            t = t > T(0) ? t : T(0);
+            if (out) out[(sg * n + x) * n + j] = t;
+            sum_t += double(t);
+            mx = fmax(mx, double(t));
+        }
+        or_flags(&stats[sg].status, bad);
+        const double ts = block_sum<NT>(sum_t, red);
+        const double tm = block_max<NT>(mx, red);
+        if (threadIdx.x == 0) {
+            atomicAdd(&stats[sg].sum_rise, ts);
+            atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
+            if (x0 == 0) stats[sg].mu = mu_s;
+        }
     }
 }
 
@@ -396,24 +451,28 @@ __global__ void mc_finalize(gtd_sample_stats* stats, int sample0, int count, int
 template <typename T, int M>
 struct MCLaunch {
     using Gm = MCGeom<T, M>;
-    static size_t smem1() {
-        return sizeof(cplx<T>) * (M * Gm::LP + M) + sizeof(T) * 2 * Gm::L * Gm::SP + 64 * sizeof(double);
-    }
-    static size_t smem2() {
-        return sizeof(cplx<T>) * (M * Gm::L + M) + sizeof(T) * Gm::n * Gm::W;
-    }
+    static size_t smem1() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
+    static size_t smem2() { return sizeof(cplx<T>) * (M * Gm::L + M) + sizeof(T) * Gm::n * Gm::W; }
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
 
     static int run(const gtd_greens* g, const MCIn<T>& in, int batch, const gtd_mc_opts* o,
                    T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st,
                    gtd_mark_fn mark, void* ctx) {
-        constexpr int n = Gm::n, hp = Gm::hp, L = Gm::L, NT = Gm::NT;
-        static bool init = false;
-        if (!init) {
+        constexpr int n = Gm::n, hp = Gm::hp, L = Gm::L, NT = Gm::NT, W = Gm::W;
+        constexpr int RB = (n + L - 1) / L, CT = hp / W;
+        static int res[3] = {0, 0, 0};
+        static int sms = 0;
+        if (!sms) {
             cudaFuncSetAttribute(mc_pass1<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem1()));
             cudaFuncSetAttribute(mc_pass2<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
             cudaFuncSetAttribute(mc_pass3<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem3()));
-            init = true;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1<T, M>, NT, smem1());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, NT, smem2());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3<T, M>, NT, smem3());
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            for (int& r : res) r = r < 1 ? 1 : r;
         }
         const size_t per = static_cast<size_t>(n) * hp;
         cplx<T>* A = reinterpret_cast<cplx<T>*>(scratch);
@@ -424,19 +483,20 @@ struct MCLaunch {
         const T* gt = reinterpret_cast<const T*>(g->gtab);
         const cplx<T>* k1 = reinterpret_cast<const cplx<T>*>(g->k1);
         const T var_lo = T(exp(-o->exponent_cap)), var_hi = T(exp(o->exponent_cap));
+        auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
-            dim3 g1((n + L - 1) / L, cnt), g2(hp / Gm::W, cnt);
             if (mark) mark(ctx, 0, st);
-            mc_pass1<T, M><<<g1, NT, smem1(), st>>>(in, s0, A, B, S, stats, tw, var_lo, var_hi);
+            mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
+                                                                         var_lo, var_hi);
             if (mark) mark(ctx, 1, st);
-            mc_pass2<T, M><<<g2, NT, smem2(), st>>>(in, s0, A, B, S, stats, tw, fk, gt, k1,
-                                                   T(g->alpha), T(g->beta), o->mu_per_sample,
-                                                   T(g->mu_fixed));
+            mc_pass2<T, M><<<grid(cnt * CT, res[1]), NT, smem2(), st>>>(in, s0, cnt, A, B, S, stats, tw, fk, gt,
+                                                                         k1, T(g->alpha), T(g->beta),
+                                                                         o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
-            mc_pass3<T, M><<<g1, NT, smem3(), st>>>(in, s0, A, B, stats, tw, out,
-                                                   T(g->rand_scale), o->with_rand);
+            mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
+                                                                         T(g->rand_scale), o->with_rand);
             if (mark) mark(ctx, 3, st);
             mc_finalize<<<(cnt + 127) / 128, 128, 0, st>>>(stats, s0, cnt, n);
         }
