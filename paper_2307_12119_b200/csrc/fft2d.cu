@@ -16,7 +16,7 @@ template <typename T, int M, int SIGN>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT)
 fft_rows(cplx<T>* __restrict__ X, const cplx<T>* __restrict__ g_tw, int rows) {
     using G = TileGeom<T, M>;
-    constexpr int L = G::L, LP = L + 1, NT = G::NT;
+    constexpr int L = G::L, LP = L + 2, NT = G::NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + M * LP;
@@ -66,7 +66,7 @@ int run_fft2d(void* data, int batch, int sign, const void* tw, cudaStream_t st) 
     using G = TileGeom<T, M>;
     constexpr int L = G::L, NT = G::NT;
     constexpr int LL = L < M ? L : M;
-    const size_t sm_r = sizeof(cplx<T>) * (M * (L + 1) + M);
+    const size_t sm_r = sizeof(cplx<T>) * (M * (L + 2) + M);
     const size_t sm_c = sizeof(cplx<T>) * (M * L + M);
     static bool init = false;
     if (!init) {

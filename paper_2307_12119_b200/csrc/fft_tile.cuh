@@ -192,17 +192,90 @@ __device__ __forceinline__ void stockham_stage(cplx<T>* tile, const cplx<T>* tw)
     __syncthreads();
 }
 
+// Two adjacent lines per thread: one vector shared-memory access moves both
+// lines' elements and the twiddles are loaded once for the pair (halves the
+// LDS count per point, the MIO pressure the single-line stage runs into).
+template <typename T>
+struct LinePair {
+    cplx<T> a, b;
+};
+__device__ __forceinline__ LinePair<float> ld_pair(const float2* p) {
+    const float4 q = *reinterpret_cast<const float4*>(p);
+    return {make_float2(q.x, q.y), make_float2(q.z, q.w)};
+}
+__device__ __forceinline__ void st_pair(float2* p, const LinePair<float>& v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.a.x, v.a.y, v.b.x, v.b.y);
+}
+__device__ __forceinline__ LinePair<double> ld_pair(const double2* p) { return {p[0], p[1]}; }
+__device__ __forceinline__ void st_pair(double2* p, const LinePair<double>& v) {
+    p[0] = v.a;
+    p[1] = v.b;
+}
+
+template <typename T, int M, int L, int LP, int NT, int SIGN, int R, int NS>
+__device__ __forceinline__ void stockham_stage_pairs(cplx<T>* tile, const cplx<T>* tw) {
+    constexpr int L2 = L / 2;
+    constexpr int NB = (M / R) * L2;
+    static_assert(NB % NT == 0, "pair butterflies must divide evenly over threads");
+    constexpr int BPT = NB / NT;
+    cplx<T> va[BPT][R], vb[BPT][R];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int lp = id % L2, j = id / L2;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const LinePair<T> q = ld_pair(&tile[(j + r * (M / R)) * LP + 2 * lp]);
+            va[b][r] = q.a;
+            vb[b][r] = q.b;
+        }
+        if constexpr (NS > 1) {
+            const int k = j % NS;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                cplx<T> w = tw[k * r * (M / (NS * R))];
+                if (SIGN > 0) w.y = -w.y;
+                va[b][r] = cmul<T>(va[b][r], w);
+                vb[b][r] = cmul<T>(vb[b][r], w);
+            }
+        }
+        dftR<R, SIGN, T>(va[b]);
+        dftR<R, SIGN, T>(vb[b]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int lp = id % L2, j = id / L2;
+        const int k = j % NS;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) st_pair(&tile[(base + r * NS) * LP + 2 * lp], LinePair<T>{va[b][r], vb[b][r]});
+    }
+    __syncthreads();
+}
+
+template <typename T, int M, int L, int LP, int NT, int SIGN, int R, int NS>
+__device__ __forceinline__ void stage(cplx<T>* tile, const cplx<T>* tw) {
+    // pairs when the tile has enough pair-butterflies for every thread and the
+    // pitch keeps pairs 16-byte aligned
+    if constexpr (LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
+        stockham_stage_pairs<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);
+    else
+        stockham_stage<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);
+}
+
 template <typename T, int M, int L, int LP, int NT, int SIGN, int S>
 struct StageRunner {
     using G = TileGeom<T, M>;
     __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* tw) {
         if constexpr (S < G::N8) {
             constexpr int NS = 1 << (3 * S);
-            stockham_stage<T, M, L, LP, NT, SIGN, 8, NS>(tile, tw);
+            stage<T, M, L, LP, NT, SIGN, 8, NS>(tile, tw);
             StageRunner<T, M, L, LP, NT, SIGN, S + 1>::run(tile, tw);
         } else if constexpr (G::RLAST > 1) {
             constexpr int NS = 1 << (3 * G::N8);
-            stockham_stage<T, M, L, LP, NT, SIGN, G::RLAST, NS>(tile, tw);
+            stage<T, M, L, LP, NT, SIGN, G::RLAST, NS>(tile, tw);
         }
     }
 };

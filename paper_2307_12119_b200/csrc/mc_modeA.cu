@@ -111,7 +111,7 @@ struct MCGeom {
     static constexpr int NT = G::NT;
     static constexpr int W = L / 2;  // columns per pass-2 tile
     static constexpr int hp = ((h + W - 1) / W) * W;
-    static constexpr int LP = L + 1;  // padded pitch for row tiles (transposing I/O)
+    static constexpr int LP = L + 2;  // padded pitch for row tiles (transposing I/O; even for pairs)
     static constexpr int SP = n + 1;  // padded pitch of the row staging arrays
 };
 
@@ -313,16 +313,18 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             // deterministic closed form (greens.cpp:203-216)
             const T a1 = T(1) - alpha * g * (T(1) + fmu);
             const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
-            if (cabs2<T>(den1) < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
-            const cplx<T> Fdet = cdiv<T>(f, den1);
-            const cplx<T> Y = cmul<T>(Fdet, Ah);
             // random closed form (greens.cpp:225-251)
             const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
-            const cplx<T> num = cmul<T>(Fdet, t1);
-            const cplx<T> den2 = mk<T>(a1 - alpha * g * Bp.x - mu_g * beta * f.x - beta * q * f.x,
-                                       -alpha * g * Bp.y - mu_g * beta * f.y - beta * q * f.y);
-            if (cabs2<T>(den2) < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
-            const cplx<T> R = cdiv<T>(num, den2);
+            const cplx<T> den2 = mk<T>(den1.x - alpha * g * Bp.x - beta * q * f.x,
+                                       den1.y - alpha * g * Bp.y - beta * q * f.y);
+            const T d1 = cabs2<T>(den1), d2 = cabs2<T>(den2);
+            if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
+            if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
+            // Y = f A / den1, R = f t1 / (den1 den2): one reciprocal for both quotients
+            const T rinv = T(1) / (d1 * d2);
+            const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));           // f conj(den1)
+            const cplx<T> Y = cscale<T>(cmul<T>(cmul<T>(fc1, Ah), mk<T>(d2, T(0))), rinv);
+            const cplx<T> R = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
             tile[u * L + 2 * w] = Y;
             tile[u * L + 2 * w + 1] = R;
         }
