@@ -23,6 +23,7 @@
 #include "../../include/greentherm.h"
 #include "../../include/greentherm_b200.h"
 #include "gt_device.h"
+#include "devctx.hpp"
 #include "gt_ops.h"
 #include "host.hpp"
 
@@ -56,39 +57,6 @@ double ms_since(wall::time_point t0) {
     return std::chrono::duration<double, std::milli>(wall::now() - t0).count();
 }
 
-void cuda_ok(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) fail(ST_INTERNAL, "device", std::string(what) + ": " + cudaGetErrorString(e));
-}
-void cuda_ok(int e, const char* what) { cuda_ok(static_cast<cudaError_t>(e), what); }
-
-void need_device() {
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1)
-        fail(ST_INTERNAL, "device", "no CUDA device available (this library has no CPU solve path)");
-}
-
-bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
-
-// RAII device buffer.
-struct DBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    DBuf() = default;
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() {
-        if (p) cudaFree(p);
-    }
-    void ensure(size_t b) {
-        if (b <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        cuda_ok(cudaMalloc(&p, b), "cudaMalloc");
-        bytes = b;
-    }
-};
-
 }  // namespace
 
 // ------------------------------------------------------------ handle types
@@ -107,137 +75,7 @@ struct gt_trace {
     std::vector<Field> frames;
 };
 
-struct gt_device_greens {
-    int device = 0;
-    int fp64 = 0;
-    gtd_greens d{};
-    Greens host;  // copy of the set the tables were built from
-    cudaStream_t stream = nullptr;
-    DBuf fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
-    // batch scratch (guarded by mu)
-    std::mutex mu;
-    DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
-    cudaStream_t slot_stream[2] = {nullptr, nullptr};
-    void* host_stats = nullptr;
-    size_t host_stats_bytes = 0;
-    // profiling (gt_profile_begin/end): events recorded between pass launches
-    bool profiling = false;
-    std::vector<std::pair<int, cudaEvent_t>> marks;
-    std::vector<cudaEvent_t> event_pool;
-    size_t pool_used = 0;
-    long long kernels = 0, calls = 0;
-    static void mark(void* ctx, int point, cudaStream_t st) {
-        auto* self = static_cast<gt_device_greens*>(ctx);
-        if (self->pool_used == self->event_pool.size()) {
-            cudaEvent_t e;
-            cudaEventCreate(&e);
-            self->event_pool.push_back(e);
-        }
-        cudaEvent_t e = self->event_pool[self->pool_used++];
-        cudaEventRecord(e, st);
-        self->marks.emplace_back(point, e);
-    }
-    ~gt_device_greens() {
-        for (auto e : event_pool) cudaEventDestroy(e);
-        if (host_stats) cudaFreeHost(host_stats);
-        for (auto& s : slot_stream)
-            if (s) cudaStreamDestroy(s);
-        if (stream) cudaStreamDestroy(stream);
-    }
-};
-
 namespace {
-
-// Host-computed fp64 constant tables (analytic; no transform work).
-std::vector<double> twiddles(int m) {
-    std::vector<double> t(2 * static_cast<size_t>(m));
-    for (int k = 0; k < m; ++k) {
-        const double a = -2.0 * M_PI * static_cast<double>(k) / m;
-        t[2 * k] = std::cos(a);
-        t[2 * k + 1] = std::sin(a);
-    }
-    return t;
-}
-
-// k1[u] = sum_{x<n} exp(-2 pi i u (x - c) / m): spectrum of the centred die box.
-std::vector<double> box_spectrum(int n) {
-    const int m = 2 * n, c = n / 2;
-    std::vector<double> k(2 * static_cast<size_t>(m));
-    for (int u = 0; u < m; ++u) {
-        double re = 0.0, im = 0.0;
-        for (int x = 0; x < n; ++x) {
-            const long long e = (static_cast<long long>(u) * (x - c)) % m;
-            const double a = -2.0 * M_PI * static_cast<double>((e + m) % m) / m;
-            re += std::cos(a);
-            im += std::sin(a);
-        }
-        k[2 * u] = re;
-        k[2 * u + 1] = im;
-    }
-    return k;
-}
-
-template <typename T>
-std::vector<T> narrow(const std::vector<double>& v) {
-    return std::vector<T>(v.begin(), v.end());
-}
-
-void upload(DBuf& b, const void* src, size_t bytes, cudaStream_t st) {
-    b.ensure(bytes);
-    cuda_ok(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), "upload");
-}
-
-std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision, int device) {
-    need_device();
-    const int n = g.n;
-    if (!pow2(n) || n < 16 || n > 512)
-        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..512, got n=" + std::to_string(n));
-    if (precision != GT_FP32 && precision != GT_FP64) fail(ST_CONFIG, "device", "precision must be GT_FP32 or GT_FP64");
-    cuda_ok(cudaSetDevice(device), "cudaSetDevice");
-    auto d = std::make_unique<gt_device_greens>();
-    d->device = device;
-    d->fp64 = precision == GT_FP64;
-    d->host = g;
-    cuda_ok(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
-    const int m = 2 * n, hp = gtd_padded_width(n, d->fp64);
-    const size_t cb = d->fp64 ? 16 : 8, rb = d->fp64 ? 8 : 4;
-    cudaStream_t st = d->stream;
-
-    const std::vector<double> tw = twiddles(m), k1 = box_spectrum(n);
-    upload(d->tw64, tw.data(), tw.size() * 8, st);
-    if (d->fp64) {
-        upload(d->tw, tw.data(), tw.size() * 8, st);
-        upload(d->k1, k1.data(), k1.size() * 8, st);
-    } else {
-        auto twf = narrow<float>(tw), k1f = narrow<float>(k1);
-        upload(d->tw, twf.data(), twf.size() * 4, st);
-        upload(d->k1, k1f.data(), k1f.size() * 4, st);
-        cuda_ok(cudaStreamSynchronize(st), "sync");
-    }
-    upload(d->fsp0, g.f_sp0.v.data(), g.f_sp0.v.size() * 8, st);
-    upload(d->gsp0, g.g_sp0.v.data(), g.g_sp0.v.size() * 8, st);
-    d->work.ensure(static_cast<size_t>(m) * m * 16);
-    d->fk.ensure(static_cast<size_t>(m) * hp * cb);
-    d->gtab.ensure(static_cast<size_t>(n + 1) * hp * rb);
-    cuda_ok(gtd_greens_tables(static_cast<const double*>(d->fsp0.p), static_cast<const double*>(d->gsp0.p),
-                              g.phi, n, hp, d->fp64, d->tw64.p, d->work.p, d->fk.p, d->gtab.p, st),
-            "greens tables");
-    cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
-    d->d.n = n;
-    d->d.m = m;
-    d->d.h = n + 1;
-    d->d.hp = hp;
-    d->d.fp64 = d->fp64;
-    d->d.fk = d->fk.p;
-    d->d.gtab = d->gtab.p;
-    d->d.k1 = d->k1.p;
-    d->d.tw = d->tw.p;
-    d->d.alpha = g.alpha;
-    d->d.beta = g.beta;
-    d->d.rand_scale = g.rand_scale;
-    d->d.mu_fixed = g.mu;
-    return d;
-}
 
 gtd_mc_opts to_dev_opts(const gt_batch_opts* o) {
     gtd_mc_opts r{};

@@ -1,0 +1,92 @@
+// devctx.hpp — device-side context shared by the C-ABI entry points: RAII
+// device buffers, error mapping and the prepared, device-resident GreensSet
+// (the reference's PreparedGreens, solver.cpp:113-121, plus the per-frequency
+// tables the kernels read).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/greentherm_b200.h"
+#include "gt_device.h"
+#include "host.hpp"
+
+namespace gth {
+
+void cuda_ok(cudaError_t e, const char* what);
+inline void cuda_ok(int e, const char* what) { cuda_ok(static_cast<cudaError_t>(e), what); }
+void need_device();
+inline bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// RAII device buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b);
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+void upload(DBuf& b, const void* src, size_t bytes, cudaStream_t st);
+
+}  // namespace gth
+
+struct gt_device_greens {
+    // fp64 full-spectrum tables for the reference-API solves (steady/step/trace)
+    gth::DBuf fk_full;  // [m][m] double2: baseline kernel spectrum incl. DC term
+    int device = 0;
+    int fp64 = 0;
+    gtd_greens d{};
+    gth::Greens host;  // copy of the set the tables were built from
+    cudaStream_t stream = nullptr;
+    gth::DBuf fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
+    // batch scratch (guarded by mu)
+    std::mutex mu;
+    gth::DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
+    cudaStream_t slot_stream[2] = {nullptr, nullptr};
+    void* host_stats = nullptr;
+    size_t host_stats_bytes = 0;
+    // profiling (gt_profile_begin/end): events recorded between pass launches
+    bool profiling = false;
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    std::vector<cudaEvent_t> event_pool;
+    size_t pool_used = 0;
+    long long kernels = 0, calls = 0;
+    static void mark(void* ctx, int point, cudaStream_t st) {
+        auto* self = static_cast<gt_device_greens*>(ctx);
+        if (self->pool_used == self->event_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            self->event_pool.push_back(e);
+        }
+        cudaEvent_t e = self->event_pool[self->pool_used++];
+        cudaEventRecord(e, st);
+        self->marks.emplace_back(point, e);
+    }
+    ~gt_device_greens() {
+        for (auto e : event_pool) cudaEventDestroy(e);
+        if (host_stats) cudaFreeHost(host_stats);
+        for (auto& s : slot_stream)
+            if (s) cudaStreamDestroy(s);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+
+namespace gth {
+std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision, int device);
+}

@@ -116,16 +116,19 @@ __global__ void k_center_kernel(const double* __restrict__ f, double phi, int n,
     K[static_cast<size_t>(i) * m + j] = make_double2(v, 0.0);
 }
 
-// fk half spectrum in the hot-path precision, DC term + phi*m^2/4.
+// fk[0] += phi m^2 / 4 (greens.cpp:199-200): the spreader constant counted once
+// per die source across its four mirror images.
+__global__ void k_dc_add(double2* K, double dc_add) { K[0].x += dc_add; }
+
+// fk half spectrum (v < m/2+1) in the hot-path precision.
 template <typename T>
-__global__ void k_fk_half(const double2* __restrict__ K, int m, int hp, double dc_add,
+__global__ void k_fk_half(const double2* __restrict__ K, int m, int hp,
                           cplx<T>* __restrict__ fk) {
     const int u = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= hp) return;
     const int h = m / 2 + 1;
     double2 z = make_double2(0.0, 0.0);
     if (v < h) z = K[static_cast<size_t>(u) * m + v];
-    if (u == 0 && v == 0) z.x += dc_add;
     fk[static_cast<size_t>(u) * hp + v] = mk<T>(T(z.x), T(z.y));
 }
 
@@ -153,7 +156,8 @@ int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, 
 }
 
 // Builds the device tables of a prepared GreensSet. f_sp0_d, g_sp0_d: device
-// n x n fp64 maps; tw64_d: fp64 twiddles for m; work_d: m*m double2 scratch.
+// n x n fp64 maps; tw64_d: fp64 twiddles for m; work_d: m*m double2 that
+// receives the full fp64 baseline kernel spectrum fk (kept by the caller).
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
                       int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out,
                       cudaStream_t st) {
@@ -163,13 +167,14 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
     int e = dispatch_fft2d<double>(K, m, 1, -1, tw64_d, st);
     if (e) return e;
     const double dc_add = 0.25 * phi * double(m) * double(m);
+    k_dc_add<<<1, 1, 0, st>>>(K, dc_add);
     if (fp64) {
-        k_fk_half<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp, dc_add,
+        k_fk_half<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                       static_cast<double2*>(fk_out));
         k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                           static_cast<double*>(gtab_out));
     } else {
-        k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp, dc_add,
+        k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                      static_cast<float2*>(fk_out));
         k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                          static_cast<float*>(gtab_out));

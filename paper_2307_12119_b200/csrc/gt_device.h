@@ -100,3 +100,29 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
 #ifdef __cplusplus
 }
 #endif
+
+/* ---- fp64 full-spectrum kernels of the reference-API solves (ops.cu) ---- */
+#ifdef __cplusplus
+extern "C" {
+#endif
+int gtd_mirror_pad(const double* a, const double* b, int n, void* X, cudaStream_t st);
+int gtd_fdet_full(const void* fk, const double* gtab, int n, int hp, double alpha, double beta, double mu,
+                  void* Fd, int* flag, cudaStream_t st);
+int gtd_transient(const void* fk, const double* gtab, const void* Fd, int n, int hp, double alpha, double cap,
+                  double fk_floor, double t, void* out, double dt, int kwin, void* r, void* rk, int* flag,
+                  cudaStream_t st);
+int gtd_spec_mul(void* X, const void* S, size_t count, cudaStream_t st);
+int gtd_crop(const void* X, int n, double scale, double* out, cudaStream_t st);
+int gtd_trace_step(const void* dlt, const void* dk, const void* r, const void* rk, const void* F, void* E,
+                   void* Pacc, void* X, size_t count, cudaStream_t st);
+int gtd_saturation(const void* F, const void* r, size_t count, int k, double re_sum_F, double* part, int blocks,
+                   double* sat, cudaStream_t st);
+int gtd_trace_scale(const double* totals, const double* sat, int steps, int k, double* scale, cudaStream_t st);
+int gtd_add_rand(double* T, const double* a, const double* b, const double* scale, double scale_mul, size_t nn,
+                 int maps, cudaStream_t st);
+int gtd_reduce(const double* x, size_t count, double* out3, cudaStream_t st);   /* sum, min, max */
+int gtd_creduce(const void* x, size_t count, double* out3, cudaStream_t st);   /* Re sum, Im sum, max|.| */
+int gtd_clamp(double* x, size_t count, unsigned long long* neg, cudaStream_t st);
+#ifdef __cplusplus
+}
+#endif
