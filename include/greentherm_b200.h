@@ -96,6 +96,37 @@ gt_status gt_mc_batch_device(const gt_device_greens* d, const void* p_dyn, const
                              int batch, const gt_batch_opts* opts, void* t_out,
                              gt_sample_stats* stats, void* stream);
 
+/* ---- mode B: the north-star leakage fixed point ----
+ * Per sample, the outer loop of the reference FDM oracle (fdm.cpp:167-205)
+ * with the linear solve replaced by the Green convolution of the baseline
+ * kernel spectrum on the mirror-padded torus:
+ *   theta_{k+1} - T0 = crop(IFFT(fk . FFT(mirror(P + L0 f(T_k)))))
+ *   L0 = leak_frac * p_dyn * var, f(dT) = exp(beta dT) (law 1) or 1 + beta dT (law 0)
+ *   T = Kirchhoff inverse of theta for k = k_ref (T/T0)^-eta (kirchhoff = 1)
+ * Stops when max|T_{k+1} - T_k| < tol after iteration 1; max_iters ->
+ * GT_SAMPLE_NOCONVERGE (ConvergenceError); non-finite / Kirchhoff-invalid
+ * temperatures (thermal runaway) -> GT_SAMPLE_NONFINITE / GT_SAMPLE_KIRCHHOFF. */
+typedef struct gt_fp_opts {
+    double leak_frac;
+    int law;
+    int kirchhoff;
+    double beta, t_ambient, eta, tol;
+    int max_iters;
+    int chunk;
+} gt_fp_opts;
+
+void gt_fp_opts_default(gt_fp_opts* o);
+
+/* Host arrays (device precision); t_out / iters_out / status_out / max_out may be NULL. */
+gt_status gt_fp_batch(const gt_device_greens* d, const void* p_dyn, const void* var, int batch,
+                      const gt_fp_opts* opts, void* t_out, int* iters_out, int* status_out, double* max_out,
+                      double* online_ms);
+/* Device arrays; t_out (batch x n x n, required) holds the state and the result. */
+gt_status gt_fp_batch_device(const gt_device_greens* d, const void* p_dyn, const void* var, int batch,
+                             const gt_fp_opts* opts, void* t_out, int* iters_out, int* status_out,
+                             double* max_out, double* mean_out, void* stream);
+size_t gt_fp_scratch_bytes(int n, int precision);
+
 /* Bytes of device scratch a device-resident batch uses per in-flight sample,
  * and the number of kernels it launches for (batch, chunk). */
 size_t gt_mc_scratch_bytes(int n, int precision);

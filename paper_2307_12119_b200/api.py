@@ -90,6 +90,11 @@ class SampleStats(C.Structure):
                 ("pad_", cint)]
 
 
+class FPOpts(C.Structure):
+    _fields_ = [("leak_frac", dbl), ("law", cint), ("kirchhoff", cint), ("beta", dbl), ("t_ambient", dbl),
+                ("eta", dbl), ("tol", dbl), ("max_iters", cint), ("chunk", cint)]
+
+
 SAMPLE_STATS_DTYPE = np.dtype([("sum_leak", "f8"), ("sum_applied", "f8"), ("sum_rise", "f8"),
                                ("max_rise", "f8"), ("mean_rise", "f8"), ("mu", "f8"),
                                ("max_bits", "u8"), ("status", "i4"), ("pad_", "i4")])
@@ -107,6 +112,10 @@ _EXT = [
     ("gt_mc_scratch_bytes", C.c_size_t, [cint, cint]),
     ("gt_mc_kernel_launches", cint, [cint, cint]),
     ("gt_device_count", cint, []),
+    ("gt_fp_opts_default", None, [C.POINTER(FPOpts)]),
+    ("gt_fp_batch", cint, [vp, vp, vp, cint, C.POINTER(FPOpts), vp, C.POINTER(cint), C.POINTER(cint), pdbl, pdbl]),
+    ("gt_fp_batch_device", cint, [vp, vp, vp, cint, C.POINTER(FPOpts), vp, vp, vp, vp, vp, vp]),
+    ("gt_fp_scratch_bytes", C.c_size_t, [cint, cint]),
     ("gt_profile_begin", cint, [vp]),
     ("gt_profile_end", cint, [vp, pdbl, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("gt_kernel_launches", C.c_longlong, [vp]),
@@ -263,6 +272,40 @@ class DeviceGreens:
         sp = None if stream is None else C.c_void_p(stream if stream else 1)
         check(L, L.gt_mc_batch_device(self._d, C.c_void_p(p_ptr), C.c_void_p(v_ptr), batch, C.byref(opts),
                                       C.c_void_p(out_ptr) if out_ptr else None, C.c_void_p(stats_ptr), sp))
+
+    def fp_opts(self, **kw) -> "FPOpts":
+        o = FPOpts()
+        lib().gt_fp_opts_default(C.byref(o))
+        for k, v in kw.items():
+            setattr(o, k, v)
+        return o
+
+    def fp_batch_host(self, p_dyn: np.ndarray, var: np.ndarray, opts: "FPOpts | None" = None):
+        """Mode B from host arrays -> (maps, iters, status, max, ms)."""
+        L = lib()
+        dt = np.float64 if self.precision == GT_FP64 else np.float32
+        p = np.ascontiguousarray(p_dyn, dtype=dt)
+        v = np.ascontiguousarray(var, dtype=dt)
+        B = p.shape[0]
+        out = np.empty_like(p)
+        it = np.empty(B, np.int32)
+        st = np.empty(B, np.int32)
+        mx = np.empty(B)
+        ms = C.c_double()
+        o = opts or self.fp_opts()
+        check(L, L.gt_fp_batch(self._d, p.ctypes.data_as(vp), v.ctypes.data_as(vp), B, C.byref(o),
+                               out.ctypes.data_as(vp), it.ctypes.data_as(C.POINTER(cint)),
+                               st.ctypes.data_as(C.POINTER(cint)), mx.ctypes.data_as(pdbl), C.byref(ms)))
+        return out, it, st, mx, ms.value
+
+    def fp_batch_device(self, p_ptr, v_ptr, batch, opts, out_ptr, iters_ptr, status_ptr, max_ptr=None,
+                        mean_ptr=None, stream=None) -> None:
+        L = lib()
+        sp = None if stream is None else C.c_void_p(stream if stream else 1)
+        check(L, L.gt_fp_batch_device(self._d, C.c_void_p(p_ptr), C.c_void_p(v_ptr), batch, C.byref(opts),
+                                      C.c_void_p(out_ptr), C.c_void_p(iters_ptr), C.c_void_p(status_ptr),
+                                      C.c_void_p(max_ptr) if max_ptr else None,
+                                      C.c_void_p(mean_ptr) if mean_ptr else None, sp))
 
     def profile_begin(self) -> None:
         check(lib(), lib().gt_profile_begin(self._d))

@@ -527,6 +527,106 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
     });
 }
 
+void gt_fp_opts_default(gt_fp_opts* o) {
+    o->leak_frac = 0.3;
+    o->law = 1;
+    o->kirchhoff = 1;
+    o->beta = 0.017;
+    o->t_ambient = 318.15;
+    o->eta = 1.3;
+    o->tol = 1e-4;
+    o->max_iters = 50;
+    o->chunk = 0;
+}
+
+size_t gt_fp_scratch_bytes(int n, int precision) { return gtd_fp_scratch_bytes_per_sample(n, precision == GT_FP64); }
+
+namespace {
+void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, const gt_fp_opts* opts, void* t_out,
+            int* iters, int* status, double* mx, double* mean, cudaStream_t st) {
+    if (!opts) fail(ST_CONFIG, "capi", "fixed point needs options");
+    if (!(opts->tol > 0.0)) fail(ST_CONFIG, "oracle", "outer tolerance must be positive");
+    if (opts->max_iters < 1) fail(ST_CONFIG, "oracle", "max_iters must be >= 1");
+    const int n = d->d.n;
+    int chunk = opts->chunk > 0 ? std::min(opts->chunk, batch) : 0;
+    if (!chunk) {
+        const size_t per = gtd_fp_scratch_bytes_per_sample(n, d->fp64);
+        chunk = static_cast<int>(std::max<size_t>(1, (48ull << 20) / per));
+        chunk = std::min(chunk, batch);
+    }
+    d->fp_scratch.ensure(gtd_fp_scratch_bytes_per_sample(n, d->fp64) * chunk);
+    d->fp_state.ensure(gtd_fp_state_bytes() * batch);
+    d->fp_counter.ensure(sizeof(int));
+    if (!d->fp_counter_h) cuda_ok(cudaMallocHost(reinterpret_cast<void**>(&d->fp_counter_h), sizeof(int)), "pinned");
+    gtd_mc_in in{};
+    in.P = p_dyn;
+    in.N = p_dyn;
+    in.V = var;
+    in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
+    in.nom_scale = opts->leak_frac;
+    gtd_fp_opts o{};
+    o.law = opts->law;
+    o.kirchhoff = opts->kirchhoff;
+    o.beta = opts->beta;
+    o.t_ambient = opts->t_ambient;
+    o.eta = opts->eta;
+    o.tol = opts->tol;
+    o.max_iters = opts->max_iters;
+    o.poll = 4;
+    long long launches = 0;
+    cuda_ok(gtd_fp_batch(&d->d, &in, batch, &o, t_out, iters, status, mx, mean, d->fp_scratch.p, d->fp_state.p,
+                         d->fp_counter.as<int>(), d->fp_counter_h, chunk, st, &launches),
+            "fixed point");
+    d->kernels += launches;
+    d->calls += 1;
+}
+}  // namespace
+
+gt_status gt_fp_batch_device(const gt_device_greens* dc, const void* p_dyn, const void* var, int batch,
+                             const gt_fp_opts* opts, void* t_out, int* iters_out, int* status_out, double* max_out,
+                             double* mean_out, void* stream) {
+    return guarded([&] {
+        if (batch < 1 || !p_dyn || !var || !t_out || !iters_out || !status_out)
+            fail(ST_CONFIG, "capi", "fixed point needs inputs, t_out, iters and status arrays");
+        auto* d = const_cast<gt_device_greens*>(dc);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        run_fp(d, p_dyn, var, batch, opts, t_out, iters_out, status_out, max_out, mean_out, st);
+    });
+}
+
+gt_status gt_fp_batch(const gt_device_greens* dc, const void* p_dyn, const void* var, int batch,
+                      const gt_fp_opts* opts, void* t_out, int* iters_out, int* status_out, double* max_out,
+                      double* online_ms) {
+    return guarded([&] {
+        if (batch < 1 || !p_dyn || !var) fail(ST_CONFIG, "capi", "fixed point needs inputs");
+        auto t0 = wall::now();
+        auto* d = const_cast<gt_device_greens*>(dc);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        const int n = d->d.n;
+        const size_t es = d->fp64 ? 8 : 4, map = static_cast<size_t>(n) * n * es;
+        DBuf P, V, T, it, st, mx;
+        P.ensure(map * batch);
+        V.ensure(map * batch);
+        T.ensure(map * batch);
+        it.ensure(sizeof(int) * batch);
+        st.ensure(sizeof(int) * batch);
+        mx.ensure(sizeof(double) * batch);
+        cudaStream_t s = d->stream;
+        cuda_ok(cudaMemcpyAsync(P.p, p_dyn, map * batch, cudaMemcpyHostToDevice, s), "h2d");
+        cuda_ok(cudaMemcpyAsync(V.p, var, map * batch, cudaMemcpyHostToDevice, s), "h2d");
+        run_fp(d, P.p, V.p, batch, opts, T.p, it.as<int>(), st.as<int>(), mx.as<double>(), nullptr, s);
+        if (t_out) cuda_ok(cudaMemcpyAsync(t_out, T.p, map * batch, cudaMemcpyDeviceToHost, s), "d2h");
+        if (iters_out) cuda_ok(cudaMemcpyAsync(iters_out, it.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, s), "d2h");
+        if (status_out) cuda_ok(cudaMemcpyAsync(status_out, st.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, s), "d2h");
+        if (max_out) cuda_ok(cudaMemcpyAsync(max_out, mx.p, sizeof(double) * batch, cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        if (online_ms) *online_ms = ms_since(t0);
+    });
+}
+
 gt_status gt_profile_begin(gt_device_greens* d) {
     return guarded([&] {
         std::lock_guard<std::mutex> lk(d->mu);

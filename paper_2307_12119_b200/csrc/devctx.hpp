@@ -56,6 +56,8 @@ struct gt_device_greens {
     gth::DBuf fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
     // batch scratch (guarded by mu)
     std::mutex mu;
+    gth::DBuf fp_scratch, fp_state, fp_counter;
+    int* fp_counter_h = nullptr;
     gth::DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
     cudaStream_t slot_stream[2] = {nullptr, nullptr};
     void* host_stats = nullptr;
@@ -80,6 +82,7 @@ struct gt_device_greens {
     ~gt_device_greens() {
         for (auto e : event_pool) cudaEventDestroy(e);
         if (host_stats) cudaFreeHost(host_stats);
+        if (fp_counter_h) cudaFreeHost(fp_counter_h);
         for (auto& s : slot_stream)
             if (s) cudaStreamDestroy(s);
         if (stream) cudaStreamDestroy(stream);

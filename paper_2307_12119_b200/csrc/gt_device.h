@@ -126,3 +126,27 @@ int gtd_clamp(double* x, size_t count, unsigned long long* neg, cudaStream_t st)
 #ifdef __cplusplus
 }
 #endif
+
+/* ---- mode B: leakage fixed point with the Kirchhoff transform (fixed_point.cu) ---- */
+#ifdef __cplusplus
+extern "C" {
+#endif
+typedef struct gtd_fp_opts {
+    int law;          /* 1: exp(beta dT) (north star), 0: 1 + beta dT (reference leakage_at_temperature) */
+    int kirchhoff;    /* 1: T(theta) inverse for k = k_ref (T/T0)^-eta */
+    double beta, t_ambient, eta, tol;
+    int max_iters;
+    int poll;         /* host convergence poll interval in iterations (0 = 4) */
+} gtd_fp_opts;
+size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64);
+size_t gtd_fp_state_bytes(void);
+/* t_state: [B][n][n] rise maps (state and result); iters/status: [B] device ints;
+ * max_out/mean_out: [B] device doubles (may be NULL); state: B * gtd_fp_state_bytes();
+ * counter_d: device int; counter_h: pinned host int. Synchronises the stream every
+ * `poll` iterations to stop when every sample of a chunk is done. */
+int gtd_fp_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_fp_opts* opts, void* t_state,
+                 int* iters, int* status, double* max_out, double* mean_out, void* scratch, void* state,
+                 int* counter_d, int* counter_h, int chunk, cudaStream_t stream, long long* launches);
+#ifdef __cplusplus
+}
+#endif
