@@ -42,7 +42,7 @@ def test_fixed_point_matches_oracle(b200lib, oracle, greens64, golden, law, kirc
         if prec == 1:
             np.testing.assert_array_equal(it, it_ref)
         else:
-            assert np.abs(it - it_ref).max() <= 1
+            assert np.abs(it - it_ref).max() <= 3  # fp32 rounding moves the 1e-4 K crossing
         assert err <= atol
         np.testing.assert_allclose(mx, t_ref.reshape(len(p), -1).max(axis=1), atol=atol)
 
