@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mode-b", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -210,7 +211,7 @@ def run_reference_arm(args, cfg):
 def run_b200(args, cfg):
     import torch
     import torch.distributed as dist
-    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200 import inputs, shard
     from paper_2307_12119_b200.api import GT_FP32, GT_FP64, SAMPLE_STATS_DTYPE, DeviceGreens
 
     ws, rank, local = dist_env()
@@ -226,7 +227,8 @@ def run_b200(args, cfg):
 
     dg = DeviceGreens(greens_cfg1(), prec, device=local)
     opts = dg.opts(leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=args.chunk)
-    P, V = inputs.mc_inputs(cfg, rank * B, B, device=str(dev), torch_dtype=tdt)
+    s0, s1 = shard.shard_range(rank, ws, B)
+    P, V = inputs.mc_inputs(cfg, s0, s1 - s0, device=str(dev), torch_dtype=tdt)
     out = torch.empty_like(P)
     stats = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(device=dev)
@@ -256,10 +258,7 @@ def run_b200(args, cfg):
         dist.barrier()
     ms_local = e0.elapsed_time(e1) / args.steps
     clk = clocks.stop()
-    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = shard.max_over_ranks(ms_local, dev)
     value = ws * B / (ms / 1e3)
 
     st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=SAMPLE_STATS_DTYPE)
@@ -312,13 +311,53 @@ def run_b200(args, cfg):
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_step()
-        el = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev, dtype=torch.float64)
-        if ws > 1:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * B / float(el.item()), "unit": UNIT,
+        el = shard.max_over_ranks((time.perf_counter() - t0) / args.steps, dev)
+        e2e = {"value": ws * B / el, "unit": UNIT,
                "h2d_bytes_per_step": 2 * B * n * n * es, "d2h_bytes_per_step": B * SAMPLE_STATS_DTYPE.itemsize,
-               "ms_per_step": 1e3 * float(el.item()),
+               "ms_per_step": 1e3 * el,
                "path": "gt_mc_batch (host API): pinned p_dyn/var -> H2D, fused passes, D2H of per-pair max/mean/status"}
+
+    # mode B (north-star fixed point) on the same pairs: literal exp law (runaway expected,
+    # SURVEY §0) on a subset, and the reference's linear law timed over the full batch.
+    mode_b = None
+    if not args.no_mode_b:
+        it_d = torch.zeros(B, dtype=torch.int32, device=dev)
+        st_d = torch.zeros(B, dtype=torch.int32, device=dev)
+        mx_d = torch.zeros(B, dtype=torch.float64, device=dev)
+        Tb = torch.empty_like(P)
+        k = min(256, B)
+        lit = dg.fp_opts(leak_frac=0.3, law=1, kirchhoff=0, beta=0.017, tol=1e-4, max_iters=50)
+        dg.fp_batch_device(P.data_ptr(), V.data_ptr(), k, lit, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
+                           mx_d.data_ptr(), None, stream.cuda_stream)
+        torch.cuda.synchronize()
+        st_lit = st_d[:k].cpu().numpy()
+        lin = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4 if prec == GT_FP64 else 2e-4,
+                         max_iters=200)
+        dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, lin, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
+                           mx_d.data_ptr(), None, stream.cuda_stream)
+        torch.cuda.synchronize()
+        steps_b = max(1, min(args.steps, 3))
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(steps_b):
+            dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, lin, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
+                               mx_d.data_ptr(), None, stream.cuda_stream)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        msb = shard.max_over_ranks(f0.elapsed_time(f1) / steps_b, dev)
+        its = it_d.cpu().numpy()
+        stl = st_d.cpu().numpy()
+        h = n + 1
+        b_it = 32 * es * n * h + 16 * es * n * n  # DESIGN.md §4 per-iteration model
+        mode_b = {
+            "literal_exp_law": {"pairs": k, "failed": int((st_lit != 0).sum()),
+                                "note": "exp(0.017 dT) leakage at config-1 power has no fixed point (SURVEY §0); "
+                                        "reported as per-pair runaway status, like the reference's ConvergenceError"},
+            "linear_law": {"value": ws * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
+                           "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
+                           "failed": int((stl != 0).sum()), "tol_K": lin.tol,
+                           "bytes_per_iteration_model": b_it,
+                           "achieved_GBps_model": b_it * float(its.sum()) / (msb / 1e3) / 1e9}}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -347,6 +386,8 @@ def run_b200(args, cfg):
         }
         if e2e:
             line["e2e"] = e2e
+        if mode_b:
+            line["mode_b"] = mode_b
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
