@@ -348,7 +348,7 @@ def run_b200(args, cfg):
         its = it_d.cpu().numpy()
         stl = st_d.cpu().numpy()
         h = n + 1
-        b_it = 32 * es * n * h + 16 * es * n * n  # DESIGN.md §4 per-iteration model
+        b_it = 8 * es * n * h + 4 * es * n * n  # DESIGN.md §4 per-iteration model (32nh + 16n^2 B in fp32)
         mode_b = {
             "literal_exp_law": {"pairs": k, "failed": int((st_lit != 0).sum()),
                                 "note": "exp(0.017 dT) leakage at config-1 power has no fixed point (SURVEY §0); "

@@ -139,20 +139,26 @@ __device__ __forceinline__ void dftR(cplx<T>* v) {
 }
 
 // ------------------------------------------------------------- tile geometry
-// Lines per tile: keep a tile near 64 KiB so 2-3 CTAs share an SM.
+#ifndef GT_TILE_BYTES
+#define GT_TILE_BYTES 32768
+#endif
+// Lines per tile: a tile of GT_TILE_BYTES so several CTAs share an SM and hide
+// each other's barrier / load latency.
 template <typename T, int M>
 struct TileGeom {
     static constexpr int CB = int(sizeof(cplx<T>));
-    static constexpr int Lraw = 65536 / (M * CB);
+    static constexpr int Lraw = GT_TILE_BYTES / (M * CB);
     static constexpr int L = Lraw > 32 ? 32 : (Lraw < 4 ? 4 : Lraw);
     static constexpr int LOG2M = ilog2(M);
     static constexpr int N8 = LOG2M / 3;           // radix-8 stages
     static constexpr int RLAST = 1 << (LOG2M % 3); // 1, 2 or 4
-    // threads: one radix-8 butterfly per thread per step of the widest stage
-    static constexpr int NBMIN = (M / 8) * L;
-    static constexpr int NT = NBMIN >= 512 ? 512 : NBMIN;
-    // resident CTAs the register budget must allow (<= 64 regs/thread at 1024 threads/SM)
-    static constexpr int MINB = 1024 / NT;
+    // threads: one radix-8 pair-butterfly (two lines) per thread in the widest stage
+    static constexpr int NBMIN = (M / 8) * (L / 2);
+    static constexpr int NT = NBMIN >= 512 ? 512 : (NBMIN < 32 ? 32 : NBMIN);
+    // resident CTAs the register budget must allow: 64 regs/thread for fp32,
+    // 128 for fp64 (a pair-butterfly holds 16 complex values)
+    static constexpr int REGS = sizeof(T) == 8 ? 128 : 64;
+    static constexpr int MINB = (65536 / REGS) / NT < 1 ? 1 : (65536 / REGS) / NT;
 };
 
 // One Stockham stage over a whole tile, in place (all loads, barrier, stores).

@@ -84,6 +84,9 @@ __device__ __forceinline__ void or_flags(int* dst, int flags) {
     if ((threadIdx.x & 31) == 0 && w) atomicOr(dst, w);
 }
 
+__device__ __forceinline__ float fast_rcp(float x) { return __fdividef(1.0f, x); }
+__device__ __forceinline__ double fast_rcp(double x) { return 1.0 / x; }
+
 template <typename T>
 __device__ __forceinline__ bool finite_(T v) {
     return isfinite(v);
@@ -321,7 +324,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
             if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
             // Y = f A / den1, R = f t1 / (den1 den2): one reciprocal for both quotients
-            const T rinv = T(1) / (d1 * d2);
+            const T rinv = fast_rcp(d1 * d2);
             const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));           // f conj(den1)
             const cplx<T> Y = cscale<T>(cmul<T>(cmul<T>(fc1, Ah), mk<T>(d2, T(0))), rinv);
             const cplx<T> R = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
@@ -500,8 +503,8 @@ struct MCLaunch {
             mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
                                                                          T(g->rand_scale), o->with_rand);
             if (mark) mark(ctx, 3, st);
-            mc_finalize<<<(cnt + 127) / 128, 128, 0, st>>>(stats, s0, cnt, n);
         }
+        mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n);
         return static_cast<int>(cudaGetLastError());
     }
 };
@@ -560,7 +563,7 @@ size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64) {
 
 int gtd_mc_launch_count(int batch, int chunk) {
     const int chunks = (batch + chunk - 1) / chunk;
-    return chunks * 4;  // kernels: pass1, pass2, pass3, finalize per chunk (plus one memset node)
+    return chunks * 3 + 1;  // pass1, pass2, pass3 per chunk + one finalize (plus one memset node)
 }
 
 int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_mc_opts* opts,
