@@ -140,7 +140,7 @@ __device__ __forceinline__ void dftR(cplx<T>* v) {
 
 // ------------------------------------------------------------- tile geometry
 #ifndef GT_TILE_BYTES
-#define GT_TILE_BYTES 32768
+#define GT_TILE_BYTES 65536
 #endif
 // Lines per tile: a tile of GT_TILE_BYTES so several CTAs share an SM and hide
 // each other's barrier / load latency.
@@ -282,6 +282,75 @@ struct StageRunner {
         } else if constexpr (G::RLAST > 1) {
             constexpr int NS = 1 << (3 * G::N8);
             stage<T, M, L, LP, NT, SIGN, G::RLAST, NS>(tile, tw);
+        }
+    }
+};
+
+// --------------------------------------------------------------- stage plan
+// Forward transforms run radices (8, ..., 8, RL); inverse transforms run the
+// reverse (RL, 8, ..., 8). Then the last forward stage's outputs for butterfly
+// j (positions j + q M/RL) are exactly the inputs of the first inverse stage's
+// butterfly j, and the last inverse stage (radix 8, NS = M/8) outputs the
+// positions j + r M/8 -- so kernels can fuse spectral algebra between the two
+// transforms in registers and move the first/last stage data straight between
+// registers and global memory.
+template <int M>
+struct Plan {
+    static constexpr int LOG2M = ilog2(M);
+    static constexpr int N8 = LOG2M / 3;
+    static constexpr int RL = 1 << (LOG2M % 3);
+    static constexpr int K = N8 + (RL > 1 ? 1 : 0);
+    __host__ __device__ static constexpr int fr(int s) { return s < N8 ? 8 : RL; }
+    __host__ __device__ static constexpr int fns(int s) { return s == 0 ? 1 : fns(s - 1) * fr(s - 1); }
+    __host__ __device__ static constexpr int ir(int s) { return RL > 1 ? (s == 0 ? RL : 8) : 8; }
+    __host__ __device__ static constexpr int ins(int s) { return s == 0 ? 1 : ins(s - 1) * ir(s - 1); }
+    static constexpr int RLAST_F = fr(K - 1);  // radix of the last forward stage
+};
+
+template <int R, int NS, int M, int SIGN, typename T>
+__device__ __forceinline__ void pair_twiddle_dft(cplx<T>* va, cplx<T>* vb, int j, const cplx<T>* tw) {
+    if constexpr (NS > 1) {
+        const int k = j % NS;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            cplx<T> w = tw[k * r * (M / (NS * R))];
+            if (SIGN > 0) w.y = -w.y;
+            va[r] = cmul<T>(va[r], w);
+            vb[r] = cmul<T>(vb[r], w);
+        }
+    }
+    dftR<R, SIGN, T>(va);
+    dftR<R, SIGN, T>(vb);
+}
+
+template <typename T, int M, int LP, int R>
+__device__ __forceinline__ void pair_load(const cplx<T>* tile, int j, int lp, cplx<T>* va, cplx<T>* vb) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const LinePair<T> q = ld_pair(&tile[(j + r * (M / R)) * LP + 2 * lp]);
+        va[r] = q.a;
+        vb[r] = q.b;
+    }
+}
+
+template <typename T, int M, int LP, int R, int NS>
+__device__ __forceinline__ void pair_store(cplx<T>* tile, int j, int lp, const cplx<T>* va, const cplx<T>* vb) {
+    const int k = j % NS;
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) st_pair(&tile[(base + r * NS) * LP + 2 * lp], LinePair<T>{va[r], vb[r]});
+}
+
+// In-place pair stages s in [S, E) of the forward (INV=false) or inverse plan.
+template <typename T, int M, int L, int LP, int NT, bool INV, int S, int E>
+struct PlanStages {
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* tw) {
+        if constexpr (S < E) {
+            using Pl = Plan<M>;
+            constexpr int R = INV ? Pl::ir(S) : Pl::fr(S);
+            constexpr int NS = INV ? Pl::ins(S) : Pl::fns(S);
+            stockham_stage_pairs<T, M, L, LP, NT, INV ? +1 : -1, R, NS>(tile, tw);
+            PlanStages<T, M, L, LP, NT, INV, S + 1, E>::run(tile, tw);
         }
     }
 };

@@ -228,9 +228,47 @@ mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 }
 
 // ------------------------------------------------------------------ pass 2
-// Persistent over (sample, tile of W half-spectrum columns). Tile line 2w holds
-// the A column v0+w (mirror-expanded), line 2w+1 the B column (centre-embedded),
-// so one thread reads both operands of a frequency with one vector access.
+// Closed forms at one frequency (u, v): returns Y = F_det A and R = F_rand
+// (greens.cpp:203-251) with one shared reciprocal; sets runaway flags.
+template <typename T, int M>
+struct ClosedForm {
+    static constexpr int n = M / 2, c = n / 2, hp = MCGeom<T, M>::hp, W = MCGeom<T, M>::W;
+    const cplx<T>* __restrict__ fk;
+    const T* __restrict__ gtab;
+    const cplx<T>* __restrict__ k1;
+    const T* s_srow;  // [n][W] row-symmetrised leakage of this column tile
+    T alpha, beta, mu_g, mus, qshift;
+
+    __device__ __forceinline__ void eval(cplx<T>& a, cplx<T>& b, int u, int v, int w, int& flags) const {
+        const int du = u <= M - u ? u : M - u;
+        const cplx<T> K = cmul<T>(k1[u], k1[v]);
+        const cplx<T> Bp = mk<T>(b.x - mus * K.x, b.y - mus * K.y);  // F(p_var) = F(p_leak0) - mu k1 k1
+        const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
+        const T g = gtab[du * hp + v];
+        const int ip = min(c + du, n - 1), im = max(c - du, 0);
+        const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
+        const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
+        const T a1 = T(1) - alpha * g * (T(1) + fmu);
+        const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
+        const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
+        const cplx<T> den2 = mk<T>(den1.x - alpha * g * Bp.x - beta * q * f.x, den1.y - alpha * g * Bp.y - beta * q * f.y);
+        const T d1 = cabs2<T>(den1), d2 = cabs2<T>(den2);
+        if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
+        if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
+        const T rinv = fast_rcp(d1 * d2);
+        const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));
+        a = cscale<T>(cmul<T>(fc1, a), d2 * rinv);
+        b = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
+    }
+};
+
+// Persistent over (sample, tile of W half-spectrum columns). Lines 2w / 2w+1
+// are the A / B columns v0+w, processed as a pair by one thread. The first
+// forward stage reads straight from the row spectra (mirror / centre
+// expansion in the address), the last forward stage, the closed forms and the
+// first inverse stage run in registers, and the last inverse stage writes the
+// kept rows straight back: 4 shared-memory round trips per column pair
+// instead of 8, and no separate load / algebra / store phases.
 template <typename T, int M>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
 mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
@@ -239,10 +277,19 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          const cplx<T>* __restrict__ fk, const T* __restrict__ gtab,
          const cplx<T>* __restrict__ k1, T alpha, T beta, int mu_per_sample, T mu_fixed) {
     using Gm = MCGeom<T, M>;
+    using Pl = Plan<M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT, W = Gm::W;
     constexpr int hp = Gm::hp;
     constexpr int CT = hp / W;
-    constexpr int EPT = (n * W + NT - 1) / NT;
+    constexpr int K = Pl::K;
+    constexpr int R0 = Pl::fr(0);
+    constexpr int BPT0 = (M / R0) * W / NT;
+    constexpr int RL = Pl::RLAST_F;
+    constexpr int BPTL = (M / RL) * W / NT;
+    constexpr int RI = Pl::ir(K - 1);  // last inverse stage radix (8)
+    constexpr int BPTI = (M / RI) * W / NT;
+    static_assert(K >= 2 && R0 == 8 && RI == 8, "plan");
+    static_assert((M / 8) * W % NT == 0 && BPT0 >= 1, "threads");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + M * L;
@@ -254,95 +301,107 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
         const int v0 = (item - s * CT) * W;
         const size_t sg = static_cast<size_t>(sample0) + s;
         const size_t sbase = static_cast<size_t>(s) * n * hp;
+        __syncthreads();  // previous item's readers of tile / s_srow are done
 
-        for (int idx = threadIdx.x; idx < (M - 2 * c) * W; idx += NT) {
-            const int w = idx % W, u = c + idx / W;
-            tile[u * L + 2 * w + 1] = mk<T>(T(0), T(0));
-        }
-        cplx<T> av[EPT], bv[EPT];
-        T sv[EPT];
+        // ---- forward stage 0 (radix 8, NS = 1) straight from the row spectra
+        cplx<T> va[BPT0][8], vb[BPT0][8];
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            const int idx = threadIdx.x + k * NT;
-            if (idx < n * W) {
-                const int w = idx % W, x = idx / W;
-                const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
-                av[k] = Aspec[o];
-                bv[k] = Bspec[o];
-                sv[k] = Srow[o];
+        for (int b = 0; b < BPT0; ++b) {
+            const int id = threadIdx.x + b * NT;
+            const int lp = id % W, j = id / W;
+            const int v = v0 + lp;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int i = j + r * (M / 8);
+                const int xa = i < n ? i : M - 1 - i;       // mirror_pad
+                const int xb = (i + c) & (M - 1);           // centre_kernel: row i holds die row x
+                va[b][r] = Aspec[sbase + static_cast<size_t>(xa) * hp + v];
+                vb[b][r] = xb < n ? Bspec[sbase + static_cast<size_t>(xb) * hp + v] : mk<T>(T(0), T(0));
             }
         }
+        for (int idx = threadIdx.x; idx < n * W; idx += NT) {
+            const int w = idx % W, x = idx / W;
+            s_srow[x * W + w] = Srow[sbase + static_cast<size_t>(x) * hp + v0 + w];
+        }
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            const int idx = threadIdx.x + k * NT;
-            if (idx < n * W) {
-                const int w = idx % W, x = idx / W;
-                tile[x * L + 2 * w] = av[k];
-                tile[(M - 1 - x) * L + 2 * w] = av[k];
-                tile[((x - c) & (M - 1)) * L + 2 * w + 1] = bv[k];
-                s_srow[x * W + w] = sv[k];
-            }
+        for (int b = 0; b < BPT0; ++b) {
+            const int id = threadIdx.x + b * NT;
+            const int lp = id % W, j = id / W;
+            dftR<8, -1, T>(va[b]);
+            dftR<8, -1, T>(vb[b]);
+            pair_store<T, M, L, 8, 1>(tile, j, lp, va[b], vb[b]);
         }
         // Per-sample scalars (pass 1 has completed: kernel boundary).
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
-        const T mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
         const T* Nm = in.nn(sg);
         const T* V = in.v(sg);
-        const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
-        const T pl_00 = in.nom_scale * Nm[0] * V[0];
-        // q = sym(Q), Q = p_var + p_var(c,c) - p_var(0,0)  (greens.cpp:177-184)
-        const T qshift = T(double(pl_cc) - double(pl_00) - mu_s);
-        const T mus = T(mu_s);
+        ClosedForm<T, M> cf;
+        cf.fk = fk;
+        cf.gtab = gtab;
+        cf.k1 = k1;
+        cf.s_srow = s_srow;
+        cf.alpha = alpha;
+        cf.beta = beta;
+        cf.mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
+        cf.mus = T(mu_s);
+        {
+            const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
+            const T pl_00 = in.nom_scale * Nm[0] * V[0];
+            cf.qshift = T(double(pl_cc) - double(pl_00) - mu_s);  // greens.cpp:177-184
+        }
         __syncthreads();
-        tile_fft<T, M, L, L, NT, -1>(tile, s_tw);
-
+        // ---- middle forward stages
+        PlanStages<T, M, L, L, NT, false, 1, K - 1>::run(tile, s_tw);
+        // ---- last forward stage + closed forms + first inverse stage, in registers
         int flags = 0;
-#pragma unroll 4
-        for (int idx = threadIdx.x; idx < M * W; idx += NT) {
-            const int w = idx % W, u = idx / W;
-            const int v = v0 + w;
-            if (v >= h) continue;
-            const int du = u <= M - u ? u : M - u;
-            const cplx<T> Ah = tile[u * L + 2 * w];
-            const cplx<T> Bh = tile[u * L + 2 * w + 1];
-            const cplx<T> K = cmul<T>(k1[u], k1[v]);
-            const cplx<T> Bp = mk<T>(Bh.x - mus * K.x, Bh.y - mus * K.y);  // F(p_var)
-            const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
-            const T g = gtab[du * hp + v];
-            const int ip = min(c + du, n - 1), im = max(c - du, 0);
-            const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
-            const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
-            // deterministic closed form (greens.cpp:203-216)
-            const T a1 = T(1) - alpha * g * (T(1) + fmu);
-            const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
-            // random closed form (greens.cpp:225-251)
-            const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
-            const cplx<T> den2 = mk<T>(den1.x - alpha * g * Bp.x - beta * q * f.x,
-                                       den1.y - alpha * g * Bp.y - beta * q * f.y);
-            const T d1 = cabs2<T>(den1), d2 = cabs2<T>(den2);
-            if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
-            if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
-            // Y = f A / den1, R = f t1 / (den1 den2): one reciprocal for both quotients
-            const T rinv = fast_rcp(d1 * d2);
-            const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));           // f conj(den1)
-            const cplx<T> Y = cscale<T>(cmul<T>(cmul<T>(fc1, Ah), mk<T>(d2, T(0))), rinv);
-            const cplx<T> R = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
-            tile[u * L + 2 * w] = Y;
-            tile[u * L + 2 * w + 1] = R;
+        {
+            constexpr int NSL = Pl::fns(K - 1);
+            cplx<T> la[BPTL][RL], lb[BPTL][RL];
+#pragma unroll
+            for (int b = 0; b < BPTL; ++b) {
+                const int id = threadIdx.x + b * NT;
+                const int lp = id % W, j = id / W;
+                const int v = v0 + lp;
+                pair_load<T, M, L, RL>(tile, j, lp, la[b], lb[b]);
+                pair_twiddle_dft<RL, NSL, M, -1, T>(la[b], lb[b], j, s_tw);
+                if (v < h) {
+#pragma unroll
+                    for (int q = 0; q < RL; ++q) cf.eval(la[b][q], lb[b][q], j + q * (M / RL), v, lp, flags);
+                }
+                dftR<RL, +1, T>(la[b]);
+                dftR<RL, +1, T>(lb[b]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < BPTL; ++b) {
+                const int id = threadIdx.x + b * NT;
+                pair_store<T, M, L, RL, 1>(tile, id / W, id % W, la[b], lb[b]);
+            }
+            __syncthreads();
         }
         or_flags(&stats[sg].status, flags);
-        __syncthreads();
-        tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
-
-        // Keep rows [0, n) of Y (crop) and rows rho(x) of R (kernel_to_die), in place.
-        for (int idx = threadIdx.x; idx < n * W; idx += NT) {
-            const int w = idx % W, x = idx / W;
-            const size_t o = sbase + static_cast<size_t>(x) * hp + v0 + w;
-            Aspec[o] = tile[x * L + 2 * w];
-            Bspec[o] = tile[((x - c) & (M - 1)) * L + 2 * w + 1];
+        // ---- middle inverse stages
+        PlanStages<T, M, L, L, NT, true, 1, K - 1>::run(tile, s_tw);
+        // ---- last inverse stage (radix 8, NS = M/8): keep rows [0, n) of Y, rows rho(x) of R
+        {
+#pragma unroll
+            for (int b = 0; b < BPTI; ++b) {
+                const int id = threadIdx.x + b * NT;
+                const int lp = id % W, j = id / W;
+                const int v = v0 + lp;
+                cplx<T> ya[8], yb[8];
+                pair_load<T, M, L, 8>(tile, j, lp, ya, yb);
+                pair_twiddle_dft<8, M / 8, M, +1, T>(ya, yb, j, s_tw);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int i = j + r * (M / 8);
+                    if (i < n) Aspec[sbase + static_cast<size_t>(i) * hp + v] = ya[r];
+                    const int x = (i + c) & (M - 1);
+                    if (x < n) Bspec[sbase + static_cast<size_t>(x) * hp + v] = yb[r];
+                }
+            }
         }
-        __syncthreads();
     }
 }
 
