@@ -165,7 +165,7 @@ mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
                 vv[k] = V[x * n + y];
             }
         }
-        double sum_l = 0.0, sum_a = 0.0;
+        T part_l = T(0), part_a = T(0);  // per-thread partials (<= EPT terms), fp64 across threads
         int bad = 0;
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -177,15 +177,15 @@ mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             if (!(vr >= var_lo && vr <= var_hi)) bad |= GTD_ST_BAD_VAR;
             const T lk = in.nom_scale * nm * vr;
             const T a = p + lk;
-            sum_l += double(lk);
-            sum_a += double(a);
+            part_l += lk;
+            part_a += a;
             tileT[2 * (y * LP + l)] = a;
             tileT[2 * ((M - 1 - y) * LP + l)] = a;
             tileT[2 * (((y - c) & (M - 1)) * LP + l) + 1] = lk;
         }
         or_flags(&stats[sg].status, bad);
-        const double tl = block_sum<NT>(sum_l, red);  // (contains the barrier for the tile)
-        const double ta = block_sum<NT>(sum_a, red);
+        const double tl = block_sum<NT>(double(part_l), red);  // (contains the barrier for the tile)
+        const double ta = block_sum<NT>(double(part_a), red);
         if (threadIdx.x == 0) {
             atomicAdd(&stats[sg].sum_leak, tl);
             atomicAdd(&stats[sg].sum_applied, ta);
@@ -473,9 +473,9 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
             }
         }
 
-        double sum_t = 0.0;
-        double mx = 0.0;
+        T part_t = T(0), mxt = T(0);
         int bad = 0;
+        const T mu_t = T(mu_s);
 #pragma unroll
         for (int k = 0; k < EPO; ++k) {
             const int idx = threadIdx.x + k * NT;
@@ -484,17 +484,17 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
             const T yd = tile[j * LP + l].x * inv;
             const int jr = (j - c) & (M - 1);
             const T rd = tile[jr * LP + l].y * inv;
-            const T pvar = T(double(in.nom_scale * nv[k] * vv[k]) - mu_s);
+            const T pvar = in.nom_scale * nv[k] * vv[k] - mu_t;
             T t = yd + rd * pvar * scale;
             if (!finite_(t)) bad = GTD_ST_NONFINITE;
             t = t > T(0) ? t : T(0);
             if (out) out[(sg * n + x) * n + j] = t;
-            sum_t += double(t);
-            mx = fmax(mx, double(t));
+            part_t += t;
+            mxt = mxt > t ? mxt : t;
         }
         or_flags(&stats[sg].status, bad);
-        const double ts = block_sum<NT>(sum_t, red);
-        const double tm = block_max<NT>(mx, red);
+        const double ts = block_sum<NT>(double(part_t), red);
+        const double tm = block_max<NT>(double(mxt), red);
         if (threadIdx.x == 0) {
             atomicAdd(&stats[sg].sum_rise, ts);
             atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
