@@ -150,3 +150,50 @@ int gtd_fp_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_
 #ifdef __cplusplus
 }
 #endif
+
+/* ---- calibration: modal kernel producer and variation / closed-form maps (calib.cu, variation.cu) ---- */
+#ifdef __cplusplus
+extern "C" {
+#endif
+typedef struct gtd_stack {  /* reference ChipStack (stack.hpp:17-26) */
+    int n;
+    double die_edge, t_die, k_die, c_die, t_tim, k_tim, c_tim, t_spr, k_spr, c_spr, ambient, sink_resistance;
+} gtd_stack;
+/* f_sp0 (n x n fp64, device) of a uniform-k die by the modal DCT-II solution; work: 3 n^2 doubles. */
+int gtd_modal_impulse(const gtd_stack* s, double k_die, double* work, double* out, cudaStream_t st);
+/* centre values f_sp0(c,c) for up to 64 die conductivities; d_nets: count * gtd_modal_net_bytes(). */
+int gtd_modal_center(const gtd_stack* s, const double* k_values, int count, double* d_nets, double* out,
+                     cudaStream_t st);
+size_t gtd_modal_net_bytes(void);
+/* backward-Euler centre-cell step response after steps_d[i] (cumulative) steps of dt. */
+int gtd_modal_transient(const gtd_stack* s, double k_die, double dt, const int* steps_d, int ntimes,
+                        double* part, int blocks, double* out, cudaStream_t st);
+/* fit_capacitance centre-cell model for capacitance `cap` (<= 16 times). */
+int gtd_cap_model(const void* fk_full, size_t count, double floor_abs, double cap, const double* times_d,
+                  int ntimes, double inv_m2, double* part, int blocks, double* out, cudaStream_t st);
+
+/* variation.cu */
+/* sqrt(lambda * fix) of the spherical-correlogram circulant embedding (variation.cpp:87-132). */
+int gtd_var_eigs(int n, double pitch, double range, int fp64_twiddles_dummy, const void* tw64, void* work_cplx,
+                 double* sqrt_lam, double* red3, cudaStream_t st);
+/* out[n][n] = sigma * Re(IFFT(sqrt_lam . FFT(noise)))[top-left]; noise: m*m doubles; work: m*m double2. */
+int gtd_var_shape(const double* noise, const double* sqrt_lam, int n, double sigma, const void* tw64, void* work,
+                  double* out, cudaStream_t st);
+/* expo = bl * dl + bt * dt; flag |= 1 if |expo| > cap; out = nominal * exp(expo) (or exp only if nominal NULL). */
+int gtd_leak_exp(const double* nominal, const double* dl, const double* dt, double bl, double bt, double cap, int n,
+                 double* out, int* flag, cudaStream_t st);
+int gtd_add_maps(const double* a, const double* b, size_t count, double* out, cudaStream_t st);
+int gtd_sub_scalar(const double* a, double s, size_t count, double* out, cudaStream_t st);
+/* K = centre_kernel(f - phi) (spectral.cpp:126-141) as complex; out: m*m double2. */
+int gtd_center_kernel(const double* f, double phi, int n, void* K, cudaStream_t st);
+/* kernel_to_die (spectral.cpp:150-165) with scale: out[x][y] = scale * Re K[(x-c) mod m][(y-c) mod m]. */
+int gtd_kernel_to_die(const void* K, int n, double scale, double* out, cudaStream_t st);
+/* q(du, dv) = 1/4 sum f(clamp(c+-du), clamp(c+-dv)) + shift, table [(n+1)][n+1] (symmetric_multiplier). */
+int gtd_sym_table(const double* f, int n, double shift, double* tab, cudaStream_t st);
+/* random_greens spectral algebra (greens.cpp:225-251) over the full m x m spectrum, in place on Fp (= F(p_var)):
+ * Fp <- F_det (beta fk q + alpha Fp g) / (1 - alpha (1 + F(mu) + Fp) g - mu beta fk - beta fk q). */
+int gtd_rand_spectrum(const void* Fd, const void* fk, const double* gtab, int hp, const double* qtab, int n,
+                      double alpha, double beta, double mu, void* Fp, int* flag, cudaStream_t st);
+#ifdef __cplusplus
+}
+#endif

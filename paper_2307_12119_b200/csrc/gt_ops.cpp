@@ -303,12 +303,3 @@ std::vector<Field> gt_ops_trace(const Greens& g, double dt, const std::vector<Fi
     if (online_ms) *online_ms = ms_since(t0);
     return out;
 }
-
-Greens gt_ops_calibrate_modal(const Stack&, const VarParams&, const Field*, double) {
-    fail(ST_INTERNAL, "calibrate", "device calibration not built yet");
-}
-
-void gt_ops_monte_carlo(const Greens&, const VarParams&, const Field&, const Field&,
-                        const std::vector<unsigned long long>&, int, const std::string&, double*, double*) {
-    fail(ST_INTERNAL, "solver", "monte carlo path not built yet");
-}
