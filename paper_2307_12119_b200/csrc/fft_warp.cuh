@@ -1,0 +1,138 @@
+// fft_warp.cuh — one-warp FFT of a single length-M line, M = 32 P (P = 4, 8, 16).
+//
+// Used by the row passes, whose global data is contiguous along the line: a
+// warp loads / stores a row coalesced straight from / to registers, and the
+// only data exchange inside the transform is one warp-private shared-memory
+// transpose plus a cross-lane step by shuffles -- no CTA barriers, no
+// transposing staging tile (the tile engine needs both for rows).
+//
+// Four-step factorisation M = 32 x P, input index i = j + 32 k (lane j holds
+// k = 0..P-1), output index f = k' + P m1 + P^2 h:
+//   1. P-point DFT in registers over k, twiddle w_M^{j k'};
+//   2. transpose through shared memory: lane (k', h) takes the decimated
+//      sequence j = h + Q t (Q = 32 / P lanes per 32-point sub-transform);
+//   3. P-point DFT over t, twiddle w_32^{h m1}, Q-point DFT across the Q lanes
+//      sharing k' (shuffles).
+// On return lane (k' + P h) holds X[k' + P m1 + P^2 h] in v[m1].
+#pragma once
+
+#include "fft_tile.cuh"
+
+namespace gtb {
+
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft16(cplx<T>* v) {
+    // radix-4 x radix-4 with w16 twiddles, in place: after the first layer slot
+    // n2 + 4 k1 holds a[n2][k1]; the second layer leaves X[k1 + 4 k2] in slot
+    // 4 k1 + k2, undone by a compile-time register permutation.
+    const T c1 = T(0.92387953251128675613), s1 = T(0.38268343236508977173);  // cos/sin(pi/8)
+    const T r2 = T(0.70710678118654752440);
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+        cplx<T> q[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+        dft4<SIGN, T>(q);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[n2 + 4 * k1] = q[k1];
+    }
+    const T sg = SIGN < 0 ? T(-1) : T(1);
+    v[5] = cmul<T>(v[5], mk<T>(c1, sg * s1));     // n2=1,k1=1: w^1
+    v[9] = cmul<T>(v[9], mk<T>(r2, sg * r2));     // n2=1,k1=2: w^2
+    v[13] = cmul<T>(v[13], mk<T>(s1, sg * c1));   // n2=1,k1=3: w^3
+    v[6] = cmul<T>(v[6], mk<T>(r2, sg * r2));     // n2=2,k1=1: w^2
+    v[10] = mul_si<SIGN, T>(v[10]);               // n2=2,k1=2: w^4
+    v[14] = cmul<T>(v[14], mk<T>(-r2, sg * r2));  // n2=2,k1=3: w^6
+    v[7] = cmul<T>(v[7], mk<T>(s1, sg * c1));     // n2=3,k1=1: w^3
+    v[11] = cmul<T>(v[11], mk<T>(-r2, sg * r2));  // n2=3,k1=2: w^6
+    v[15] = cmul<T>(v[15], mk<T>(-c1, -sg * s1)); // n2=3,k1=3: w^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        cplx<T> q[4] = {v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]};
+        dft4<SIGN, T>(q);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[4 * k1 + k2] = q[k2];
+    }
+    cplx<T> t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+template <int P, int SIGN, typename T>
+__device__ __forceinline__ void dftP(cplx<T>* v) {
+    if constexpr (P == 16)
+        dft16<SIGN, T>(v);
+    else if constexpr (P == 8)
+        dft8<SIGN, T>(v);
+    else if constexpr (P == 4)
+        dft4<SIGN, T>(v);
+}
+
+template <typename T>
+__device__ __forceinline__ cplx<T> shfl_c(cplx<T> a, int src) {
+    cplx<T> r;
+    r.x = __shfl_sync(0xffffffffu, a.x, src);
+    r.y = __shfl_sync(0xffffffffu, a.y, src);
+    return r;
+}
+
+template <typename T, int M>
+struct WarpFFT {
+    static constexpr int P = M / 32;
+    static constexpr int Q = 32 / P;
+    static constexpr int SP = 33;  // scratch pitch (complex) of the P x 32 transpose
+    static constexpr int SCRATCH = P * SP > M ? P * SP : M;  // complex elements per warp
+    static_assert(P == 4 || P == 8 || P == 16, "warp FFT supports M = 128, 256, 512");
+
+    // tw: M-entry table exp(-2 pi i t / M) (shared); scratch: SCRATCH complex per warp.
+    template <int SIGN>
+    __device__ __forceinline__ static void run(cplx<T>* v, cplx<T>* scratch, const cplx<T>* tw, int lane) {
+        dftP<P, SIGN, T>(v);
+#pragma unroll
+        for (int k = 1; k < P; ++k) {
+            cplx<T> w = tw[lane * k];  // w_M^{j k'}, j k' < 32 P = M
+            if (SIGN > 0) w.y = -w.y;
+            v[k] = cmul<T>(v[k], w);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) scratch[k * SP + lane] = v[k];
+        __syncwarp();
+        const int kq = lane % P, h = lane / P;
+#pragma unroll
+        for (int t = 0; t < P; ++t) v[t] = scratch[kq * SP + h + Q * t];
+        __syncwarp();
+        dftP<P, SIGN, T>(v);
+#pragma unroll
+        for (int m1 = 1; m1 < P; ++m1) {
+            cplx<T> w = tw[h * m1 * P];  // w_32^{h m1} = w_M^{h m1 P}
+            if (SIGN > 0) w.y = -w.y;
+            v[m1] = cmul<T>(v[m1], w);
+        }
+        // Q-point DFT across the lanes kq + P h' (direct form: lane h keeps output g = h)
+        if constexpr (Q > 1) {
+#pragma unroll
+            for (int m1 = 0; m1 < P; ++m1) {
+                cplx<T> acc = v[m1];
+#pragma unroll
+                for (int d = 1; d < Q; ++d) {
+                    const int hs = (h + d) % Q;  // source h'
+                    const cplx<T> z = shfl_c<T>(v[m1], kq + P * hs);
+                    // w_Q^{h' g}, g = h: exponent (hs * h) mod Q, table index * (M / Q)
+                    cplx<T> w = tw[((hs * h) % Q) * (M / Q)];
+                    if (SIGN > 0) w.y = -w.y;
+                    acc = cadd<T>(acc, cmul<T>(z, w));
+                }
+                v[m1] = acc;
+            }
+        }
+    }
+
+    // position of v[m1] held by `lane` on return
+    __device__ __forceinline__ static int out_pos(int lane, int m1) {
+        return (lane % P) + P * m1 + P * P * (lane / P);
+    }
+};
+
+}  // namespace gtb

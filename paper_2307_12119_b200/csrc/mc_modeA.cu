@@ -29,6 +29,7 @@
 #include <cstdio>
 
 #include "fft_tile.cuh"
+#include "fft_warp.cuh"
 #include "gt_device.h"
 
 namespace gtb {
@@ -319,9 +320,13 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
                 vb[b][r] = xb < n ? Bspec[sbase + static_cast<size_t>(xb) * hp + v] : mk<T>(T(0), T(0));
             }
         }
-        for (int idx = threadIdx.x; idx < n * W; idx += NT) {
-            const int w = idx % W, x = idx / W;
-            s_srow[x * W + w] = Srow[sbase + static_cast<size_t>(x) * hp + v0 + w];
+        // S rows into registers now, into shared memory after the stage-0 math (latency overlap)
+        constexpr int ES = (n * W + NT - 1) / NT;
+        T sv[ES];
+#pragma unroll
+        for (int k = 0; k < ES; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            sv[k] = idx < n * W ? Srow[sbase + static_cast<size_t>(idx / W) * hp + v0 + idx % W] : T(0);
         }
 #pragma unroll
         for (int b = 0; b < BPT0; ++b) {
@@ -330,6 +335,11 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             dftR<8, -1, T>(va[b]);
             dftR<8, -1, T>(vb[b]);
             pair_store<T, M, L, 8, 1>(tile, j, lp, va[b], vb[b]);
+        }
+#pragma unroll
+        for (int k = 0; k < ES; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx < n * W) s_srow[(idx / W) * W + idx % W] = sv[k];
         }
         // Per-sample scalars (pass 1 has completed: kernel boundary).
         const double n2 = double(n) * double(n);
@@ -503,6 +513,200 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
     }
 }
 
+// --------------------------------------------------- warp-per-row passes
+// Row passes for M = 128 / 256 / 512: each warp owns one die row at a time,
+// loads and stores it coalesced straight from / to registers and transforms it
+// with the one-warp FFT (fft_warp.cuh): no CTA barriers, no transposing tile.
+constexpr int WARPS = 16;
+template <typename T>
+struct WarpMinBlocks {
+    static constexpr int value = sizeof(T) == 8 ? 1 : 2;  // fp64 lines need 128 registers
+};
+
+template <typename T, int M>
+__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T>::value)
+mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
+          cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
+          const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
+    using Gm = MCGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, hp = Gm::hp, P = WF::P;
+    constexpr int E = n / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_tw + M + warp * WF::SCRATCH;
+    T* st_a = reinterpret_cast<T*>(scr);
+    T* st_l = st_a + n;
+    for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
+    __syncthreads();
+
+    for (int item = blockIdx.x * WARPS + warp; item < count * n; item += gridDim.x * WARPS) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const T* P_ = in.p(sg) + x * n;
+        const T* N_ = in.nn(sg) + x * n;
+        const T* V_ = in.v(sg) + x * n;
+        const bool n_is_p = in.N == in.P && in.sN == in.sP;
+        T pv[E], nv[E], vv[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int y = lane + 32 * t;
+            pv[t] = P_[y];
+            vv[t] = V_[y];
+            nv[t] = n_is_p ? pv[t] : N_[y];
+        }
+        T part_l = T(0), part_a = T(0);
+        int bad = 0;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int y = lane + 32 * t;
+            if (!(pv[t] >= T(0)) || !finite_(pv[t]) || !(nv[t] >= T(0)) || !finite_(nv[t])) bad |= GTD_ST_BAD_POWER;
+            if (!(vv[t] >= var_lo && vv[t] <= var_hi)) bad |= GTD_ST_BAD_VAR;
+            const T lk = in.nom_scale * nv[t] * vv[t];
+            const T a = pv[t] + lk;
+            part_l += lk;
+            part_a += a;
+            st_a[y] = a;
+            st_l[y] = lk;
+        }
+        __syncwarp();
+        // row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185)
+        T* Srow_x = Srow + (static_cast<size_t>(s) * n + x) * hp;
+        for (int v = lane; v < hp; v += 32) {
+            T val = T(0);
+            if (v < h) val = st_l[min(c + v, n - 1)] + st_l[max(c - v, 0)];
+            Srow_x[v] = val;
+        }
+        // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int i = lane + 32 * k;
+            const T re = st_a[i < n ? i : M - 1 - i];
+            T im = T(0);
+            if (i < c)
+                im = st_l[i + c];
+            else if (i >= M - c)
+                im = st_l[i - M + c];
+            z[k] = mk<T>(re, im);
+        }
+        __syncwarp();
+        WF::template run<-1>(z, scr, s_tw, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        // split into the two real-input half spectra
+        cplx<T>* A_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
+        cplx<T>* B_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+        for (int v = lane; v < hp; v += 32) {
+            cplx<T> A = mk<T>(T(0), T(0)), B = A;
+            if (v < h) {
+                const cplx<T> Z = scr[v];
+                const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
+                A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
+                B = mk<T>(T(0.5) * (Z.y - Zc.y), T(-0.5) * (Z.x - Zc.x));
+            }
+            A_x[v] = A;
+            B_x[v] = B;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double tl = warp_sum(double(part_l)), ta = warp_sum(double(part_a));
+        if (lane == 0) {
+            atomicAdd(&stats[sg].sum_leak, tl);
+            atomicAdd(&stats[sg].sum_applied, ta);
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T>::value)
+mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
+          const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
+          const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
+    using Gm = MCGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, hp = Gm::hp, P = WF::P;
+    constexpr int E = n / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_tw + M + warp * WF::SCRATCH;
+    for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
+    __syncthreads();
+    const T inv = T(1.0 / (double(M) * double(M)));
+
+    for (int item = blockIdx.x * WARPS + warp; item < count * n; item += gridDim.x * WARPS) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const cplx<T>* Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
+        const cplx<T>* R_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+        // Z = Y + i R over the full line from the Hermitian half spectra
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int v = lane + 32 * k;
+            const int w = v <= n ? v : M - v;
+            const cplx<T> y = Y_x[w], r = R_x[w];
+            if (v == 0 || v == n)
+                z[k] = mk<T>(y.x, r.x);
+            else if (v < n)
+                z[k] = mk<T>(y.x - r.y, y.y + r.x);
+            else
+                z[k] = mk<T>(y.x + r.y, r.x - y.y);
+        }
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T mu_t = T(mu_s);
+        const T* N_ = in.nn(sg) + x * n;
+        const T* V_ = in.v(sg) + x * n;
+        WF::template run<+1>(z, scr, s_tw, lane);
+        T nv[E], vv[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            nv[t] = N_[lane + 32 * t];
+            vv[t] = V_[lane + 32 * t];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        T part = T(0), mxt = T(0);
+        int bad = 0;
+        T* O_x = out ? out + (sg * n + x) * n : nullptr;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int f = lane + 32 * t;
+            const T yd = scr[f].x * inv;
+            const T rd = scr[(f - c) & (M - 1)].y * inv;
+            const T pvar = in.nom_scale * nv[t] * vv[t] - mu_t;
+            T tt = yd + rd * pvar * scale;
+            if (!finite_(tt)) bad = GTD_ST_NONFINITE;
+            tt = tt > T(0) ? tt : T(0);
+            if (O_x) O_x[f] = tt;
+            part += tt;
+            mxt = mxt > tt ? mxt : tt;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double ts = warp_sum(double(part));
+        const double tm = warp_max(double(mxt));
+        if (lane == 0) {
+            atomicAdd(&stats[sg].sum_rise, ts);
+            atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
+            if (x == 0) stats[sg].mu = mu_s;
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, int M>
+constexpr bool use_warp_rows() {
+    return M == 128 || M == 256 || M == 512;
+}
+
 __global__ void mc_finalize(gtd_sample_stats* stats, int sample0, int count, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
@@ -518,6 +722,12 @@ struct MCLaunch {
     static size_t smem1() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
     static size_t smem2() { return sizeof(cplx<T>) * (M * Gm::L + M) + sizeof(T) * Gm::n * Gm::W; }
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
+    static size_t smemw() {
+        if constexpr (use_warp_rows<T, M>())
+            return sizeof(cplx<T>) * (M + WARPS * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
 
     static int run(const gtd_greens* g, const MCIn<T>& in, int batch, const gtd_mc_opts* o,
                    T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st,
@@ -533,6 +743,12 @@ struct MCLaunch {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1<T, M>, NT, smem1());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, NT, smem2());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3<T, M>, NT, smem3());
+            if constexpr (use_warp_rows<T, M>()) {
+                cudaFuncSetAttribute(mc_pass1w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
+                cudaFuncSetAttribute(mc_pass3w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1w<T, M>, WARPS * 32, smemw());
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3w<T, M>, WARPS * 32, smemw());
+            }
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -552,15 +768,23 @@ struct MCLaunch {
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
             if (mark) mark(ctx, 0, st);
-            mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
-                                                                         var_lo, var_hi);
+            if constexpr (use_warp_rows<T, M>())
+                mc_pass1w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(), st>>>(
+                    in, s0, cnt, A, B, S, stats, tw, var_lo, var_hi);
+            else
+                mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
+                                                                             var_lo, var_hi);
             if (mark) mark(ctx, 1, st);
             mc_pass2<T, M><<<grid(cnt * CT, res[1]), NT, smem2(), st>>>(in, s0, cnt, A, B, S, stats, tw, fk, gt,
                                                                          k1, T(g->alpha), T(g->beta),
                                                                          o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
-            mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
-                                                                         T(g->rand_scale), o->with_rand);
+            if constexpr (use_warp_rows<T, M>())
+                mc_pass3w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[2]), WARPS * 32, smemw(), st>>>(
+                    in, s0, cnt, A, B, stats, tw, out, T(g->rand_scale), o->with_rand);
+            else
+                mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
+                                                                             T(g->rand_scale), o->with_rand);
             if (mark) mark(ctx, 3, st);
         }
         mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n);
