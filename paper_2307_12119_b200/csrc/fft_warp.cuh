@@ -114,7 +114,10 @@ struct WarpFFT {
         if constexpr (Q > 1) {
 #pragma unroll
             for (int m1 = 0; m1 < P; ++m1) {
-                cplx<T> acc = v[m1];
+                // own term h' = h carries w_Q^{h h}
+                cplx<T> w0 = tw[((h * h) % Q) * (M / Q)];
+                if (SIGN > 0) w0.y = -w0.y;
+                cplx<T> acc = cmul<T>(v[m1], w0);
 #pragma unroll
                 for (int d = 1; d < Q; ++d) {
                     const int hs = (h + d) % Q;  // source h'
