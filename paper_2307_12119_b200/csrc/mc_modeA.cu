@@ -517,7 +517,8 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
 // Row passes for M = 128 / 256 / 512: each warp owns one die row at a time,
 // loads and stores it coalesced straight from / to registers and transforms it
 // with the one-warp FFT (fft_warp.cuh): no CTA barriers, no transposing tile.
-constexpr int WARPS = 16;
+constexpr int WARPS = 16;   // warps per CTA of the warp-per-row pass 1
+constexpr int WARPS3 = 12;  // pass 3 holds more live state: 12 warps x 2 CTAs at <= 85 registers
 template <typename T>
 struct WarpMinBlocks {
     static constexpr int value = sizeof(T) == 8 ? 1 : 2;  // fp64 lines need 128 registers
@@ -622,7 +623,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 }
 
 template <typename T, int M>
-__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T>::value)
+__global__ void __launch_bounds__(WARPS3 * 32, WarpMinBlocks<T>::value)
 mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
           const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
           const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
@@ -634,11 +635,11 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
     cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx<T>* scr = s_tw + M + warp * WF::SCRATCH;
-    for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
+    for (int t = threadIdx.x; t < M; t += WARPS3 * 32) s_tw[t] = g_tw[t];
     __syncthreads();
     const T inv = T(1.0 / (double(M) * double(M)));
 
-    for (int item = blockIdx.x * WARPS + warp; item < count * n; item += gridDim.x * WARPS) {
+    for (int item = blockIdx.x * WARPS3 + warp; item < count * n; item += gridDim.x * WARPS3) {
         const int s = item / n, x = item - s * n;
         const size_t sg = static_cast<size_t>(sample0) + s;
         const cplx<T>* Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
@@ -656,6 +657,8 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
                 z[k] = mk<T>(y.x - r.y, y.y + r.x);
             else
                 z[k] = mk<T>(y.x + r.y, r.x - y.y);
+            // bound the loads in flight (register pressure): fence every 4 lines of the row
+            if ((k & 3) == 3) asm volatile("" ::: "memory");
         }
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
@@ -664,6 +667,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
         const T* N_ = in.nn(sg) + x * n;
         const T* V_ = in.v(sg) + x * n;
         WF::template run<+1>(z, scr, s_tw, lane);
+        asm volatile("" ::: "memory");  // keep the epilogue loads below the transform (registers)
         T nv[E], vv[E];
 #pragma unroll
         for (int t = 0; t < E; ++t) {
@@ -728,6 +732,12 @@ struct MCLaunch {
         else
             return 0;
     }
+    static size_t smemw3() {
+        if constexpr (use_warp_rows<T, M>())
+            return sizeof(cplx<T>) * (M + WARPS3 * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
 
     static int run(const gtd_greens* g, const MCIn<T>& in, int batch, const gtd_mc_opts* o,
                    T* out, gtd_sample_stats* stats, void* scratch, int chunk, cudaStream_t st,
@@ -745,9 +755,9 @@ struct MCLaunch {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3<T, M>, NT, smem3());
             if constexpr (use_warp_rows<T, M>()) {
                 cudaFuncSetAttribute(mc_pass1w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
-                cudaFuncSetAttribute(mc_pass3w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
+                cudaFuncSetAttribute(mc_pass3w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw3()));
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1w<T, M>, WARPS * 32, smemw());
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3w<T, M>, WARPS * 32, smemw());
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3w<T, M>, WARPS3 * 32, smemw3());
             }
             int dev = 0;
             cudaGetDevice(&dev);
@@ -780,7 +790,7 @@ struct MCLaunch {
                                                                          o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
             if constexpr (use_warp_rows<T, M>())
-                mc_pass3w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[2]), WARPS * 32, smemw(), st>>>(
+                mc_pass3w<T, M><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32, smemw3(), st>>>(
                     in, s0, cnt, A, B, stats, tw, out, T(g->rand_scale), o->with_rand);
             else
                 mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
