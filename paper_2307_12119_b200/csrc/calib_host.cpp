@@ -171,8 +171,8 @@ Greens gt_ops_calibrate_modal(const Stack& s, const VarParams& v, const Field* n
     v.validate();
     need_device();
     const int n = s.n;
-    if (!pow2(n) || n < 16 || n > 512)
-        fail(ST_CONFIG, "calibrate", "device calibration supports power-of-two grids 16..512, got n=" + std::to_string(n));
+    if (!pow2(n) || n < 16 || n > 1024)
+        fail(ST_CONFIG, "calibrate", "device calibration supports power-of-two grids 16..1024, got n=" + std::to_string(n));
     if (v.dopant_spread != 0.0)
         fail(ST_CONFIG, "calibrate",
              "device calibration needs a uniform die conductivity (variation dopant_spread = 0): the modal kernel is "

@@ -70,8 +70,8 @@ void upload(DBuf& b, const void* src, size_t bytes, cudaStream_t st) {
 std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision, int device) {
     need_device();
     const int n = g.n;
-    if (!pow2(n) || n < 16 || n > 512)
-        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..512, got n=" + std::to_string(n));
+    if (!pow2(n) || n < 16 || n > 1024)
+        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..1024, got n=" + std::to_string(n));
     if (precision != GT_FP32 && precision != GT_FP64) fail(ST_CONFIG, "device", "precision must be GT_FP32 or GT_FP64");
     cuda_ok(cudaSetDevice(device), "cudaSetDevice");
     auto d = std::make_unique<gt_device_greens>();

@@ -99,6 +99,7 @@ int dispatch_fft2d(void* data, int m, int batch, int sign, const void* tw, cudaS
         case 256: return run_fft2d<T, 256>(data, batch, sign, tw, st);
         case 512: return run_fft2d<T, 512>(data, batch, sign, tw, st);
         case 1024: return run_fft2d<T, 1024>(data, batch, sign, tw, st);
+        case 2048: return run_fft2d<T, 2048>(data, batch, sign, tw, st);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }

@@ -148,7 +148,7 @@ template <typename T, int M>
 struct TileGeom {
     static constexpr int CB = int(sizeof(cplx<T>));
     static constexpr int Lraw = GT_TILE_BYTES / (M * CB);
-    static constexpr int L = Lraw > 32 ? 32 : (Lraw < 4 ? 4 : Lraw);
+    static constexpr int L = Lraw > 32 ? 32 : (Lraw < 2 ? 2 : Lraw);
     static constexpr int LOG2M = ilog2(M);
     static constexpr int N8 = LOG2M / 3;           // radix-8 stages
     static constexpr int RLAST = 1 << (LOG2M % 3); // 1, 2 or 4

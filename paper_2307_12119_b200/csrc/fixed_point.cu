@@ -368,6 +368,7 @@ int dispatch_fp(const gtd_greens* g, const gtd_mc_in* i, int batch, const gtd_fp
         GT_FP_CASE(256)
         GT_FP_CASE(512)
         GT_FP_CASE(1024)
+        GT_FP_CASE(2048)
 #undef GT_FP_CASE
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
@@ -382,6 +383,7 @@ int fp_hp(int m) {
         case 256: return FPGeom<T, 256>::hp;
         case 512: return FPGeom<T, 512>::hp;
         case 1024: return FPGeom<T, 1024>::hp;
+        case 2048: return FPGeom<T, 2048>::hp;
         default: return -1;
     }
 }

@@ -826,6 +826,7 @@ static int dispatch_mc(const gtd_greens* g, const gtd_mc_in* i, int batch, const
         case 256: return MCLaunch<T, 256>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
         case 512: return MCLaunch<T, 512>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
         case 1024: return MCLaunch<T, 1024>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
+        case 2048: return MCLaunch<T, 2048>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -839,6 +840,7 @@ static int geom_hp(int m) {
         case 256: return MCGeom<T, 256>::hp;
         case 512: return MCGeom<T, 512>::hp;
         case 1024: return MCGeom<T, 1024>::hp;
+        case 2048: return MCGeom<T, 2048>::hp;
         default: return -1;
     }
 }

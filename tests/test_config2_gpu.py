@@ -1,0 +1,76 @@
+"""Config 2 grid (n = 1024, m = 2048): the fused batched paths at the largest
+single-die size, against the CPU oracle on the same inputs.
+
+The GreensSet comes from this library's own device calibration (modal kernel
+producer, pinned against the reference calibrate() at n = 32/64 in
+test_calib_gpu.py): the reference FDM calibration is infeasible at n = 1024 on
+a CPU.
+"""
+import ctypes as C
+import dataclasses
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def greens1024(b200lib, tmp_path_factory):
+    from paper_2307_12119_b200.api import GreensArrays
+    d = tmp_path_factory.mktemp("cfg2")
+    (d / "stack.txt").write_text("n 1024\ndie_edge 0.016\n")
+    (d / "var.txt").write_text("dopant_spread 0\nbeta 0.017\n")
+    L = b200lib
+    g = C.c_void_p()
+    assert L.gt_calibrate(str(d / "stack.txt").encode(), str(d / "var.txt").encode(), None, 90.0, C.byref(g),
+                          None) == 0, L.gt_last_error()
+    maps = {}
+    for k in ("f_sp0", "g_sp0"):
+        f = C.c_void_p()
+        assert L.gt_greens_field(g, k.encode(), C.byref(f)) == 0
+        maps[k] = np.ctypeslib.as_array(L.gt_field_data(f), shape=(1024, 1024)).copy()
+        L.gt_field_free(f)
+    f_sp0 = maps["f_sp0"]
+    ga = GreensArrays(n=1024, pitch=0.016 / 1024, f_sp0=f_sp0, g_sp0=maps["g_sp0"],
+                      phi=float(np.mean(np.concatenate([f_sp0[0], f_sp0[-1], f_sp0[1:-1, 0], f_sp0[1:-1, -1]]))),
+                      kappa_inf=float(f_sp0[0, 0]), alpha=L.gt_greens_alpha(g), beta=0.017, mu=L.gt_greens_mu(g),
+                      rand_scale=1.0)
+    L.gt_greens_free(g)
+    return ga
+
+
+def test_config2_mc_matches_oracle(b200lib, oracle, greens1024):
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import DeviceGreens
+    cfg = inputs.CONFIGS["cfg2"]
+    p = inputs.power_batch(cfg, 0, 2, np.float32)
+    v = inputs.variation_batch(cfg, 0, 2).numpy().astype(np.float32)
+    t_ref, mx_ref, _, st_ref, secs = oracle.mc_batch(greens1024, p, v, jobs=2)
+    assert (st_ref == 0).all()
+    for prec, atol in ((1, 1e-8), (0, 1e-3)):
+        dg = DeviceGreens(greens1024, prec)
+        out, mx, _, st, _ = dg.mc_batch_host(p, v, dg.opts())
+        assert (st == 0).all(), st
+        err = np.abs(out.astype(np.float64) - t_ref).max()
+        print(f"n=1024 prec={prec}: max|dT| {err:.3e} K on peak {t_ref.max():.1f} K (oracle {secs:.1f} s)")
+        assert err <= atol
+
+
+def test_config2_fixed_point_kirchhoff(b200lib, oracle, greens1024):
+    """Mode B with the Kirchhoff transform (config 2's k(T) = k0 (T/300)^-1.3) at n = 1024, fp64."""
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import DeviceGreens
+    cfg = inputs.CONFIGS["cfg2"]
+    p = inputs.power_batch(cfg, 0, 1, np.float64) * 0.3
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=1, tol=1e-4, max_iters=60)
+    t_ref, it_ref, st_ref, secs = oracle.fixed_point_batch(greens1024, p, v, jobs=1, **kw)
+    assert st_ref[0] == 0
+    dg = DeviceGreens(greens1024, 1)
+    out, it, st, _, _ = dg.fp_batch_host(p, v, dg.fp_opts(**kw))
+    assert st[0] == 0
+    err = np.abs(out - t_ref).max()
+    print(f"n=1024 mode B Kirchhoff: iters {it[0]} vs {it_ref[0]}, max|dT| {err:.3e} K, peak {t_ref.max():.1f} K")
+    assert it[0] == it_ref[0]
+    assert err <= 1e-8
