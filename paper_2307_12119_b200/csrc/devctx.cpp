@@ -99,8 +99,9 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     d->fk_full.ensure(static_cast<size_t>(m) * m * 16);
     d->fk.ensure(static_cast<size_t>(m) * hp * cb);
     d->gtab.ensure(static_cast<size_t>(n + 1) * hp * rb);
+    d->fg.ensure(static_cast<size_t>(m) * hp * 4 * rb);
     cuda_ok(gtd_greens_tables(static_cast<const double*>(d->fsp0.p), static_cast<const double*>(d->gsp0.p),
-                              g.phi, n, hp, d->fp64, d->tw64.p, d->fk_full.p, d->fk.p, d->gtab.p, st),
+                              g.phi, n, hp, d->fp64, d->tw64.p, d->fk_full.p, d->fk.p, d->gtab.p, d->fg.p, st),
             "greens tables");
     cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
     d->d.n = n;
@@ -112,6 +113,7 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     d->d.gtab = d->gtab.p;
     d->d.k1 = d->k1.p;
     d->d.tw = d->tw.p;
+    d->d.fg = d->fg.p;
     d->d.alpha = g.alpha;
     d->d.beta = g.beta;
     d->d.rand_scale = g.rand_scale;

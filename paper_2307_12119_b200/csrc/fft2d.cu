@@ -145,6 +145,27 @@ __global__ void k_gtab(const double* __restrict__ g_sp0, int n, int hp, T* __res
     gt[du * hp + dv] = T(g_sp0[c * n + c] - 0.25 * s);
 }
 
+// Packed per-frequency table {fk.re, fk.im, g(du, v), 0} for the fused column pass.
+template <typename T>
+__global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g_sp0, int n, int hp, T* __restrict__ fg) {
+    const int m = 2 * n, u = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= hp) return;
+    T* o = fg + (static_cast<size_t>(u) * hp + v) * 4;
+    if (v > n) {
+        o[0] = o[1] = o[2] = o[3] = T(0);
+        return;
+    }
+    const double2 z = K[static_cast<size_t>(u) * m + v];
+    const int c = n / 2, du = u <= m - u ? u : m - u;
+    auto cl = [n](int i) { return i < 0 ? 0 : (i > n - 1 ? n - 1 : i); };
+    const int ip = cl(c + du), im = cl(c - du), jp = cl(c + v), jm = cl(c - v);
+    const double s = g_sp0[ip * n + jp] + g_sp0[ip * n + jm] + g_sp0[im * n + jp] + g_sp0[im * n + jm];
+    o[0] = T(z.x);
+    o[1] = T(z.y);
+    o[2] = T(g_sp0[c * n + c] - 0.25 * s);
+    o[3] = T(0);
+}
+
 }  // namespace gtb
 
 using namespace gtb;
@@ -160,7 +181,7 @@ int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, 
 // n x n fp64 maps; tw64_d: fp64 twiddles for m; work_d: m*m double2 that
 // receives the full fp64 baseline kernel spectrum fk (kept by the caller).
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
-                      int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out,
+                      int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out, void* fg_out,
                       cudaStream_t st) {
     const int m = 2 * n;
     double2* K = static_cast<double2*>(work_d);
@@ -174,11 +195,15 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
                                                                       static_cast<double2*>(fk_out));
         k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                           static_cast<double*>(gtab_out));
+        if (fg_out)
+            k_fg<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, static_cast<double*>(fg_out));
     } else {
         k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                      static_cast<float2*>(fk_out));
         k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                          static_cast<float*>(gtab_out));
+        if (fg_out)
+            k_fg<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, static_cast<float*>(fg_out));
     }
     return static_cast<int>(cudaGetLastError());
 }

@@ -128,6 +128,30 @@ __device__ __forceinline__ void dft8(cplx<T>* v) {
     v[7] = o[3];
 }
 
+// DFT8 of an input whose slots 2..5 are zero (never read): the first radix-2
+// layer degenerates to copies / negations.
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft8_outer_only(cplx<T>* v) {
+    const T r = T(0.70710678118654752440084436210485);
+    cplx<T> a0 = v[0], a4 = v[0], a1 = v[1], a5 = v[1];
+    cplx<T> a2 = v[6], a6 = mk<T>(-v[6].x, -v[6].y), a3 = v[7], a7 = mk<T>(-v[7].x, -v[7].y);
+    a5 = SIGN < 0 ? mk<T>((a5.x + a5.y) * r, (a5.y - a5.x) * r) : mk<T>((a5.x - a5.y) * r, (a5.y + a5.x) * r);
+    a6 = mul_si<SIGN, T>(a6);
+    a7 = SIGN < 0 ? mk<T>((a7.y - a7.x) * r, -(a7.x + a7.y) * r) : mk<T>(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);
+    cplx<T> e[4] = {a0, a1, a2, a3};
+    cplx<T> o[4] = {a4, a5, a6, a7};
+    dft4<SIGN, T>(e);
+    dft4<SIGN, T>(o);
+    v[0] = e[0];
+    v[2] = e[1];
+    v[4] = e[2];
+    v[6] = e[3];
+    v[1] = o[0];
+    v[3] = o[1];
+    v[5] = o[2];
+    v[7] = o[3];
+}
+
 template <int R, int SIGN, typename T>
 __device__ __forceinline__ void dftR(cplx<T>* v) {
     if constexpr (R == 8)

@@ -42,6 +42,7 @@ typedef struct gtd_greens {
     void* gtab;           /* [(n+1)][hp] real: alpha multiplier g(du,dv) (C6)   */
     void* k1;             /* [m] complex: 1-D spectrum of the centred die box  */
     void* tw;             /* [m] complex: exp(-2 pi i t/m)                     */
+    void* fg;             /* [m][hp] {fk.re, fk.im, g(du,v), 0}: one vector load per frequency */
     double alpha, beta, rand_scale, mu_fixed;
 } gtd_greens;
 
@@ -95,7 +96,7 @@ int gtd_padded_width(int n, int fp64);
 int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, cudaStream_t st);
 /* GreensSet device tables from fp64 f_sp0 / g_sp0 (device n x n maps). */
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
-                      int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out,
+                      int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out, void* fg_out,
                       cudaStream_t st);
 #ifdef __cplusplus
 }

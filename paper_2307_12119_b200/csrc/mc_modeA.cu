@@ -231,11 +231,21 @@ mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 // ------------------------------------------------------------------ pass 2
 // Closed forms at one frequency (u, v): returns Y = F_det A and R = F_rand
 // (greens.cpp:203-251) with one shared reciprocal; sets runaway flags.
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+    using type = float4;
+};
+template <>
+struct Vec4<double> {
+    using type = double4;
+};
+
 template <typename T, int M>
 struct ClosedForm {
     static constexpr int n = M / 2, c = n / 2, hp = MCGeom<T, M>::hp, W = MCGeom<T, M>::W;
-    const cplx<T>* __restrict__ fk;
-    const T* __restrict__ gtab;
+    const typename Vec4<T>::type* __restrict__ fg;  // {fk.re, fk.im, g, 0} per (u, v)
     const cplx<T>* __restrict__ k1;
     const T* s_srow;  // [n][W] row-symmetrised leakage of this column tile
     T alpha, beta, mu_g, mus, qshift;
@@ -244,8 +254,9 @@ struct ClosedForm {
         const int du = u <= M - u ? u : M - u;
         const cplx<T> K = cmul<T>(k1[u], k1[v]);
         const cplx<T> Bp = mk<T>(b.x - mus * K.x, b.y - mus * K.y);  // F(p_var) = F(p_leak0) - mu k1 k1
-        const cplx<T> f = fk[static_cast<size_t>(u) * hp + v];
-        const T g = gtab[du * hp + v];
+        const typename Vec4<T>::type t4 = fg[static_cast<size_t>(u) * hp + v];
+        const cplx<T> f = mk<T>(t4.x, t4.y);
+        const T g = t4.z;
         const int ip = min(c + du, n - 1), im = max(c - du, 0);
         const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
         const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
@@ -275,8 +286,8 @@ __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
 mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
          gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
-         const cplx<T>* __restrict__ fk, const T* __restrict__ gtab,
-         const cplx<T>* __restrict__ k1, T alpha, T beta, int mu_per_sample, T mu_fixed) {
+         const T* __restrict__ fgtab, const cplx<T>* __restrict__ k1, T alpha, T beta, int mu_per_sample,
+         T mu_fixed) {
     using Gm = MCGeom<T, M>;
     using Pl = Plan<M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT, W = Gm::W;
@@ -317,7 +328,8 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
                 const int xa = i < n ? i : M - 1 - i;       // mirror_pad
                 const int xb = (i + c) & (M - 1);           // centre_kernel: row i holds die row x
                 va[b][r] = Aspec[sbase + static_cast<size_t>(xa) * hp + v];
-                vb[b][r] = xb < n ? Bspec[sbase + static_cast<size_t>(xb) * hp + v] : mk<T>(T(0), T(0));
+                // the centre embedding fills rows [0, M/4) u [3M/4, M): r in {0,1,6,7} only
+                if (r < 2 || r >= 6) vb[b][r] = Bspec[sbase + static_cast<size_t>(xb) * hp + v];
             }
         }
         // S rows into registers now, into shared memory after the stage-0 math (latency overlap)
@@ -333,7 +345,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             const int id = threadIdx.x + b * NT;
             const int lp = id % W, j = id / W;
             dftR<8, -1, T>(va[b]);
-            dftR<8, -1, T>(vb[b]);
+            dft8_outer_only<-1, T>(vb[b]);
             pair_store<T, M, L, 8, 1>(tile, j, lp, va[b], vb[b]);
         }
 #pragma unroll
@@ -347,8 +359,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
         const T* Nm = in.nn(sg);
         const T* V = in.v(sg);
         ClosedForm<T, M> cf;
-        cf.fk = fk;
-        cf.gtab = gtab;
+        cf.fg = reinterpret_cast<const typename Vec4<T>::type*>(fgtab);
         cf.k1 = k1;
         cf.s_srow = s_srow;
         cf.alpha = alpha;
@@ -785,9 +796,9 @@ struct MCLaunch {
                 mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
                                                                              var_lo, var_hi);
             if (mark) mark(ctx, 1, st);
-            mc_pass2<T, M><<<grid(cnt * CT, res[1]), NT, smem2(), st>>>(in, s0, cnt, A, B, S, stats, tw, fk, gt,
-                                                                         k1, T(g->alpha), T(g->beta),
-                                                                         o->mu_per_sample, T(g->mu_fixed));
+            mc_pass2<T, M><<<grid(cnt * CT, res[1]), NT, smem2(), st>>>(
+                in, s0, cnt, A, B, S, stats, tw, static_cast<const T*>(g->fg), k1, T(g->alpha), T(g->beta),
+                o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
             if constexpr (use_warp_rows<T, M>())
                 mc_pass3w<T, M><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32, smemw3(), st>>>(
