@@ -133,7 +133,10 @@ def bind(cdll: C.CDLL, extension: bool = True) -> C.CDLL:
 
 
 def library_path() -> Path:
-    return _HERE / _LIBNAME
+    # GT_B200_LIB selects an in-tree tuning variant built by ``build.py --variant``.
+    import os
+    alt = os.environ.get("GT_B200_LIB")
+    return Path(alt) if alt else _HERE / _LIBNAME
 
 
 _LIB: C.CDLL | None = None

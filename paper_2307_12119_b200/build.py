@@ -52,11 +52,11 @@ def _headers() -> list[Path]:
                   + list(INCLUDE.glob("*.h")))
 
 
-def _compile(src: Path, nvcc: str, hdr_mtime: float) -> Path:
-    obj = BUILD / (src.name + ".o")
+def _compile(src: Path, nvcc: str, hdr_mtime: float, objdir: Path = BUILD, extra: tuple = ()) -> Path:
+    obj = objdir / (src.name + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    flags = (ARCH + CU_FLAGS) if src.suffix == ".cu" else CXX_FLAGS
+    flags = (ARCH + CU_FLAGS + list(extra)) if src.suffix == ".cu" else CXX_FLAGS
     cmd = [nvcc, *_host_compiler(), *flags, "-I", str(CSRC), "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -64,27 +64,37 @@ def _compile(src: Path, nvcc: str, hdr_mtime: float) -> Path:
     return obj
 
 
-def build(verbose: bool = False) -> Path:
+def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) -> Path:
+    """Build the library; ``variant`` + ``extra`` nvcc defines build a tuning
+    variant to ``variants/libgreentherm_b200_<variant>.so`` (selected at run
+    time with GT_B200_LIB) without touching the product library."""
     nvcc = _nvcc()
-    BUILD.mkdir(parents=True, exist_ok=True)
+    objdir = BUILD if variant is None else BUILD.parent / f"obj_{variant}"
+    lib = LIB if variant is None else PKG / f"libgreentherm_b200_v{variant}.so"
+    objdir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     hdr_mtime = max(p.stat().st_mtime for p in _headers())
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, nvcc, hdr_mtime), srcs))
+        objs = list(ex.map(lambda s: _compile(s, nvcc, hdr_mtime, objdir, extra), srcs))
     newest = max(o.stat().st_mtime for o in objs)
-    if LIB.exists() and LIB.stat().st_mtime >= newest:
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+    if lib.exists() and lib.stat().st_mtime >= newest:
+        return lib
+    LIB_ = lib
+    tmp = LIB_.with_suffix(".so.tmp")
     cmd = [nvcc, *_host_compiler(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, LIB_)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {LIB_}")
+    return LIB_
 
 
 if __name__ == "__main__":
-    build(verbose=True)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        build(verbose=True, variant=sys.argv[2], extra=tuple(sys.argv[3:]))
+    else:
+        build(verbose=True)
     sys.exit(0)

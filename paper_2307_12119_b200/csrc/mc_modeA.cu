@@ -117,6 +117,17 @@ struct MCGeom {
     static constexpr int hp = ((h + W - 1) / W) * W;
     static constexpr int LP = L + 2;  // padded pitch for row tiles (transposing I/O; even for pairs)
     static constexpr int SP = n + 1;  // padded pitch of the row staging arrays
+    // pass 2 threads: GT_P2_NT caps the CTA (more butterflies per thread, more
+    // registers each); the register budget still targets P2_CTAS CTAs per SM
+#ifndef GT_P2_NT
+#define GT_P2_NT 256
+#endif
+#ifndef GT_P2_CTAS
+#define GT_P2_CTAS 2
+#endif
+    static constexpr int NT2 = NT > GT_P2_NT ? GT_P2_NT : NT;
+    static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
+    static constexpr int MINB2 = NT2 == NT ? G::MINB : GT_P2_CTAS;
 };
 
 // ------------------------------------------------------------------ pass 1
@@ -282,7 +293,7 @@ struct ClosedForm {
 // kept rows straight back: 4 shared-memory round trips per column pair
 // instead of 8, and no separate load / algebra / store phases.
 template <typename T, int M>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+__global__ void __launch_bounds__(MCGeom<T, M>::NT2, MCGeom<T, M>::MINB2)
 mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
          gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
@@ -290,7 +301,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
          T mu_fixed) {
     using Gm = MCGeom<T, M>;
     using Pl = Plan<M>;
-    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT, W = Gm::W;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT2, W = Gm::W;
     constexpr int hp = Gm::hp;
     constexpr int CT = hp / W;
     constexpr int K = Pl::K;
@@ -528,15 +539,27 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
 // Row passes for M = 128 / 256 / 512: each warp owns one die row at a time,
 // loads and stores it coalesced straight from / to registers and transforms it
 // with the one-warp FFT (fft_warp.cuh): no CTA barriers, no transposing tile.
-constexpr int WARPS = 16;   // warps per CTA of the warp-per-row pass 1
-constexpr int WARPS3 = 12;  // pass 3 holds more live state: 12 warps x 2 CTAs at <= 85 registers
-template <typename T>
+#ifndef GT_W1
+#define GT_W1 16
+#endif
+#ifndef GT_W3
+#define GT_W3 8
+#endif
+#ifndef GT_W1_CTAS
+#define GT_W1_CTAS 2
+#endif
+#ifndef GT_W3_CTAS
+#define GT_W3_CTAS 2
+#endif
+constexpr int WARPS = GT_W1;   // warps per CTA of the warp-per-row pass 1
+constexpr int WARPS3 = GT_W3;  // pass 3 holds more live state: 8 warps x 2 CTAs at 128 registers
+template <typename T, int CTAS>
 struct WarpMinBlocks {
-    static constexpr int value = sizeof(T) == 8 ? 1 : 2;  // fp64 lines need 128 registers
+    static constexpr int value = sizeof(T) == 8 ? 1 : CTAS;  // fp64 lines need 128 registers
 };
 
 template <typename T, int M>
-__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T>::value)
+__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T, GT_W1_CTAS>::value)
 mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
           cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
           const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
@@ -634,7 +657,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 }
 
 template <typename T, int M>
-__global__ void __launch_bounds__(WARPS3 * 32, WarpMinBlocks<T>::value)
+__global__ void __launch_bounds__(WARPS3 * 32, WarpMinBlocks<T, GT_W3_CTAS>::value)
 mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
           const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
           const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
@@ -762,7 +785,7 @@ struct MCLaunch {
             cudaFuncSetAttribute(mc_pass2<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
             cudaFuncSetAttribute(mc_pass3<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem3()));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1<T, M>, NT, smem1());
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, NT, smem2());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, Gm::NT2, smem2());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3<T, M>, NT, smem3());
             if constexpr (use_warp_rows<T, M>()) {
                 cudaFuncSetAttribute(mc_pass1w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
@@ -796,7 +819,7 @@ struct MCLaunch {
                 mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
                                                                              var_lo, var_hi);
             if (mark) mark(ctx, 1, st);
-            mc_pass2<T, M><<<grid(cnt * CT, res[1]), NT, smem2(), st>>>(
+            mc_pass2<T, M><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), st>>>(
                 in, s0, cnt, A, B, S, stats, tw, static_cast<const T*>(g->fg), k1, T(g->alpha), T(g->beta),
                 o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
