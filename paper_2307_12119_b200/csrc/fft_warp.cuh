@@ -110,8 +110,17 @@ struct WarpFFT {
             if (SIGN > 0) w.y = -w.y;
             v[m1] = cmul<T>(v[m1], w);
         }
-        // Q-point DFT across the lanes kq + P h' (direct form: lane h keeps output g = h)
-        if constexpr (Q > 1) {
+        // Q-point DFT across the lanes kq + P h' (lane h keeps output g = h)
+        if constexpr (Q == 2) {
+            // radix-2 butterfly with the partner lane: g = 0 -> v0 + v1, g = 1 -> v0 - v1
+            const T sg = h ? T(-1) : T(1);
+#pragma unroll
+            for (int m1 = 0; m1 < P; ++m1) {
+                const cplx<T> z = shfl_c<T>(v[m1], lane ^ P);
+                v[m1] = mk<T>(fma(sg, v[m1].x, z.x), fma(sg, v[m1].y, z.y));
+            }
+        } else if constexpr (Q > 1) {
+            // direct form
 #pragma unroll
             for (int m1 = 0; m1 < P; ++m1) {
                 // own term h' = h carries w_Q^{h h}

@@ -36,6 +36,14 @@ namespace gtb {
 
 template <typename T>
 struct Real;
+template <>
+struct Real<float> {
+    static constexpr float max() { return 3.402823466e38f; }
+};
+template <>
+struct Real<double> {
+    static constexpr double max() { return 1.7976931348623157e308; }
+};
 
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
@@ -596,7 +604,9 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 #pragma unroll
         for (int t = 0; t < E; ++t) {
             const int y = lane + 32 * t;
-            if (!(pv[t] >= T(0)) || !finite_(pv[t]) || !(nv[t] >= T(0)) || !finite_(nv[t])) bad |= GTD_ST_BAD_POWER;
+            // NaN fails both compares, +-inf fails one: same verdict as !(x >= 0) || !isfinite(x)
+            if (!(pv[t] >= T(0) && pv[t] <= Real<T>::max()) || !(nv[t] >= T(0) && nv[t] <= Real<T>::max()))
+                bad |= GTD_ST_BAD_POWER;
             if (!(vv[t] >= var_lo && vv[t] <= var_hi)) bad |= GTD_ST_BAD_VAR;
             const T lk = in.nom_scale * nv[t] * vv[t];
             const T a = pv[t] + lk;
