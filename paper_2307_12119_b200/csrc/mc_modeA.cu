@@ -265,7 +265,7 @@ template <typename T, int M>
 struct ClosedForm {
     static constexpr int n = M / 2, c = n / 2, hp = MCGeom<T, M>::hp, W = MCGeom<T, M>::W;
     const typename Vec4<T>::type* __restrict__ fg;  // {fk.re, fk.im, g, 0} per (u, v)
-    const cplx<T>* __restrict__ k1;
+    const cplx<T>* k1;  // shared-memory copy of the die-box spectrum
     const T* s_srow;  // [n][W] row-symmetrised leakage of this column tile
     T alpha, beta, mu_g, mus, qshift;
 
@@ -324,9 +324,11 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + M * L;
-    T* s_srow = reinterpret_cast<T*>(s_tw + M);
+    cplx<T>* s_k1 = s_tw + M;
+    T* s_srow = reinterpret_cast<T*>(s_k1 + M);
 
     load_twiddles<T, M, NT>(s_tw, g_tw);
+    load_twiddles<T, M, NT>(s_k1, k1);
     for (int item = blockIdx.x; item < count * CT; item += gridDim.x) {
         const int s = item / CT;
         const int v0 = (item - s * CT) * W;
@@ -379,7 +381,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
         const T* V = in.v(sg);
         ClosedForm<T, M> cf;
         cf.fg = reinterpret_cast<const typename Vec4<T>::type*>(fgtab);
-        cf.k1 = k1;
+        cf.k1 = s_k1;
         cf.s_srow = s_srow;
         cf.alpha = alpha;
         cf.beta = beta;
@@ -768,7 +770,7 @@ template <typename T, int M>
 struct MCLaunch {
     using Gm = MCGeom<T, M>;
     static size_t smem1() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
-    static size_t smem2() { return sizeof(cplx<T>) * (M * Gm::L + M) + sizeof(T) * Gm::n * Gm::W; }
+    static size_t smem2() { return sizeof(cplx<T>) * (M * Gm::L + 2 * M) + sizeof(T) * Gm::n * Gm::W; }
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
     static size_t smemw() {
         if constexpr (use_warp_rows<T, M>())
