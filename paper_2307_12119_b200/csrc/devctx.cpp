@@ -37,6 +37,17 @@ std::vector<double> twiddles(int m) {
     return t;
 }
 
+// hs[t] = exp(-i pi t / m): half-step twiddles (w^{t/2}, w = exp(-2 pi i / m)).
+std::vector<double> half_twiddles(int m) {
+    std::vector<double> t(2 * static_cast<size_t>(m));
+    for (int k = 0; k < m; ++k) {
+        const double a = -M_PI * static_cast<double>(k) / m;
+        t[2 * k] = std::cos(a);
+        t[2 * k + 1] = std::sin(a);
+    }
+    return t;
+}
+
 // k1[u] = sum_{x<n} exp(-2 pi i u (x - c) / m): spectrum of the centred die box.
 std::vector<double> box_spectrum(int n) {
     const int m = 2 * n, c = n / 2;
@@ -83,15 +94,17 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     const size_t cb = d->fp64 ? 16 : 8, rb = d->fp64 ? 8 : 4;
     cudaStream_t st = d->stream;
 
-    const std::vector<double> tw = twiddles(m), k1 = box_spectrum(n);
+    const std::vector<double> tw = twiddles(m), k1 = box_spectrum(n), hs = half_twiddles(m);
     upload(d->tw64, tw.data(), tw.size() * 8, st);
     if (d->fp64) {
         upload(d->tw, tw.data(), tw.size() * 8, st);
         upload(d->k1, k1.data(), k1.size() * 8, st);
+        upload(d->hs, hs.data(), hs.size() * 8, st);
     } else {
-        auto twf = narrow<float>(tw), k1f = narrow<float>(k1);
+        auto twf = narrow<float>(tw), k1f = narrow<float>(k1), hsf = narrow<float>(hs);
         upload(d->tw, twf.data(), twf.size() * 4, st);
         upload(d->k1, k1f.data(), k1f.size() * 4, st);
+        upload(d->hs, hsf.data(), hsf.size() * 4, st);
         cuda_ok(cudaStreamSynchronize(st), "sync");
     }
     upload(d->fsp0, g.f_sp0.v.data(), g.f_sp0.v.size() * 8, st);
@@ -114,6 +127,7 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     d->d.k1 = d->k1.p;
     d->d.tw = d->tw.p;
     d->d.fg = d->fg.p;
+    d->d.hs = d->hs.p;
     d->d.alpha = g.alpha;
     d->d.beta = g.beta;
     d->d.rand_scale = g.rand_scale;

@@ -53,7 +53,7 @@ struct gt_device_greens {
     gtd_greens d{};
     gth::Greens host;  // copy of the set the tables were built from
     cudaStream_t stream = nullptr;
-    gth::DBuf fg, fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
+    gth::DBuf hs, fg, fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
     // batch scratch (guarded by mu)
     std::mutex mu;
     gth::DBuf fp_scratch, fp_state, fp_counter;

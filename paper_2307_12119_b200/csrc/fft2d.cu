@@ -163,7 +163,9 @@ __global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g
     o[0] = T(z.x);
     o[1] = T(z.y);
     o[2] = T(g_sp0[c * n + c] - 0.25 * s);
-    o[3] = T(0);
+    // die-box spectrum k1[u] k1[v] = conj(w^{u/2} w^{v/2}) D(u) D(v), D(u) = sin(pi u/2) / sin(pi u/m)
+    auto D = [n, m](int t) { return t == 0 ? double(n) : sinpi(0.5 * t) / sinpi(double(t) / m); };
+    o[3] = T(D(u) * D(v));
 }
 
 }  // namespace gtb

@@ -42,6 +42,7 @@ typedef struct gtd_greens {
     void* gtab;           /* [(n+1)][hp] real: alpha multiplier g(du,dv) (C6)   */
     void* k1;             /* [m] complex: 1-D spectrum of the centred die box  */
     void* tw;             /* [m] complex: exp(-2 pi i t/m)                     */
+    void* hs;             /* [m] complex: exp(-i pi t/m) (half-step twiddles)    */
     void* fg;             /* [m][hp] {fk.re, fk.im, g(du,v), 0}: one vector load per frequency */
     double alpha, beta, rand_scale, mu_fixed;
 } gtd_greens;

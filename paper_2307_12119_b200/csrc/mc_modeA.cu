@@ -130,22 +130,35 @@ struct MCGeom {
 #ifndef GT_P2_NT
 #define GT_P2_NT 256
 #endif
+#ifndef GT_P2_TILE_MAJOR
+#define GT_P2_TILE_MAJOR 0
+#endif
 #ifndef GT_P2_CTAS
 #define GT_P2_CTAS 2
 #endif
     static constexpr int NT2 = NT > GT_P2_NT ? GT_P2_NT : NT;
     static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
-    static constexpr int MINB2 = NT2 == NT ? G::MINB : GT_P2_CTAS;
+    // pass 2 holds three lines per thread-butterfly: 128 registers (fp32) / 255 (fp64)
+    static constexpr int MINB2 = sizeof(T) == 8 ? 1 : ((512 / NT2) < 1 ? 1 : (512 / NT2));
 };
 
 // ------------------------------------------------------------------ pass 1
+// The applied map enters the row transform mirror-padded, so its half spectrum
+// is A[v] = w^{-v/2} At[v] with At real (the DCT-II of the row; w = e^{-2 pi i/M}).
+// Pass 1 stores only At = Re(w^{v/2} A), A = (Z[v] + conj Z[M-v]) / 2, with
+// hs[v] = w^{v/2}; At[n] = 0 exactly.
+template <typename T>
+__device__ __forceinline__ T dct_part(cplx<T> Z, cplx<T> Zc, cplx<T> hs) {
+    return T(0.5) * ((Z.x + Zc.x) * hs.x - (Z.y + Zc.y) * hs.y);
+}
+
 // Persistent over (sample, block of L die rows). Each die row x becomes one
 // complex line z = mirror(applied row) + i * centre-embedded(p_leak0 row).
 template <typename T, int M>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
-mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
+mc_pass1(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
          cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
-         const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
+         const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T var_lo, T var_hi) {
     using Gm = MCGeom<T, M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
     constexpr int hp = Gm::hp;
@@ -231,16 +244,17 @@ mc_pass1(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             const int l = idx / hp, v = idx - l * hp;
             const int x = x0 + l;
             if (x >= n) continue;
-            cplx<T> A = mk<T>(T(0), T(0)), B = A;
+            T Ar = T(0);
+            cplx<T> B = mk<T>(T(0), T(0));
             if (v < h) {
                 const cplx<T> Z = tile[v * LP + l];
                 const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
-                A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
+                if (v < n) Ar = dct_part<T>(Z, Zc, g_hs[v]);
                 const T dx = Z.x - Zc.x, dy = Z.y - Zc.y;
                 B = mk<T>(T(0.5) * dy, T(-0.5) * dx);
             }
             const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
-            Aspec[o] = A;
+            Areal[o] = Ar;
             Bspec[o] = B;
         }
         __syncthreads();
@@ -264,48 +278,250 @@ struct Vec4<double> {
 template <typename T, int M>
 struct ClosedForm {
     static constexpr int n = M / 2, c = n / 2, hp = MCGeom<T, M>::hp, W = MCGeom<T, M>::W;
-    const typename Vec4<T>::type* __restrict__ fg;  // {fk.re, fk.im, g, 0} per (u, v)
-    const cplx<T>* k1;  // shared-memory copy of the die-box spectrum
+    const typename Vec4<T>::type* __restrict__ fg;  // {fk.re, fk.im, g, D(u) D(v)} per (u, v)
     const T* s_srow;  // [n][W] row-symmetrised leakage of this column tile
     T alpha, beta, mu_g, mus, qshift;
 
-    __device__ __forceinline__ void eval(cplx<T>& a, cplx<T>& b, int u, int v, int w, int& flags) const {
+    // At frequency (u, v): A_hat = ph C (ph = conj(w^{u/2} w^{v/2}), C the real
+    // 2-D DCT coefficient), b = F(p_leak0) on entry; returns Y = F_det A_hat
+    // and leaves R = F_rand in b. K1 = k1 (x) k1 = ph D(u) D(v).
+    __device__ __forceinline__ typename Vec4<T>::type table(int u, int v) const {
+        return fg[static_cast<size_t>(u) * hp + v];
+    }
+    __device__ __forceinline__ cplx<T> eval(T C, cplx<T>& b, cplx<T> ph, const typename Vec4<T>::type& t4, int u,
+                                            int v, int w, int& flags) const {
         const int du = u <= M - u ? u : M - u;
-        const cplx<T> K = cmul<T>(k1[u], k1[v]);
-        const cplx<T> Bp = mk<T>(b.x - mus * K.x, b.y - mus * K.y);  // F(p_var) = F(p_leak0) - mu k1 k1
-        const typename Vec4<T>::type t4 = fg[static_cast<size_t>(u) * hp + v];
         const cplx<T> f = mk<T>(t4.x, t4.y);
-        const T g = t4.z;
+        const T g = t4.z, mk1 = mus * t4.w;
+        const cplx<T> Bp = mk<T>(b.x - mk1 * ph.x, b.y - mk1 * ph.y);  // F(p_var) = F(p_leak0) - mu K1
         const int ip = min(c + du, n - 1), im = max(c - du, 0);
         const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
         const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
         const T a1 = T(1) - alpha * g * (T(1) + fmu);
         const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
         const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
-        const cplx<T> den2 = mk<T>(den1.x - alpha * g * Bp.x - beta * q * f.x, den1.y - alpha * g * Bp.y - beta * q * f.y);
+        const cplx<T> den2 = mk<T>(den1.x - t1.x, den1.y - t1.y);
         const T d1 = cabs2<T>(den1), d2 = cabs2<T>(den2);
         if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
         if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
         const T rinv = fast_rcp(d1 * d2);
         const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));
-        a = cscale<T>(cmul<T>(fc1, a), d2 * rinv);
         b = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
+        return cscale<T>(cmul<T>(fc1, ph), C * d2 * rinv);
     }
 };
 
-// Persistent over (sample, tile of W half-spectrum columns). Lines 2w / 2w+1
-// are the A / B columns v0+w, processed as a pair by one thread. The first
-// forward stage reads straight from the row spectra (mirror / centre
-// expansion in the address), the last forward stage, the closed forms and the
-// first inverse stage run in registers, and the last inverse stage writes the
-// kept rows straight back: 4 shared-memory round trips per column pair
-// instead of 8, and no separate load / algebra / store phases.
+// Per-stage twiddle tables, r-major: entry off(s) + (r-1) NS + k holds the
+// stage-s twiddle w_M^{k r M/(NS R)} (conjugated for the inverse plan). The
+// k = j mod NS of a warp's butterflies are consecutive, so a warp's twiddle
+// loads for one r hit consecutive words -- the flat table's k*r stride makes
+// them bank conflicts.
+template <int M, bool INV>
+struct StageTw {
+    using Pl = Plan<M>;
+    __host__ __device__ static constexpr int R(int s) { return INV ? Pl::ir(s) : Pl::fr(s); }
+    __host__ __device__ static constexpr int NS(int s) { return INV ? Pl::ins(s) : Pl::fns(s); }
+    __host__ __device__ static constexpr int off(int s) { return s == 0 ? 0 : off(s - 1) + (R(s - 1) - 1) * NS(s - 1); }
+    static constexpr int SIZE = off(Pl::K);
+};
+
+template <typename T, int M, bool INV, int NT>
+__device__ __forceinline__ void build_stage_tw(cplx<T>* dst, const cplx<T>* tw) {
+    using ST = StageTw<M, INV>;
+    for (int idx = threadIdx.x; idx < ST::SIZE; idx += NT) {
+        int s = 0;
+#pragma unroll
+        for (int t = 1; t < Plan<M>::K; ++t)
+            if (idx >= ST::off(t)) s = t;
+        const int R = ST::R(s), NS = ST::NS(s);
+        const int rel = idx - ST::off(s);
+        const int r = 1 + rel / NS, k = rel % NS;
+        cplx<T> w = tw[(k * r * (M / (NS * R))) & (M - 1)];
+        if (INV) w.y = -w.y;
+        dst[idx] = w;
+    }
+}
+
+// Stage twiddles for butterfly j of stage S: v[r] *= tws[off + (r-1) NS + j mod NS].
+template <typename T, int M, bool INV, int S, int NL>
+__device__ __forceinline__ void stage_twiddle(cplx<T> (*v)[StageTw<M, INV>::R(S)], int j, const cplx<T>* tws) {
+    using ST = StageTw<M, INV>;
+    constexpr int R = ST::R(S), NS = ST::NS(S);
+    if constexpr (NS > 1) {
+        const int k = j % NS;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            const cplx<T> w = tws[ST::off(S) + (r - 1) * NS + k];
+#pragma unroll
+            for (int l = 0; l < NL; ++l) v[l][r] = cmul<T>(v[l][r], w);
+        }
+    }
+}
+
+// Pass-2 tile layouts. Both insert padding every 8 rows so that a warp's
+// stride-8 row accesses (the Stockham stores, the fused stage's first inverse
+// stores) land in different banks; the padding is a function of row >> 3, so
+// for row = base + r S (S a multiple of 8, or S = 1 inside one 8-row block)
+// the physical offset is base_offset + r * const and folds into immediates.
+//
+// Forward phase: the tile's W columns form GA = max(1, W/2) groups; group g
+// holds columns v0 + g and v0 + g + GA and three lines: the packed A line
+// z = At_v + i At_{v+GA} (both columns' real DCT parts, pass 1) in plane PA,
+// and the two B lines as one LinePair in plane PB; one pad row per 8 rows.
+// S == 1 requires base and base + r in one 8-row block (the callers' rows j RL + r, RL | 8).
+template <int S>
+__device__ __forceinline__ int prow(int base, int r) {
+    if constexpr (S % 8 == 0 || S == 1) {
+        return base + (base >> 3) + r * (S % 8 == 0 ? S + S / 8 : 1);
+    } else {
+        const int row = base + r * S;
+        return row + (row >> 3);
+    }
+}
+template <typename T, int GA, int M>
+struct FwdLayout {
+    static constexpr int ROWS = M + M / 8;
+    static constexpr int PA_OFF = 2 * ROWS * GA;  // PB first (16-B aligned pairs), then PA
+    static constexpr int SIZE = 3 * ROWS * GA;
+    __device__ __forceinline__ static int pa(int prow_, int g) { return PA_OFF + prow_ * GA + g; }
+    __device__ __forceinline__ static int pb(int prow_, int g) { return (prow_ * GA + g) * 2; }
+};
+
+// Inverse phase: pairs (Y_w, R_w) of column v0 + w, W pairs per row, half a
+// row of padding per 8 rows (the fused stage writes half-rows at stride 8).
+template <int W, int M>
+struct InvLayout {
+    static constexpr int PITCH = 2 * W;
+    static constexpr int PADI = W >= 2 ? W : 2;
+    static constexpr int SIZE = M * PITCH + (M / 8) * PADI;
+    template <int S>
+    __device__ __forceinline__ static int off(int base, int r, int w) {
+        if constexpr (S % 8 == 0 || S == 1) {
+            return base * PITCH + (base >> 3) * PADI + 2 * w + r * (S * PITCH + (S % 8 == 0 ? (S / 8) * PADI : 0));
+        } else {
+            const int row = base + r * S;
+            return row * PITCH + (row >> 3) * PADI + 2 * w;
+        }
+    }
+};
+
+// One forward Stockham stage over the (A, B, B') line groups of the tile.
+template <typename T, int M, int GA, int NT, int S>
+__device__ __forceinline__ void fwd_stage_ab(cplx<T>* tile, const cplx<T>* twf) {
+    using FL = FwdLayout<T, GA, M>;
+    using ST = StageTw<M, false>;
+    constexpr int R = ST::R(S), NS = ST::NS(S);
+    constexpr int NB = (M / R) * GA;
+    constexpr int BPT = (NB + NT - 1) / NT;
+    cplx<T> v[BPT][3][R];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        if (NB % NT != 0 && id >= NB) break;
+        const int g = id % GA, j = id / GA;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pr = prow<M / R>(j, r);
+            v[b][0][r] = tile[FL::pa(pr, g)];
+            const LinePair<T> q = ld_pair(&tile[FL::pb(pr, g)]);
+            v[b][1][r] = q.a;
+            v[b][2][r] = q.b;
+        }
+        stage_twiddle<T, M, false, S, 3>(v[b], j, twf);
+#pragma unroll
+        for (int l = 0; l < 3; ++l) dftR<R, -1, T>(v[b][l]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        if (NB % NT != 0 && id >= NB) break;
+        const int g = id % GA, j = id / GA;
+        const int k = j % NS;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pr = prow<NS>(base, r);
+            tile[FL::pa(pr, g)] = v[b][0][r];
+            st_pair(&tile[FL::pb(pr, g)], LinePair<T>{v[b][1][r], v[b][2][r]});
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T, int M, int GA, int NT, int S, int E>
+struct FwdStagesAB {
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* twf) {
+        if constexpr (S < E) {
+            fwd_stage_ab<T, M, GA, NT, S>(tile, twf);
+            FwdStagesAB<T, M, GA, NT, S + 1, E>::run(tile, twf);
+        }
+    }
+};
+
+// One inverse Stockham stage over the (Y, R) column pairs (swizzled layout).
+template <typename T, int M, int W, int NT, int S>
+__device__ __forceinline__ void inv_stage_pairs(cplx<T>* tile, const cplx<T>* twi) {
+    using ST = StageTw<M, true>;
+    constexpr int R = ST::R(S), NS = ST::NS(S);
+    constexpr int NB = (M / R) * W;
+    static_assert(NB % NT == 0, "pair butterflies must divide evenly over threads");
+    constexpr int BPT = NB / NT;
+    cplx<T> v[BPT][2][R];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int w = id % W, j = id / W;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const LinePair<T> q = ld_pair(&tile[InvLayout<W, M>::template off<M / R>(j, r, w)]);
+            v[b][0][r] = q.a;
+            v[b][1][r] = q.b;
+        }
+        stage_twiddle<T, M, true, S, 2>(v[b], j, twi);
+        dftR<R, +1, T>(v[b][0]);
+        dftR<R, +1, T>(v[b][1]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        const int w = id % W, j = id / W;
+        const int k = j % NS;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            st_pair(&tile[InvLayout<W, M>::template off<NS>(base, r, w)], LinePair<T>{v[b][0][r], v[b][1][r]});
+    }
+    __syncthreads();
+}
+
+template <typename T, int M, int W, int NT, int S, int E>
+struct InvStagesPairs {
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* twi) {
+        if constexpr (S < E) {
+            inv_stage_pairs<T, M, W, NT, S>(tile, twi);
+            InvStagesPairs<T, M, W, NT, S + 1, E>::run(tile, twi);
+        }
+    }
+};
+
+// Persistent over (sample, tile of W half-spectrum columns).
+//   forward: per column group one packed A line (two columns' real DCT parts:
+//            the mirrored column of a real DCT row spectrum is again a DCT, so
+//            the column transform of At_v + i At_v' separates locally:
+//            C_v + i C_v' = w^{u/2} Z[u], A_hat_v = w^{-(u+v)/2} C_v) plus the
+//            two B lines -- 3 lines per 2 columns instead of 4;
+//   stage 0 reads straight from the row spectra (mirror / centre expansion in
+//   the address; the centre embedding leaves half the B inputs zero), the last
+//   forward stage, the closed forms and the first inverse stage run in
+//   registers, and the last inverse stage writes the kept rows to global.
 template <typename T, int M>
 __global__ void __launch_bounds__(MCGeom<T, M>::NT2, MCGeom<T, M>::MINB2)
-mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
-         cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
+mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
+         cplx<T>* __restrict__ Yspec, cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
          gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
-         const T* __restrict__ fgtab, const cplx<T>* __restrict__ k1, T alpha, T beta, int mu_per_sample,
+         const cplx<T>* __restrict__ g_hs, const T* __restrict__ fgtab, T alpha, T beta, int mu_per_sample,
          T mu_fixed) {
     using Gm = MCGeom<T, M>;
     using Pl = Plan<M>;
@@ -313,44 +529,64 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
     constexpr int hp = Gm::hp;
     constexpr int CT = hp / W;
     constexpr int K = Pl::K;
-    constexpr int R0 = Pl::fr(0);
-    constexpr int BPT0 = (M / R0) * W / NT;
+    constexpr int GA = W >= 2 ? W / 2 : 1;  // column groups per tile
+    constexpr int CG = W >= 2 ? 2 : 1;      // columns per group (v0 + g, v0 + g + GA)
+    using FL = FwdLayout<T, GA, M>;
+    using IL = InvLayout<W, M>;
+    constexpr int U0 = (M / 8) * GA;
+    constexpr int B0 = (U0 + NT - 1) / NT;
     constexpr int RL = Pl::RLAST_F;
-    constexpr int BPTL = (M / RL) * W / NT;
+    constexpr int UL = (M / RL) * GA;
+    constexpr int BL = (UL + NT - 1) / NT;
     constexpr int RI = Pl::ir(K - 1);  // last inverse stage radix (8)
     constexpr int BPTI = (M / RI) * W / NT;
-    static_assert(K >= 2 && R0 == 8 && RI == 8, "plan");
-    static_assert((M / 8) * W % NT == 0 && BPT0 >= 1, "threads");
+    constexpr int TWF = StageTw<M, false>::SIZE, TWI = StageTw<M, true>::SIZE;
+    static_assert(K >= 2 && Pl::fr(0) == 8 && RI == 8, "plan");
+    static_assert((M / 8) * W % NT == 0 && BPTI >= 1, "threads");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
-    cplx<T>* s_tw = tile + M * L;
-    cplx<T>* s_k1 = s_tw + M;
-    T* s_srow = reinterpret_cast<T*>(s_k1 + M);
+    cplx<T>* s_twf = tile + (IL::SIZE > FL::SIZE ? IL::SIZE : FL::SIZE);
+    cplx<T>* s_twi = s_twf + TWF;
+    cplx<T>* s_hs = s_twi + TWI;
+    T* s_srow = reinterpret_cast<T*>(s_hs + M);
 
-    load_twiddles<T, M, NT>(s_tw, g_tw);
-    load_twiddles<T, M, NT>(s_k1, k1);
+    build_stage_tw<T, M, false, NT>(s_twf, g_tw);
+    build_stage_tw<T, M, true, NT>(s_twi, g_tw);
+    load_twiddles<T, M, NT>(s_hs, g_hs);
     for (int item = blockIdx.x; item < count * CT; item += gridDim.x) {
-        const int s = item / CT;
-        const int v0 = (item - s * CT) * W;
+        // column-tile-major order: a CTA revisits the same column tile for
+        // successive samples, so that tile's closed-form table stays in L1
+#if GT_P2_TILE_MAJOR
+        const int tI = item / count, s = item - tI * count;
+#else
+        const int s = item / CT, tI = item - s * CT;
+#endif
+        const int v0 = tI * W;
         const size_t sg = static_cast<size_t>(sample0) + s;
         const size_t sbase = static_cast<size_t>(s) * n * hp;
-        __syncthreads();  // previous item's readers of tile / s_srow are done
+        __syncthreads();  // previous item's readers of tile / s_srow are done (and the tables are built)
 
         // ---- forward stage 0 (radix 8, NS = 1) straight from the row spectra
-        cplx<T> va[BPT0][8], vb[BPT0][8];
+        cplx<T> v[B0][3][8];
 #pragma unroll
-        for (int b = 0; b < BPT0; ++b) {
+        for (int b = 0; b < B0; ++b) {
             const int id = threadIdx.x + b * NT;
-            const int lp = id % W, j = id / W;
-            const int v = v0 + lp;
+            if (U0 % NT != 0 && id >= U0) break;
+            const int g = id % GA, j = id / GA;
+            const int va = v0 + g;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int i = j + r * (M / 8);
-                const int xa = i < n ? i : M - 1 - i;       // mirror_pad
-                const int xb = (i + c) & (M - 1);           // centre_kernel: row i holds die row x
-                va[b][r] = Aspec[sbase + static_cast<size_t>(xa) * hp + v];
+                const int xa = i < n ? i : M - 1 - i;  // mirror_pad
+                const int xb = (i + c) & (M - 1);      // centre_kernel: row i holds die row x
+                const T* ar = Areal + sbase + static_cast<size_t>(xa) * hp + va;
+                v[b][0][r] = mk<T>(ar[0], CG == 2 ? ar[GA] : T(0));
                 // the centre embedding fills rows [0, M/4) u [3M/4, M): r in {0,1,6,7} only
-                if (r < 2 || r >= 6) vb[b][r] = Bspec[sbase + static_cast<size_t>(xb) * hp + v];
+                if (r < 2 || r >= 6) {
+                    const cplx<T>* bp = Bspec + sbase + static_cast<size_t>(xb) * hp + va;
+                    v[b][1][r] = bp[0];
+                    v[b][2][r] = CG == 2 ? bp[GA] : mk<T>(T(0), T(0));
+                }
             }
         }
         // S rows into registers now, into shared memory after the stage-0 math (latency overlap)
@@ -362,12 +598,19 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
             sv[k] = idx < n * W ? Srow[sbase + static_cast<size_t>(idx / W) * hp + v0 + idx % W] : T(0);
         }
 #pragma unroll
-        for (int b = 0; b < BPT0; ++b) {
+        for (int b = 0; b < B0; ++b) {
             const int id = threadIdx.x + b * NT;
-            const int lp = id % W, j = id / W;
-            dftR<8, -1, T>(va[b]);
-            dft8_outer_only<-1, T>(vb[b]);
-            pair_store<T, M, L, 8, 1>(tile, j, lp, va[b], vb[b]);
+            if (U0 % NT != 0 && id >= U0) break;
+            const int g = id % GA, j = id / GA;
+            dftR<8, -1, T>(v[b][0]);
+            dft8_outer_only<-1, T>(v[b][1]);
+            dft8_outer_only<-1, T>(v[b][2]);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int pr = prow<1>(j * 8, r);
+                tile[FL::pa(pr, g)] = v[b][0][r];
+                st_pair(&tile[FL::pb(pr, g)], LinePair<T>{v[b][1][r], v[b][2][r]});
+            }
         }
 #pragma unroll
         for (int k = 0; k < ES; ++k) {
@@ -378,69 +621,106 @@ mc_pass2(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
         const T* Nm = in.nn(sg);
-        const T* V = in.v(sg);
+        const T* Vm = in.v(sg);
         ClosedForm<T, M> cf;
         cf.fg = reinterpret_cast<const typename Vec4<T>::type*>(fgtab);
-        cf.k1 = s_k1;
         cf.s_srow = s_srow;
         cf.alpha = alpha;
         cf.beta = beta;
         cf.mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
         cf.mus = T(mu_s);
         {
-            const T pl_cc = in.nom_scale * Nm[c * n + c] * V[c * n + c];
-            const T pl_00 = in.nom_scale * Nm[0] * V[0];
+            const T pl_cc = in.nom_scale * Nm[c * n + c] * Vm[c * n + c];
+            const T pl_00 = in.nom_scale * Nm[0] * Vm[0];
             cf.qshift = T(double(pl_cc) - double(pl_00) - mu_s);  // greens.cpp:177-184
         }
         __syncthreads();
         // ---- middle forward stages
-        PlanStages<T, M, L, L, NT, false, 1, K - 1>::run(tile, s_tw);
+        FwdStagesAB<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
         // ---- last forward stage + closed forms + first inverse stage, in registers
         int flags = 0;
         {
-            constexpr int NSL = Pl::fns(K - 1);
-            cplx<T> la[BPTL][RL], lb[BPTL][RL];
+            cplx<T> y[BL][2 * CG][RL];  // Y_0, R_0, Y_1, R_1
 #pragma unroll
-            for (int b = 0; b < BPTL; ++b) {
+            for (int b = 0; b < BL; ++b) {
                 const int id = threadIdx.x + b * NT;
-                const int lp = id % W, j = id / W;
-                const int v = v0 + lp;
-                pair_load<T, M, L, RL>(tile, j, lp, la[b], lb[b]);
-                pair_twiddle_dft<RL, NSL, M, -1, T>(la[b], lb[b], j, s_tw);
-                if (v < h) {
+                if (UL % NT != 0 && id >= UL) break;
+                const int g = id % GA, j = id / GA;
+                cplx<T> z[3][RL];
 #pragma unroll
-                    for (int q = 0; q < RL; ++q) cf.eval(la[b][q], lb[b][q], j + q * (M / RL), v, lp, flags);
+                for (int q = 0; q < RL; ++q) {
+                    const int pr = prow<M / RL>(j, q);
+                    z[0][q] = tile[FL::pa(pr, g)];
+                    const LinePair<T> p = ld_pair(&tile[FL::pb(pr, g)]);
+                    z[1][q] = p.a;
+                    z[2][q] = p.b;
                 }
-                dftR<RL, +1, T>(la[b]);
-                dftR<RL, +1, T>(lb[b]);
+                stage_twiddle<T, M, false, K - 1, 3>(z, j, s_twf);
+#pragma unroll
+                for (int l = 0; l < 3; ++l) dftR<RL, -1, T>(z[l]);
+                // C_v + i C_v' = w^{u/2} Z[u]
+#pragma unroll
+                for (int q = 0; q < RL; ++q) z[0][q] = cmul<T>(s_hs[j + q * (M / RL)], z[0][q]);
+#pragma unroll
+                for (int col = 0; col < CG; ++col) {
+                    const int w = g + col * GA, vv = v0 + w;
+                    const cplx<T> hv = s_hs[vv];
+#pragma unroll
+                    for (int q = 0; q < RL; ++q) {
+                        const int u = j + q * (M / RL);
+                        // A_hat_v = conj(w^{u/2} w^{v/2}) C_v. Padded columns (v > n) see
+                        // an all-zero table entry and S = 0: they evaluate to 0, no flags.
+                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+                        cplx<T> bb = z[1 + col][q];
+                        y[b][2 * col][q] = cf.eval(col == 0 ? z[0][q].x : z[0][q].y, bb, ph, cf.table(u, vv), u,
+                                                   vv, w, flags);
+                        y[b][2 * col + 1][q] = bb;
+                    }
+                    dftR<RL, +1, T>(y[b][2 * col]);
+                    dftR<RL, +1, T>(y[b][2 * col + 1]);
+                }
             }
             __syncthreads();
 #pragma unroll
-            for (int b = 0; b < BPTL; ++b) {
+            for (int b = 0; b < BL; ++b) {
                 const int id = threadIdx.x + b * NT;
-                pair_store<T, M, L, RL, 1>(tile, id / W, id % W, la[b], lb[b]);
+                if (UL % NT != 0 && id >= UL) break;
+                const int g = id % GA, j = id / GA;
+#pragma unroll
+                for (int col = 0; col < CG; ++col)
+#pragma unroll
+                    for (int r = 0; r < RL; ++r)
+                        st_pair(&tile[IL::template off<1>(j * RL, r, g + col * GA)],
+                                LinePair<T>{y[b][2 * col][r], y[b][2 * col + 1][r]});
             }
             __syncthreads();
         }
         or_flags(&stats[sg].status, flags);
         // ---- middle inverse stages
-        PlanStages<T, M, L, L, NT, true, 1, K - 1>::run(tile, s_tw);
+        InvStagesPairs<T, M, W, NT, 1, K - 1>::run(tile, s_twi);
         // ---- last inverse stage (radix 8, NS = M/8): keep rows [0, n) of Y, rows rho(x) of R
         {
 #pragma unroll
             for (int b = 0; b < BPTI; ++b) {
                 const int id = threadIdx.x + b * NT;
-                const int lp = id % W, j = id / W;
-                const int v = v0 + lp;
-                cplx<T> ya[8], yb[8];
-                pair_load<T, M, L, 8>(tile, j, lp, ya, yb);
-                pair_twiddle_dft<8, M / 8, M, +1, T>(ya, yb, j, s_tw);
+                const int w = id % W, j = id / W;
+                const int vv = v0 + w;
+                cplx<T> o[2][8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const LinePair<T> q = ld_pair(&tile[IL::template off<M / 8>(j, r, w)]);
+                    o[0][r] = q.a;
+                    o[1][r] = q.b;
+                }
+                stage_twiddle<T, M, true, K - 1, 2>(o, j, s_twi);
+                dftR<8, +1, T>(o[0]);
+                dftR<8, +1, T>(o[1]);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int i = j + r * (M / 8);
-                    if (i < n) Aspec[sbase + static_cast<size_t>(i) * hp + v] = ya[r];
+                    if (i < n) Yspec[sbase + static_cast<size_t>(i) * hp + vv] = o[0][r];
                     const int x = (i + c) & (M - 1);
-                    if (x < n) Bspec[sbase + static_cast<size_t>(x) * hp + v] = yb[r];
+                    if (x < n) Bspec[sbase + static_cast<size_t>(x) * hp + vv] = o[1][r];
                 }
             }
         }
@@ -570,9 +850,9 @@ struct WarpMinBlocks {
 
 template <typename T, int M>
 __global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T, GT_W1_CTAS>::value)
-mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
+mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
           cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
-          const cplx<T>* __restrict__ g_tw, T var_lo, T var_hi) {
+          const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T var_lo, T var_hi) {
     using Gm = MCGeom<T, M>;
     using WF = WarpFFT<T, M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, hp = Gm::hp, P = WF::P;
@@ -644,18 +924,19 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, cplx<T>* __restrict__ Aspec,
 #pragma unroll
         for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
         __syncwarp();
-        // split into the two real-input half spectra
-        cplx<T>* A_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
+        // split into the two real-input half spectra (A as its real DCT part)
+        T* A_x = Areal + (static_cast<size_t>(s) * n + x) * hp;
         cplx<T>* B_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
         for (int v = lane; v < hp; v += 32) {
-            cplx<T> A = mk<T>(T(0), T(0)), B = A;
+            T Ar = T(0);
+            cplx<T> B = mk<T>(T(0), T(0));
             if (v < h) {
                 const cplx<T> Z = scr[v];
                 const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
-                A = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
+                if (v < n) Ar = dct_part<T>(Z, Zc, g_hs[v]);
                 B = mk<T>(T(0.5) * (Z.y - Zc.y), T(-0.5) * (Z.x - Zc.x));
             }
-            A_x[v] = A;
+            A_x[v] = Ar;
             B_x[v] = B;
         }
         or_flags(&stats[sg].status, bad);
@@ -770,7 +1051,12 @@ template <typename T, int M>
 struct MCLaunch {
     using Gm = MCGeom<T, M>;
     static size_t smem1() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
-    static size_t smem2() { return sizeof(cplx<T>) * (M * Gm::L + 2 * M) + sizeof(T) * Gm::n * Gm::W; }
+    static constexpr int GA2 = Gm::W >= 2 ? Gm::W / 2 : 1;
+    static size_t smem2() {
+        constexpr int FS = FwdLayout<T, GA2, M>::SIZE, IS = InvLayout<Gm::W, M>::SIZE;
+        return sizeof(cplx<T>) * ((FS > IS ? FS : IS) + StageTw<M, false>::SIZE + StageTw<M, true>::SIZE + M) +
+               sizeof(T) * Gm::n * Gm::W;
+    }
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
     static size_t smemw() {
         if constexpr (use_warp_rows<T, M>())
@@ -811,13 +1097,12 @@ struct MCLaunch {
             for (int& r : res) r = r < 1 ? 1 : r;
         }
         const size_t per = static_cast<size_t>(n) * hp;
-        cplx<T>* A = reinterpret_cast<cplx<T>*>(scratch);
-        cplx<T>* B = A + per * chunk;
-        T* S = reinterpret_cast<T*>(B + per * chunk);
+        cplx<T>* A = reinterpret_cast<cplx<T>*>(scratch);  // Y (pass 2 -> pass 3)
+        cplx<T>* B = A + per * chunk;                      // B (pass 1 -> 2), R (pass 2 -> 3)
+        T* S = reinterpret_cast<T*>(B + per * chunk);       // row-symmetrised leakage
+        T* Ar = S + per * chunk;                            // real DCT part of A (pass 1 -> 2)
+        const cplx<T>* hs = reinterpret_cast<const cplx<T>*>(g->hs);
         const cplx<T>* tw = reinterpret_cast<const cplx<T>*>(g->tw);
-        const cplx<T>* fk = reinterpret_cast<const cplx<T>*>(g->fk);
-        const T* gt = reinterpret_cast<const T*>(g->gtab);
-        const cplx<T>* k1 = reinterpret_cast<const cplx<T>*>(g->k1);
         const T var_lo = T(exp(-o->exponent_cap)), var_hi = T(exp(o->exponent_cap));
         auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
@@ -826,13 +1111,13 @@ struct MCLaunch {
             if (mark) mark(ctx, 0, st);
             if constexpr (use_warp_rows<T, M>())
                 mc_pass1w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(), st>>>(
-                    in, s0, cnt, A, B, S, stats, tw, var_lo, var_hi);
+                    in, s0, cnt, Ar, B, S, stats, tw, hs, var_lo, var_hi);
             else
-                mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, A, B, S, stats, tw,
+                mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, Ar, B, S, stats, tw, hs,
                                                                              var_lo, var_hi);
             if (mark) mark(ctx, 1, st);
             mc_pass2<T, M><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), st>>>(
-                in, s0, cnt, A, B, S, stats, tw, static_cast<const T*>(g->fg), k1, T(g->alpha), T(g->beta),
+                in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fg), T(g->alpha), T(g->beta),
                 o->mu_per_sample, T(g->mu_fixed));
             if (mark) mark(ctx, 2, st);
             if constexpr (use_warp_rows<T, M>())
@@ -899,7 +1184,7 @@ size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64) {
     const int hp = gtd_padded_width(n, fp64);
     if (hp < 0) return 0;
     const size_t cb = fp64 ? 16 : 8, rb = fp64 ? 8 : 4;
-    return static_cast<size_t>(n) * hp * (2 * cb + rb);
+    return static_cast<size_t>(n) * hp * (2 * cb + 2 * rb);
 }
 
 int gtd_mc_launch_count(int batch, int chunk) {
