@@ -86,13 +86,22 @@ struct WarpFFT {
     static constexpr int SCRATCH = P * SP > M ? P * SP : M;  // complex elements per warp
     static_assert(P == 4 || P == 8 || P == 16, "warp FFT supports M = 128, 256, 512");
 
-    // tw: M-entry table exp(-2 pi i t / M) (shared); scratch: SCRATCH complex per warp.
+    // Step-1 twiddles lane-major: tw1[(k - 1) 32 + j] = w_M^{j k}, so a warp's
+    // loads for one k are 32 consecutive entries (the flat table's j k stride is
+    // a k-way bank conflict).
+    static constexpr int TW1 = (P - 1) * 32;
+    __device__ __forceinline__ static void build_tw1(cplx<T>* tw1, const cplx<T>* tw, int tid, int nthr) {
+        for (int i = tid; i < TW1; i += nthr) tw1[i] = tw[(i & 31) * (1 + (i >> 5))];
+    }
+
+    // tw: M-entry table exp(-2 pi i t / M), tw1 (above), both shared; scratch: SCRATCH complex per warp.
     template <int SIGN>
-    __device__ __forceinline__ static void run(cplx<T>* v, cplx<T>* scratch, const cplx<T>* tw, int lane) {
+    __device__ __forceinline__ static void run(cplx<T>* v, cplx<T>* scratch, const cplx<T>* tw,
+                                               const cplx<T>* tw1, int lane) {
         dftP<P, SIGN, T>(v);
 #pragma unroll
         for (int k = 1; k < P; ++k) {
-            cplx<T> w = tw[lane * k];  // w_M^{j k'}, j k' < 32 P = M
+            cplx<T> w = tw1[(k - 1) * 32 + lane];  // w_M^{j k'}
             if (SIGN > 0) w.y = -w.y;
             v[k] = cmul<T>(v[k], w);
         }

@@ -859,11 +859,15 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     constexpr int E = n / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_hs = s_tw + M;
+    cplx<T>* s_tw1 = s_hs + n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    cplx<T>* scr = s_tw + M + warp * WF::SCRATCH;
+    cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
     T* st_a = reinterpret_cast<T*>(scr);
     T* st_l = st_a + n;
     for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
+    for (int t = threadIdx.x; t < n; t += WARPS * 32) s_hs[t] = g_hs[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS * 32);
     __syncthreads();
 
     for (int item = blockIdx.x * WARPS + warp; item < count * n; item += gridDim.x * WARPS) {
@@ -919,7 +923,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             z[k] = mk<T>(re, im);
         }
         __syncwarp();
-        WF::template run<-1>(z, scr, s_tw, lane);
+        WF::template run<-1>(z, scr, s_tw, s_tw1, lane);
         __syncwarp();
 #pragma unroll
         for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
@@ -933,7 +937,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             if (v < h) {
                 const cplx<T> Z = scr[v];
                 const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
-                if (v < n) Ar = dct_part<T>(Z, Zc, g_hs[v]);
+                if (v < n) Ar = dct_part<T>(Z, Zc, s_hs[v]);
                 B = mk<T>(T(0.5) * (Z.y - Zc.y), T(-0.5) * (Z.x - Zc.x));
             }
             A_x[v] = Ar;
@@ -961,8 +965,10 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    cplx<T>* scr = s_tw + M + warp * WF::SCRATCH;
+    cplx<T>* s_tw1 = s_tw + M;
+    cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
     for (int t = threadIdx.x; t < M; t += WARPS3 * 32) s_tw[t] = g_tw[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS3 * 32);
     __syncthreads();
     const T inv = T(1.0 / (double(M) * double(M)));
 
@@ -993,7 +999,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
         const T mu_t = T(mu_s);
         const T* N_ = in.nn(sg) + x * n;
         const T* V_ = in.v(sg) + x * n;
-        WF::template run<+1>(z, scr, s_tw, lane);
+        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
         asm volatile("" ::: "memory");  // keep the epilogue loads below the transform (registers)
         T nv[E], vv[E];
 #pragma unroll
@@ -1060,13 +1066,13 @@ struct MCLaunch {
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
     static size_t smemw() {
         if constexpr (use_warp_rows<T, M>())
-            return sizeof(cplx<T>) * (M + WARPS * WarpFFT<T, M>::SCRATCH);
+            return sizeof(cplx<T>) * (M + M / 2 + WarpFFT<T, M>::TW1 + WARPS * WarpFFT<T, M>::SCRATCH);
         else
             return 0;
     }
     static size_t smemw3() {
         if constexpr (use_warp_rows<T, M>())
-            return sizeof(cplx<T>) * (M + WARPS3 * WarpFFT<T, M>::SCRATCH);
+            return sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + WARPS3 * WarpFFT<T, M>::SCRATCH);
         else
             return 0;
     }
