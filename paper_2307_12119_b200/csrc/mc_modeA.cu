@@ -863,8 +863,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     cplx<T>* s_tw1 = s_hs + n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
-    T* st_a = reinterpret_cast<T*>(scr);
-    T* st_l = st_a + n;
+    T* st_l = reinterpret_cast<T*>(scr);
     for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
     for (int t = threadIdx.x; t < n; t += WARPS * 32) s_hs[t] = g_hs[t];
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS * 32);
@@ -887,6 +886,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
         }
         T part_l = T(0), part_a = T(0);
         int bad = 0;
+        T av[E], lv[E];  // applied / leakage row, element lane + 32 t
 #pragma unroll
         for (int t = 0; t < E; ++t) {
             const int y = lane + 32 * t;
@@ -894,12 +894,11 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             if (!(pv[t] >= T(0) && pv[t] <= Real<T>::max()) || !(nv[t] >= T(0) && nv[t] <= Real<T>::max()))
                 bad |= GTD_ST_BAD_POWER;
             if (!(vv[t] >= var_lo && vv[t] <= var_hi)) bad |= GTD_ST_BAD_VAR;
-            const T lk = in.nom_scale * nv[t] * vv[t];
-            const T a = pv[t] + lk;
-            part_l += lk;
-            part_a += a;
-            st_a[y] = a;
-            st_l[y] = lk;
+            lv[t] = in.nom_scale * nv[t] * vv[t];
+            av[t] = pv[t] + lv[t];
+            part_l += lv[t];
+            part_a += av[t];
+            st_l[y] = lv[t];
         }
         __syncwarp();
         // row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185)
@@ -909,17 +908,14 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             if (v < h) val = st_l[min(c + v, n - 1)] + st_l[max(c - v, 0)];
             Srow_x[v] = val;
         }
-        // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k
+        // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k,
+        // from registers: mirror(i) = M-1-i = (31 - lane) + 32 (P-1-k) for k >= E
+        // (one shuffle); the centre embedding keeps the lane (t = k + E/2, k - 3E/2).
         cplx<T> z[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-            const int i = lane + 32 * k;
-            const T re = st_a[i < n ? i : M - 1 - i];
-            T im = T(0);
-            if (i < c)
-                im = st_l[i + c];
-            else if (i >= M - c)
-                im = st_l[i - M + c];
+            const T re = k < E ? av[k] : __shfl_xor_sync(0xffffffffu, av[P - 1 - k], 31);
+            const T im = k < E / 2 ? lv[k + E / 2] : (k >= P - E / 2 ? lv[k - (P - E / 2)] : T(0));
             z[k] = mk<T>(re, im);
         }
         __syncwarp();
