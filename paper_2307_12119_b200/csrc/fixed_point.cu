@@ -20,7 +20,9 @@
 //   fp_update: per-sample iteration count / convergence / failure state.
 #include <cuda_runtime.h>
 
+#include "col_pass.cuh"
 #include "fft_tile.cuh"
+#include "fft_warp.cuh"
 #include "gt_device.h"
 
 namespace gtb {
@@ -73,9 +75,9 @@ __device__ __forceinline__ bool finite_val(T v) {
 // ----------------------------------------------------------------- rows
 template <typename T, int M, bool FIRST>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
-fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Tst,
-        FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw, T beta,
-        int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient) {
+fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
+        FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
+        const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient) {
     using Gm = FPGeom<T, M>;
     constexpr int n = Gm::n, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT, hp = Gm::hp;
     constexpr int RB = Gm::RB;
@@ -164,16 +166,13 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
             const int l = lr >> 1, half = lr & 1;
             const int x = 2 * p0 + lr;
             if (x >= n) continue;
-            cplx<T> o = mk<T>(T(0), T(0));
-            if (v < h) {
+            T o = T(0);  // real DCT part of the row's half spectrum (col_pass.cuh)
+            if (v < n) {
                 const cplx<T> Z = tile[v * LP + l];
                 const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
-                if (!half)
-                    o = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y + Zc.y));
-                else
-                    o = mk<T>(T(0.5) * (Z.y - Zc.y), T(-0.5) * (Z.x - Zc.x));
+                o = half ? dct_part_im<T>(Z, Zc, g_hs[v]) : dct_part<T>(Z, Zc, g_hs[v]);
             }
-            As[static_cast<size_t>(x) * hp + v] = o;
+            Ar[static_cast<size_t>(s) * n * hp + static_cast<size_t>(x) * hp + v] = o;
         }
         if (!FIRST) {
             or_flags_fp(&status[sg], bad);
@@ -187,45 +186,350 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
     }
 }
 
-// ----------------------------------------------------------------- columns
+// ----------------------------------------------------------------- rows (warp per row pair)
+// M = 128 / 256 / 512: one warp owns the die-row pair (2p, 2p+1) of a sample:
+// inverse row transform of Y_2p + i Y_2p+1 (both Hermitian) -> theta rows ->
+// Kirchhoff inverse -> residual -> T written -> next applied rows -> forward
+// transform of mirror(a_2p) + i mirror(a_2p+1) -> the two rows' real DCT parts.
+// Rows are loaded / stored coalesced straight from registers.
+constexpr int FPW_WARPS = 8;
+
 template <typename T, int M>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
-fp_cols(int sample0, int count, cplx<T>* __restrict__ A, const FPState* __restrict__ state,
-        const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ fk, int fk_pitch) {
+constexpr bool fp_warp_rows() {
+    return M == 128 || M == 256 || M == 512;
+}
+
+template <typename T, int M, bool FIRST>
+__global__ void __launch_bounds__(FPW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
+fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec, T* __restrict__ Ar,
+          T* __restrict__ Tst, FPState* __restrict__ state, int* __restrict__ status,
+          const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka,
+          T kb, T kexp, T t_ambient) {
     using Gm = FPGeom<T, M>;
-    constexpr int n = Gm::n, h = Gm::h, L = Gm::L, NT = Gm::NT, hp = Gm::hp, CT = Gm::CT;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, h = Gm::h, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw1 = s_tw + M;
+    cplx<T>* s_hs = s_tw1 + WF::TW1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_hs + n + warp * WF::SCRATCH;
+    for (int t = threadIdx.x; t < M; t += FPW_WARPS * 32) s_tw[t] = g_tw[t];
+    for (int t = threadIdx.x; t < n; t += FPW_WARPS * 32) s_hs[t] = g_hs[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, FPW_WARPS * 32);
+    __syncthreads();
+    constexpr T inv = T(1.0 / (double(M) * double(M)));
+
+    for (int item = blockIdx.x * FPW_WARPS + warp; item < count * RP; item += gridDim.x * FPW_WARPS) {
+        const int s = item / RP, x0 = 2 * (item - s * RP);
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        if (!FIRST && !state[sg].active) continue;  // warp-uniform
+        T* T0r = Tst + sg * n * n + static_cast<size_t>(x0) * n;
+        T* T1r = T0r + n;
+        // Every global input of the item is requested up front (one exposed
+        // round trip per row pair instead of three): previous T rows, P rows,
+        // leakage rows L0 = nom N V.
+        T t0[E], t1[E], p0[E], p1[E], l0[E], l1[E];
+        {
+            const T* P0 = in.P + sg * in.sP + static_cast<size_t>(x0) * n;
+            const T* N0 = in.N + sg * in.sN + static_cast<size_t>(x0) * n;
+            const T* V0 = in.V + sg * in.sV + static_cast<size_t>(x0) * n;
+            const bool n_is_p = in.N == in.P && in.sN == in.sP;
+#pragma unroll
+            for (int t = 0; t < E; ++t) {
+                const int j = lane + 32 * t;
+                if constexpr (!FIRST) {
+                    t0[t] = T0r[j];
+                    t1[t] = T1r[j];
+                }
+                p0[t] = P0[j];
+                p1[t] = P0[n + j];
+                const T n0 = n_is_p ? p0[t] : N0[j], n1 = n_is_p ? p1[t] : N0[n + j];
+                l0[t] = in.nom_scale * n0 * V0[j];
+                l1[t] = in.nom_scale * n1 * V0[n + j];
+            }
+        }
+        double dmax = 0.0;
+        int bad = 0;
+        if constexpr (!FIRST) {
+            const cplx<T>* Y0 = Yspec + (static_cast<size_t>(s) * n + x0) * hp;
+            const cplx<T>* Y1 = Y0 + hp;
+            cplx<T> z[P];
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int v = lane + 32 * k;
+                const int w = v <= n ? v : M - v;
+                const cplx<T> y = Y0[w], r = Y1[w];
+                if (v == 0 || v == n)
+                    z[k] = mk<T>(y.x, r.x);
+                else if (v < n)
+                    z[k] = mk<T>(y.x - r.y, y.y + r.x);
+                else
+                    z[k] = mk<T>(y.x + r.y, r.x - y.y);
+            }
+            WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
+            __syncwarp();
+#pragma unroll
+            for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < E; ++t) {
+                const int j = lane + 32 * t;
+                const cplx<T> th = scr[j];
+                T a = th.x * inv, b = th.y * inv;  // theta - T0 of rows x0, x0+1
+                if (kirchhoff) {
+                    const T ba = ka + kb * a, bb = ka + kb * b;
+                    if (!(ba > T(0)) || !(bb > T(0))) bad |= GTD_ST_KIRCHHOFF;
+                    a = pow(ba, kexp) - t_ambient;
+                    b = pow(bb, kexp) - t_ambient;
+                }
+                if (!finite_val(a) || !finite_val(b)) bad |= GTD_ST_NONFINITE;
+                dmax = fmax(dmax, fmax(double(fabs(a - t0[t])), double(fabs(b - t1[t]))));
+                T0r[j] = a;
+                T1r[j] = b;
+                t0[t] = a;
+                t1[t] = b;
+            }
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int t = 0; t < E; ++t) t0[t] = t1[t] = T(0);
+        }
+        // next applied rows a = P + L0 f(T)
+        T a0[E], a1[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const T f0 = law ? T(exp(beta * t0[t])) : T(1) + beta * t0[t];
+            const T f1 = law ? T(exp(beta * t1[t])) : T(1) + beta * t1[t];
+            a0[t] = p0[t] + l0[t] * f0;
+            a1[t] = p1[t] + l1[t] * f1;
+        }
+        // z[i] = mirror(a0)[i] + i mirror(a1)[i]: mirror(i) = (31 - lane) + 32 (P-1-k) for k >= E
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (k < E)
+                z[k] = mk<T>(a0[k], a1[k]);
+            else
+                z[k] = mk<T>(__shfl_xor_sync(0xffffffffu, a0[P - 1 - k], 31),
+                             __shfl_xor_sync(0xffffffffu, a1[P - 1 - k], 31));
+        }
+        WF::template run<-1>(z, scr, s_tw, s_tw1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        T* A0 = Ar + (static_cast<size_t>(s) * n + x0) * hp;
+        T* A1 = A0 + hp;
+        for (int v = lane; v < hp; v += 32) {
+            T r0 = T(0), r1 = T(0);
+            if (v < n) {
+                const cplx<T> Z = scr[v];
+                const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
+                const cplx<T> hv = s_hs[v];
+                r0 = dct_part<T>(Z, Zc, hv);
+                r1 = dct_part_im<T>(Z, Zc, hv);
+            }
+            A0[v] = r0;
+            A1[v] = r1;
+        }
+        if constexpr (!FIRST) {
+            or_flags_fp(&status[sg], bad);
+            dmax = warp_max_d(dmax);
+            if (lane == 0) atomicMax(&state[sg].res_bits, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        }
+        __syncwarp();
+    }
+}
+
+// ----------------------------------------------------------------- columns (real-DCT packed)
+// Per tile of W = 2 GA half-spectrum columns: GA packed A lines (two columns'
+// real DCT parts At_v + i At_{v+GA}, mirror expansion in the stage-0 address),
+// forward column FFT, C_v + i C_v' = w^{u/2} Z[u], Y_v = fk (conj(w^{(u+v)/2}) C_v)
+// in registers between the last forward and first inverse stage, inverse column
+// FFT on the pairs (Y_g, Y_{g+GA}), rows [0, n) stored.
+template <typename T, int M>
+struct FPCGeom {
+    static constexpr int n = M / 2, h = n + 1;
+    static constexpr int GA = FPGeom<T, M>::L / 2 > 0 ? FPGeom<T, M>::L / 2 : 1;
+    static constexpr int W = 2 * GA;
+    static constexpr int hp = FPGeom<T, M>::hp;
+    static constexpr int CT = hp / W;
+    static constexpr int U8 = (M / 8) * GA;
+    static constexpr int NT = U8 >= 256 ? 256 : (U8 < 32 ? 32 : U8);
+    static constexpr int MINB = sizeof(T) == 8 ? 1 : ((512 / NT) < 1 ? 1 : 512 / NT);
+    static constexpr int APLANE = (M + M / 8) * GA;
+    static constexpr int TILE = InvLayout<GA, M>::SIZE > APLANE ? InvLayout<GA, M>::SIZE : APLANE;
+    static_assert(hp % W == 0, "column tiles");
+};
+
+template <typename T, int M, int GA, int NT, int S>
+__device__ __forceinline__ void fwd_stage_a(cplx<T>* tile, const cplx<T>* twf) {
+    using ST = StageTw<M, false>;
+    constexpr int R = ST::R(S), NS = ST::NS(S);
+    constexpr int NB = (M / R) * GA;
+    constexpr int BPT = (NB + NT - 1) / NT;
+    cplx<T> v[BPT][1][R];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        if (NB % NT != 0 && id >= NB) break;
+        const int g = id % GA, j = id / GA;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][0][r] = tile[prow<M / R>(j, r) * GA + g];
+        stage_twiddle<T, M, false, S, 1>(v[b], j, twf);
+        dftR<R, -1, T>(v[b][0]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int id = threadIdx.x + b * NT;
+        if (NB % NT != 0 && id >= NB) break;
+        const int g = id % GA, j = id / GA;
+        const int k = j % NS;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) tile[prow<NS>(base, r) * GA + g] = v[b][0][r];
+    }
+    __syncthreads();
+}
+
+template <typename T, int M, int GA, int NT, int S, int E>
+struct FwdStagesA {
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* twf) {
+        if constexpr (S < E) {
+            fwd_stage_a<T, M, GA, NT, S>(tile, twf);
+            FwdStagesA<T, M, GA, NT, S + 1, E>::run(tile, twf);
+        }
+    }
+};
+
+template <typename T, int M>
+__global__ void __launch_bounds__(FPCGeom<T, M>::NT, FPCGeom<T, M>::MINB)
+fp_cols_d(int sample0, int count, const T* __restrict__ Ar, cplx<T>* __restrict__ Yspec,
+          const FPState* __restrict__ state, const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs,
+          const cplx<T>* __restrict__ fk, int fk_pitch) {
+    using Gc = FPCGeom<T, M>;
+    using Pl = Plan<M>;
+    using IL = InvLayout<Gc::GA, M>;
+    constexpr int n = Gc::n, h = Gc::h, GA = Gc::GA, W = Gc::W, hp = Gc::hp, CT = Gc::CT, NT = Gc::NT;
+    constexpr int K = Pl::K, RL = Pl::RLAST_F;
+    constexpr int U0 = (M / 8) * GA, B0 = (U0 + NT - 1) / NT;
+    constexpr int UL = (M / RL) * GA, BL = (UL + NT - 1) / NT;
+    constexpr int BPTI = (M / 8) * GA / NT;
+    constexpr int TWF = StageTw<M, false>::SIZE, TWI = StageTw<M, true>::SIZE;
+    static_assert(K >= 2 && Pl::fr(0) == 8 && Pl::ir(K - 1) == 8, "plan");
+    static_assert((M / 8) * GA % NT == 0 && BPTI >= 1, "threads");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
-    cplx<T>* s_tw = tile + M * L;
-    load_twiddles<T, M, NT>(s_tw, g_tw);
-    __syncthreads();
+    cplx<T>* s_twf = tile + Gc::TILE;
+    cplx<T>* s_twi = s_twf + TWF;
+    cplx<T>* s_hs = s_twi + TWI;
+    build_stage_tw<T, M, false, NT>(s_twf, g_tw);
+    build_stage_tw<T, M, true, NT>(s_twi, g_tw);
+    for (int t = threadIdx.x; t < M; t += NT) s_hs[t] = g_hs[t];
+
     for (int item = blockIdx.x; item < count * CT; item += gridDim.x) {
-        const int s = item / CT;
-        const int v0 = (item - s * CT) * L;
+        const int s = item / CT, v0 = (item - s * CT) * W;
         const size_t sg = static_cast<size_t>(sample0) + s;
-        if (!state[sg].active) continue;
-        cplx<T>* As = A + static_cast<size_t>(s) * n * hp;
-        for (int idx = threadIdx.x; idx < n * L; idx += NT) {
-            const int w = idx % L, x = idx / L;
-            const cplx<T> a = As[static_cast<size_t>(x) * hp + v0 + w];
-            tile[x * L + w] = a;
-            tile[(M - 1 - x) * L + w] = a;
+        if (!state[sg].active) continue;  // CTA-uniform
+        const size_t sbase = static_cast<size_t>(s) * n * hp;
+        __syncthreads();  // previous item's tile readers done (and the tables are built)
+        // ---- forward stage 0 straight from the real DCT rows (mirror in the address)
+        {
+            cplx<T> v[B0][8];
+#pragma unroll
+            for (int b = 0; b < B0; ++b) {
+                const int id = threadIdx.x + b * NT;
+                if (U0 % NT != 0 && id >= U0) break;
+                const int g = id % GA, j = id / GA;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int i = j + r * (M / 8);
+                    const int xa = i < n ? i : M - 1 - i;
+                    const T* ar = Ar + sbase + static_cast<size_t>(xa) * hp + v0 + g;
+                    v[b][r] = mk<T>(ar[0], ar[GA]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B0; ++b) {
+                const int id = threadIdx.x + b * NT;
+                if (U0 % NT != 0 && id >= U0) break;
+                const int g = id % GA, j = id / GA;
+                dftR<8, -1, T>(v[b]);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) tile[prow<1>(j * 8, r) * GA + g] = v[b][r];
+            }
         }
         __syncthreads();
-        tile_fft<T, M, L, L, NT, -1>(tile, s_tw);
-        for (int idx = threadIdx.x; idx < M * L; idx += NT) {
-            const int w = idx % L, u = idx / L;
-            const int v = v0 + w;
-            if (v >= h) continue;
-            tile[u * L + w] = cmul<T>(tile[u * L + w], fk[static_cast<size_t>(u) * fk_pitch + v]);
+        FwdStagesA<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
+        // ---- last forward stage + spectral multiply + first inverse stage, in registers
+        {
+            cplx<T> y[BL][2][RL];
+#pragma unroll
+            for (int b = 0; b < BL; ++b) {
+                const int id = threadIdx.x + b * NT;
+                if (UL % NT != 0 && id >= UL) break;
+                const int g = id % GA, j = id / GA;
+                cplx<T> z[1][RL];
+#pragma unroll
+                for (int q = 0; q < RL; ++q) z[0][q] = tile[prow<M / RL>(j, q) * GA + g];
+                stage_twiddle<T, M, false, K - 1, 1>(z, j, s_twf);
+                dftR<RL, -1, T>(z[0]);
+#pragma unroll
+                for (int q = 0; q < RL; ++q) z[0][q] = cmul<T>(s_hs[j + q * (M / RL)], z[0][q]);  // C_v + i C_v'
+#pragma unroll
+                for (int col = 0; col < 2; ++col) {
+                    const int vv = v0 + g + col * GA;
+                    const cplx<T> hv = s_hs[vv];
+#pragma unroll
+                    for (int q = 0; q < RL; ++q) {
+                        const int u = j + q * (M / RL);
+                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+                        const cplx<T> f = vv < h ? fk[static_cast<size_t>(u) * fk_pitch + vv] : mk<T>(T(0), T(0));
+                        y[b][col][q] = cscale<T>(cmul<T>(f, ph), col == 0 ? z[0][q].x : z[0][q].y);
+                    }
+                    dftR<RL, +1, T>(y[b][col]);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < BL; ++b) {
+                const int id = threadIdx.x + b * NT;
+                if (UL % NT != 0 && id >= UL) break;
+                const int g = id % GA, j = id / GA;
+#pragma unroll
+                for (int r = 0; r < RL; ++r)
+                    st_pair(&tile[IL::template off<1>(j * RL, r, g)], LinePair<T>{y[b][0][r], y[b][1][r]});
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        tile_fft<T, M, L, L, NT, +1>(tile, s_tw);
-        for (int idx = threadIdx.x; idx < n * L; idx += NT) {
-            const int w = idx % L, x = idx / L;
-            As[static_cast<size_t>(x) * hp + v0 + w] = tile[x * L + w];
+        InvStagesPairs<T, M, GA, NT, 1, K - 1>::run(tile, s_twi);
+        // ---- last inverse stage: rows [0, n) of both columns
+#pragma unroll
+        for (int b = 0; b < BPTI; ++b) {
+            const int id = threadIdx.x + b * NT;
+            const int g = id % GA, j = id / GA;
+            cplx<T> o[2][8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const LinePair<T> q = ld_pair(&tile[IL::template off<M / 8>(j, r, g)]);
+                o[0][r] = q.a;
+                o[1][r] = q.b;
+            }
+            stage_twiddle<T, M, true, K - 1, 2>(o, j, s_twi);
+            dftR<8, +1, T>(o[0]);
+            dftR<8, +1, T>(o[1]);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int i = j + r * (M / 8);
+                if (i < n) {
+                    cplx<T>* yr = Yspec + sbase + static_cast<size_t>(i) * hp + v0 + g;
+                    yr[0] = o[0][r];
+                    yr[GA] = o[1][r];
+                }
+            }
         }
-        __syncthreads();
     }
 }
 
@@ -294,45 +598,86 @@ __global__ void fp_stats(const T* __restrict__ Tst, int n, int sample0, double* 
 template <typename T, int M>
 struct FPLaunch {
     using Gm = FPGeom<T, M>;
+    using Gc = FPCGeom<T, M>;
     static size_t smem_rows() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
-    static size_t smem_cols() { return sizeof(cplx<T>) * (M * Gm::L + M); }
+    static size_t smem_rows_w() {
+        if constexpr (fp_warp_rows<T, M>())
+            return sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + M / 2 + FPW_WARPS * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
+    static size_t smem_cols() {
+        return sizeof(cplx<T>) * (Gc::TILE + StageTw<M, false>::SIZE + StageTw<M, true>::SIZE + M);
+    }
 
     static int run(const gtd_greens* g, const FPIn<T>& in, int batch, const gtd_fp_opts* o, T* Tst, int* iters,
                    int* status, double* mx, double* mean, void* scratch, FPState* state, int* counter_d,
                    int* counter_h, int chunk, cudaStream_t st, long long* launches) {
         constexpr int n = Gm::n, hp = Gm::hp, NT = Gm::NT;
+        constexpr int RP = n / 2;
         static int res[3] = {0, 0, 0}, sms = 0;
         if (!sms) {
             cudaFuncSetAttribute(fp_rows<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
             cudaFuncSetAttribute(fp_rows<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
-            cudaFuncSetAttribute(fp_cols<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cols()));
+            cudaFuncSetAttribute(fp_cols_d<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cols()));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], fp_rows<T, M, false>, NT, smem_rows());
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], fp_cols<T, M>, NT, smem_cols());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], fp_cols_d<T, M>, Gc::NT, smem_cols());
+            if constexpr (fp_warp_rows<T, M>()) {
+                cudaFuncSetAttribute(fp_rows_w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem_rows_w()));
+                cudaFuncSetAttribute(fp_rows_w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem_rows_w()));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], fp_rows_w<T, M, false>, FPW_WARPS * 32,
+                                                              smem_rows_w());
+            }
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             for (int& r : res) r = r < 1 ? 1 : r;
         }
-        cplx<T>* A = static_cast<cplx<T>*>(scratch);
+        const size_t per = static_cast<size_t>(n) * hp;
+        cplx<T>* A = static_cast<cplx<T>*>(scratch);             // Y: column pass -> row pass
+        T* Ar = reinterpret_cast<T*>(A + per * chunk);           // real DCT rows: row pass -> column pass
         const cplx<T>* tw = static_cast<const cplx<T>*>(g->tw);
+        const cplx<T>* hs = static_cast<const cplx<T>*>(g->hs);
         const cplx<T>* fk = static_cast<const cplx<T>*>(g->fk);
         const T kexp = T(1.0 / (1.0 - o->eta));
         const T ka = T(pow(o->t_ambient, 1.0 - o->eta)), kb = T((1.0 - o->eta) * pow(o->t_ambient, -o->eta));
         auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         const int poll = o->poll > 0 ? o->poll : 4;
         long long k = 0;
+        auto rows = [&](bool first, int s0, int cnt) {
+            if constexpr (fp_warp_rows<T, M>()) {
+                const int gw = grid((cnt * RP + FPW_WARPS - 1) / FPW_WARPS, res[2]);
+                if (first)
+                    fp_rows_w<T, M, true><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
+                        in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
+                        kexp, T(o->t_ambient));
+                else
+                    fp_rows_w<T, M, false><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
+                        in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
+                        kexp, T(o->t_ambient));
+            } else {
+                const int gr = grid(cnt * Gm::RB, res[0]);
+                if (first)
+                    fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
+                                                                     T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
+                                                                     T(o->t_ambient));
+                else
+                    fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
+                                                                      T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
+                                                                      T(o->t_ambient));
+            }
+        };
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
-            const int gr = grid(cnt * Gm::RB, res[0]), gc = grid(cnt * Gm::CT, res[1]);
+            const int gc = grid(cnt * Gc::CT, res[1]);
             fp_init<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt);
-            fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Tst, state, status, tw, T(o->beta),
-                                                             o->law, o->kirchhoff, ka, kb, kexp, T(o->t_ambient));
+            rows(true, s0, cnt);
             k += 2;
             for (int it = 1; it <= o->max_iters; ++it) {
-                fp_cols<T, M><<<gc, NT, smem_cols(), st>>>(s0, cnt, A, state, tw, fk, g->hp);
-                fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Tst, state, status, tw,
-                                                                  T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                  T(o->t_ambient));
+                fp_cols_d<T, M><<<gc, Gc::NT, smem_cols(), st>>>(s0, cnt, Ar, A, state, tw, hs, fk, g->hp);
+                rows(false, s0, cnt);
                 cudaMemsetAsync(counter_d, 0, sizeof(int), st);
                 fp_update<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt, o->tol, o->max_iters,
                                                             counter_d);
@@ -398,7 +743,7 @@ extern "C" {
 size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64) {
     const int hp = fp64 ? fp_hp<double>(2 * n) : fp_hp<float>(2 * n);
     if (hp < 0) return 0;
-    return static_cast<size_t>(n) * hp * (fp64 ? 16 : 8);
+    return static_cast<size_t>(n) * hp * (fp64 ? 16 + 8 : 8 + 4);  // Y (complex) + real DCT rows
 }
 
 size_t gtd_fp_state_bytes(void) { return sizeof(FPState); }
