@@ -697,6 +697,9 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
 #ifndef GT_W1
 #define GT_W1 16
 #endif
+#ifndef GT_P3_EARLY_NV
+#define GT_P3_EARLY_NV 1
+#endif
 #ifndef GT_W3
 #define GT_W3 8
 #endif
@@ -838,6 +841,19 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
         const size_t sg = static_cast<size_t>(sample0) + s;
         const cplx<T>* Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
         const cplx<T>* R_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+#if GT_P3_EARLY_NV
+        // epilogue inputs requested up front (one exposed round trip per row)
+        T nv[E], vv[E];
+        {
+            const T* N_ = in.nn(sg) + x * n;
+            const T* V_ = in.v(sg) + x * n;
+#pragma unroll
+            for (int t = 0; t < E; ++t) {
+                nv[t] = N_[lane + 32 * t];
+                vv[t] = V_[lane + 32 * t];
+            }
+        }
+#endif
         // Z = Y + i R over the full line from the Hermitian half spectra
         cplx<T> z[P];
 #pragma unroll
@@ -851,16 +867,19 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
                 z[k] = mk<T>(y.x - r.y, y.y + r.x);
             else
                 z[k] = mk<T>(y.x + r.y, r.x - y.y);
+#if !GT_P3_EARLY_NV
             // bound the loads in flight (register pressure): fence every 4 lines of the row
             if ((k & 3) == 3) asm volatile("" ::: "memory");
+#endif
         }
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
         const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
         const T mu_t = T(mu_s);
+        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
+#if !GT_P3_EARLY_NV
         const T* N_ = in.nn(sg) + x * n;
         const T* V_ = in.v(sg) + x * n;
-        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
         asm volatile("" ::: "memory");  // keep the epilogue loads below the transform (registers)
         T nv[E], vv[E];
 #pragma unroll
@@ -868,6 +887,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
             nv[t] = N_[lane + 32 * t];
             vv[t] = V_[lane + 32 * t];
         }
+#endif
         __syncwarp();
 #pragma unroll
         for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
