@@ -127,6 +127,35 @@ gt_status gt_fp_batch_device(const gt_device_greens* d, const void* p_dyn, const
                              double* max_out, double* mean_out, void* stream);
 size_t gt_fp_scratch_bytes(int n, int precision);
 
+/* ---- Batched transient traces with the leakage update every step (config 3).
+ * Per trace b (north-star; oracle: the reference's time_varying_profile,
+ * solver.cpp:212-287, driven one step at a time):
+ *   P_n = P_dyn,n + L0 o f(T_{n-1}),  T_0 = 0,  f = 1 + beta dT (law 0, variation.cpp:213-222) or exp
+ *   T_n = max(0, windowed superposition over window k of P_1..P_n)   (with_rand off)
+ * P_dyn,n is piecewise constant over blocks: P_dyn,n(x,y) = sched[b][n-1][blk[b][x][y]]
+ * (per-cell watts). blk / leak0 with stride 0 are shared by all traces.
+ * T_n is stored for n = out_stride, 2 out_stride, ... into t_out[b][frame][n][n];
+ * max_out[b][frame] is its maximum. Spectra r = exp(-dt/tau), r^(k+1) and F_det
+ * come from the GreensSet (alpha, beta, mu, capacitance) exactly as for
+ * gt_solve_trace; a non-positive Re tau or a runaway F_det is GT_ERR_SOLVER. */
+typedef struct gt_trace_opts {
+    double dt;       /* seconds per step */
+    int steps;
+    int window;      /* k; <= 0 selects ceil(5 ms / dt) (solver.cpp:224-226); clipped to steps */
+    int law;         /* 0 linear, 1 exp */
+    double beta;     /* leakage temperature coefficient, 1/K */
+    int out_stride;  /* store every out_stride-th step (steps % out_stride frames) */
+    int chunk;       /* traces per in-flight chunk; 0 = auto */
+} gt_trace_opts;
+
+void gt_trace_opts_default(gt_trace_opts* o);
+/* Device arrays in the device precision (blk: int32). */
+gt_status gt_trace_batch_device(const gt_device_greens* d, const int* blk, long long blk_stride, const void* sched,
+                                int nblk, const void* leak0, long long leak_stride, int batch,
+                                const gt_trace_opts* opts, void* t_out, double* max_out, void* stream);
+/* Device scratch bytes per in-flight trace (power ring of window + 2 maps, spectral state). */
+size_t gt_trace_scratch_bytes(int n, int precision, int window);
+
 /* Bytes of device scratch a device-resident batch uses per in-flight sample,
  * and the number of kernels it launches for (batch, chunk). */
 size_t gt_mc_scratch_bytes(int n, int precision);

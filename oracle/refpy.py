@@ -78,6 +78,9 @@ def restate_lib() -> C.CDLL:
         L.ref_fixed_point_batch.restype = dbl
         L.ref_fixed_point_batch.argtypes = [C.POINTER(RefGreens), pdbl, pdbl, cint, dbl, dbl, cint, cint, dbl, dbl,
                                             dbl, cint, cint, pdbl, pint, pint]
+        L.ref_trace_leak_batch.restype = dbl
+        L.ref_trace_leak_batch.argtypes = [C.POINTER(RefGreens), C.POINTER(C.c_int), C.c_longlong, pdbl, cint, pdbl,
+                                           C.c_longlong, cint, dbl, cint, cint, cint, dbl, cint, cint, pdbl, pint]
         _RST = L
     return _RST
 
@@ -123,6 +126,25 @@ def fixed_point_batch(g, p_dyn, var, leak_frac=0.3, beta=0.017, law=1, kirchhoff
                                                t_ambient, eta, tol, max_iters, jobs or os.cpu_count() or 1, _p(out),
                                                it.ctypes.data_as(pint), st.ctypes.data_as(pint))
     return out, it, st, secs
+
+
+def trace_leak_batch(g, blk, sched, leak0, dt, window, law=0, beta=0.017, out_stride=1, jobs=None):
+    """Config-3 oracle: blk [B|1, n, n] int, sched [B, steps, nblk], leak0 [B|1, n, n].
+    Returns (frames [B, steps // out_stride, n, n], status, seconds)."""
+    k = _Keep(g)
+    blk = np.ascontiguousarray(blk, np.int32)
+    sched = np.ascontiguousarray(sched, np.float64)
+    leak0 = np.ascontiguousarray(leak0, np.float64)
+    B, steps, nblk = sched.shape
+    n = g.n
+    nn = n * n
+    out = np.zeros((B, steps // out_stride, n, n))
+    st = np.empty(B, np.int32)
+    secs = restate_lib().ref_trace_leak_batch(
+        C.byref(k.s), blk.ctypes.data_as(C.POINTER(C.c_int)), nn if blk.shape[0] > 1 else 0, _p(sched), nblk,
+        _p(leak0), nn if leak0.shape[0] > 1 else 0, B, dt, steps, window, law, beta, out_stride,
+        jobs or os.cpu_count() or 1, _p(out), st.ctypes.data_as(pint))
+    return out, st, secs
 
 
 def save_greens_dir(g, path) -> None:

@@ -269,4 +269,47 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+double ref_trace_leak_batch(const ref_greens* g, const int* blk, long long blk_stride, const double* sched,
+                            int nblk, const double* leak0, long long leak_stride, int batch, double dt, int steps,
+                            int window, int law, double beta, int out_stride, int jobs, double* t_out,
+                            int* status_out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const GreensSet gs = to_greens(g);
+    const int n = gs.n;
+    const size_t nn = static_cast<size_t>(n) * n;
+    const int frames = steps / out_stride;
+    pool(batch, jobs, [&](int b) {
+        int st = 0;
+        try {
+            const PreparedGreens pg(gs);
+            const int* bm = blk + b * blk_stride;
+            const double* l0 = leak0 + b * leak_stride;
+            PowerTrace tr;
+            tr.dt = dt;
+            std::vector<double> rise(nn, 0.0);
+            const FieldMap no_var;  // p_var of another shape: shift-variant term off
+            ProfileOptions opt;
+            opt.with_rand = false;
+            for (int s = 1; s <= steps; ++s) {
+                FieldMap P(n, gs.pitch, Unit::Watts);
+                const double* sc = sched + (static_cast<size_t>(b) * steps + (s - 1)) * nblk;
+                for (size_t k = 0; k < nn; ++k) {
+                    const double f = law == 0 ? 1.0 + beta * rise[k] : std::exp(beta * rise[k]);
+                    P.values()[k] = sc[bm[k]] + l0[k] * f;
+                }
+                tr.frames.push_back(std::move(P));
+                const ThermalResult res = time_varying_profile(pg, tr, window, no_var, opt);
+                const FieldMap& last = res.rise.back();
+                std::copy(last.values().begin(), last.values().end(), rise.begin());
+                if (s % out_stride == 0 && t_out)
+                    std::copy(rise.begin(), rise.end(), t_out + (static_cast<size_t>(b) * frames + s / out_stride - 1) * nn);
+            }
+        } catch (const Error& e) {
+            st = status_class(e);
+        }
+        if (status_out) status_out[b] = st;
+    });
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 }  // extern "C"

@@ -66,6 +66,19 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
                              double eta, double tol, int max_iters, int jobs, double* t_out,
                              int* iters_out, int* status_out);
 
+/* Config 3 (north star (5) + (4)): batched power traces with the leakage
+ * update every step, driven through the reference's own windowed superposition
+ * time_varying_profile (solver.cpp:212-287, with_rand off), one step at a time:
+ *   P_n = P_dyn,n + leak0 o f(T_{n-1}), T_0 = 0, f = 1 + beta dT (law 0,
+ *   leakage_at_temperature, variation.cpp:213-222) or exp(beta dT) (law 1);
+ *   T_n = last map of time_varying_profile(P_1..P_n, window)  (clamped >= 0)
+ * P_dyn,n(x,y) = sched[b][n-1][blk[b][x][y]]; blk/leak0 stride 0 = shared.
+ * T_n is stored every out_stride steps into t_out[b][frame]. Returns seconds. */
+double ref_trace_leak_batch(const ref_greens* g, const int* blk, long long blk_stride, const double* sched,
+                            int nblk, const double* leak0, long long leak_stride, int batch, double dt, int steps,
+                            int window, int law, double beta, int out_stride, int jobs, double* t_out,
+                            int* status_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,11 @@ SAMPLE_STATS_DTYPE = np.dtype([("sum_leak", "f8"), ("sum_applied", "f8"), ("sum_
                                ("max_bits", "u8"), ("status", "i4"), ("pad_", "i4")])
 
 # greentherm_b200.h
+class TraceOpts(C.Structure):
+    _fields_ = [("dt", dbl), ("steps", cint), ("window", cint), ("law", cint), ("beta", dbl),
+                ("out_stride", cint), ("chunk", cint)]
+
+
 _EXT = [
     ("gt_greens_from_arrays", cint, [cint, dbl, pdbl, pdbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, pdbl, pdbl,
                                      pdbl, pvp]),
@@ -116,6 +121,10 @@ _EXT = [
     ("gt_fp_batch", cint, [vp, vp, vp, cint, C.POINTER(FPOpts), vp, C.POINTER(cint), C.POINTER(cint), pdbl, pdbl]),
     ("gt_fp_batch_device", cint, [vp, vp, vp, cint, C.POINTER(FPOpts), vp, vp, vp, vp, vp, vp]),
     ("gt_fp_scratch_bytes", C.c_size_t, [cint, cint]),
+    ("gt_trace_opts_default", None, [C.POINTER(TraceOpts)]),
+    ("gt_trace_batch_device", cint, [vp, vp, C.c_longlong, vp, cint, vp, C.c_longlong, cint, C.POINTER(TraceOpts),
+                                     vp, vp, vp]),
+    ("gt_trace_scratch_bytes", C.c_size_t, [cint, cint, cint]),
     ("gt_profile_begin", cint, [vp]),
     ("gt_profile_end", cint, [vp, pdbl, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("gt_kernel_launches", C.c_longlong, [vp]),
@@ -309,6 +318,22 @@ class DeviceGreens:
                                       C.c_void_p(out_ptr), C.c_void_p(iters_ptr), C.c_void_p(status_ptr),
                                       C.c_void_p(max_ptr) if max_ptr else None,
                                       C.c_void_p(mean_ptr) if mean_ptr else None, sp))
+
+    def trace_opts(self, **kw) -> "TraceOpts":
+        o = TraceOpts()
+        lib().gt_trace_opts_default(C.byref(o))
+        for k, v in kw.items():
+            setattr(o, k, v)
+        return o
+
+    def trace_batch_device(self, blk_ptr, blk_stride, sched_ptr, nblk, leak_ptr, leak_stride, batch, opts, out_ptr,
+                           max_ptr=None, stream=None) -> None:
+        """Config-3 batched traces (include/greentherm_b200.h gt_trace_batch_device); device pointers."""
+        L = lib()
+        sp = None if stream is None else C.c_void_p(stream if stream else 1)
+        check(L, L.gt_trace_batch_device(self._d, C.c_void_p(blk_ptr), blk_stride, C.c_void_p(sched_ptr), nblk,
+                                         C.c_void_p(leak_ptr), leak_stride, batch, C.byref(opts),
+                                         C.c_void_p(out_ptr), C.c_void_p(max_ptr) if max_ptr else None, sp))
 
     def profile_begin(self) -> None:
         check(lib(), lib().gt_profile_begin(self._d))

@@ -585,6 +585,96 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
 }
 }  // namespace
 
+void gt_trace_opts_default(gt_trace_opts* o) {
+    if (!o) return;
+    o->dt = 1e-5;
+    o->steps = 2000;
+    o->window = 0;
+    o->law = 0;
+    o->beta = 0.017;
+    o->out_stride = 100;
+    o->chunk = 0;
+}
+
+size_t gt_trace_scratch_bytes(int n, int precision, int window) {
+    return gtd_trace_bytes_per_trace(n, precision == GT_FP64, window);
+}
+
+gt_status gt_trace_batch_device(const gt_device_greens* dc, const int* blk, long long blk_stride, const void* sched,
+                                int nblk, const void* leak0, long long leak_stride, int batch,
+                                const gt_trace_opts* opts, void* t_out, double* max_out, void* stream) {
+    return guarded([&] {
+        if (!dc || !opts || batch < 1 || !blk || !sched || !leak0 || !t_out || nblk < 1)
+            fail(ST_CONFIG, "capi", "trace batch needs block maps, schedule, leakage base and an output buffer");
+        if (!(opts->dt > 0.0)) fail(ST_CONFIG, "solver", "power trace dt must be positive");
+        if (opts->steps < 1) fail(ST_CONFIG, "solver", "power trace is empty");
+        if (opts->out_stride < 1 || opts->out_stride > opts->steps)
+            fail(ST_CONFIG, "capi", "out_stride must be in [1, steps]");
+        if (opts->law != 0 && opts->law != 1) fail(ST_CONFIG, "capi", "law must be 0 (linear) or 1 (exp)");
+        auto* d = const_cast<gt_device_greens*>(dc);
+        std::lock_guard<std::mutex> lk(d->mu);
+        const Greens& g = d->host;
+        if (!(g.capacitance > 0.0)) fail(ST_SOLVER, "solver", "GreensSet has no fitted capacitance");
+        const int n = g.n, m = 2 * n;
+        if (gtd_trace_pitch(n, d->fp64) < 0) fail(ST_CONFIG, "device", "trace batch supports n = 32..1024");
+        int k = opts->window > 0 ? opts->window : static_cast<int>(std::ceil(0.005 / opts->dt));  // solver.cpp:224-226
+        k = std::max(1, std::min(k, opts->steps));
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        // fp64 spectra exactly as gt_solve_trace: F_det at the set's mu, r = exp(-dt/tau), r^(k+1)
+        auto d64 = prepare_device(g, GT_FP64, d->device);
+        cudaStream_t s64 = d64->stream;
+        const size_t mm = static_cast<size_t>(m) * m;
+        DBuf Fd, r, rk, flag, red;
+        Fd.ensure(mm * 16);
+        r.ensure(mm * 16);
+        rk.ensure(mm * 16);
+        flag.ensure(sizeof(int) * 4);
+        red.ensure(sizeof(double) * 8);
+        cuda_ok(cudaMemsetAsync(flag.p, 0, sizeof(int) * 4, s64), "memset");
+        cuda_ok(gtd_fdet_full(d64->fk_full.p, d64->gtab.as<double>(), n, d64->d.hp, g.alpha, g.beta, g.mu, Fd.p,
+                              flag.as<int>(), s64),
+                "fdet");
+        double fk3[3];
+        cuda_ok(gtd_creduce(d64->fk_full.p, mm, red.as<double>(), s64), "creduce");
+        cuda_ok(cudaMemcpyAsync(fk3, red.p, sizeof fk3, cudaMemcpyDeviceToHost, s64), "d2h");
+        int fl = 0;
+        cuda_ok(cudaMemcpyAsync(&fl, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s64), "d2h");
+        cuda_ok(cudaStreamSynchronize(s64), "sync");
+        if (fl & GTD_ST_RUNAWAY_DET)
+            fail(ST_SOLVER, "greens",
+                 "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
+        cuda_ok(cudaMemsetAsync(flag.p, 0, sizeof(int), s64), "memset");
+        cuda_ok(gtd_transient(d64->fk_full.p, d64->gtab.as<double>(), Fd.p, n, d64->d.hp, g.alpha, g.capacitance,
+                              1e-6 * fk3[2], 0.0, nullptr, opts->dt, k, r.p, rk.p, flag.as<int>(), s64),
+                "transient");
+        cuda_ok(cudaMemcpyAsync(&fl, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s64), "d2h");
+        cuda_ok(cudaStreamSynchronize(s64), "sync");
+        if (fl & 1) fail(ST_SOLVER, "solver", "non-positive transient time constant");
+        d->trace_tab.ensure(gtd_trace_table_bytes(n, d->fp64));
+        cuda_ok(gtd_trace_tables(&d->d, Fd.p, r.p, rk.p, d->trace_tab.p, s64), "trace tables");
+        cuda_ok(cudaStreamSynchronize(s64), "sync");
+        // traces in flight: the power ring is (k + 2) maps per trace; up to 60% of free memory
+        const size_t per = gtd_trace_bytes_per_trace(n, d->fp64, k);
+        int chunk = opts->chunk > 0 ? std::min(opts->chunk, batch) : 0;
+        if (!chunk) {
+            size_t fr = 0, tot = 0;
+            cuda_ok(cudaMemGetInfo(&fr, &tot), "meminfo");
+            fr += d->trace_scratch.bytes;
+            chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(batch, (fr / 10 * 6) / per)));
+        }
+        d->trace_scratch.ensure(per * chunk);
+        gtd_trace_in in{blk, blk_stride, sched, nblk, opts->steps, leak0, leak_stride};
+        gtd_trace_opts o{k, opts->law, opts->beta, opts->out_stride};
+        long long launches = 0;
+        cuda_ok(gtd_trace_batch(&d->d, d->trace_tab.p, &in, batch, &o, t_out, max_out, d->trace_scratch.p, chunk, st,
+                                &launches),
+                "trace batch");
+        d->kernels += launches;
+        d->calls += 1;
+    });
+}
+
 gt_status gt_fp_batch_device(const gt_device_greens* dc, const void* p_dyn, const void* var, int batch,
                              const gt_fp_opts* opts, void* t_out, int* iters_out, int* status_out, double* max_out,
                              double* mean_out, void* stream) {

@@ -105,10 +105,11 @@ struct InvLayout {
     }
 };
 
-// One inverse Stockham stage over the (Y, R) column pairs (swizzled layout).
-template <typename T, int M, int W, int NT, int S>
-__device__ __forceinline__ void inv_stage_pairs(cplx<T>* tile, const cplx<T>* twi) {
-    using ST = StageTw<M, true>;
+// One Stockham stage (forward plan if !INV, inverse plan if INV) over the
+// line pairs of an InvLayout tile (W pairs per row).
+template <typename T, int M, int W, int NT, int S, bool INV>
+__device__ __forceinline__ void pair_stage(cplx<T>* tile, const cplx<T>* tws) {
+    using ST = StageTw<M, INV>;
     constexpr int R = ST::R(S), NS = ST::NS(S);
     constexpr int NB = (M / R) * W;
     static_assert(NB % NT == 0, "pair butterflies must divide evenly over threads");
@@ -124,9 +125,9 @@ __device__ __forceinline__ void inv_stage_pairs(cplx<T>* tile, const cplx<T>* tw
             v[b][0][r] = q.a;
             v[b][1][r] = q.b;
         }
-        stage_twiddle<T, M, true, S, 2>(v[b], j, twi);
-        dftR<R, +1, T>(v[b][0]);
-        dftR<R, +1, T>(v[b][1]);
+        stage_twiddle<T, M, INV, S, 2>(v[b], j, tws);
+        dftR<R, INV ? +1 : -1, T>(v[b][0]);
+        dftR<R, INV ? +1 : -1, T>(v[b][1]);
     }
     __syncthreads();
 #pragma unroll
@@ -142,12 +143,12 @@ __device__ __forceinline__ void inv_stage_pairs(cplx<T>* tile, const cplx<T>* tw
     __syncthreads();
 }
 
-template <typename T, int M, int W, int NT, int S, int E>
+template <typename T, int M, int W, int NT, int S, int E, bool INV = true>
 struct InvStagesPairs {
-    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* twi) {
+    __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* tws) {
         if constexpr (S < E) {
-            inv_stage_pairs<T, M, W, NT, S>(tile, twi);
-            InvStagesPairs<T, M, W, NT, S + 1, E>::run(tile, twi);
+            pair_stage<T, M, W, NT, S, INV>(tile, tws);
+            InvStagesPairs<T, M, W, NT, S + 1, E, INV>::run(tile, tws);
         }
     }
 };

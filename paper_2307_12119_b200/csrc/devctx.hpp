@@ -57,6 +57,7 @@ struct gt_device_greens {
     // batch scratch (guarded by mu)
     std::mutex mu;
     gth::DBuf fp_scratch, fp_state, fp_counter;
+    gth::DBuf trace_scratch, trace_tab;
     int* fp_counter_h = nullptr;
     gth::DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
     cudaStream_t slot_stream[2] = {nullptr, nullptr};

@@ -141,6 +141,29 @@ typedef struct gtd_fp_opts {
     int poll;         /* host convergence poll interval in iterations (0 = 4) */
 } gtd_fp_opts;
 size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64);
+
+/* ---- config-3 batched transient traces (trace_batch.cu) */
+typedef struct gtd_trace_in {
+    const int* blk;
+    long long blk_stride; /* elements between traces' block maps (0: shared) */
+    const void* sched;    /* [B][steps][nblk] per-cell watts, device precision */
+    int nblk, steps;
+    const void* leak0;    /* [B][n*n] leakage base L0 (device precision) */
+    long long leak_stride;
+} gtd_trace_in;
+typedef struct gtd_trace_opts {
+    int window; /* k >= 1 */
+    int law;
+    double beta;
+    int out_stride;
+} gtd_trace_opts;
+int gtd_trace_pitch(int n, int fp64);
+size_t gtd_trace_bytes_per_trace(int n, int fp64, int window);
+size_t gtd_trace_table_bytes(int n, int fp64);
+/* tab = {(1 - r) F, r, r^(k+1) F} half width, from fp64 full (m x m) F_det, r, r^(k+1). */
+int gtd_trace_tables(const gtd_greens* g, const void* Fd, const void* r, const void* rk, void* tab, cudaStream_t st);
+int gtd_trace_batch(const gtd_greens* g, const void* tab, const gtd_trace_in* in, int batch, const gtd_trace_opts* o,
+                    void* t_out, double* max_out, void* scratch, int chunk, cudaStream_t st, long long* launches);
 size_t gtd_fp_state_bytes(void);
 /* t_state: [B][n][n] rise maps (state and result); iters/status: [B] device ints;
  * max_out/mean_out: [B] device doubles (may be NULL); state: B * gtd_fp_state_bytes();

@@ -152,19 +152,33 @@ def mc_inputs(cfg: Config, start: int, count: int, device: str = "cpu", torch_dt
     return p, v
 
 
-def markov_trace(cfg: Config, index: int, steps: int, switch_prob: float = 1.0 / 50.0,
-                 off_frac: float = 0.1) -> np.ndarray:
-    """(steps, n, n) W/cell: per-block two-state Markov chain (on density
-    U[0.5, 2] W/mm^2 drawn once per block, off at off_frac of it)."""
+def markov_blocks(cfg: Config, index: int, steps: int, switch_prob: float = 1.0 / 50.0,
+                  off_frac: float = 0.1):
+    """Compact form of trace `index`: per-block two-state Markov chain (on
+    density U[0.5, 2] W/mm^2 drawn once per block, off at off_frac of it,
+    switching with probability switch_prob per step = mean dwell 50 steps).
+    Returns (blk (n, n) int32 block ids, sched (steps, nblk) W/cell per block and
+    step, on (n, n) W/cell of the all-on state)."""
     rng = np.random.default_rng(sample_seed(cfg.base_seed, PURPOSE_TRACE, index))
     n, pm = cfg.n, cfg.pitch_mm
     blocks = guillotine_blocks(n, cfg.blocks, rng)
     on = rng.uniform(0.5, 2.0, size=len(blocks))
     state = rng.random(len(blocks)) < 0.5
-    out = np.empty((steps, n, n))
+    blk = np.zeros((n, n), np.int32)
+    on_map = np.zeros((n, n))
+    for b, (r0, r1, c0, c1) in enumerate(blocks):
+        blk[r0:r1, c0:c1] = b
+        on_map[r0:r1, c0:c1] = on[b] * pm * pm
+    sched = np.empty((steps, len(blocks)))
     for t in range(steps):
         flip = rng.random(len(blocks)) < switch_prob
         state = np.where(flip, ~state, state)
-        for b, (r0, r1, c0, c1) in enumerate(blocks):
-            out[t, r0:r1, c0:c1] = on[b] * (1.0 if state[b] else off_frac) * pm * pm
-    return out
+        sched[t] = on * np.where(state, 1.0, off_frac) * pm * pm
+    return blk, sched, on_map
+
+
+def markov_trace(cfg: Config, index: int, steps: int, switch_prob: float = 1.0 / 50.0,
+                 off_frac: float = 0.1) -> np.ndarray:
+    """(steps, n, n) W/cell frames of trace `index` (markov_blocks expanded)."""
+    blk, sched, _ = markov_blocks(cfg, index, steps, switch_prob, off_frac)
+    return sched[:, blk]
