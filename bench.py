@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mode-b", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the config-3 transient-trace sub-benchmark")
+    ap.add_argument("--cfg3-steps", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -208,6 +210,92 @@ def run_reference_arm(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU arm
+def device_calibrated_greens(n):
+    """GreensSet from this library's device calibration (modal kernel producer,
+    pinned against the reference calibrate() in tests/test_calib_gpu.py)."""
+    import ctypes as C
+    import tempfile
+    from paper_2307_12119_b200.api import GreensArrays, lib
+    L = lib()
+    d = Path(tempfile.mkdtemp())
+    (d / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    (d / "var.txt").write_text("dopant_spread 0\nbeta 0.017\n")
+    g = C.c_void_p()
+    if L.gt_calibrate(str(d / "stack.txt").encode(), str(d / "var.txt").encode(), None, 90.0, C.byref(g), None):
+        raise RuntimeError(L.gt_last_error().decode())
+    maps = {}
+    for k in ("f_sp0", "g_sp0"):
+        f = C.c_void_p()
+        L.gt_greens_field(g, k.encode(), C.byref(f))
+        maps[k] = np.ctypeslib.as_array(L.gt_field_data(f), shape=(n, n)).copy()
+        L.gt_field_free(f)
+    f = maps["f_sp0"]
+    ga = GreensArrays(n=n, pitch=0.016 / n, f_sp0=f, g_sp0=maps["g_sp0"],
+                      phi=float(np.mean(np.concatenate([f[0], f[-1], f[1:-1, 0], f[1:-1, -1]]))),
+                      kappa_inf=float(f[0, 0]), alpha=L.gt_greens_alpha(g), beta=0.017, mu=L.gt_greens_mu(g),
+                      capacitance=L.gt_greens_capacitance(g), rand_scale=1.0)
+    L.gt_greens_free(g)
+    return ga
+
+
+def run_cfg3(args, dev, ws, rank):
+    """Config 3: 64 Markov power traces x 2000 steps at 512x512, dt = 10 us, window k = 500,
+    leakage (0.3 x on-state power x variation map, linear law, beta 0.017) updated every step,
+    T stored every 100 steps. Traces are sharded over ranks (weak: 64 per GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2307_12119_b200 import inputs, shard
+    from paper_2307_12119_b200.api import GT_FP32, GT_FP64, DeviceGreens
+    c3 = inputs.CONFIGS["cfg3"]
+    n, B, steps, k, stride = c3.n, c3.batch, args.cfg3_steps, 500, 100
+    prec = GT_FP32 if args.precision == "fp32" else GT_FP64
+    es = 4 if prec == GT_FP32 else 8
+    dt_t = torch.float32 if prec == GT_FP32 else torch.float64
+    ga = device_calibrated_greens(n)
+    b0 = rank * B
+    blks, scheds, ons = zip(*(inputs.markov_blocks(c3, b0 + b, steps) for b in range(B)))
+    nblk = max(s.shape[1] for s in scheds)
+    sched = np.zeros((B, steps, nblk))
+    for b, sc in enumerate(scheds):
+        sched[b, :, :sc.shape[1]] = sc
+    var = inputs.variation_batch(c3, b0, B, device=dev, dtype=dt_t)
+    leak0 = torch.from_numpy(0.3 * np.stack(ons)).to(dev, dt_t) * var
+    blk = torch.from_numpy(np.stack(blks)).to(dev)
+    sch = torch.from_numpy(sched).to(dev, dt_t)
+    dg = DeviceGreens(ga, prec, device=dev.index or 0)
+    frames = steps // stride
+    out = torch.zeros((B, frames, n, n), dtype=dt_t, device=dev)
+    mx = torch.zeros((B, frames), dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(dev)
+
+    def once(nsteps):
+        o = dg.trace_opts(dt=1e-5, steps=nsteps, window=min(k, nsteps), law=0, beta=0.017,
+                          out_stride=min(stride, nsteps))
+        dg.trace_batch_device(blk.data_ptr(), n * n, sch.data_ptr(), nblk, leak0.data_ptr(), n * n, B, o,
+                              out.data_ptr(), mx.data_ptr(), stream.cuda_stream)
+
+    once(min(steps, 20))  # warm-up: module load, tables, scratch
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    once(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), dev)
+    m, h = 2 * n, n + 1
+    b_ts = 4 * es * m * h + 8 * es * n * h + 4 * es * n * n  # DESIGN.md §4 config-3 per trace-step model
+    rate = ws * B * steps / (ms / 1e3)
+    dg.close()
+    return {"value": rate, "unit": "trace-steps/s", "traces_per_gpu": B, "steps": steps, "window": k,
+            "dt_s": 1e-5, "out_stride": stride, "n": n, "ms": ms, "ms_per_step": ms / steps,
+            "peak_K": float(mx.max().item()), "bytes_per_trace_step_model": b_ts,
+            "achieved_GBps_model": b_ts * rate / ws / 1e9,
+            "greens": "device calibration at n=512 (modal kernel, capacitance fit)",
+            "leakage": "L0 = 0.3 x on-state block power x variation map (sigma/mu 0.10), linear law, every step"}
+
+
 def run_b200(args, cfg):
     import torch
     import torch.distributed as dist
@@ -359,6 +447,10 @@ def run_b200(args, cfg):
                            "bytes_per_iteration_model": b_it,
                            "achieved_GBps_model": b_it * float(its.sum()) / (msb / 1e3) / 1e9}}
 
+    cfg3 = None
+    if not args.no_cfg3:
+        cfg3 = run_cfg3(args, dev, ws, rank)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_rate(cfg, args.cpu_seconds, os.cpu_count() or 1)
@@ -388,6 +480,8 @@ def run_b200(args, cfg):
             line["e2e"] = e2e
         if mode_b:
             line["mode_b"] = mode_b
+        if cfg3:
+            line["cfg3"] = cfg3
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
