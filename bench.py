@@ -137,8 +137,8 @@ def bytes_per_sample(n: int, es: int) -> list[float]:
     pass: h = n+1 half-spectrum columns."""
     h = n + 1
     cb = 2 * es
-    p1 = 2 * es * n * n + 2 * cb * n * h + es * n * h      # P,var in; A,B half spectra + S out
-    p2 = (2 * cb + es) * n * h + 2 * cb * n * h             # A,B,S in; Y',R' out
+    p1 = 2 * es * n * n + (2 * es + cb) * n * h             # P,var in; real DCT part of A, B, S out
+    p2 = (2 * es + cb) * n * h + 2 * cb * n * h             # A~,B,S in; Y,R out
     p3 = 2 * cb * n * h + 2 * es * n * n + es * n * n       # Y',R' + P,var in; T out
     return [p1, p2, p3]
 
