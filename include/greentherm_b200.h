@@ -156,6 +156,31 @@ gt_status gt_trace_batch_device(const gt_device_greens* d, const int* blk, long 
 /* Device scratch bytes per in-flight trace (power ring of window + 2 maps, spectral state). */
 size_t gt_trace_scratch_bytes(int n, int precision, int window);
 
+/* ---- Large single grid (config 4), fp64, one slab of a multi-GPU solve per call.
+ * The mode-B fixed point of gt_fp_batch on ONE map of side n (m = 2n = M1 * M2,
+ * four-step transforms), split into three phases so a driver can place an
+ * all-to-all transpose between the row and the column phases
+ * (paper_2307_12119_b200/slab.py). All pointers are device pointers; the
+ * device GreensSet must be GT_FP64.
+ *   rows_fwd : applied rows [2 pairs][n] -> Z [pairs][m] (spectra of the
+ *              mirrored rows, two rows per line); s1 = pairs x m complex scratch
+ *   cols     : Z of ALL pairs (compact = 0: [n/2][m]; 1: [n/2][2 hc] columns
+ *              c0.. and their mirrors m - c0 - c) -> y [n][hc] = rows [0, n) of
+ *              IFFT_col(fk . FFT_col(.)) for half-spectrum columns [c0, c0+hc);
+ *              c1, c2 = m x hc complex scratch
+ *   rows_inv : y [2 pairs][hy] (columns 0..n) -> theta -> T (t, [2 pairs][n], in
+ *              place: old T in, new T out) -> next applied rows P + L0 f(T);
+ *              max |T_new - T_old| is atomically max-ed into res_bits (double
+ *              bits), sample status bits OR-ed into *status. */
+gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2);
+gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
+                            void* stream);
+gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, int c0, int hc, void* c1, void* c2,
+                        void* y, void* stream);
+gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
+                            double* app, const double* p, const double* l0, const gt_fp_opts* opts,
+                            unsigned long long* res_bits, int* status, void* stream);
+
 /* Bytes of device scratch a device-resident batch uses per in-flight sample,
  * and the number of kernels it launches for (batch, chunk). */
 size_t gt_mc_scratch_bytes(int n, int precision);

@@ -585,6 +585,65 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
 }
 }  // namespace
 
+namespace {
+gtd_lg large_geom(const gt_device_greens* d) {
+    if (!d) fail(ST_CONFIG, "capi", "null device GreensSet");
+    if (!d->fp64) fail(ST_CONFIG, "device", "the large-grid path runs in fp64: prepare the GreensSet with GT_FP64");
+    gtd_lg g{};
+    g.n = d->d.n;
+    g.m = d->d.m;
+    if (gtd_lg_split(g.m, &g.M1, &g.M2))
+        fail(ST_CONFIG, "device", "the large-grid path needs a power-of-two grid with m = 2n in [1024, 262144]");
+    g.tw = d->tw64.p;
+    g.fk = d->fk.p;
+    g.fkp = d->d.hp;
+    return g;
+}
+}  // namespace
+
+gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (m1) *m1 = g.M1;
+        if (m2) *m2 = g.M2;
+    });
+}
+
+gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
+                            void* stream) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        cuda_ok(gtd_lg_rows_fwd(&g, app, pairs, s1, z, static_cast<cudaStream_t>(stream)), "large rows fwd");
+    });
+}
+
+gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, int c0, int hc, void* c1, void* c2,
+                        void* y, void* stream) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (c0 < 0 || hc < 1 || c0 + hc > g.n + 1) fail(ST_CONFIG, "capi", "column range outside [0, n]");
+        cuda_ok(gtd_lg_cols(&g, z, compact, c0, hc, c1, c2, y, static_cast<cudaStream_t>(stream)), "large cols");
+    });
+}
+
+gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
+                            double* app, const double* p, const double* l0, const gt_fp_opts* opts,
+                            unsigned long long* res_bits, int* status, void* stream) {
+    return guarded([&] {
+        if (!opts) fail(ST_CONFIG, "capi", "large rows_inv needs fixed-point options");
+        const gtd_lg g = large_geom(d);
+        gtd_fp_opts o{};
+        o.law = opts->law;
+        o.kirchhoff = opts->kirchhoff;
+        o.beta = opts->beta;
+        o.t_ambient = opts->t_ambient;
+        o.eta = opts->eta;
+        cuda_ok(gtd_lg_rows_inv(&g, y, hy, pairs, s1, t, app, p, l0, &o, res_bits, status,
+                                static_cast<cudaStream_t>(stream)),
+                "large rows inv");
+    });
+}
+
 void gt_trace_opts_default(gt_trace_opts* o) {
     if (!o) return;
     o->dt = 1e-5;

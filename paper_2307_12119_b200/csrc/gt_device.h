@@ -142,6 +142,28 @@ typedef struct gtd_fp_opts {
 } gtd_fp_opts;
 size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64);
 
+/* ---- config 4: large-grid mode B by four-step passes (large.cu), fp64.
+ * m = M1 * M2 (gtd_lg_split); rows phase on `pairs` die-row pairs of a slab,
+ * columns phase on half-spectrum columns [c0, c0 + hc) of all rows. */
+typedef struct gtd_lg {
+    int n, m, M1, M2;
+    const void* tw; /* [m] double2 exp(-2 pi i t / m) */
+    const void* fk; /* [m][fkp] double2 baseline kernel half spectrum */
+    int fkp;
+} gtd_lg;
+int gtd_lg_split(int m, int* M1, int* M2);
+/* applied rows [2 pairs][n] -> Z [pairs][m] (mirrored rows' spectra, two rows per line) */
+int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st);
+/* Z (all pairs) -> Y [n][hc] = rows [0,n) of IFFT_col(fk . FFT_col(mirror(A))) for columns c0..c0+hc.
+ * compact = 0: Z is [n/2][m]; 1: Z is [n/2][2 hc] = (Z_p[c0 + c], Z_p[(m - c0 - c) mod m]) per column c. */
+int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, void* C1, void* C2, void* Y,
+                cudaStream_t st);
+/* Y [2 pairs][hy] (all columns 0..n of the slab's rows) -> theta -> T (Tst), residual (max bits),
+ * status bits, next applied rows */
+int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1, double* Tst, double* app,
+                    const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
+                    int* status, cudaStream_t st);
+
 /* ---- config-3 batched transient traces (trace_batch.cu) */
 typedef struct gtd_trace_in {
     const int* blk;

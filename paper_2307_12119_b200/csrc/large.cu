@@ -1,0 +1,378 @@
+// large.cu — config 4: the mode-B leakage fixed point on a single large grid
+// (n up to 8192, m = 16384), fp64, as seven four-step FFT passes per iteration,
+// each usable on a slab of rows or columns so that a multi-GPU driver can put an
+// all-to-all transpose between the row and the column phases.
+//
+// Same math as fixed_point.cu (oracle: oracle/restate.cpp ref_fixed_point_batch):
+//   theta - T0 = crop(IFFT(fk . FFT(mirror(P + L0 f(T)))))
+// A length-m line transform is split four-step, m = M1 M2, i = i1 + M1 i2,
+// k = k2 + M2 k1:
+//   forward : FFT_M2 over i2 (per i1) x W_m^{i1 k2}, then FFT_M1 over i1 (per k2)
+//   inverse : IFFT_M1 over k1 (per k2) x W_m^{-i_a k2}, then IFFT_M2 over k2 (per
+//             i_a), output i = i_a + M1 i_b
+// and every sub-transform runs in the shared-memory tile engine (fft_tile.cuh)
+// on L lines at a time, with the passes' loads and stores coalesced across the
+// L lines. Passes per iteration (p = die-row pair, v = half-spectrum column):
+//   rows   : FwdA (applied rows, mirrored, two rows per line) -> S1 -> FwdB -> Z
+//   columns: ColA (split Z into the rows' half spectra, mirror) -> C1 -> ColB
+//            (forward, x fk, inverse) -> C2 -> ColC (rows [0, n)) -> Y
+//   rows   : RinvA (Hermitian merge of two rows) -> S1 -> RinvB (theta -> T,
+//            residual, next applied rows)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fft_tile.cuh"
+#include "gt_device.h"
+
+namespace gtb {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ cplx<T> twm(const double2* __restrict__ tw, int M, long long e, bool inv) {
+    const double2 w = tw[e & (M - 1)];
+    return mk<T>(T(w.x), T(inv ? -w.y : w.y));
+}
+
+// ------------------------------------------------------------------ pass ops
+template <typename T>
+struct FwdA {
+    static constexpr bool REDUCE = false;  // group p (row pair), line i1, j = i2
+    static constexpr int SIGN = -1;
+    static constexpr bool LINE_FAST = true;
+    const T* app;  // [rows][n] applied power, rows of this slab
+    cplx<T>* S1;   // [pairs][m]
+    const double2* tw;
+    int n, M, M1;
+    __device__ cplx<T> load(int p, int i1, int j) const {
+        const int i = i1 + M1 * j, y = i < n ? i : M - 1 - i;
+        return mk<T>(app[static_cast<size_t>(2 * p) * n + y], app[static_cast<size_t>(2 * p + 1) * n + y]);
+    }
+    __device__ void store(int p, int i1, int k2, cplx<T> v) const {
+        S1[static_cast<size_t>(p) * M + i1 + static_cast<size_t>(M1) * k2] =
+            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(i1) * k2, false));
+    }
+};
+
+template <typename T>
+struct FwdB {
+    static constexpr bool REDUCE = false;  // group p, line k2, j = i1
+    static constexpr int SIGN = -1;
+    static constexpr bool LINE_FAST = false;
+    const cplx<T>* S1;
+    cplx<T>* Z;  // [pairs][m] natural order spectra of (row 2p) + i (row 2p+1), mirrored
+    int M, M1, M2;
+    __device__ cplx<T> load(int p, int k2, int j) const {
+        return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M1) * k2];
+    }
+    __device__ void store(int p, int k2, int k1, cplx<T> v) const {
+        Z[static_cast<size_t>(p) * M + k2 + static_cast<size_t>(M2) * k1] = v;
+    }
+};
+
+template <typename T>
+struct ColA {
+    static constexpr bool REDUCE = false;  // group i1, line = local column c (v = c0 + c), j = i2
+    static constexpr int SIGN = -1;
+    static constexpr bool LINE_FAST = true;
+    // Spectra of ALL row pairs: Z[p zs + oa + c] = Z_p[v], Z[p zs + ((ob + sb c) & mask)] = Z_p[m - v].
+    // Full layout (one GPU): zs = m, oa = c0, ob = m - c0, sb = -1, mask = m - 1.
+    // Compact layout (after the all-to-all): zs = 2 hc, oa = 0, ob = hc, sb = +1, mask = ~0.
+    const cplx<T>* Z;
+    cplx<T>* C1;  // [m][hc] (row i1 + M1 k2)
+    const double2* tw;
+    int n, M, M1, c0, hc;
+    long long zs;
+    int oa, ob, sb, mask;
+    __device__ cplx<T> load(int i1, int c, int j) const {
+        const int i = i1 + M1 * j, x = i < n ? i : M - 1 - i;
+        const cplx<T>* Zp = Z + static_cast<size_t>(x >> 1) * zs;
+        const cplx<T> a = Zp[oa + c], b = cconj<T>(Zp[(ob + sb * c) & mask]);
+        // half spectra of the two real rows packed in Zp (x even: real part's, odd: imaginary part's)
+        return (x & 1) ? mk<T>(T(0.5) * (a.y - b.y), T(-0.5) * (a.x - b.x))
+                       : mk<T>(T(0.5) * (a.x + b.x), T(0.5) * (a.y + b.y));
+    }
+    __device__ void store(int i1, int c, int k2, cplx<T> v) const {
+        C1[(static_cast<size_t>(i1) + static_cast<size_t>(M1) * k2) * hc + c] =
+            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(i1) * k2, false));
+    }
+};
+
+template <typename T>
+struct ColB {
+    static constexpr bool REDUCE = false;  // group k2, line c, j = i1; forward -> x fk -> inverse over k1
+    static constexpr int SIGN = -1;
+    static constexpr bool LINE_FAST = true;
+    const cplx<T>* C1;
+    cplx<T>* C2;  // [m][hc] (row k2 + M2 i_a)
+    const cplx<T>* fk;
+    int fkp;
+    const double2* tw;
+    int h, M, M1, M2, c0, hc;
+    __device__ cplx<T> load(int k2, int c, int j) const {
+        return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
+    }
+    __device__ cplx<T> mid(int k2, int c, int k1, cplx<T> v) const {
+        const int u = k2 + M2 * k1, vv = c0 + c;
+        return vv < h ? cmul<T>(v, fk[static_cast<size_t>(u) * fkp + vv]) : mk<T>(T(0), T(0));
+    }
+    __device__ void store(int k2, int c, int ia, cplx<T> v) const {
+        C2[(static_cast<size_t>(k2) + static_cast<size_t>(M2) * ia) * hc + c] =
+            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(ia) * k2, true));
+    }
+};
+
+template <typename T>
+struct ColC {
+    static constexpr bool REDUCE = false;  // group i_a, line c, j = k2; output rows i = i_a + M1 i_b < n
+    static constexpr int SIGN = +1;
+    static constexpr bool LINE_FAST = true;
+    const cplx<T>* C2;
+    cplx<T>* Y;  // [n][hc]
+    int n, M, M1, M2, hc;
+    __device__ cplx<T> load(int ia, int c, int j) const {
+        return C2[(static_cast<size_t>(j) + static_cast<size_t>(M2) * ia) * hc + c];
+    }
+    __device__ void store(int ia, int c, int ib, cplx<T> v) const {
+        const int i = ia + M1 * ib;
+        if (i < n) Y[static_cast<size_t>(i) * hc + c] = v;
+    }
+};
+
+template <typename T>
+struct RinvA {
+    static constexpr bool REDUCE = false;  // group p, line k2, j = k1: Hermitian merge of rows 2p, 2p+1
+    static constexpr int SIGN = +1;
+    static constexpr bool LINE_FAST = true;
+    const cplx<T>* Y;  // [rows][hy] all columns of this slab's rows (after the transpose back)
+    cplx<T>* S1;
+    const double2* tw;
+    int n, M, M2, hy;
+    __device__ cplx<T> load(int p, int k2, int j) const {
+        const int f = k2 + M2 * j, w = f <= n ? f : M - f;
+        const cplx<T> y = Y[static_cast<size_t>(2 * p) * hy + w], r = Y[static_cast<size_t>(2 * p + 1) * hy + w];
+        if (f == 0 || f == n) return mk<T>(y.x, r.x);
+        return f < n ? mk<T>(y.x - r.y, y.y + r.x) : mk<T>(y.x + r.y, r.x - y.y);
+    }
+    __device__ void store(int p, int k2, int ia, cplx<T> v) const {
+        S1[static_cast<size_t>(p) * M + k2 + static_cast<size_t>(M2) * ia] =
+            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(ia) * k2, true));
+    }
+};
+
+template <typename T>
+struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
+    static constexpr bool REDUCE = true;
+    static constexpr int SIGN = +1;
+    static constexpr bool LINE_FAST = false;
+    const cplx<T>* S1;
+    T* Tst;        // [rows][n] rise state
+    T* app;        // [rows][n] next applied
+    const T* P;    // [rows][n]
+    const T* L0;   // [rows][n]
+    unsigned long long* res_bits;
+    int* status;
+    int n, M, M1, M2, law, kirchhoff;
+    T beta, ka, kb, kexp, t_ambient, inv;
+    __device__ cplx<T> load(int p, int ia, int j) const {
+        return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M2) * ia];
+    }
+    __device__ void store(int p, int ia, int ib, cplx<T> v, double& dmax, int& bad) const {
+        const int i = ia + M1 * ib;
+        if (i >= n) return;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const size_t o = static_cast<size_t>(2 * p + half) * n + i;
+            T t = (half ? v.y : v.x) * inv;
+            if (kirchhoff) {
+                const T br = ka + kb * t;
+                if (!(br > T(0))) bad |= GTD_ST_KIRCHHOFF;
+                t = pow(br, kexp) - t_ambient;
+            }
+            if (!isfinite(t)) bad |= GTD_ST_NONFINITE;
+            dmax = fmax(dmax, double(fabs(t - Tst[o])));
+            Tst[o] = t;
+            const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
+            app[o] = P[o] + L0[o] * f;
+        }
+    }
+};
+
+// ------------------------------------------------------------------ generic pass
+// L lines of N points per work item; items = groups x ceil(nlines / L).
+template <typename T, int N, class Op, bool TWO>
+__global__ void __launch_bounds__(TileGeom<T, N>::NT, TileGeom<T, N>::MINB)
+lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines) {
+    using G = TileGeom<T, N>;
+    constexpr int L = G::L, LP = L + 2, NT = G::NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + N * LP;
+    for (int t = threadIdx.x; t < N; t += NT) {
+        const double2 w = twm_g[static_cast<size_t>(t) * (M / N)];
+        s_tw[t] = mk<T>(T(w.x), T(w.y));
+    }
+    const int bpg = (nlines + L - 1) / L;
+    for (int item = blockIdx.x; item < groups * bpg; item += gridDim.x) {
+        const int g = item / bpg, l0 = (item - g * bpg) * L;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+            int l, j;
+            if constexpr (Op::LINE_FAST) {
+                l = idx % L;
+                j = idx / L;
+            } else {
+                j = idx % N;
+                l = idx / N;
+            }
+            tile[j * LP + l] = l0 + l < nlines ? op.load(g, l0 + l, j) : mk<T>(T(0), T(0));
+        }
+        __syncthreads();
+        tile_fft<T, N, L, LP, NT, Op::SIGN>(tile, s_tw);
+        if constexpr (TWO) {
+            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+                const int l = idx % L, k = idx / L;
+                if (l0 + l < nlines) tile[k * LP + l] = op.mid(g, l0 + l, k, tile[k * LP + l]);
+            }
+            __syncthreads();
+            tile_fft<T, N, L, LP, NT, -Op::SIGN>(tile, s_tw);
+        }
+        if constexpr (Op::REDUCE) {
+            double dmax = 0.0;
+            int bad = 0;
+            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+                const int l = idx % L, k = idx / L;
+                if (l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l], dmax, bad);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+            bad = __reduce_or_sync(0xffffffffu, bad);
+            if ((threadIdx.x & 31) == 0) {
+                atomicMax(op.res_bits, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+                if (bad) atomicOr(op.status, bad);
+            }
+        } else {
+            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+                const int l = idx % L, k = idx / L;
+                if (l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l]);
+            }
+        }
+    }
+}
+
+template <typename T, int N>
+size_t lg_smem() {
+    return sizeof(cplx<T>) * (N * (TileGeom<T, N>::L + 2) + N);
+}
+
+template <typename T, int N, class Op, bool TWO>
+int launch_n(const Op& op, const double2* tw, int M, int groups, int nlines, cudaStream_t st) {
+    static int res = 0, sms = 0;
+    auto k = lg_pass<T, N, Op, TWO>;
+    if (!sms) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lg_smem<T, N>()));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k, TileGeom<T, N>::NT, lg_smem<T, N>());
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = res < 1 ? 1 : res;
+    }
+    const int items = groups * ((nlines + TileGeom<T, N>::L - 1) / TileGeom<T, N>::L);
+    const int grid = items < sms * res ? items : sms * res;
+    if (grid > 0) k<<<grid, TileGeom<T, N>::NT, lg_smem<T, N>(), st>>>(op, tw, M, groups, nlines);
+    return static_cast<int>(cudaGetLastError());
+}
+
+template <typename T, class Op, bool TWO = false>
+int launch(int N, const Op& op, const double2* tw, int M, int groups, int nlines, cudaStream_t st) {
+    switch (N) {
+        case 32: return launch_n<T, 32, Op, TWO>(op, tw, M, groups, nlines, st);
+        case 64: return launch_n<T, 64, Op, TWO>(op, tw, M, groups, nlines, st);
+        case 128: return launch_n<T, 128, Op, TWO>(op, tw, M, groups, nlines, st);
+        case 256: return launch_n<T, 256, Op, TWO>(op, tw, M, groups, nlines, st);
+        case 512: return launch_n<T, 512, Op, TWO>(op, tw, M, groups, nlines, st);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
+}  // namespace
+}  // namespace gtb
+
+using namespace gtb;
+
+extern "C" {
+
+int gtd_lg_split(int m, int* M1, int* M2) {
+    int lg = 0;
+    while ((1 << lg) < m) ++lg;
+    if ((1 << lg) != m || m < 1024 || m > 262144) return static_cast<int>(cudaErrorInvalidValue);
+    *M1 = 1 << ((lg + 1) / 2);
+    *M2 = 1 << (lg / 2);
+    return 0;
+}
+
+int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st) {
+    FwdA<double> a{app, static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M1};
+    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
+    if (e) return e;
+    FwdB<double> b{static_cast<const double2*>(S1), static_cast<double2*>(Z), g->m, g->M1, g->M2};
+    return launch<double>(g->M1, b, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
+}
+
+int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, void* C1, void* C2, void* Y,
+                cudaStream_t st) {
+    ColA<double> a{static_cast<const double2*>(Z), static_cast<double2*>(C1), static_cast<const double2*>(g->tw),
+                   g->n, g->m, g->M1, c0, hc};
+    if (compact) {
+        a.zs = 2LL * hc;
+        a.oa = 0;
+        a.ob = hc;
+        a.sb = 1;
+        a.mask = 0x7fffffff;
+    } else {
+        a.zs = g->m;
+        a.oa = c0;
+        a.ob = g->m - c0;
+        a.sb = -1;
+        a.mask = g->m - 1;
+    }
+    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
+    if (e) return e;
+    ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
+                   g->fkp, static_cast<const double2*>(g->tw), g->n + 1, g->m, g->M1, g->M2, c0, hc};
+    e = launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2, hc, st);
+    if (e) return e;
+    ColC<double> c{static_cast<const double2*>(C2), static_cast<double2*>(Y), g->n, g->m, g->M1, g->M2, hc};
+    return launch<double>(g->M2, c, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
+}
+
+int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1, double* Tst, double* app,
+                    const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
+                    int* status, cudaStream_t st) {
+    RinvA<double> a{static_cast<const double2*>(Y), static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M2, hy};
+    int e = launch<double>(g->M1, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
+    if (e) return e;
+    RinvB<double> b{};
+    b.S1 = static_cast<const double2*>(S1);
+    b.Tst = Tst;
+    b.app = app;
+    b.P = P;
+    b.L0 = L0;
+    b.res_bits = res_bits;
+    b.status = status;
+    b.n = g->n;
+    b.M = g->m;
+    b.M1 = g->M1;
+    b.M2 = g->M2;
+    b.law = o->law;
+    b.kirchhoff = o->kirchhoff;
+    b.beta = o->beta;
+    b.kexp = 1.0 / (1.0 - o->eta);
+    b.ka = pow(o->t_ambient, 1.0 - o->eta);
+    b.kb = (1.0 - o->eta) * pow(o->t_ambient, -o->eta);
+    b.t_ambient = o->t_ambient;
+    b.inv = 1.0 / (double(g->m) * double(g->m));
+    return launch<double>(g->M2, b, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+"""Config 4: the mode-B fixed point on one large map, slab-decomposed over ranks.
+
+One process per GPU (torch.distributed, NCCL on GPUs; gloo in the CPU tests).
+Rank r owns die-row pairs [r P, (r+1) P) (P = n / 2 / world) for the row
+phases and half-spectrum columns [c0_r, c0_r + hc_r) for the column phase
+(SURVEY §8e). Per iteration:
+
+  rows_fwd (local rows)  -> Z [P][m]   spectra of the mirrored row pairs
+  all-to-all             -> every rank gets, for ALL row pairs, the columns it
+                            owns and their mirrors (compact [n/2][2 hc] layout)
+  cols (local columns)   -> Y [n][hc]  rows [0, n) of IFFT_col(fk . FFT_col)
+  all-to-all             -> every rank gets its rows for all columns
+  rows_inv (local rows)  -> theta -> T, residual, next applied rows
+
+The stop rule is the reference outer loop's (fdm.cpp:190-200): converged when
+max|T_{k+1} - T_k| < tol after iteration 1 (max over ranks), max_iters ->
+GT_SAMPLE_NOCONVERGE. With world = 1 no exchange happens and the column phase
+reads the row spectra in place.
+
+The arithmetic lives in the sm_100a passes of libgreentherm_b200.so
+(`GpuLargeOps`, C ABI gt_large_*); this module only moves blocks between ranks.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+GT_SAMPLE_NONFINITE, GT_SAMPLE_KIRCHHOFF, GT_SAMPLE_NOCONVERGE = 0x4, 0x8, 0x10
+
+
+def column_ranges(h: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous (c0, hc) per rank covering [0, h)."""
+    base, extra = divmod(h, world)
+    out, c0 = [], 0
+    for r in range(world):
+        hc = base + (1 if r < extra else 0)
+        out.append((c0, hc))
+        c0 += hc
+    return out
+
+
+class GpuLargeOps:
+    """The three phases on the device (C ABI gt_large_*; torch CUDA tensors)."""
+
+    def __init__(self, dg):
+        from .api import lib
+        self.L = lib()
+        self.dg = dg
+        m1, m2 = C.c_int(), C.c_int()
+        self._check(self.L.gt_large_geometry(dg._d, C.byref(m1), C.byref(m2)))
+        self.M1, self.M2 = m1.value, m2.value
+
+    def _check(self, st):
+        from .api import check
+        check(self.L, st)
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr())
+
+    def rows_fwd(self, app, pairs, s1, z, stream):
+        self._check(self.L.gt_large_rows_fwd(self.dg._d, self._p(app), pairs, self._p(s1), self._p(z),
+                                             C.c_void_p(stream)))
+
+    def cols(self, z, compact, c0, hc, c1, c2, y, stream):
+        self._check(self.L.gt_large_cols(self.dg._d, self._p(z), int(compact), c0, hc, self._p(c1), self._p(c2),
+                                         self._p(y), C.c_void_p(stream)))
+
+    def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream):
+        self._check(self.L.gt_large_rows_inv(self.dg._d, self._p(y), hy, pairs, self._p(s1), self._p(t),
+                                             self._p(app), self._p(p), self._p(l0), C.byref(opts),
+                                             self._p(res_bits), self._p(status), C.c_void_p(stream)))
+
+
+@dataclass
+class SlabResult:
+    t: "object"          # local rows of the converged rise map [2P][n]
+    iterations: int
+    status: int
+    residual: float
+
+
+def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 1, stream: int | None = None,
+               exchange=None) -> SlabResult:
+    """Fixed point on the local slab. p_local / v_local: [2P][n] float64 tensors of
+    this rank's rows; opts: api.FPOpts (leak_frac, law, kirchhoff, beta, t_ambient,
+    eta, tol, max_iters). Device work is issued on `stream` (default: torch's
+    current stream, which the NCCL exchange also uses). `exchange` (default
+    torch.distributed.all_to_all_single) is injectable for tests."""
+    import torch
+    import torch.distributed as dist
+    if (n // 2) % world:
+        raise ValueError("world size must divide n / 2 (whole row pairs per rank)")
+    dev = p_local.device
+    m, h = 2 * n, n + 1
+    P = (n // 2) // world
+    rows = 2 * P
+    ranges = column_ranges(h, world)
+    c0, hc = ranges[rank]
+    exchange = exchange or dist.all_to_all_single
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
+    cd = torch.complex128
+    l0 = opts.leak_frac * p_local * v_local
+    app = (p_local + l0).contiguous()
+    t = torch.zeros_like(p_local)
+    s1 = torch.empty((P, m), dtype=cd, device=dev)
+    z = torch.empty((P, m), dtype=cd, device=dev)
+    c1 = torch.empty((m, hc), dtype=cd, device=dev)
+    c2 = torch.empty((m, hc), dtype=cd, device=dev)
+    ycol = torch.empty((n, hc), dtype=cd, device=dev)
+    res_bits = torch.zeros(1, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if world > 1:
+        zrecv = torch.empty((world, P, 2 * hc), dtype=cd, device=dev)
+        yrow = torch.empty((rows, h), dtype=cd, device=dev)
+        mir = [torch.remainder(m - cq - torch.arange(hq, device=dev), m) for cq, hq in ranges]
+    it, res, st = 0, float("inf"), 0
+    for it in range(1, opts.max_iters + 1):
+        ops.rows_fwd(app, P, s1, z, stream)
+        if world == 1:
+            ops.cols(z, False, c0, hc, c1, c2, ycol, stream)
+            yrow_t, hy = ycol, h
+        else:
+            send = torch.cat([torch.cat([z[:, cq:cq + hq], z[:, mir[q]]], dim=1).reshape(-1)
+                              for q, (cq, hq) in enumerate(ranges)])
+            # output splits: what each source sends me; input splits: what I send each rank
+            exchange(zrecv.view(-1), send, [P * 2 * hc] * world, [P * 2 * hq for _, hq in ranges])
+            ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, c1, c2, ycol, stream)
+            send = ycol.reshape(world, rows, hc).reshape(-1).contiguous()
+            recv = torch.empty(sum(rows * hq for _, hq in ranges), dtype=cd, device=dev)
+            exchange(recv, send, [rows * hq for _, hq in ranges], [rows * hc] * world)
+            off = 0
+            for q, (cq, hq) in enumerate(ranges):
+                yrow[:, cq:cq + hq] = recv[off:off + rows * hq].view(rows, hq)
+                off += rows * hq
+            yrow_t, hy = yrow, h
+        res_bits.zero_()
+        ops.rows_inv(yrow_t, hy, P, s1, t, app, p_local, l0, opts, res_bits, status, stream)
+        rs = torch.stack([res_bits.view(torch.float64)[0], status.to(torch.float64)[0]])
+        if world > 1:
+            flags = [torch.zeros_like(rs) for _ in range(world)]
+            dist.all_gather(flags, rs)
+            res = max(float(f[0]) for f in flags)
+            st = 0
+            for f in flags:
+                st |= int(f[1])
+        else:
+            res, st = float(rs[0]), int(rs[1])
+        if st:
+            break
+        if it > 1 and res < opts.tol:
+            break
+        if it == opts.max_iters:
+            st |= GT_SAMPLE_NOCONVERGE
+    return SlabResult(t=t, iterations=it, status=st, residual=res)

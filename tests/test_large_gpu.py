@@ -1,0 +1,76 @@
+"""Config 4 on the device: the four-step large-grid passes (large.cu) driven by
+paper_2307_12119_b200/slab.py at world size 1, against the mode-B oracle
+(oracle/restate.cpp ref_fixed_point_batch, fp64) and the batched mode-B kernels
+on the same map. n = 512 (m = 1024 = 32 x 32) keeps the CPU oracle in seconds."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def greens512(b200lib, tmp_path_factory):
+    from paper_2307_12119_b200.api import GreensArrays
+    d = tmp_path_factory.mktemp("g512")
+    n = 512
+    (d / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    (d / "var.txt").write_text("dopant_spread 0\nbeta 0.017\n")
+    L = b200lib
+    g = C.c_void_p()
+    assert L.gt_calibrate(str(d / "stack.txt").encode(), str(d / "var.txt").encode(), None, 90.0, C.byref(g),
+                          None) == 0, L.gt_last_error()
+    maps = {}
+    for k in ("f_sp0", "g_sp0"):
+        f = C.c_void_p()
+        assert L.gt_greens_field(g, k.encode(), C.byref(f)) == 0
+        maps[k] = np.ctypeslib.as_array(L.gt_field_data(f), shape=(n, n)).copy()
+        L.gt_field_free(f)
+    f_sp0 = maps["f_sp0"]
+    ga = GreensArrays(n=n, pitch=0.016 / n, f_sp0=f_sp0, g_sp0=maps["g_sp0"],
+                      phi=float(np.mean(np.concatenate([f_sp0[0], f_sp0[-1], f_sp0[1:-1, 0], f_sp0[1:-1, -1]]))),
+                      kappa_inf=float(f_sp0[0, 0]), alpha=L.gt_greens_alpha(g), beta=0.017, mu=L.gt_greens_mu(g),
+                      rand_scale=1.0)
+    L.gt_greens_free(g)
+    return ga
+
+
+@pytest.mark.parametrize("law,kirchhoff,beta", [(0, 0, 0.017), (1, 0, 0.004), (0, 1, 0.017)])
+def test_large_grid_matches_oracle(b200lib, oracle, greens512, law, kirchhoff, beta):
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    cfg = inputs.CONFIGS["cfg4"]
+    import dataclasses
+    cfg = dataclasses.replace(cfg, n=512, blocks=64, hotspots=8)
+    p = inputs.power_batch(cfg, 0, 1, np.float64) * 0.3
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=beta, law=law, kirchhoff=kirchhoff, tol=1e-4, max_iters=60)
+    t_ref, it_ref, st_ref, secs = oracle.fixed_point_batch(greens512, p, v, jobs=1, **kw)
+    assert st_ref[0] == 0
+    dg = DeviceGreens(greens512, 1)
+    ops = slab.GpuLargeOps(dg)
+    o = dg.fp_opts(**kw)
+    res = slab.solve_slab(ops, 512, torch.from_numpy(p[0]).cuda(), torch.from_numpy(v[0]).cuda(), o)
+    torch.cuda.synchronize()
+    t = res.t.cpu().numpy()
+    err = np.abs(t - t_ref[0]).max()
+    print(f"large n=512 law={law} kirchhoff={kirchhoff}: iters {res.iterations} vs {it_ref[0]}, "
+          f"max|dT| {err:.3e} K on peak {t_ref.max():.1f} K (oracle {secs:.1f} s)")
+    assert res.status == 0
+    assert res.iterations == it_ref[0]
+    assert err <= 1e-8
+    # same map through the batched mode-B kernels (tile passes)
+    out, it, st, _, _ = dg.fp_batch_host(p, v, o)
+    assert it[0] == res.iterations
+    assert np.abs(out[0] - t).max() <= 1e-9
+
+
+def test_large_grid_needs_fp64(b200lib, greens512):
+    from paper_2307_12119_b200 import slab
+    from paper_2307_12119_b200.api import DeviceGreens, GtError
+    dg = DeviceGreens(greens512, 0)
+    with pytest.raises(GtError) as e:
+        slab.GpuLargeOps(dg)
+    assert e.value.status == 2
