@@ -172,6 +172,10 @@ size_t gt_trace_scratch_bytes(int n, int precision, int window);
  *              place: old T in, new T out) -> next applied rows P + L0 f(T);
  *              max |T_new - T_old| is atomically max-ed into res_bits (double
  *              bits), sample status bits OR-ed into *status. */
+/* f_sp0 alone (the reference impulse_response, 1 W at (c, c), fdm.cpp:288-296) by the
+ * device modal solution of the stack file's network, for power-of-two n up to 16384
+ * (the full gt_calibrate is limited to n <= 1024). Call with f_sp0_out = NULL to read n. */
+gt_status gt_modal_kernel(const char* stack_path, int* n_out, double* f_sp0_out);
 gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2);
 gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
                             void* stream);

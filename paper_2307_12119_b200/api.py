@@ -125,6 +125,7 @@ _EXT = [
     ("gt_trace_batch_device", cint, [vp, vp, C.c_longlong, vp, cint, vp, C.c_longlong, cint, C.POINTER(TraceOpts),
                                      vp, vp, vp]),
     ("gt_trace_scratch_bytes", C.c_size_t, [cint, cint, cint]),
+    ("gt_modal_kernel", cint, [cstr, C.POINTER(cint), pdbl]),
     ("gt_large_geometry", cint, [vp, C.POINTER(cint), C.POINTER(cint)]),
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),

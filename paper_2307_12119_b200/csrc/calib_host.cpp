@@ -166,6 +166,23 @@ void d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 
 }  // namespace
 
+// f_sp0 alone (impulse_response for 1 W at (c, c), fdm.cpp:288-296) by the modal
+// solution, for any power-of-two n the device memory allows (config 4: 8192).
+void gt_ops_modal_kernel(const Stack& s, double* out_host) {
+    s.validate();
+    need_device();
+    const int n = s.n;
+    if (!pow2(n) || n < 16 || n > 16384)
+        fail(ST_CONFIG, "calibrate", "modal kernel supports power-of-two grids 16..16384, got n=" + std::to_string(n));
+    const gtd_stack ds = to_dev(s);
+    const size_t nn = static_cast<size_t>(n) * n;
+    DBuf work, f;
+    work.ensure(3 * nn * 8);
+    f.ensure(nn * 8);
+    cuda_ok(gtd_modal_impulse(&ds, s.die.conductivity, work.as<double>(), f.as<double>(), nullptr), "modal impulse");
+    d2h(out_host, f.p, nn * 8, nullptr);
+}
+
 Greens gt_ops_calibrate_modal(const Stack& s, const VarParams& v, const Field* nominal_leak, double leak_total) {
     s.validate();
     v.validate();

@@ -186,6 +186,13 @@ gt_status gt_calibrate(const char* stack_path, const char* variation_path, const
         *out = new gt_greens{std::move(g)};
     });
 }
+gt_status gt_modal_kernel(const char* stack_path, int* n_out, double* f_sp0_out) {
+    return guarded([&] {
+        Stack s = stack_path ? load_stack_file(stack_path) : Stack{};
+        if (n_out) *n_out = s.n;
+        if (f_sp0_out) gt_ops_modal_kernel(s, f_sp0_out);
+    });
+}
 gt_status gt_greens_save(const gt_greens* g, const char* dir) {
     return guarded([&] { save_greens_dir(g->g, dir); });
 }

@@ -78,11 +78,67 @@ void upload(DBuf& b, const void* src, size_t bytes, cudaStream_t st) {
     cuda_ok(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), "upload");
 }
 
+// Large grids (n > 1024, config 4): fp64 only, and only what the four-step
+// large-grid passes read -- twiddles and the baseline kernel half spectrum fk,
+// built on the device by the same passes (large.cu). The batched mode-A/B and
+// reference-API paths reject these grids (their tables are not built).
+std::unique_ptr<gt_device_greens> prepare_device_large(const Greens& g, int device) {
+    const int n = g.n, m = 2 * n;
+    cuda_ok(cudaSetDevice(device), "cudaSetDevice");
+    auto d = std::make_unique<gt_device_greens>();
+    d->device = device;
+    d->fp64 = 1;
+    d->host = g;
+    cuda_ok(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
+    cudaStream_t st = d->stream;
+    const int hp = ((n + 1 + 7) / 8) * 8;
+    const std::vector<double> tw = twiddles(m), hs = half_twiddles(m);
+    upload(d->tw64, tw.data(), tw.size() * 8, st);
+    upload(d->tw, tw.data(), tw.size() * 8, st);
+    upload(d->hs, hs.data(), hs.size() * 8, st);
+    upload(d->fsp0, g.f_sp0.v.data(), g.f_sp0.v.size() * 8, st);
+    d->fk.ensure(static_cast<size_t>(m) * hp * 16);
+    gtd_lg lg{};
+    lg.n = n;
+    lg.m = m;
+    if (gtd_lg_split(m, &lg.M1, &lg.M2)) fail(ST_CONFIG, "device", "large grid: m out of range");
+    lg.tw = d->tw64.p;
+    lg.fkp = hp;
+    {
+        DBuf s1, z, c1;
+        s1.ensure(static_cast<size_t>(n / 2) * m * 16);
+        z.ensure(static_cast<size_t>(n / 2) * m * 16);
+        c1.ensure(static_cast<size_t>(m) * hp * 16);
+        cuda_ok(gtd_lg_kernel_spectrum(&lg, d->fsp0.as<double>(), g.phi, s1.p, z.p, c1.p, d->fk.p, st),
+                "large kernel spectrum");
+        cuda_ok(cudaStreamSynchronize(st), "sync");
+    }
+    d->d.n = n;
+    d->d.m = m;
+    d->d.h = n + 1;
+    d->d.hp = hp;
+    d->d.fp64 = 1;
+    d->d.fk = d->fk.p;
+    d->d.tw = d->tw.p;
+    d->d.hs = d->hs.p;
+    d->d.alpha = g.alpha;
+    d->d.beta = g.beta;
+    d->d.rand_scale = g.rand_scale;
+    d->d.mu_fixed = g.mu;
+    return d;
+}
+
 std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision, int device) {
     need_device();
     const int n = g.n;
+    if (pow2(n) && n > 1024 && n <= 16384) {
+        if (precision != GT_FP64)
+            fail(ST_CONFIG, "device", "grids above n = 1024 run the fp64 large-grid path only (use GT_FP64)");
+        return prepare_device_large(g, device);
+    }
     if (!pow2(n) || n < 16 || n > 1024)
-        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..1024, got n=" + std::to_string(n));
+        fail(ST_CONFIG, "device", "device path supports power-of-two grids 16..1024 (16384 in fp64), got n=" +
+                                      std::to_string(n));
     if (precision != GT_FP32 && precision != GT_FP64) fail(ST_CONFIG, "device", "precision must be GT_FP32 or GT_FP64");
     cuda_ok(cudaSetDevice(device), "cudaSetDevice");
     auto d = std::make_unique<gt_device_greens>();

@@ -164,6 +164,11 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
                     const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
                     int* status, cudaStream_t st);
 
+/* fk = FFT2(center_kernel(f_sp0 - phi)) + phi m^2/4 at DC, [m][fkp] (g->fk unused);
+ * S1, Z: (n/2) x m complex scratch; C1: m x fkp complex scratch. */
+int gtd_lg_kernel_spectrum(const gtd_lg* g, const double* f_sp0, double phi, void* S1, void* Z, void* C1,
+                           void* fk_out, cudaStream_t st);
+
 /* ---- config-3 batched transient traces (trace_batch.cu) */
 typedef struct gtd_trace_in {
     const int* blk;

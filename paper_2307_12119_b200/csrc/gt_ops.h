@@ -7,6 +7,7 @@
 
 #include "host.hpp"
 
+void gt_ops_modal_kernel(const gth::Stack& s, double* out_host);
 gth::Greens gt_ops_calibrate_modal(const gth::Stack& s, const gth::VarParams& v, const gth::Field* nominal_leak,
                                    double leak_total);
 gth::Field gt_ops_steady(const gth::Greens& g, const gth::Field& p_dyn, bool with_rand, double* online_ms);

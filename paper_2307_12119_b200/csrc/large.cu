@@ -44,9 +44,18 @@ struct FwdA {
     cplx<T>* S1;   // [pairs][m]
     const double2* tw;
     int n, M, M1;
+    int embed = 0;  // 0: mirror_pad (spectral.cpp:105-114); 1: center_kernel of (app - shift) (spectral.cpp:126-141)
+    T shift = T(0);
     __device__ cplx<T> load(int p, int i1, int j) const {
-        const int i = i1 + M1 * j, y = i < n ? i : M - 1 - i;
-        return mk<T>(app[static_cast<size_t>(2 * p) * n + y], app[static_cast<size_t>(2 * p + 1) * n + y]);
+        const int i = i1 + M1 * j;
+        int y;
+        if (embed) {
+            y = (i + n / 2) & (M - 1);
+            if (y >= n) return mk<T>(T(0), T(0));
+        } else {
+            y = i < n ? i : M - 1 - i;
+        }
+        return mk<T>(app[static_cast<size_t>(2 * p) * n + y] - shift, app[static_cast<size_t>(2 * p + 1) * n + y] - shift);
     }
     __device__ void store(int p, int i1, int k2, cplx<T> v) const {
         S1[static_cast<size_t>(p) * M + i1 + static_cast<size_t>(M1) * k2] =
@@ -84,8 +93,16 @@ struct ColA {
     int n, M, M1, c0, hc;
     long long zs;
     int oa, ob, sb, mask;
+    int embed = 0;  // rows: 0 mirror_pad, 1 center_kernel
     __device__ cplx<T> load(int i1, int c, int j) const {
-        const int i = i1 + M1 * j, x = i < n ? i : M - 1 - i;
+        const int i = i1 + M1 * j;
+        int x;
+        if (embed) {
+            x = (i + n / 2) & (M - 1);
+            if (x >= n) return mk<T>(T(0), T(0));
+        } else {
+            x = i < n ? i : M - 1 - i;
+        }
         const cplx<T>* Zp = Z + static_cast<size_t>(x >> 1) * zs;
         const cplx<T> a = Zp[oa + c], b = cconj<T>(Zp[(ob + sb * c) & mask]);
         // half spectra of the two real rows packed in Zp (x even: real part's, odd: imaginary part's)
@@ -119,6 +136,25 @@ struct ColB {
     __device__ void store(int k2, int c, int ia, cplx<T> v) const {
         C2[(static_cast<size_t>(k2) + static_cast<size_t>(M2) * ia) * hc + c] =
             cmul<T>(v, twm<T>(tw, M, static_cast<long long>(ia) * k2, true));
+    }
+};
+
+template <typename T>
+struct KColB {  // group k2, line c, j = i1: forward only; fk[u][v] natural order (+ DC term)
+    static constexpr bool REDUCE = false;
+    static constexpr int SIGN = -1;
+    static constexpr bool LINE_FAST = true;
+    const cplx<T>* C1;
+    cplx<T>* fk;
+    int fkp, M, M1, M2, hc;
+    T dc;
+    __device__ cplx<T> load(int k2, int c, int j) const {
+        return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
+    }
+    __device__ void store(int k2, int c, int k1, cplx<T> v) const {
+        const int u = k2 + M2 * k1;
+        if (u == 0 && c == 0) v.x += dc;  // baseline_kernel_spectrum: fk[0] += phi m^2 / 4 (greens.cpp:194-201)
+        fk[static_cast<size_t>(u) * fkp + c] = v;
     }
 };
 
@@ -373,6 +409,35 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
     b.t_ambient = o->t_ambient;
     b.inv = 1.0 / (double(g->m) * double(g->m));
     return launch<double>(g->M2, b, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
+}
+
+// fk = FFT2(center_kernel(f_sp0 - phi)) with fk[0] += phi m^2 / 4, half width [m][fkp]
+// (baseline_kernel_spectrum, greens.cpp:194-201), by the same four-step passes.
+int gtd_lg_kernel_spectrum(const gtd_lg* g, const double* f_sp0, double phi, void* S1, void* Z, void* C1,
+                           void* fk_out, cudaStream_t st) {
+    const int n = g->n, M = g->m, pairs = n / 2;
+    const double2* tw = static_cast<const double2*>(g->tw);
+    FwdA<double> a{f_sp0, static_cast<double2*>(S1), tw, n, M, g->M1};
+    a.embed = 1;
+    a.shift = phi;
+    int e = launch<double>(g->M2, a, tw, M, pairs, g->M1, st);
+    if (e) return e;
+    FwdB<double> b{static_cast<const double2*>(S1), static_cast<double2*>(Z), M, g->M1, g->M2};
+    e = launch<double>(g->M1, b, tw, M, pairs, g->M2, st);
+    if (e) return e;
+    const int hc = g->fkp;  // every stored column (v >= n+1 are harmless extras)
+    ColA<double> ca{static_cast<const double2*>(Z), static_cast<double2*>(C1), tw, n, M, g->M1, 0, hc};
+    ca.zs = M;
+    ca.oa = 0;
+    ca.ob = M;
+    ca.sb = -1;
+    ca.mask = M - 1;
+    ca.embed = 1;
+    e = launch<double>(g->M2, ca, tw, M, g->M1, hc, st);
+    if (e) return e;
+    KColB<double> kb{static_cast<const double2*>(C1), static_cast<double2*>(fk_out), g->fkp, M, g->M1, g->M2, hc,
+                     phi * double(M) * double(M) / 4.0};
+    return launch<double>(g->M1, kb, tw, M, g->M2, hc, st);
 }
 
 }  // extern "C"

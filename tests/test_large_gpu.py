@@ -74,3 +74,37 @@ def test_large_grid_needs_fp64(b200lib, greens512):
     with pytest.raises(GtError) as e:
         slab.GpuLargeOps(dg)
     assert e.value.status == 2
+
+
+def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path):
+    """n = 2048 takes the large-grid preparation (fk built by the four-step passes from
+    the modal f_sp0): three iterations against a direct numpy restatement."""
+    import sys
+    from pathlib import Path
+    import torch
+    from paper_2307_12119_b200 import slab
+    from paper_2307_12119_b200.api import DeviceGreens, GreensArrays
+    sys.path.insert(0, str(Path(__file__).parent))
+    from slab_numpy_ops import baseline_fk, fixed_point_numpy
+    n = 2048
+    (tmp_path / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    f = np.empty((n, n))
+    nn = C.c_int()
+    assert b200lib.gt_modal_kernel(str(tmp_path / "stack.txt").encode(), C.byref(nn),
+                                   f.ctypes.data_as(C.POINTER(C.c_double))) == 0, b200lib.gt_last_error()
+    assert nn.value == n and f.argmax() == (n // 2) * n + n // 2
+    phi = float(np.mean(np.concatenate([f[0], f[-1], f[1:-1, 0], f[1:-1, -1]])))
+    ga = GreensArrays(n=n, pitch=0.016 / n, f_sp0=f, g_sp0=f, phi=phi, kappa_inf=float(f[0, 0]), alpha=0.0,
+                      beta=0.017, mu=0.0, rand_scale=1.0)
+    rng = np.random.default_rng(5)
+    P = rng.uniform(0.0, 4.0 / n ** 2 * 64, (n, n))
+    V = 1.0 + 0.1 * rng.standard_normal((n, n))
+    dg = DeviceGreens(ga, 1)
+    o = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-30, max_iters=3)
+    res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(P).cuda(), torch.from_numpy(V).cuda(), o)
+    torch.cuda.synchronize()
+    ref, _ = fixed_point_numpy(P, V, baseline_fk(f, phi), 0.3, 0.017, 0, 1e-30, 3)
+    err = np.abs(res.t.cpu().numpy() - ref).max()
+    print(f"large n=2048: 3 iterations, max|dT| {err:.3e} K on peak {ref.max():.2f} K")
+    assert res.iterations == 3 and res.status == slab.GT_SAMPLE_NOCONVERGE
+    assert err <= 1e-9 * max(1.0, ref.max())
