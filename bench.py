@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-mode-b", action="store_true")
     ap.add_argument("--no-cfg3", action="store_true", help="skip the config-3 transient-trace sub-benchmark")
     ap.add_argument("--cfg3-steps", type=int, default=2000)
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 large-grid sub-benchmark")
+    ap.add_argument("--cfg4-n", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -296,6 +298,69 @@ def run_cfg3(args, dev, ws, rank):
             "leakage": "L0 = 0.3 x on-state block power x variation map (sigma/mu 0.10), linear law, every step"}
 
 
+def run_cfg4(args, dev, ws, rank):
+    """Config 4: one n x n map (8192 by default), mode-B leakage loop to 1e-4 K in fp64,
+    slab-decomposed over the ranks (row pairs / half-spectrum columns) with an
+    all-to-all transpose between the row and the column phases (paper_2307_12119_b200/
+    slab.py); strong scaling. The generator's literal map (1024 blocks + 64 hotspots)
+    draws ~1 kW, for which the leakage loop has no fixed point (runaway, like mode B's
+    exp law at config 1); it is rescaled to 300 W total so the loop converges."""
+    import ctypes as C
+    import dataclasses
+    import torch
+    import torch.distributed as dist
+    from paper_2307_12119_b200 import inputs, shard, slab
+    from paper_2307_12119_b200.api import DeviceGreens, GreensArrays, lib
+    n = args.cfg4_n
+    c4 = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n)
+    t0 = time.time()
+    d = Path(tempfile.mkdtemp())
+    (d / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    f = np.empty((n, n))
+    nn = C.c_int()
+    L = lib()
+    if L.gt_modal_kernel(str(d / "stack.txt").encode(), C.byref(nn), f.ctypes.data_as(C.POINTER(C.c_double))):
+        raise RuntimeError(L.gt_last_error().decode())
+    phi = float(np.mean(np.concatenate([f[0], f[-1], f[1:-1, 0], f[1:-1, -1]])))
+    ga = GreensArrays(n=n, pitch=0.016 / n, f_sp0=f, g_sp0=f, phi=phi, kappa_inf=float(f[0, 0]), alpha=0.0,
+                      beta=0.017, mu=0.0, rand_scale=1.0)
+    dg = DeviceGreens(ga, 1, device=dev.index or 0)
+    del f
+    P = inputs.power_map_torch(c4, 0, device=dev)
+    P_total = float(P.sum())
+    P *= 300.0 / P_total
+    V = inputs.variation_batch(c4, 0, 1, device=dev, dtype=torch.float64)[0]
+    rows = n // ws
+    Pl = P[rank * rows:(rank + 1) * rows].contiguous()
+    Vl = V[rank * rows:(rank + 1) * rows].contiguous()
+    del P, V
+    prep_s = time.time() - t0
+    ops = slab.GpuLargeOps(dg)
+    o = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    warm = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=2)
+    slab.solve_slab(ops, n, Pl, Vl, warm, rank=rank, world=ws)
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = slab.solve_slab(ops, n, Pl, Vl, o, rank=rank, world=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), dev)
+    peak = shard.max_over_ranks(float(res.t.max()), dev)
+    h = n + 1
+    b_it = 5 * 8 * n * n + 8 * 8 * n * h  # SURVEY §8(d) B_it for config 4 (fp64): 6.98 GB
+    dg.close()
+    return {"value": 1e3 / ms, "unit": "solves/s", "n": n, "ms": ms, "iterations": res.iterations,
+            "ms_per_iteration": ms / res.iterations, "status": res.status, "peak_K": peak,
+            "bytes_per_iteration_model": b_it, "achieved_GBps_model": b_it * res.iterations / (ms / 1e3) / 1e9,
+            "scaling": "strong", "parallelism": f"slab over {ws} rank(s): row pairs / half-spectrum columns, "
+                                              "all-to-all transposes" if ws > 1 else "one GPU (no exchange)",
+            "power_W": {"generated": P_total, "used": 300.0}, "prep_s": prep_s, "precision": "fp64",
+            "law": "linear (1 + beta dT), beta 0.017, leak 0.3 x P x var, tol 1e-4 K"}
+
+
 def run_b200(args, cfg):
     import torch
     import torch.distributed as dist
@@ -451,6 +516,10 @@ def run_b200(args, cfg):
     if not args.no_cfg3:
         cfg3 = run_cfg3(args, dev, ws, rank)
 
+    cfg4 = None
+    if not args.no_cfg4:
+        cfg4 = run_cfg4(args, dev, ws, rank)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_rate(cfg, args.cpu_seconds, os.cpu_count() or 1)
@@ -482,6 +551,8 @@ def run_b200(args, cfg):
             line["mode_b"] = mode_b
         if cfg3:
             line["cfg3"] = cfg3
+        if cfg4:
+            line["cfg4"] = cfg4
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

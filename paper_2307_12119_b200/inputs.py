@@ -104,6 +104,26 @@ def power_map(cfg: Config, index: int) -> np.ndarray:
     return dens * pm * pm
 
 
+def power_map_torch(cfg: Config, index: int, device="cuda"):
+    """power_map for large grids (config 4): identical draws, the hotspot sum and the
+    block fill done with torch on `device` (float64 (n, n) tensor, W per cell)."""
+    import torch
+    rng = np.random.default_rng(sample_seed(cfg.base_seed, PURPOSE_POWER, index))
+    n, pm = cfg.n, cfg.pitch_mm
+    dens = torch.zeros((n, n), dtype=torch.float64, device=device)
+    for r0, r1, c0, c1 in guillotine_blocks(n, cfg.blocks, rng):
+        dens[r0:r1, c0:c1] = rng.uniform(0.2, 2.0)
+    if cfg.hotspots:
+        x = (torch.arange(n, dtype=torch.float64, device=device) + 0.5) * pm
+        for _ in range(cfg.hotspots):
+            cx, cy = rng.uniform(0.0, cfg.die_mm, size=2)
+            peak = rng.uniform(5.0, 10.0)
+            gx = torch.exp(-((x - cx) ** 2) / (2 * 0.5 ** 2))
+            gy = torch.exp(-((x - cy) ** 2) / (2 * 0.5 ** 2))
+            dens += peak * torch.outer(gx, gy)
+    return dens * pm * pm
+
+
 def power_batch(cfg: Config, start: int, count: int, dtype=np.float32) -> np.ndarray:
     out = np.empty((count, cfg.n, cfg.n), dtype=dtype)
     for k in range(count):
