@@ -122,7 +122,11 @@ struct MCGeom {
     static constexpr int h = n + 1;
     static constexpr int L = G::L;
     static constexpr int NT = G::NT;
+#ifdef GT_P2_W
+    static constexpr int W = M >= 512 ? GT_P2_W : L / 2;  // pass-2 tile width (tuning override)
+#else
     static constexpr int W = L / 2;  // columns per pass-2 tile
+#endif
     static constexpr int hp = ((h + W - 1) / W) * W;
     static constexpr int LP = L + 2;  // padded pitch for row tiles (transposing I/O; even for pairs)
     static constexpr int SP = n + 1;  // padded pitch of the row staging arrays
@@ -137,7 +141,7 @@ struct MCGeom {
 #ifndef GT_P2_CTAS
 #define GT_P2_CTAS 2
 #endif
-    static constexpr int NT2 = NT > GT_P2_NT ? GT_P2_NT : NT;
+    static constexpr int NT2 = (M / 8) * W > GT_P2_NT ? GT_P2_NT : (M / 8) * W;
     static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
     // pass 2 holds three lines per thread-butterfly: 128 registers (fp32) / 255 (fp64)
     static constexpr int MINB2 = sizeof(T) == 8 ? 1 : ((512 / NT2) < 1 ? 1 : (512 / NT2));
