@@ -316,7 +316,7 @@ tr_rows_inv(int b0, int count, TRBuf<T> bf, TRStep sp, int nframes, int law, T b
                 Pnext[o] = sch[blk[o]] + L0[o] * f;
             }
         }
-        if (O) {
+        if (O && fmax_bits) {
             double m = double(mx);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));

@@ -81,3 +81,46 @@ def test_trace_batch_without_capacitance_is_solver_error(b200lib, greens64):
     with pytest.raises(GtError) as e:
         _run_gpu(g0, 1, blk, sched, 0.3 * on, 2e-4, 2, 0, 0.017, 2)
     assert e.value.status == 3
+
+
+def test_trace_batch_chunking_window1_and_ragged_stride(b200lib, oracle, greens64):
+    """window = 1 (tail term every step), steps not a multiple of out_stride (trailing steps
+    unstored), traces split over several in-flight chunks: same frames as the oracle."""
+    import torch
+    from paper_2307_12119_b200.api import DeviceGreens
+    B, steps, dt, stride = 5, 11, 2e-4, 3
+    blk, sched, on = _traces(B, steps)
+    leak0 = 0.3 * on
+    ref, st, _ = oracle.trace_leak_batch(greens64, blk, sched, leak0, dt, 1, law=0, beta=0.017, out_stride=stride)
+    assert (st == 0).all()
+    dg = DeviceGreens(greens64, 1)
+    n = greens64.n
+    blk_d = torch.from_numpy(blk).cuda()
+    sch_d = torch.from_numpy(sched).cuda()
+    l0_d = torch.from_numpy(leak0).cuda()
+    out = torch.zeros((B, steps // stride, n, n), dtype=torch.float64, device="cuda")
+    o = dg.trace_opts(dt=dt, steps=steps, window=1, law=0, beta=0.017, out_stride=stride, chunk=2)
+    dg.trace_batch_device(blk_d.data_ptr(), n * n, sch_d.data_ptr(), sched.shape[2], l0_d.data_ptr(), n * n, B, o,
+                          out.data_ptr())
+    torch.cuda.synchronize()
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-8
+
+
+def test_trace_batch_rejects_bad_options(b200lib, greens64):
+    import torch
+    from paper_2307_12119_b200.api import DeviceGreens, GtError
+    dg = DeviceGreens(greens64, 1)
+    blk, sched, on = _traces(1, 4)
+    n = greens64.n
+    blk_d = torch.from_numpy(blk).cuda()
+    sch_d = torch.from_numpy(sched).cuda()
+    l0_d = torch.from_numpy(0.3 * on).cuda()
+    out = torch.zeros((1, 4, n, n), dtype=torch.float64, device="cuda")
+    for kw in (dict(dt=0.0), dict(steps=0), dict(out_stride=0), dict(out_stride=5), dict(law=2)):
+        base = dict(dt=2e-4, steps=4, window=2, law=0, beta=0.017, out_stride=1)
+        base.update(kw)
+        o = dg.trace_opts(**base)
+        with pytest.raises(GtError) as e:
+            dg.trace_batch_device(blk_d.data_ptr(), 0, sch_d.data_ptr(), sched.shape[2], l0_d.data_ptr(), 0, 1, o,
+                                  out.data_ptr())
+        assert e.value.status == 2, kw
