@@ -213,7 +213,24 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
     __device__ cplx<T> load(int p, int ia, int j) const {
         return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M2) * ia];
     }
-    __device__ void store(int p, int ia, int ib, cplx<T> v, double& dmax, int& bad) const {
+    struct Pre {
+        T told[2], p[2], l0[2];
+    };
+    // the epilogue's global inputs, issued ahead of the stores (lg_pass batches 4 elements)
+    __device__ Pre pre(int p, int ia, int ib) const {
+        Pre r{};
+        const int i = ia + M1 * ib;
+        if (i >= n) return r;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const size_t o = static_cast<size_t>(2 * p + half) * n + i;
+            r.told[half] = Tst[o];
+            r.p[half] = P[o];
+            r.l0[half] = L0[o];
+        }
+        return r;
+    }
+    __device__ void store(int p, int ia, int ib, cplx<T> v, const Pre& q, double& dmax, int& bad) const {
         const int i = ia + M1 * ib;
         if (i >= n) return;
 #pragma unroll
@@ -226,10 +243,10 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
                 t = pow(br, kexp) - t_ambient;
             }
             if (!isfinite(t)) bad |= GTD_ST_NONFINITE;
-            dmax = fmax(dmax, double(fabs(t - Tst[o])));
+            dmax = fmax(dmax, double(fabs(t - q.told[half])));
             Tst[o] = t;
             const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
-            app[o] = P[o] + L0[o] * f;
+            app[o] = q.p[half] + q.l0[half] * f;
         }
     }
 };
@@ -249,19 +266,27 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
         s_tw[t] = mk<T>(T(w.x), T(w.y));
     }
     const int bpg = (nlines + L - 1) / L;
+    double r_dmax = 0.0;  // REDUCE ops: per-thread residual / status over all of the CTA's items
+    int r_bad = 0;
     for (int item = blockIdx.x; item < groups * bpg; item += gridDim.x) {
         const int g = item / bpg, l0 = (item - g * bpg) * L;
         __syncthreads();
-        for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-            int l, j;
-            if constexpr (Op::LINE_FAST) {
-                l = idx % L;
-                j = idx / L;
-            } else {
-                j = idx % N;
-                l = idx / N;
+        // loads in groups of U elements, all issued before the shared-memory stores
+        constexpr int U = 4;
+        for (int base = threadIdx.x; base < N * L; base += NT * U) {
+            cplx<T> vals[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = base + u * NT;
+                const int l = Op::LINE_FAST ? idx % L : idx / N, j = Op::LINE_FAST ? idx / L : idx % N;
+                vals[u] = (idx < N * L && l0 + l < nlines) ? op.load(g, l0 + l, j) : mk<T>(T(0), T(0));
             }
-            tile[j * LP + l] = l0 + l < nlines ? op.load(g, l0 + l, j) : mk<T>(T(0), T(0));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = base + u * NT;
+                const int l = Op::LINE_FAST ? idx % L : idx / N, j = Op::LINE_FAST ? idx / L : idx % N;
+                if (idx < N * L) tile[j * LP + l] = vals[u];
+            }
         }
         __syncthreads();
         tile_fft<T, N, L, LP, NT, Op::SIGN>(tile, s_tw);
@@ -274,24 +299,46 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
             tile_fft<T, N, L, LP, NT, -Op::SIGN>(tile, s_tw);
         }
         if constexpr (Op::REDUCE) {
-            double dmax = 0.0;
-            int bad = 0;
-            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-                const int l = idx % L, k = idx / L;
-                if (l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l], dmax, bad);
-            }
+            constexpr int U = 4;
+            for (int base = threadIdx.x; base < N * L; base += NT * U) {
+                typename Op::Pre q[U];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-            bad = __reduce_or_sync(0xffffffffu, bad);
-            if ((threadIdx.x & 31) == 0) {
-                atomicMax(op.res_bits, static_cast<unsigned long long>(__double_as_longlong(dmax)));
-                if (bad) atomicOr(op.status, bad);
+                for (int u = 0; u < U; ++u) {
+                    const int idx = base + u * NT, l = idx % L, k = idx / L;
+                    if (idx < N * L && l0 + l < nlines) q[u] = op.pre(g, l0 + l, k);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = base + u * NT, l = idx % L, k = idx / L;
+                    if (idx < N * L && l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l], q[u], r_dmax, r_bad);
+                }
             }
         } else {
             for (int idx = threadIdx.x; idx < N * L; idx += NT) {
                 const int l = idx % L, k = idx / L;
                 if (l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l]);
             }
+        }
+    }
+    if constexpr (Op::REDUCE) {
+        // one atomic per CTA (a per-warp atomic on one address serialised the pass)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r_dmax = fmax(r_dmax, __shfl_xor_sync(0xffffffffu, r_dmax, o));
+        r_bad = __reduce_or_sync(0xffffffffu, r_bad);
+        __shared__ double s_m[NT / 32];
+        __shared__ int s_b[NT / 32];
+        if ((threadIdx.x & 31) == 0) {
+            s_m[threadIdx.x >> 5] = r_dmax;
+            s_b[threadIdx.x >> 5] = r_bad;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NT / 32; ++w) {
+                r_dmax = fmax(r_dmax, s_m[w]);
+                r_bad |= s_b[w];
+            }
+            atomicMax(op.res_bits, static_cast<unsigned long long>(__double_as_longlong(r_dmax)));
+            if (r_bad) atomicOr(op.status, r_bad);
         }
     }
 }
