@@ -60,9 +60,56 @@ __device__ __forceinline__ void dft16(cplx<T>* v) {
         for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
 }
 
+// 32-point DFT in registers: radix 8 over n1 (inputs n2 + 4 n1), twiddle
+// w32^{n2 k1}, radix 4 over n2; X[k1 + 8 k2] lands in slot 4 k1 + k2 and a
+// compile-time register permutation restores natural order.
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft32(cplx<T>* v) {
+    constexpr double C32[8] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                               0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                               0.19509032201612826785};  // cos(2 pi t / 32), t = 0..7
+    cplx<T> a[4][8];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+#pragma unroll
+        for (int n1 = 0; n1 < 8; ++n1) a[n2][n1] = v[n2 + 4 * n1];
+        dft8<SIGN, T>(a[n2]);
+    }
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 8; ++k1) {
+            const int e = n2 * k1;  // w32^e, e < 32: cos / sin from the first octant table
+            const int q = e & 7, oct = e >> 3;
+            // cos / sin(2 pi e / 32) with e = 8 oct + q
+            const double c0 = C32[q], s0 = C32[(8 - q) & 7] * (q == 0 ? 0.0 : 1.0);
+            double c = c0, sn = s0;
+            if (oct == 1) {
+                c = -s0;
+                sn = c0;
+            } else if (oct == 2) {
+                c = -c0;
+                sn = -s0;
+            } else if (oct == 3) {
+                c = s0;
+                sn = -c0;
+            }
+            a[n2][k1] = cmul<T>(a[n2][k1], mk<T>(T(c), T(SIGN < 0 ? -sn : sn)));
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) {
+        cplx<T> q[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+        dft4<SIGN, T>(q);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 8 * k2] = q[k2];
+    }
+}
+
 template <int P, int SIGN, typename T>
 __device__ __forceinline__ void dftP(cplx<T>* v) {
-    if constexpr (P == 16)
+    if constexpr (P == 32)
+        dft32<SIGN, T>(v);
+    else if constexpr (P == 16)
         dft16<SIGN, T>(v);
     else if constexpr (P == 8)
         dft8<SIGN, T>(v);
@@ -84,7 +131,7 @@ struct WarpFFT {
     static constexpr int Q = 32 / P;
     static constexpr int SP = 33;  // scratch pitch (complex) of the P x 32 transpose
     static constexpr int SCRATCH = P * SP > M ? P * SP : M;  // complex elements per warp
-    static_assert(P == 4 || P == 8 || P == 16, "warp FFT supports M = 128, 256, 512");
+    static_assert(P == 4 || P == 8 || P == 16 || P == 32, "warp FFT supports M = 128, 256, 512, 1024");
 
     // Step-1 twiddles lane-major: tw1[(k - 1) 32 + j] = w_M^{j k}, so a warp's
     // loads for one k are 32 consecutive entries (the flat table's j k stride is

@@ -26,6 +26,7 @@
 
 #include "col_pass.cuh"
 #include "fft_tile.cuh"
+#include "fft_warp.cuh"
 #include "gt_device.h"
 
 namespace gtb {
@@ -327,6 +328,149 @@ tr_rows_inv(int b0, int count, TRBuf<T> bf, TRStep sp, int nframes, int law, T b
     }
 }
 
+// ---------------------------------------------------------------- warp-per-row rows (M = 128 .. 1024)
+constexpr int TRW_WARPS = 8;
+
+template <int M>
+constexpr bool tr_warp_rows() {
+    return M == 128 || M == 256 || M == 512 || M == 1024;
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(TRW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
+tr_rows_fwd_w(int b0, int count, TRBuf<T> bf, TRStep sp, const cplx<T>* __restrict__ g_tw,
+              const cplx<T>* __restrict__ g_hs) {
+    using Gm = TRGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, hp = Gm::hp, P = WF::P, E = n / 32;
+    constexpr size_t nn = size_t(n) * n;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw1 = s_tw + M;
+    cplx<T>* s_hs = s_tw1 + WF::TW1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_hs + n + warp * WF::SCRATCH;
+    for (int t = threadIdx.x; t < M; t += TRW_WARPS * 32) s_tw[t] = g_tw[t];
+    for (int t = threadIdx.x; t < n; t += TRW_WARPS * 32) s_hs[t] = g_hs[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, TRW_WARPS * 32);
+    __syncthreads();
+    for (int item = blockIdx.x * TRW_WARPS + warp; item < count * n; item += gridDim.x * TRW_WARPS) {
+        const int b = item / n, x = item - b * n;
+        const T* ring = bf.ring + static_cast<size_t>(b0 + b) * bf.ring_stride + static_cast<size_t>(x) * n;
+        const T* Pn = ring + sp.slot_n * nn;
+        T pv[E], dv[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int y = lane + 32 * t;
+            pv[t] = Pn[y];
+            dv[t] = T(0);
+            if (sp.has_k) dv[t] = ring[sp.slot_k * nn + y] - (sp.slot_k1 >= 0 ? ring[sp.slot_k1 * nn + y] : T(0));
+        }
+        // z[i] = mirror(P_n row)[i] + i mirror(d row)[i], i = lane + 32 k; mirror by shuffle for k >= E
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (k < E)
+                z[k] = mk<T>(pv[k], dv[k]);
+            else
+                z[k] = mk<T>(__shfl_xor_sync(0xffffffffu, pv[P - 1 - k], 31),
+                             __shfl_xor_sync(0xffffffffu, dv[P - 1 - k], 31));
+        }
+        WF::template run<-1>(z, scr, s_tw, s_tw1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        cplx<T>* Dx = bf.D + (static_cast<size_t>(b0 + b) * n + x) * hp;
+        for (int v = lane; v < hp; v += 32) {
+            cplx<T> o = mk<T>(T(0), T(0));
+            if (v < n) {
+                const cplx<T> Zv = scr[v];
+                const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
+                o = mk<T>(dct_part<T>(Zv, Zc, s_hs[v]), dct_part_im<T>(Zv, Zc, s_hs[v]));
+            }
+            Dx[v] = o;
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(TRW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
+tr_rows_inv_w(int b0, int count, TRBuf<T> bf, TRStep sp, int nframes, int law, T beta, T* __restrict__ out,
+              double* __restrict__ fmax_bits, const cplx<T>* __restrict__ g_tw) {
+    using Gm = TRGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
+    constexpr size_t nn = size_t(n) * n;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw1 = s_tw + M;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
+    for (int t = threadIdx.x; t < M; t += TRW_WARPS * 32) s_tw[t] = g_tw[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, TRW_WARPS * 32);
+    __syncthreads();
+    constexpr T inv = T(1.0 / (double(M) * double(M)));
+    for (int item = blockIdx.x * TRW_WARPS + warp; item < count * RP; item += gridDim.x * TRW_WARPS) {
+        const int b = item / RP, x0 = 2 * (item - b * RP);
+        const int bg = b0 + b;
+        const cplx<T>* Y0 = bf.D + (static_cast<size_t>(bg) * n + x0) * hp;
+        const cplx<T>* Y1 = Y0 + hp;
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int v = lane + 32 * k;
+            const int w = v <= n ? v : M - v;
+            const cplx<T> y = Y0[w], r = Y1[w];
+            if (v == 0 || v == n)
+                z[k] = mk<T>(y.x, r.x);
+            else if (v < n)
+                z[k] = mk<T>(y.x - r.y, y.y + r.x);
+            else
+                z[k] = mk<T>(y.x + r.y, r.x - y.y);
+        }
+        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        T* ring = bf.ring + static_cast<size_t>(bg) * bf.ring_stride;
+        T* Pnext = sp.slot_next >= 0 ? ring + sp.slot_next * nn : nullptr;
+        const int* blk = bf.blk + static_cast<size_t>(bg) * bf.blk_stride;
+        const T* sch = bf.sched + (static_cast<size_t>(bg) * bf.steps + (sp.step < bf.steps ? sp.step : 0)) * bf.nblk;
+        const T* L0 = bf.leak0 + static_cast<size_t>(bg) * bf.leak_stride;
+        T* O = sp.frame >= 0 ? out + (static_cast<size_t>(bg) * nframes + sp.frame) * nn : nullptr;
+        T mx = T(0);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const size_t rowo = static_cast<size_t>(x0 + half) * n;
+#pragma unroll 4
+            for (int t = 0; t < E; ++t) {
+                const int j = lane + 32 * t;
+                const cplx<T> zz = scr[j];
+                T tv = (half ? zz.y : zz.x) * inv;
+                tv = tv > T(0) ? tv : T(0);  // clamp_negatives (solver.cpp:33-46)
+                if (O) O[rowo + j] = tv;
+                mx = mx > tv ? mx : tv;
+                if (Pnext) {
+                    const T f = law ? T(exp(beta * tv)) : T(1) + beta * tv;
+                    Pnext[rowo + j] = sch[blk[rowo + j]] + L0[rowo + j] * f;
+                }
+            }
+        }
+        if (O && fmax_bits) {
+            double m = double(mx);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+            if (lane == 0)
+                atomicMax(reinterpret_cast<unsigned long long*>(fmax_bits) + static_cast<size_t>(bg) * nframes + sp.frame,
+                          static_cast<unsigned long long>(__double_as_longlong(m)));
+        }
+        __syncwarp();
+    }
+}
+
 // P_1 = P_dyn,1 + L0 (T_0 = 0); Z = 0
 template <typename T>
 __global__ void tr_init(int b0, int count, TRBuf<T> bf, int nn, size_t zcount) {
@@ -370,6 +514,13 @@ struct TRLaunch {
     using Gm = TRGeom<T, M>;
     static size_t smem_rf() { return sizeof(cplx<T>) * (M * Gm::LP + M + Gm::n); }
     static size_t smem_ri() { return sizeof(cplx<T>) * (M * Gm::LP + M); }
+    static size_t smem_w(bool fwd) {
+        if constexpr (tr_warp_rows<M>())
+            return sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + (fwd ? Gm::n : 0) +
+                                      TRW_WARPS * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
     static size_t smem_c() {
         return sizeof(cplx<T>) * (Gm::TILEC + StageTw<M, false>::SIZE + StageTw<M, true>::SIZE + M);
     }
@@ -384,6 +535,15 @@ struct TRLaunch {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], tr_rows_fwd<T, M>, Gm::NT, smem_rf());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], tr_cols<T, M>, Gm::NTC, smem_c());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], tr_rows_inv<T, M>, Gm::NT, smem_ri());
+            if constexpr (tr_warp_rows<M>()) {
+                cudaFuncSetAttribute(tr_rows_fwd_w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_w(true)));
+                cudaFuncSetAttribute(tr_rows_inv_w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem_w(false)));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], tr_rows_fwd_w<T, M>, TRW_WARPS * 32,
+                                                              smem_w(true));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], tr_rows_inv_w<T, M>, TRW_WARPS * 32,
+                                                              smem_w(false));
+            }
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -429,10 +589,19 @@ struct TRLaunch {
                 sp.slot_k1 = (sp.has_k && s - k - 1 >= 1) ? (s - k - 1) % (k + 2) : -1;
                 sp.slot_next = s < steps ? (s + 1) % (k + 2) : -1;
                 sp.frame = (s % os == 0) ? s / os - 1 : -1;
-                tr_rows_fwd<T, M><<<grid(cnt * Gm::RB, res[0]), Gm::NT, smem_rf(), st>>>(b0, cnt, cb, sp, tw, hs);
+                if constexpr (tr_warp_rows<M>())
+                    tr_rows_fwd_w<T, M><<<grid((cnt * n + TRW_WARPS - 1) / TRW_WARPS, res[0]), TRW_WARPS * 32,
+                                          smem_w(true), st>>>(b0, cnt, cb, sp, tw, hs);
+                else
+                    tr_rows_fwd<T, M><<<grid(cnt * Gm::RB, res[0]), Gm::NT, smem_rf(), st>>>(b0, cnt, cb, sp, tw, hs);
                 tr_cols<T, M><<<grid(cnt * Gm::CT, res[1]), Gm::NTC, smem_c(), st>>>(b0, cnt, cb, sp, tw, hs, tab);
-                tr_rows_inv<T, M><<<grid(cnt * Gm::RPB, res[2]), Gm::NT, smem_ri(), st>>>(
-                    b0, cnt, cb, sp, nframes, o->law, T(o->beta), static_cast<T*>(t_out), max_out, tw);
+                if constexpr (tr_warp_rows<M>())
+                    tr_rows_inv_w<T, M><<<grid((cnt * n / 2 + TRW_WARPS - 1) / TRW_WARPS, res[2]), TRW_WARPS * 32,
+                                          smem_w(false), st>>>(b0, cnt, cb, sp, nframes, o->law, T(o->beta),
+                                                               static_cast<T*>(t_out), max_out, tw);
+                else
+                    tr_rows_inv<T, M><<<grid(cnt * Gm::RPB, res[2]), Gm::NT, smem_ri(), st>>>(
+                        b0, cnt, cb, sp, nframes, o->law, T(o->beta), static_cast<T*>(t_out), max_out, tw);
                 kc += 3;
             }
         }

@@ -124,3 +124,38 @@ def test_trace_batch_rejects_bad_options(b200lib, greens64):
             dg.trace_batch_device(blk_d.data_ptr(), 0, sch_d.data_ptr(), sched.shape[2], l0_d.data_ptr(), 0, 1, o,
                                   out.data_ptr())
         assert e.value.status == 2, kw
+
+
+def test_trace_batch_n512_warp_rows(b200lib, oracle, tmp_path):
+    """n = 512 (m = 1024): the warp-per-row passes with the 32-point register DFT."""
+    import ctypes as C
+    from paper_2307_12119_b200.api import GreensArrays
+    n = 512
+    (tmp_path / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    (tmp_path / "var.txt").write_text("dopant_spread 0\nbeta 0.017\n")
+    L = b200lib
+    g = C.c_void_p()
+    assert L.gt_calibrate(str(tmp_path / "stack.txt").encode(), str(tmp_path / "var.txt").encode(), None, 90.0,
+                          C.byref(g), None) == 0, L.gt_last_error()
+    maps = {}
+    for k in ("f_sp0", "g_sp0"):
+        f = C.c_void_p()
+        assert L.gt_greens_field(g, k.encode(), C.byref(f)) == 0
+        maps[k] = np.ctypeslib.as_array(L.gt_field_data(f), shape=(n, n)).copy()
+        L.gt_field_free(f)
+    fs = maps["f_sp0"]
+    ga = GreensArrays(n=n, pitch=0.016 / n, f_sp0=fs, g_sp0=maps["g_sp0"],
+                      phi=float(np.mean(np.concatenate([fs[0], fs[-1], fs[1:-1, 0], fs[1:-1, -1]]))),
+                      kappa_inf=float(fs[0, 0]), alpha=L.gt_greens_alpha(g), beta=0.017, mu=L.gt_greens_mu(g),
+                      capacitance=L.gt_greens_capacitance(g), rand_scale=1.0)
+    L.gt_greens_free(g)
+    B, steps, dt, stride, window = 2, 6, 1e-5, 2, 3
+    blk, sched, on = _traces(B, steps, n=n, blocks=32, switch_prob=0.3)
+    leak0 = 0.3 * on
+    ref, st, secs = oracle.trace_leak_batch(ga, blk, sched, leak0, dt, window, law=0, beta=0.017, out_stride=stride)
+    assert (st == 0).all()
+    for prec, atol in ((1, 1e-8), (0, 1e-3)):
+        out, mx = _run_gpu(ga, prec, blk, sched, leak0, dt, window, 0, 0.017, stride)
+        err = np.abs(out - ref).max()
+        print(f"n=512 prec={prec}: max|dT| {err:.3e} K on peak {ref.max():.2f} K (oracle {secs:.1f} s)")
+        assert err <= atol
