@@ -514,11 +514,17 @@ def run_b200(args, cfg):
 
     cfg3 = None
     if not args.no_cfg3:
-        cfg3 = run_cfg3(args, dev, ws, rank)
+        try:
+            cfg3 = run_cfg3(args, dev, ws, rank)
+        except Exception as e:  # a sub-benchmark must not take the headline line down
+            cfg3 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cfg4 = None
     if not args.no_cfg4:
-        cfg4 = run_cfg4(args, dev, ws, rank)
+        try:
+            cfg4 = run_cfg4(args, dev, ws, rank)
+        except Exception as e:
+            cfg4 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -126,12 +126,15 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
         else:
             send = torch.cat([torch.cat([z[:, cq:cq + hq], z[:, mir[q]]], dim=1).reshape(-1)
                               for q, (cq, hq) in enumerate(ranges)])
-            # output splits: what each source sends me; input splits: what I send each rank
-            exchange(zrecv.view(-1), send, [P * 2 * hc] * world, [P * 2 * hq for _, hq in ranges])
+            # output splits: what each source sends me; input splits: what I send each rank.
+            # Complex blocks travel as their float64 (re, im) view (NCCL has no complex type).
+            exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
+                     [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
             ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, c1, c2, ycol, stream)
             send = ycol.reshape(world, rows, hc).reshape(-1).contiguous()
             recv = torch.empty(sum(rows * hq for _, hq in ranges), dtype=cd, device=dev)
-            exchange(recv, send, [rows * hq for _, hq in ranges], [rows * hc] * world)
+            exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
+                     [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)
             off = 0
             for q, (cq, hq) in enumerate(ranges):
                 yrow[:, cq:cq + hq] = recv[off:off + rows * hq].view(rows, hq)
