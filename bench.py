@@ -439,36 +439,60 @@ def run_b200(args, cfg):
     peak, peak_src = peaks()
     whole = survey_bytes_per_solve(n, es) * B / (ms / 1e3) / 1e9  # per GPU
 
-    # end to end through the public host API: pinned host inputs, H2D + compute + D2H of per-pair results
+    # end to end through the public host API: pinned host inputs, H2D + compute + D2H of per-pair results.
+    # Primary: gt_mc_batch_seeded -- the power maps and one 64-bit variation seed per pair cross
+    # PCIe and the variation maps are generated on the device (the reference monte_carlo API
+    # also takes seeds, not maps). Secondary: gt_mc_batch with both maps from the host.
     e2e = None
     if not args.no_e2e:
         Ph = P.cpu().pin_memory()
         Vh = V.cpu().pin_memory()
+        seeds_h = torch.from_numpy(np.array([inputs.sample_seed(cfg.base_seed, inputs.PURPOSE_VAR, rank * B + i)
+                                             for i in range(B)], dtype=np.uint64).view(np.int64)).pin_memory()
         import ctypes as C
         from paper_2307_12119_b200.api import check, lib
         L = lib()
+        dg.var_model(cfg.sigma_over_mu, cfg.corr_range)
         mx = np.empty(B)
         mean = np.empty(B)
         sts = np.empty(B, dtype=np.int32)
         msc = C.c_double()
+        cp = C.POINTER
 
-        def e2e_step():
+        def step_seeded():
+            check(L, L.gt_mc_batch_seeded(dg.handle, C.c_void_p(Ph.data_ptr()), C.c_void_p(seeds_h.data_ptr()), B,
+                                          C.byref(opts), None, mx.ctypes.data_as(cp(C.c_double)),
+                                          mean.ctypes.data_as(cp(C.c_double)), sts.ctypes.data_as(cp(C.c_int)),
+                                          C.byref(msc)))
+
+        def step_maps():
             check(L, L.gt_mc_batch(dg.handle, C.c_void_p(Ph.data_ptr()), C.c_void_p(Vh.data_ptr()), B,
-                                   C.byref(opts), None, mx.ctypes.data_as(C.POINTER(C.c_double)),
-                                   mean.ctypes.data_as(C.POINTER(C.c_double)),
-                                   sts.ctypes.data_as(C.POINTER(C.c_int)), C.byref(msc)))
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        if ws > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        el = shard.max_over_ranks((time.perf_counter() - t0) / args.steps, dev)
+                                   C.byref(opts), None, mx.ctypes.data_as(cp(C.c_double)),
+                                   mean.ctypes.data_as(cp(C.c_double)), sts.ctypes.data_as(cp(C.c_int)),
+                                   C.byref(msc)))
+
+        def timed(fn):
+            for _ in range(max(1, args.warmup)):
+                fn()
+            if ws > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                fn()
+            return shard.max_over_ranks((time.perf_counter() - t0) / args.steps, dev)
+
+        el = timed(step_seeded)
+        failed_seeded = int((sts != 0).sum())
+        el_maps = timed(step_maps)
         e2e = {"value": ws * B / el, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * B * n * n * es, "d2h_bytes_per_step": B * SAMPLE_STATS_DTYPE.itemsize,
-               "ms_per_step": 1e3 * el,
-               "path": "gt_mc_batch (host API): pinned p_dyn/var -> H2D, fused passes, D2H of per-pair max/mean/status"}
+               "h2d_bytes_per_step": B * n * n * es + 8 * B, "d2h_bytes_per_step": B * SAMPLE_STATS_DTYPE.itemsize,
+               "ms_per_step": 1e3 * el, "failed_pairs": failed_seeded,
+               "path": "gt_mc_batch_seeded (host API): pinned p_dyn + per-pair variation seeds -> H2D, variation "
+                       "maps generated on the device (config-1 model), fused passes, D2H of per-pair "
+                       "max/mean/status",
+               "with_host_variation_maps": {"value": ws * B / el_maps, "ms_per_step": 1e3 * el_maps,
+                                            "h2d_bytes_per_step": 2 * B * n * n * es,
+                                            "path": "gt_mc_batch: pinned p_dyn and var maps -> H2D"}}
 
     # mode B (north-star fixed point) on the same pairs: literal exp law (runaway expected,
     # SURVEY §0) on a subset, and the reference's linear law timed over the full batch.

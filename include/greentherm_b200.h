@@ -185,6 +185,26 @@ gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, in
                             double* app, const double* p, const double* l0, const gt_fp_opts* opts,
                             unsigned long long* res_bits, int* status, void* stream);
 
+/* ---- Seeded variation maps generated on the device (n = 64, 128, 256).
+ * The config-1 variation model: var = 1 + sigma_over_mu * z, z a unit-variance
+ * Gaussian random field with the reference's spherical correlogram
+ * (variation.cpp:75-79) of range range_frac x die width, by circulant embedding
+ * on the 2n torus (gen_systematic_map, variation.cpp:87-132), drawn from
+ * counter-based Philox noise: a sample depends only on its 64-bit seed, not on
+ * the batch it is generated in. Same distribution as the reference generator,
+ * not the same samples (gt_monte_carlo keeps the reference's own RNG stream).
+ *   gt_var_model       : prepare sqrt(lambda) on the device set (once)
+ *   gt_var_generate_device : device seeds -> device maps [batch][n][n]
+ *   gt_mc_batch_seeded : gt_mc_batch with var generated on the device from host
+ *                        seeds (the reference monte_carlo takes seeds, not maps):
+ *                        only the power maps cross PCIe */
+gt_status gt_var_model(gt_device_greens* d, double sigma_over_mu, double range_frac);
+gt_status gt_var_generate_device(const gt_device_greens* d, const unsigned long long* seeds, int batch, void* var_out,
+                                 void* stream);
+gt_status gt_mc_batch_seeded(const gt_device_greens* d, const void* p_dyn, const unsigned long long* seeds, int batch,
+                             const gt_batch_opts* opts, void* t_out, double* max_out, double* mean_out,
+                             int* status_out, double* online_ms);
+
 /* Bytes of device scratch a device-resident batch uses per in-flight sample,
  * and the number of kernels it launches for (batch, chunk). */
 size_t gt_mc_scratch_bytes(int n, int precision);

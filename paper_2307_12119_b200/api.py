@@ -126,6 +126,9 @@ _EXT = [
                                      vp, vp, vp]),
     ("gt_trace_scratch_bytes", C.c_size_t, [cint, cint, cint]),
     ("gt_modal_kernel", cint, [cstr, C.POINTER(cint), pdbl]),
+    ("gt_var_model", cint, [vp, dbl, dbl]),
+    ("gt_var_generate_device", cint, [vp, vp, cint, vp, vp]),
+    ("gt_mc_batch_seeded", cint, [vp, vp, vp, cint, C.POINTER(BatchOpts), vp, pdbl, pdbl, C.POINTER(cint), pdbl]),
     ("gt_large_geometry", cint, [vp, C.POINTER(cint), C.POINTER(cint)]),
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
@@ -279,6 +282,33 @@ class DeviceGreens:
         check(L, L.gt_mc_batch(self._d, p.ctypes.data_as(vp), v.ctypes.data_as(vp), B, C.byref(o),
                                None if out is None else out.ctypes.data_as(vp), mx.ctypes.data_as(pdbl),
                                mean.ctypes.data_as(pdbl), st.ctypes.data_as(C.POINTER(cint)), C.byref(ms)))
+        return out, mx, mean, st, ms.value
+
+    def var_model(self, sigma_over_mu: float = 0.10, range_frac: float = 0.5) -> None:
+        """Prepare the seeded device variation model (include/greentherm_b200.h gt_var_model)."""
+        check(lib(), lib().gt_var_model(self._d, sigma_over_mu, range_frac))
+
+    def var_generate_device(self, seeds_ptr: int, batch: int, out_ptr: int, stream: int | None = None) -> None:
+        sp = None if stream is None else C.c_void_p(stream if stream else 1)
+        check(lib(), lib().gt_var_generate_device(self._d, C.c_void_p(seeds_ptr), batch, C.c_void_p(out_ptr), sp))
+
+    def mc_batch_seeded_host(self, p_dyn: np.ndarray, seeds: np.ndarray, opts: BatchOpts | None = None,
+                             want_maps: bool = True):
+        """Host power maps + host seeds (variation generated on the device);
+        returns (maps|None, max, mean, status, ms)."""
+        L = lib()
+        dt = np.float64 if self.precision == GT_FP64 else np.float32
+        p = np.ascontiguousarray(p_dyn, dtype=dt)
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        B = p.shape[0]
+        out = np.empty_like(p) if want_maps else None
+        mx, mean = np.empty(B), np.empty(B)
+        st = np.empty(B, dtype=np.int32)
+        ms = C.c_double()
+        o = opts or self.opts()
+        check(L, L.gt_mc_batch_seeded(self._d, p.ctypes.data_as(vp), sd.ctypes.data_as(vp), B, C.byref(o),
+                                      None if out is None else out.ctypes.data_as(vp), mx.ctypes.data_as(pdbl),
+                                      mean.ctypes.data_as(pdbl), st.ctypes.data_as(C.POINTER(cint)), C.byref(ms)))
         return out, mx, mean, st, ms.value
 
     def mc_batch_device(self, p_ptr: int, v_ptr: int, batch: int, opts: BatchOpts, out_ptr: int | None,

@@ -537,6 +537,135 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
     });
 }
 
+gt_status gt_var_model(gt_device_greens* d, double sigma_over_mu, double range_frac) {
+    return guarded([&] {
+        if (!d) fail(ST_CONFIG, "capi", "null device GreensSet");
+        if (!(sigma_over_mu >= 0.0) || !(range_frac > 0.0))
+            fail(ST_CONFIG, "variation", "variation model needs sigma/mu >= 0 and a positive correlation range");
+        const int n = d->d.n, m = d->d.m;
+        if (m != 128 && m != 256 && m != 512)
+            fail(ST_CONFIG, "device", "seeded device variation supports n = 64, 128, 256");
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        cudaStream_t st = d->stream;
+        const size_t mm = static_cast<size_t>(m) * m;
+        DBuf work, lam, red;
+        work.ensure(mm * 16);
+        lam.ensure(mm * 8);
+        red.ensure(64);
+        d->var_sqlam.ensure(static_cast<size_t>(m) * gtd_var_pitch(n) * (d->fp64 ? 8 : 4));
+        const double pitch = d->host.pitch;
+        cuda_ok(gtd_var_model(&d->d, d->tw64.p, pitch, range_frac * pitch * n, work.p, lam.as<double>(),
+                              red.as<double>(), d->var_sqlam.p, st),
+                "variation model");
+        cuda_ok(cudaStreamSynchronize(st), "sync");
+        d->var_sigma = sigma_over_mu;
+    });
+}
+
+namespace {
+void need_var_model(const gt_device_greens* d) {
+    if (!d->var_sqlam.p) fail(ST_CONFIG, "variation", "call gt_var_model before generating seeded variation maps");
+}
+}  // namespace
+
+gt_status gt_var_generate_device(const gt_device_greens* dc, const unsigned long long* seeds, int batch, void* var_out,
+                                 void* stream) {
+    return guarded([&] {
+        if (!dc || batch < 1 || !seeds || !var_out) fail(ST_CONFIG, "capi", "variation generation needs seeds and output");
+        auto* d = const_cast<gt_device_greens*>(dc);
+        need_var_model(d);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        const int chunk = std::min(batch, 1024);
+        d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(d->d.n, d->fp64) * chunk);
+        cuda_ok(gtd_var_generate(&d->d, d->var_sqlam.p, seeds, batch, d->var_sigma, var_out, d->var_scratch.p, chunk, st),
+                "variation generation");
+        d->kernels += 2 * ((batch + chunk - 1) / chunk);
+    });
+}
+
+gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, const unsigned long long* seeds, int batch,
+                             const gt_batch_opts* opts, void* t_out, double* max_out, double* mean_out,
+                             int* status_out, double* online_ms) {
+    return guarded([&] {
+        if (batch < 1 || !p_dyn || !seeds) fail(ST_CONFIG, "capi", "batch needs power maps and seeds");
+        auto t0 = wall::now();
+        auto* d = const_cast<gt_device_greens*>(dc);
+        need_var_model(d);
+        std::lock_guard<std::mutex> lk(d->mu);
+        cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
+        const int n = d->d.n;
+        const size_t es = d->fp64 ? 8 : 4;
+        const size_t map = static_cast<size_t>(n) * n * es;
+        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 512);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr);
+        gtd_mc_opts o = to_dev_opts(opts);
+        d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(n, d->fp64) * chunk);
+        for (int s = 0; s < 2; ++s) {
+            if (!d->slot_stream[s]) cuda_ok(cudaStreamCreateWithFlags(&d->slot_stream[s], cudaStreamNonBlocking), "stream");
+            d->slot_in[s].ensure(2 * map * chunk);
+            d->slot_seeds[s].ensure(sizeof(unsigned long long) * chunk);
+            if (t_out) d->slot_out[s].ensure(map * chunk);
+            d->slot_scr[s].ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * inner);
+            d->slot_stats[s].ensure(sizeof(gtd_sample_stats) * chunk);
+        }
+        const size_t hs_bytes = sizeof(gtd_sample_stats) * static_cast<size_t>(batch);
+        if (d->host_stats_bytes < hs_bytes) {
+            if (d->host_stats) cudaFreeHost(d->host_stats);
+            d->host_stats = nullptr;
+            d->host_stats_bytes = 0;
+            cuda_ok(cudaMallocHost(&d->host_stats, hs_bytes), "cudaMallocHost");
+            d->host_stats_bytes = hs_bytes;
+        }
+        auto* hs = static_cast<gtd_sample_stats*>(d->host_stats);
+        const char* P = static_cast<const char*>(p_dyn);
+        // the variation scratch is shared by both slots: serialise generation across slots with an event
+        cudaEvent_t gen_done[2];
+        for (auto& e : gen_done) cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        for (int s0 = 0, k = 0; s0 < batch; s0 += chunk, ++k) {
+            const int cnt = std::min(chunk, batch - s0);
+            const int s = k & 1;
+            cudaStream_t st = d->slot_stream[s];
+            char* din = static_cast<char*>(d->slot_in[s].p);
+            cuda_ok(cudaMemcpyAsync(din, P + s0 * map, cnt * map, cudaMemcpyHostToDevice, st), "h2d p");
+            cuda_ok(cudaMemcpyAsync(d->slot_seeds[s].p, seeds + s0, sizeof(unsigned long long) * cnt,
+                                    cudaMemcpyHostToDevice, st),
+                    "h2d seeds");
+            if (k > 0) cuda_ok(cudaStreamWaitEvent(st, gen_done[s ^ 1], 0), "wait");
+            cuda_ok(gtd_var_generate(&d->d, d->var_sqlam.p, static_cast<const unsigned long long*>(d->slot_seeds[s].p),
+                                     cnt, d->var_sigma, din + chunk * map, d->var_scratch.p, cnt, st),
+                    "variation generation");
+            cuda_ok(cudaEventRecord(gen_done[s], st), "record");
+            gtd_mc_in in{};
+            in.P = din;
+            in.N = din;
+            in.V = din + chunk * map;
+            in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
+            in.nom_scale = opts ? opts->leak_frac : 0.3;
+            auto* dst = static_cast<gtd_sample_stats*>(d->slot_stats[s].p);
+            cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, t_out ? d->slot_out[s].p : nullptr, dst, d->slot_scr[s].p,
+                                 std::min(inner, cnt), st, nullptr, nullptr),
+                    "mc batch launch");
+            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt)) + 2;
+            if (t_out)
+                cuda_ok(cudaMemcpyAsync(static_cast<char*>(t_out) + s0 * map, d->slot_out[s].p, cnt * map,
+                                        cudaMemcpyDeviceToHost, st),
+                        "d2h maps");
+            cuda_ok(cudaMemcpyAsync(hs + s0, dst, sizeof(gtd_sample_stats) * cnt, cudaMemcpyDeviceToHost, st), "d2h stats");
+        }
+        for (auto& st : d->slot_stream) cuda_ok(cudaStreamSynchronize(st), "batch sync");
+        for (auto& e : gen_done) cudaEventDestroy(e);
+        for (int i = 0; i < batch; ++i) {
+            if (max_out) max_out[i] = hs[i].max_rise;
+            if (mean_out) mean_out[i] = hs[i].mean_rise;
+            if (status_out) status_out[i] = hs[i].status;
+        }
+        if (online_ms) *online_ms = ms_since(t0);
+    });
+}
+
 void gt_fp_opts_default(gt_fp_opts* o) {
     o->leak_frac = 0.3;
     o->law = 1;

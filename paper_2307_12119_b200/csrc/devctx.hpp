@@ -58,6 +58,8 @@ struct gt_device_greens {
     std::mutex mu;
     gth::DBuf fp_scratch, fp_state, fp_counter;
     gth::DBuf trace_scratch, trace_tab;
+    gth::DBuf var_sqlam, var_scratch, slot_seeds[2];  // seeded variation model (gt_var_model)
+    double var_sigma = 0.0;
     int* fp_counter_h = nullptr;
     gth::DBuf scratch, stats, slot_in[2], slot_out[2], slot_scr[2], slot_stats[2];
     cudaStream_t slot_stream[2] = {nullptr, nullptr};

@@ -169,6 +169,18 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
 int gtd_lg_kernel_spectrum(const gtd_lg* g, const double* f_sp0, double phi, void* S1, void* Z, void* C1,
                            void* fk_out, cudaStream_t st);
 
+/* ---- seeded variation maps on the device (vargen.cu), m = 128 / 256 / 512 */
+int gtd_var_pitch(int n);
+size_t gtd_var_scratch_bytes_per_sample(int n, int fp64);
+/* sqrt(lambda) [m][var_pitch] (device precision) of the spherical correlogram with `range`
+ * (same length unit as pitch), normalised to unit variance. work_d: m*m double2,
+ * lam_d: m*m double, red_d: 3 doubles. */
+int gtd_var_model(const gtd_greens* g, const void* tw64, double pitch, double range, void* work_d, double* lam_d,
+                  double* red_d, void* sqlam_out, cudaStream_t st);
+/* var[b] = 1 + sigma z_b, z_b the field of seeds[b] (device array); scratch per sample as above */
+int gtd_var_generate(const gtd_greens* g, const void* sqlam, const unsigned long long* seeds, int batch,
+                     double sigma, void* var, void* scratch, int chunk, cudaStream_t st);
+
 /* ---- config-3 batched transient traces (trace_batch.cu) */
 typedef struct gtd_trace_in {
     const int* blk;
