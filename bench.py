@@ -407,6 +407,7 @@ def run_b200(args, cfg):
     e1.record(stream)
     torch.cuda.synchronize()
     pass_ms, kernels, calls = dg.profile_end()
+    per_launch = min(B, args.chunk or 1024)  # pairs per pass launch (the library's auto chunk is 1024)
     if ws > 1:
         dist.barrier()
     ms_local = e0.elapsed_time(e1) / args.steps
@@ -437,6 +438,15 @@ def run_b200(args, cfg):
     dom = int(np.argmax(pass_ms[:3]))
     achieved = bps[dom] * B * args.steps / (pass_ms[dom] / 1e3) / 1e9
     peak, peak_src = peaks()
+    # measured DRAM bytes of the dominant kernel (ncu --set full, committed under profiles/)
+    traffic, traffic_src = None, None
+    tf = ROOT / "profiles" / "r1_traffic.json"
+    kname = ["mc_pass1w", "mc_pass2", "mc_pass3w"][dom] + f"<{'float' if es == 4 else 'double'}, {2 * n}>"
+    if tf.exists():
+        tj = json.loads(tf.read_text())
+        if kname in tj["kernels"]:
+            traffic = tj["kernels"][kname]["dram_bytes_per_pair"] * per_launch
+            traffic_src = f"{kname}: {tj['source']} (scaled to {per_launch} pairs per launch)"
     whole = survey_bytes_per_solve(n, es) * B / (ms / 1e3) / 1e9  # per GPU
 
     # end to end through the public host API: pinned host inputs, H2D + compute + D2H of per-pair results.
@@ -566,7 +576,8 @@ def run_b200(args, cfg):
                        "l2": "no flush: 2 x pairs x 256 KiB inputs per step (>> 126 MB L2)",
                        "parallelism": f"dp{ws} (independent pairs per GPU, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": bps[dom] * per_launch,
                          "kernel": ["mc_pass1 (rows)", "mc_pass2 (columns)", "mc_pass3 (rows)"][dom],
                          "pass_ms_per_step": [x / args.steps for x in pass_ms[:3]],
                          "bytes_per_pair_per_pass": bps, "peak_source": peak_src,
