@@ -69,13 +69,16 @@ LeakNoise leak_noise(const VarParams& v, int n, uint64_t base_seed, uint64_t run
 
 // Device builder of d_length / d_tox maps from host noise.
 struct VarDevice {
-    gt_device_greens* d;
     int n, m;
     size_t nn, mm;
     double pitch;
+    const void* tw64;
+    cudaStream_t stream;
     DBuf sqrt_lam, work, noise, sys, red;
-    VarDevice(gt_device_greens* dd, const VarParams& v, double pitch_) : d(dd), pitch(pitch_) {
-        n = d->d.n;
+    VarDevice(gt_device_greens* dd, const VarParams& v, double pitch_)
+        : VarDevice(dd->d.n, dd->tw64.p, dd->stream, v, pitch_) {}
+    VarDevice(int n_, const void* tw64_, cudaStream_t st_, const VarParams& v, double pitch_)
+        : n(n_), pitch(pitch_), tw64(tw64_), stream(st_) {
         m = 2 * n;
         nn = static_cast<size_t>(n) * n;
         mm = static_cast<size_t>(m) * m;
@@ -83,8 +86,8 @@ struct VarDevice {
         red.ensure(64);
         if (v.sigma_sys != 0.0) {
             sqrt_lam.ensure(mm * 8);
-            cuda_ok(gtd_var_eigs(n, pitch, v.corr_range * (n * pitch), 1, d->tw64.p, work.p, sqrt_lam.as<double>(),
-                                 red.as<double>(), d->stream),
+            cuda_ok(gtd_var_eigs(n, pitch, v.corr_range * (n * pitch), 1, tw64, work.p, sqrt_lam.as<double>(),
+                                 red.as<double>(), stream),
                     "variation eigenvalues");
         }
         noise.ensure(mm * 8);
@@ -92,12 +95,11 @@ struct VarDevice {
     }
     // out = sigma_sys * shaped(sys_noise) + rnd_noise (either part may be absent)
     void field(const VarParams& v, const std::vector<double>& sysn, const std::vector<double>& rndn, double* out) {
-        cudaStream_t st = d->stream;
+        cudaStream_t st = stream;
         cuda_ok(cudaMemsetAsync(out, 0, nn * 8, st), "memset");
         if (!sysn.empty()) {
             cuda_ok(cudaMemcpyAsync(noise.p, sysn.data(), mm * 8, cudaMemcpyHostToDevice, st), "h2d");
-            cuda_ok(gtd_var_shape(noise.as<double>(), sqrt_lam.as<double>(), n, v.sigma_sys, d->tw64.p, work.p, out,
-                                  st),
+            cuda_ok(gtd_var_shape(noise.as<double>(), sqrt_lam.as<double>(), n, v.sigma_sys, tw64, work.p, out, st),
                     "shape");
         }
         if (!rndn.empty()) {
@@ -564,4 +566,287 @@ void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nomina
     for (int i = 0; i < B; ++i)
         if (!errors[i].empty())
             fail(ST_VALIDATION, "solver", "monte carlo seed " + std::to_string(seeds[i]) + " failed: " + errors[i]);
+}
+
+// ============================================================ FDM oracle (fdm.cu)
+// The reference's ThermalNetwork (fdm.cpp:22-296) on the device: per-cell die
+// conductivity, Jacobi-preconditioned CG with Eigen's stopping rule
+// (|r|^2 < tol^2 |b|^2, 40000 iterations), the steady outer fixed point and
+// backward-Euler stepping with leakage refreshed every sub-step.
+namespace {
+
+enum : uint64_t { COND_PURPOSE = 0x31 };
+
+std::vector<double> host_twiddles(int m) {
+    std::vector<double> t(2 * static_cast<size_t>(m));
+    for (int k = 0; k < m; ++k) {
+        const double a = -2.0 * M_PI * static_cast<double>(k) / m;
+        t[2 * k] = std::cos(a);
+        t[2 * k + 1] = std::sin(a);
+    }
+    return t;
+}
+
+// conductivity_map (variation.cpp:224-238): i.i.d. clamped dopant spread per cell
+std::vector<double> conductivity_map(double k_nominal, const VarParams& v, int n) {
+    std::vector<double> k(static_cast<size_t>(n) * n, k_nominal);
+    if (v.dopant_spread == 0.0) return k;
+    std::mt19937_64 eng(derived_seed(v.seed, COND_PURPOSE, 0));
+    std::normal_distribution<double> gauss(0.0, v.dopant_spread);
+    for (double& x : k) x = k_nominal * (1.0 + std::clamp(gauss(eng), -v.cond_clamp, v.cond_clamp));
+    return k;
+}
+
+struct FdmNet {
+    Stack s;
+    int n;
+    size_t nn, N;
+    cudaStream_t st = nullptr;
+    DBuf kmap, kd, diag, x, xo, b, r, z, p, q, ax, sc, flag, red, tmp;
+    double g_sink, c_die, c_tim, c_spr;
+
+    FdmNet(const Stack& s_, const std::vector<double>& k_host) : s(s_), n(s_.n) {
+        s.validate();
+        nn = static_cast<size_t>(n) * n;
+        N = 3 * nn;
+        for (double k : k_host)
+            if (!(k > 0.0)) fail(ST_CONFIG, "oracle", "non-positive die conductivity");
+        cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        upload(kmap, k_host.data(), nn * 8, st);
+        for (DBuf* bu : {&kd}) bu->ensure(nn * 8);
+        for (DBuf* bu : {&diag, &x, &xo, &b, &r, &z, &p, &q, &ax, &tmp}) bu->ensure(N * 8);
+        sc.ensure(8 * 8);
+        flag.ensure(8);
+        red.ensure(64);
+        const double area = s.pitch() * s.pitch();
+        c_die = s.die.heat_capacity * area * s.die.thickness;
+        c_tim = s.tim.heat_capacity * area * s.tim.thickness;
+        c_spr = s.spreader.heat_capacity * area * s.spreader.thickness;
+        // spreader half-thickness plus the cell's share of the lumped sink (fdm.cpp:38-42)
+        const double r_half = s.spreader.thickness / (2.0 * s.spreader.conductivity * area);
+        g_sink = 1.0 / (r_half + static_cast<double>(n) * n * s.sink_resistance);
+        cuda_ok(cudaMemsetAsync(x.p, 0, N * 8, st), "memset");
+    }
+    ~FdmNet() {
+        if (st) cudaStreamDestroy(st);
+    }
+    gtd_fdm net(double inv_dt) const {
+        gtd_fdm f{};
+        f.n = n;
+        f.pitch = s.pitch();
+        f.t_die = s.die.thickness;
+        f.t_tim = s.tim.thickness;
+        f.t_spr = s.spreader.thickness;
+        f.k_tim = s.tim.conductivity;
+        f.k_spr = s.spreader.conductivity;
+        f.c_die = c_die;
+        f.c_tim = c_tim;
+        f.c_spr = c_spr;
+        f.g_sink = g_sink;
+        f.inv_dt = inv_dt;
+        f.kd = kd.as<double>();
+        return f;
+    }
+    // effective conductivity at the die rise (nullptr: k_map) and the operator diagonal
+    void prepare(const double* rise, double cond_c, double inv_dt) {
+        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+        cuda_ok(gtd_fdm_kcell(kmap.as<double>(), rise, cond_c, n, kd.as<double>(), flag.as<int>(), st), "kcell");
+        int fl = 0;
+        d2h(&fl, flag.p, 4, st);
+        if (fl)
+            fail(ST_VALIDATION, "oracle",
+                 "die conductivity went non-positive; outside linearization validity");
+        const gtd_fdm f = net(inv_dt);
+        cuda_ok(gtd_fdm_diag(&f, diag.as<double>(), st), "diag");
+    }
+    // Eigen ConjugateGradient<..., DiagonalPreconditioner> on A x = b (fdm.cpp:120-146);
+    // x holds the guess (zero when !guess) and the solution.
+    void solve(double inv_dt, bool guess, double tol) {
+        if (!guess) cuda_ok(cudaMemsetAsync(x.p, 0, N * 8, st), "memset");
+        const gtd_fdm f = net(inv_dt);
+        cuda_ok(gtd_fdm_spmv(&f, diag.as<double>(), x.as<double>(), ax.as<double>(), nullptr, nullptr, st), "spmv");
+        cuda_ok(gtd_cg_init(static_cast<int>(N), b.as<double>(), ax.as<double>(), diag.as<double>(), r.as<double>(),
+                            z.as<double>(), p.as<double>(), sc.as<double>(), st),
+                "cg init");
+        double h[8];
+        d2h(h, sc.p, 64, st);
+        const double rhs2 = h[2];
+        if (rhs2 == 0.0) {
+            cuda_ok(cudaMemsetAsync(x.p, 0, N * 8, st), "memset");
+            return;
+        }
+        const double threshold = std::max(tol * tol * rhs2, std::numeric_limits<double>::min());
+        if (h[1] < threshold) return;
+        const int max_iters = 40000;
+        int i = 0;
+        double rr = h[1];
+        for (; i < max_iters; ++i) {
+            cuda_ok(gtd_cg_step(&f, diag.as<double>(), x.as<double>(), r.as<double>(), z.as<double>(), p.as<double>(),
+                                q.as<double>(), sc.as<double>(), st),
+                    "cg step");
+            d2h(&rr, sc.as<double>() + 4, 8, st);
+            if (rr < threshold) break;
+            cuda_ok(gtd_cg_direction(static_cast<int>(N), z.as<double>(), p.as<double>(), sc.as<double>(), st),
+                    "cg direction");
+        }
+        if (i == max_iters)
+            fail(ST_SOLVER, "oracle", "conjugate gradient stalled, residual " + std::to_string(std::sqrt(rr / rhs2)));
+    }
+};
+
+struct OracleSetup {
+    Stack stack;
+    VarParams var;
+    std::vector<double> k_map;
+    bool have_leak = false, temp_dep_leakage = false, temp_dep_cond = false;
+    double cond_c = 0.0;
+    std::vector<double> p_leak0;  // host copy
+};
+
+// oracle_setup (reference capi.cpp:265-284)
+OracleSetup oracle_setup(const Stack& st, const VarParams* vp, const Field* nominal_leak, int tdl, int tdc) {
+    OracleSetup s;
+    s.stack = st;
+    s.stack.validate();
+    s.var = vp ? *vp : VarParams{};
+    if (!vp) s.var.dopant_spread = 0.0;
+    s.var.validate();
+    const int n = s.stack.n;
+    s.k_map = conductivity_map(s.stack.die.conductivity, s.var, n);
+    if (nominal_leak) {
+        if (nominal_leak->n != n) fail(ST_CONFIG, "oracle", "leakage map does not match the stack grid");
+        if (nominal_leak->min() < 0.0) fail(ST_CONFIG, "variation", "leakage_baseline: nominal leakage must be >= 0");
+        // make_leakage_baseline (variation.cpp:197-211), run 0
+        need_device();
+        const int m = 2 * n;
+        const size_t nn = static_cast<size_t>(n) * n;
+        cudaStream_t stx = nullptr;
+        cuda_ok(cudaStreamCreateWithFlags(&stx, cudaStreamNonBlocking), "stream");
+        DBuf tw, dl, dt, nom, pl, flag;
+        const std::vector<double> twh = host_twiddles(m);
+        upload(tw, twh.data(), twh.size() * 8, stx);
+        dl.ensure(nn * 8);
+        dt.ensure(nn * 8);
+        pl.ensure(nn * 8);
+        flag.ensure(8);
+        {
+            VarDevice vd(n, tw.p, stx, s.var, s.stack.pitch());
+            LeakNoise z = leak_noise(s.var, n, s.var.seed, 0);
+            vd.field(s.var, z.sys_l, z.rnd_l, dl.as<double>());
+            vd.field(s.var, z.sys_t, z.rnd_t, dt.as<double>());
+        }
+        upload(nom, nominal_leak->v.data(), nn * 8, stx);
+        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, stx), "memset");
+        cuda_ok(gtd_leak_exp(nom.as<double>(), dl.as<double>(), dt.as<double>(), s.var.beta_l, s.var.beta_tox,
+                             s.var.exponent_cap, n, pl.as<double>(), flag.as<int>(), stx),
+                "leakage exponent");
+        int fl = 0;
+        d2h(&fl, flag.p, 4, stx);
+        if (fl) fail(ST_VALIDATION, "variation", "leakage exponent exceeds cap (unphysical variation inputs)");
+        s.p_leak0.resize(nn);
+        d2h(s.p_leak0.data(), pl.p, nn * 8, stx);
+        cudaStreamDestroy(stx);
+        s.have_leak = true;
+        s.temp_dep_leakage = tdl != 0;
+    }
+    if (tdc) {
+        double k0p = 0.0;
+        s.temp_dep_cond = true;
+        linearize(s.stack.die.conductivity, s.var.eta, s.stack.ambient, &k0p, &s.cond_c);
+    }
+    return s;
+}
+
+}  // namespace
+
+// steady_solve (fdm.cpp:167-205) with SolveOptions defaults (max_iters 50, tol 0.01 K, linear_tol 1e-9)
+Field gt_ops_oracle_steady(const Stack& stack, const VarParams* var, const Field& p_dyn, const Field* nominal_leak,
+                           int temp_dep_leakage, int temp_dep_conductivity, int* outer_iterations) {
+    need_device();
+    OracleSetup o = oracle_setup(stack, var, nominal_leak, temp_dep_leakage, temp_dep_conductivity);
+    const int n = o.stack.n;
+    if (o.temp_dep_cond && !(o.cond_c > 0.0))
+        fail(ST_CONFIG, "oracle", "temp-dependent conductivity needs cond_c > 0");
+    if (o.temp_dep_leakage && !o.have_leak)
+        fail(ST_CONFIG, "oracle", "temp-dependent leakage needs a leakage baseline");
+    if (p_dyn.n != n) fail(ST_CONFIG, "oracle", "power map does not match the stack grid");
+    if (p_dyn.min() < 0.0) fail(ST_CONFIG, "oracle", "dynamic power must be >= 0");
+    FdmNet net(o.stack, o.k_map);
+    const size_t nn = net.nn, N = net.N;
+    DBuf pd, lk;
+    upload(pd, p_dyn.v.data(), nn * 8, net.st);
+    if (o.have_leak) upload(lk, o.p_leak0.data(), nn * 8, net.st);
+    const bool iterate = o.temp_dep_cond || o.temp_dep_leakage;
+    const int max_iters = 50;
+    const double tol = 0.01, linear_tol = 1e-9;
+    Field rise(n, o.stack.pitch(), Unit::Kelvin);
+    int it = 0;
+    for (int iter = 1; iter <= max_iters; ++iter) {
+        // p = p_dyn + leakage at the current die rise (x's die plane), x_old kept for the delta
+        cuda_ok(cudaMemcpyAsync(net.xo.p, net.x.p, N * 8, cudaMemcpyDeviceToDevice, net.st), "copy");
+        cuda_ok(gtd_fdm_rhs(pd.as<double>(), o.have_leak ? lk.as<double>() : nullptr, o.temp_dep_leakage, o.var.beta,
+                            net.xo.as<double>(), 0, 0, 0, 0.0, static_cast<int>(nn), net.b.as<double>(), net.st),
+                "rhs");
+        net.prepare(o.temp_dep_cond && iter > 1 ? net.xo.as<double>() : nullptr, o.cond_c, 0.0);
+        net.solve(0.0, iter > 1, linear_tol);
+        cuda_ok(gtd_absdiff(net.x.as<double>(), net.xo.as<double>(), N, net.tmp.as<double>(), net.st), "delta");
+        double r3[3];
+        cuda_ok(gtd_reduce(net.tmp.as<double>(), N, net.red.as<double>(), net.st), "reduce");
+        d2h(r3, net.red.p, 24, net.st);
+        const double delta = r3[2];
+        it = iter;
+        if (!iterate || (iter > 1 && delta < tol)) break;
+        if (iter == max_iters)
+            fail(ST_SOLVER, "oracle",
+                 "fixed-point loop hit max_iters with |dT| change " + std::to_string(delta) +
+                     " K (thermal runaway or tolerance too tight)");
+    }
+    d2h(rise.v.data(), net.x.p, nn * 8, net.st);
+    rise.check_finite("oracle die map");
+    if (outer_iterations) *outer_iterations = it;
+    return rise;
+}
+
+// gt_oracle_transient (reference capi.cpp:302-334): per sample time, backward Euler
+// over round(span / dt) equal sub-steps with leakage refreshed every sub-step.
+std::vector<Field> gt_ops_oracle_transient(const Stack& stack, const VarParams* var, const Field& p_dyn,
+                                           const Field* nominal_leak, int temp_dep_leakage,
+                                           const std::vector<double>& times, double dt) {
+    need_device();
+    if (times.empty()) fail(ST_CONFIG, "capi", "transient needs times");
+    OracleSetup o = oracle_setup(stack, var, nominal_leak, temp_dep_leakage, 0);
+    if (o.temp_dep_leakage && !o.have_leak)
+        fail(ST_CONFIG, "oracle", "temp-dependent leakage needs a leakage baseline");
+    const int n = o.stack.n;
+    if (p_dyn.n != n) fail(ST_CONFIG, "oracle", "trace frame does not match the stack grid");
+    if (p_dyn.min() < 0.0) fail(ST_CONFIG, "oracle", "trace powers must be >= 0");
+    const double base_dt = dt > 0.0 ? dt : 1e-4;
+    FdmNet net(o.stack, o.k_map);
+    const size_t nn = net.nn, N = net.N;
+    DBuf pd, lk;
+    upload(pd, p_dyn.v.data(), nn * 8, net.st);
+    if (o.have_leak) upload(lk, o.p_leak0.data(), nn * 8, net.st);
+    std::vector<Field> out;
+    double t_prev = 0.0;
+    for (double target : times) {
+        if (target <= t_prev) fail(ST_CONFIG, "capi", "sample times must be increasing");
+        const double span = target - t_prev;
+        const int steps = std::max(1, static_cast<int>(std::round(span / base_dt)));
+        const double h = span / steps;
+        net.prepare(nullptr, 0.0, 1.0 / h);
+        for (int k = 0; k < steps; ++k) {
+            cuda_ok(cudaMemcpyAsync(net.xo.p, net.x.p, N * 8, cudaMemcpyDeviceToDevice, net.st), "copy");
+            cuda_ok(gtd_fdm_rhs(pd.as<double>(), o.have_leak ? lk.as<double>() : nullptr, o.temp_dep_leakage,
+                                o.var.beta, net.xo.as<double>(), net.c_die, net.c_tim, net.c_spr, 1.0 / h,
+                                static_cast<int>(nn), net.b.as<double>(), net.st),
+                    "rhs");
+            net.solve(1.0 / h, true, 1e-9);
+        }
+        Field f(n, o.stack.pitch(), Unit::Kelvin);
+        d2h(f.v.data(), net.x.p, nn * 8, net.st);
+        f.check_finite("oracle die map");
+        out.push_back(std::move(f));
+        t_prev = target;
+    }
+    return out;
 }

@@ -314,19 +314,36 @@ gt_status gt_solve_trace(const gt_greens* g, const gt_trace* trace, int window, 
     });
 }
 
-// ---------------------------------------------------- FDM reference solver
-gt_status gt_oracle_steady(const char*, const char*, const gt_field*, const gt_field*, int, int, gt_field**,
-                           int*) {
+// ---------------------------------------------------- FDM reference solver (device, fdm.cu)
+gt_status gt_oracle_steady(const char* stack_path, const char* variation_path, const gt_field* p_dyn,
+                           const gt_field* nominal_leak, int temp_dep_leakage, int temp_dep_conductivity,
+                           gt_field** out, int* outer_iterations) {
     return guarded([&] {
-        fail(ST_INTERNAL, "oracle",
-             "the finite-difference reference solver is not part of the device build (see DESIGN.md: out of scope)");
+        if (!p_dyn || !out) fail(ST_CONFIG, "capi", "oracle needs a power map and an output");
+        Stack s = stack_path ? load_stack_file(stack_path) : Stack{};
+        VarParams v;
+        if (variation_path) v = load_var_file(variation_path);
+        Field f = gt_ops_oracle_steady(s, variation_path ? &v : nullptr, p_dyn->f,
+                                       nominal_leak ? &nominal_leak->f : nullptr, temp_dep_leakage,
+                                       temp_dep_conductivity, outer_iterations);
+        *out = new gt_field{std::move(f)};
     });
 }
-gt_status gt_oracle_transient(const char*, const char*, const gt_field*, const gt_field*, int, const double*,
-                              int, double, gt_result**) {
+gt_status gt_oracle_transient(const char* stack_path, const char* variation_path, const gt_field* p_dyn,
+                              const gt_field* nominal_leak, int temp_dep_leakage, const double* times, int n_times,
+                              double dt, gt_result** out) {
     return guarded([&] {
-        fail(ST_INTERNAL, "oracle",
-             "the finite-difference reference solver is not part of the device build (see DESIGN.md: out of scope)");
+        if (!times || n_times < 1) fail(ST_CONFIG, "capi", "transient needs times");
+        if (!p_dyn || !out) fail(ST_CONFIG, "capi", "oracle needs a power map and an output");
+        Stack s = stack_path ? load_stack_file(stack_path) : Stack{};
+        VarParams v;
+        if (variation_path) v = load_var_file(variation_path);
+        std::vector<double> tv(times, times + n_times);
+        auto r = std::make_unique<gt_result>();
+        r->rise = gt_ops_oracle_transient(s, variation_path ? &v : nullptr, p_dyn->f,
+                                          nominal_leak ? &nominal_leak->f : nullptr, temp_dep_leakage, tv, dt);
+        r->times = tv;
+        *out = r.release();
     });
 }
 

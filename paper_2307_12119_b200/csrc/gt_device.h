@@ -169,6 +169,29 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
 int gtd_lg_kernel_spectrum(const gtd_lg* g, const double* f_sp0, double phi, void* S1, void* Z, void* C1,
                            void* fk_out, cudaStream_t st);
 
+/* ---- FDM network oracle (fdm.cu): the reference 3-layer network, Jacobi-PCG. fp64. */
+typedef struct gtd_fdm {
+    int n;
+    double pitch, t_die, t_tim, t_spr, k_tim, k_spr;
+    double c_die, c_tim, c_spr; /* node heat capacities (J/K) */
+    double g_sink;              /* per spreader cell (W/K) */
+    double inv_dt;              /* 1/dt for backward Euler, 0 steady */
+    const double* kd;           /* [n*n] effective die conductivity */
+} gtd_fdm;
+int gtd_fdm_kcell(const double* k_map, const double* rise, double c, int n, double* kd, int* flag, cudaStream_t st);
+int gtd_fdm_diag(const gtd_fdm* f, double* diag, cudaStream_t st);
+int gtd_fdm_spmv(const gtd_fdm* f, const double* diag, const double* x, double* y, const double* w, double* dot,
+                 cudaStream_t st);
+/* CG scalars sc[8]: 0 r.z, 1 r.r, 2 b.b, 3 p.Ap, 4 r.r (new), 5 r.z (new) */
+int gtd_cg_init(int N, const double* b, const double* ax, const double* diag, double* r, double* z, double* p,
+                double* sc, cudaStream_t st);
+int gtd_cg_step(const gtd_fdm* f, const double* diag, double* x, double* r, double* z, double* p, double* q,
+                double* sc, cudaStream_t st);
+int gtd_cg_direction(int N, const double* z, double* p, double* sc, cudaStream_t st);
+int gtd_fdm_rhs(const double* p_dyn, const double* leak, int temp_dep, double beta, const double* x, double c_die,
+                double c_tim, double c_spr, double inv_dt, int nn, double* b, cudaStream_t st);
+int gtd_absdiff(const double* a, const double* b, size_t count, double* out, cudaStream_t st);
+
 /* ---- seeded variation maps on the device (vargen.cu), m = 128 / 256 / 512 */
 int gtd_var_pitch(int n);
 size_t gtd_var_scratch_bytes_per_sample(int n, int fp64);

@@ -8,6 +8,12 @@
 #include "host.hpp"
 
 void gt_ops_modal_kernel(const gth::Stack& s, double* out_host);
+gth::Field gt_ops_oracle_steady(const gth::Stack& stack, const gth::VarParams* var, const gth::Field& p_dyn,
+                                const gth::Field* nominal_leak, int temp_dep_leakage, int temp_dep_conductivity,
+                                int* outer_iterations);
+std::vector<gth::Field> gt_ops_oracle_transient(const gth::Stack& stack, const gth::VarParams* var,
+                                                const gth::Field& p_dyn, const gth::Field* nominal_leak,
+                                                int temp_dep_leakage, const std::vector<double>& times, double dt);
 gth::Greens gt_ops_calibrate_modal(const gth::Stack& s, const gth::VarParams& v, const gth::Field* nominal_leak,
                                    double leak_total);
 gth::Field gt_ops_steady(const gth::Greens& g, const gth::Field& p_dyn, bool with_rand, double* online_ms);
