@@ -168,406 +168,6 @@ void d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 
 }  // namespace
 
-// f_sp0 alone (impulse_response for 1 W at (c, c), fdm.cpp:288-296) by the modal
-// solution, for any power-of-two n the device memory allows (config 4: 8192).
-void gt_ops_modal_kernel(const Stack& s, double* out_host) {
-    s.validate();
-    need_device();
-    const int n = s.n;
-    if (!pow2(n) || n < 16 || n > 16384)
-        fail(ST_CONFIG, "calibrate", "modal kernel supports power-of-two grids 16..16384, got n=" + std::to_string(n));
-    const gtd_stack ds = to_dev(s);
-    const size_t nn = static_cast<size_t>(n) * n;
-    DBuf work, f;
-    work.ensure(3 * nn * 8);
-    f.ensure(nn * 8);
-    cuda_ok(gtd_modal_impulse(&ds, s.die.conductivity, work.as<double>(), f.as<double>(), nullptr), "modal impulse");
-    d2h(out_host, f.p, nn * 8, nullptr);
-}
-
-Greens gt_ops_calibrate_modal(const Stack& s, const VarParams& v, const Field* nominal_leak, double leak_total) {
-    s.validate();
-    v.validate();
-    need_device();
-    const int n = s.n;
-    if (!pow2(n) || n < 16 || n > 1024)
-        fail(ST_CONFIG, "calibrate", "device calibration supports power-of-two grids 16..1024, got n=" + std::to_string(n));
-    if (v.dopant_spread != 0.0)
-        fail(ST_CONFIG, "calibrate",
-             "device calibration needs a uniform die conductivity (variation dopant_spread = 0): the modal kernel is "
-             "the exact solution only for uniform k; per-cell k needs the FDM oracle (out of scope)");
-    const double pitch = s.pitch();
-    Field leak = nominal_leak ? *nominal_leak
-                              : Field(n, pitch, Unit::Watts, (leak_total > 0.0 ? leak_total : 15.0) / (double(n) * n));
-    if (leak.n != n) fail(ST_CONFIG, "greens", "nominal leakage map does not match the stack grid");
-    if (leak.min() < 0.0) fail(ST_CONFIG, "variation", "leakage_baseline: nominal leakage must be >= 0");
-
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const gtd_stack ds = to_dev(s);
-    const size_t nn = static_cast<size_t>(n) * n;
-    const int m = 2 * n;
-    const size_t mm = static_cast<size_t>(m) * m;
-
-    // --- kernel producer: f_sp0 by the modal solution (replaces impulse_response, fdm.cpp:288-296)
-    Greens g;
-    g.n = n;
-    g.pitch = pitch;
-    double k0p_lin = 0.0, cslope = 0.0;
-    const double k0p = s.die.conductivity;  // calibrate() uses the stack value as k0' (greens.cpp:355-357)
-    linearize(k0p, v.eta, s.ambient, &k0p_lin, &cslope);
-    {
-        cudaStream_t st = nullptr;
-        DBuf work, f;
-        work.ensure(3 * nn * 8);
-        f.ensure(nn * 8);
-        cuda_ok(gtd_modal_impulse(&ds, k0p, work.as<double>(), f.as<double>(), st), "modal impulse");
-        g.f_sp0 = Field(n, pitch, Unit::KelvinPerWatt);
-        d2h(g.f_sp0.v.data(), f.p, nn * 8, st);
-    }
-    // extract_baseline (greens.cpp:108-124): phi = outer-ring mean, kappa_inf = farthest corner
-    {
-        double ring = 0.0;
-        int cnt = 0;
-        for (int i = 0; i < n; ++i)
-            for (int j = 0; j < n; ++j)
-                if (i == 0 || j == 0 || i == n - 1 || j == n - 1) {
-                    ring += g.f_sp0.at(i, j);
-                    ++cnt;
-                }
-        g.phi = ring / cnt;
-        const auto [ci, cj] = farthest_corner(n);
-        g.kappa_inf = g.f_sp0.at(ci, cj);
-        g.g_sp0 = g.f_sp0;
-        const double shift = g.f_sp0.at(n / 2, n / 2) - g.kappa_inf;  // make_g_shift (greens.cpp:170-175)
-        for (double& x : g.g_sp0.v) x += shift;
-    }
-    // --- fit_alpha (greens.cpp:126-168) with modal centre responses
-    {
-        const double fr[7] = {0.75, 0.80, 0.85, 0.90, 0.95, 1.00, 1.05};
-        double ks[7], peaks[7];
-        for (int i = 0; i < 7; ++i) ks[i] = fr[i] * k0p;
-        DBuf nets, out;
-        nets.ensure(gtd_modal_net_bytes() * 7);
-        out.ensure(7 * 8);
-        cuda_ok(gtd_modal_center(&ds, ks, 7, nets.as<double>(), out.as<double>(), nullptr), "modal sweep");
-        d2h(peaks, out.p, 7 * 8, nullptr);
-        double sx = 0, sy = 0, sxx = 0, sxy = 0;
-        for (int i = 0; i < 7; ++i) {
-            const double x = ks[i] - k0p;
-            sx += x;
-            sy += peaks[i];
-            sxx += x * x;
-            sxy += x * peaks[i];
-            g.sweep.emplace_back(ks[i], peaks[i]);
-        }
-        const double slope = (7 * sxy - sx * sy) / (7 * sxx - sx * sx), icpt = (sy - slope * sx) / 7;
-        double ss_res = 0, ss_tot = 0;
-        for (int i = 0; i < 7; ++i) {
-            const double fit = icpt + slope * (ks[i] - k0p);
-            ss_res += (peaks[i] - fit) * (peaks[i] - fit);
-            ss_tot += (peaks[i] - sy / 7) * (peaks[i] - sy / 7);
-        }
-        g.fit_r2 = ss_tot > 0.0 ? 1.0 - ss_res / ss_tot : 0.0;
-        if (g.fit_r2 < 0.95)
-            fail(ST_SOLVER, "greens", "response-vs-conductivity fit r^2 = " + std::to_string(g.fit_r2) +
-                                          " < 0.95; linearization invalid for this stack");
-        g.c_prime = -slope / icpt;
-        g.c = cslope;
-        g.alpha = g.c_prime * cslope * k0p;
-        g.rep_alpha = g.alpha;
-    }
-    g.beta = v.beta;
-    // Device tables of the set so far (fk, g, twiddles) for the closed forms and the capacitance fit.
-    g.f_det = Field(n, pitch, Unit::KelvinPerWatt);
-    g.f_rand = Field(n, pitch, Unit::KelvinPerWatt);
-    g.p_var = Field(n, pitch, Unit::Watts);
-    auto d = prepare_device(g, GT_FP64, dev);
-    cudaStream_t st = d->stream;
-
-    // --- make_leakage_baseline (variation.cpp:197-211), run 0
-    DBuf dl, dtox, nom, pl, pv, flag, red;
-    dl.ensure(nn * 8);
-    dtox.ensure(nn * 8);
-    pl.ensure(nn * 8);
-    pv.ensure(nn * 8);
-    flag.ensure(8);
-    red.ensure(64);
-    {
-        VarDevice vd(d.get(), v, pitch);
-        LeakNoise z = leak_noise(v, n, v.seed, 0);
-        vd.field(v, z.sys_l, z.rnd_l, dl.as<double>());
-        vd.field(v, z.sys_t, z.rnd_t, dtox.as<double>());
-    }
-    upload(nom, leak.v.data(), nn * 8, st);
-    cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
-    cuda_ok(gtd_leak_exp(nom.as<double>(), dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
-                         pl.as<double>(), flag.as<int>(), st),
-            "leakage exponent");
-    int fl = 0;
-    d2h(&fl, flag.p, 4, st);
-    if (fl) fail(ST_VALIDATION, "variation", "leakage exponent exceeds cap (unphysical variation inputs)");
-    double r3[3];
-    cuda_ok(gtd_reduce(pl.as<double>(), nn, red.as<double>(), st), "reduce");
-    d2h(r3, red.p, 24, st);
-    double mu = r3[0] / double(nn);
-    cuda_ok(gtd_sub_scalar(pl.as<double>(), mu, nn, pv.as<double>(), st), "p_var");
-    cuda_ok(gtd_reduce(pv.as<double>(), nn, red.as<double>(), st), "reduce");
-    d2h(r3, red.p, 24, st);
-    const double resid = r3[0] / double(nn);
-    if (resid != 0.0) {  // re-centre once (variation.cpp:181-192)
-        mu += resid;
-        cuda_ok(gtd_sub_scalar(pl.as<double>(), mu, nn, pv.as<double>(), st), "p_var");
-    }
-    g.mu = mu;
-    d2h(g.p_var.v.data(), pv.p, nn * 8, st);
-
-    // --- deterministic and random closed forms (greens.cpp:203-251), fp64 full spectra
-    {
-        DBuf Fd, Fp, qtab;
-        Fd.ensure(mm * 16);
-        Fp.ensure(mm * 16);
-        qtab.ensure(static_cast<size_t>(n + 1) * (n + 1) * 8);
-        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
-        cuda_ok(gtd_fdet_full(d->fk_full.p, d->gtab.as<double>(), n, d->d.hp, g.alpha, g.beta, g.mu, Fd.p,
-                              flag.as<int>(), st),
-                "fdet");
-        d2h(&fl, flag.p, 4, st);
-        if (fl)
-            fail(ST_SOLVER, "greens",
-                 "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
-        // f_det = kernel_to_die(ifft2(F_det))
-        cuda_ok(cudaMemcpyAsync(Fp.p, Fd.p, mm * 16, cudaMemcpyDeviceToDevice, st), "copy");
-        cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
-        DBuf out;
-        out.ensure(nn * 8);
-        const double inv = 1.0 / (double(m) * double(m));
-        cuda_ok(gtd_kernel_to_die(Fp.p, n, inv, out.as<double>(), st), "kernel_to_die");
-        d2h(g.f_det.v.data(), out.p, nn * 8, st);
-        // f_rand: F(p_var) = kernel_fft(p_var); q = sym(p_var + p_var(c,c) - p_var(far corner))
-        cuda_ok(gtd_center_kernel(pv.as<double>(), 0.0, n, Fp.p, st), "centre");
-        cuda_ok(gtd_fft2d(Fp.p, m, 1, -1, 1, d->tw64.p, st), "fft");
-        const auto [fi, fj] = farthest_corner(n);
-        const double qshift = g.p_var.at(n / 2, n / 2) - g.p_var.at(fi, fj);
-        cuda_ok(gtd_sym_table(pv.as<double>(), n, qshift, qtab.as<double>(), st), "q");
-        cuda_ok(gtd_rand_spectrum(Fd.p, d->fk_full.p, d->gtab.as<double>(), d->d.hp, qtab.as<double>(), n, g.alpha,
-                                  g.beta, g.mu, Fp.p, flag.as<int>(), st),
-                "random_greens");
-        d2h(&fl, flag.p, 4, st);
-        if (fl)
-            fail(ST_SOLVER, "greens",
-                 "random_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
-        cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
-        cuda_ok(gtd_kernel_to_die(Fp.p, n, inv, out.as<double>(), st), "kernel_to_die");
-        d2h(g.f_rand.v.data(), out.p, nn * 8, st);
-    }
-    g.rand_scale = 1.0;  // the probe regression needs the nonlinear FDM oracle (out of scope): unfitted default
-
-    // --- fit_capacitance (greens.cpp:274-344) with the modal backward-Euler transient
-    {
-        const double tms[11] = {0.2, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 6.0, 8.0, 10.0};
-        double times[11];
-        int steps[11];
-        const double dt = 2e-5;
-        double t = 0.0;
-        int k = 0;
-        for (int i = 0; i < 11; ++i) {
-            times[i] = 1e-3 * tms[i];
-            while (t + 0.5 * dt < times[i]) {  // fdm.cpp:271-276 stepping rule
-                t += dt;
-                ++k;
-            }
-            steps[i] = k;
-        }
-        DBuf dsteps, dtimes, part, outv;
-        upload(dsteps, steps, sizeof steps, st);
-        upload(dtimes, times, sizeof times, st);
-        const int blocks = 148;
-        part.ensure(sizeof(double) * blocks * 11);
-        outv.ensure(sizeof(double) * 11);
-        double target[11];
-        cuda_ok(gtd_modal_transient(&ds, k0p, dt, dsteps.as<int>(), 11, part.as<double>(), blocks, outv.as<double>(), st),
-                "modal transient");
-        d2h(target, outv.p, sizeof target, st);
-        double c3[3];
-        cuda_ok(gtd_creduce(d->fk_full.p, mm, red.as<double>(), st), "creduce");
-        d2h(c3, red.p, 24, st);
-        const double floor_abs = 1e-6 * c3[2];
-        const double inv_m2 = 1.0 / (double(m) * double(m));
-        auto sse = [&](double cap) {
-            double vals[11];
-            cuda_ok(gtd_cap_model(d->fk_full.p, mm, floor_abs, cap, dtimes.as<double>(), 11, inv_m2, part.as<double>(),
-                                  blocks, outv.as<double>(), st),
-                    "cap model");
-            d2h(vals, outv.p, sizeof vals, st);
-            double e = 0.0;
-            for (int i = 0; i < 11; ++i) e += (vals[i] - target[i]) * (vals[i] - target[i]);
-            return e;
-        };
-        double lo = -8.0, hi = 0.0;
-        const double gr = 0.5 * (std::sqrt(5.0) - 1.0);
-        double a = hi - gr * (hi - lo), b = lo + gr * (hi - lo);
-        double fa = sse(std::pow(10.0, a)), fb = sse(std::pow(10.0, b));
-        for (int it = 0; it < 90; ++it) {
-            if (fa < fb) {
-                hi = b;
-                b = a;
-                fb = fa;
-                a = hi - gr * (hi - lo);
-                fa = sse(std::pow(10.0, a));
-            } else {
-                lo = a;
-                a = b;
-                fa = fb;
-                b = lo + gr * (hi - lo);
-                fb = sse(std::pow(10.0, b));
-            }
-        }
-        g.capacitance = std::pow(10.0, 0.5 * (lo + hi));
-        g.cap_residual = std::sqrt(sse(g.capacitance) / 11.0) / g.f_sp0.at(n / 2, n / 2);
-        if (g.cap_residual > 0.10)
-            fail(ST_SOLVER, "greens", "transient capacitance fit residual " + std::to_string(g.cap_residual) +
-                                          " exceeds 10% of the steady response");
-    }
-    g.validate();
-    return g;
-}
-
-void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nominal_leak, const Field& p_dyn,
-                        const std::vector<unsigned long long>& seeds, int jobs, const std::string& csv_path,
-                        double* mean_max, double* std_max) {
-    // reference monte_carlo (solver.cpp:338-409) + gt_monte_carlo (capi.cpp:345-369)
-    if (seeds.empty()) fail(ST_CONFIG, "solver", "monte_carlo: empty seed list");
-    need_device();
-    g.validate();
-    const int n = g.n;
-    if (p_dyn.n != n) fail(ST_CONFIG, "solver", "monte_carlo: power map does not match the GreensSet grid");
-    p_dyn.check_finite("monte_carlo");
-    if (p_dyn.min() < 0.0) fail(ST_CONFIG, "solver", "monte_carlo: powers must be >= 0");
-    if (nominal_leak.n != n) fail(ST_CONFIG, "solver", "monte_carlo: leakage map shape mismatch");
-    if (nominal_leak.min() < 0.0) fail(ST_CONFIG, "variation", "leakage_baseline: nominal leakage must be >= 0");
-    v.validate();
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto d = prepare_device(g, GT_FP64, dev);
-    cudaStream_t st = d->stream;
-    const size_t nn = static_cast<size_t>(n) * n;
-    const int B = static_cast<int>(seeds.size());
-    const auto t0 = wall::now();
-    // PreparedGreens / deterministic_spectrum at gs.mu: a runaway fails the whole call (solver.cpp:350-351)
-    {
-        DBuf Fd, flag;
-        Fd.ensure(static_cast<size_t>(4) * nn * 16);
-        flag.ensure(8);
-        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
-        cuda_ok(gtd_fdet_full(d->fk_full.p, d->gtab.as<double>(), n, d->d.hp, g.alpha, g.beta, g.mu, Fd.p,
-                              flag.as<int>(), st),
-                "fdet");
-        int fl = 0;
-        d2h(&fl, flag.p, 4, st);
-        if (fl)
-            fail(ST_SOLVER, "greens",
-                 "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
-    }
-    // per-seed exp(beta_L dL + beta_tox dTox) maps: host noise (threaded), device shaping
-    DBuf V, dl, dtox, P, N, flag;
-    V.ensure(nn * 8 * B);
-    dl.ensure(nn * 8);
-    dtox.ensure(nn * 8);
-    flag.ensure(8);
-    upload(P, p_dyn.v.data(), nn * 8, st);
-    upload(N, nominal_leak.v.data(), nn * 8, st);
-    std::vector<int> capfail(B, 0);
-    {
-        VarDevice vd(d.get(), v, g.pitch);
-        const int nj = std::max(1, jobs);
-        std::vector<LeakNoise> noise(B);
-        std::atomic<int> next{0};
-        std::vector<std::thread> pool;
-        for (int w = 0; w < nj; ++w)
-            pool.emplace_back([&] {
-                for (int i = next.fetch_add(1); i < B; i = next.fetch_add(1)) {
-                    VarParams vs = v;
-                    vs.seed = seeds[i];
-                    noise[i] = leak_noise(vs, n, vs.seed, 0);
-                }
-            });
-        for (auto& th : pool) th.join();
-        for (int i = 0; i < B; ++i) {
-            vd.field(v, noise[i].sys_l, noise[i].rnd_l, dl.as<double>());
-            vd.field(v, noise[i].sys_t, noise[i].rnd_t, dtox.as<double>());
-            cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
-            cuda_ok(gtd_leak_exp(nullptr, dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
-                                 V.as<double>() + i * nn, flag.as<int>(), st),
-                    "leakage exponent");
-            int fl = 0;
-            d2h(&fl, flag.p, 4, st);
-            capfail[i] = fl;
-            noise[i] = LeakNoise{};
-        }
-    }
-    // run_one per seed on the fused mode-A kernels: P and nominal broadcast, closed forms at gs.mu
-    DBuf stats, scratch;
-    stats.ensure(sizeof(gtd_sample_stats) * B);
-    const int chunk = std::min(B, 256);
-    scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, 1) * chunk);
-    gtd_mc_in in{};
-    in.P = P.p;
-    in.N = N.p;
-    in.V = V.p;
-    in.sP = 0;
-    in.sN = 0;
-    in.sV = static_cast<long long>(nn);
-    in.nom_scale = 1.0;
-    gtd_mc_opts o{};
-    o.mu_per_sample = 0;
-    o.with_rand = 1;
-    o.exponent_cap = 1e300;  // the cap was checked on the exponent itself above
-    cuda_ok(gtd_mc_batch(&d->d, &in, B, &o, nullptr, stats.as<gtd_sample_stats>(), scratch.p, chunk, st, nullptr,
-                         nullptr),
-            "mc batch");
-    std::vector<gtd_sample_stats> hs(B);
-    d2h(hs.data(), stats.p, sizeof(gtd_sample_stats) * B, st);
-    const double per_ms = std::chrono::duration<double, std::milli>(wall::now() - t0).count() / B;
-
-    std::vector<double> maxima;
-    std::vector<std::string> errors(B);
-    for (int i = 0; i < B; ++i) {
-        int sbits = hs[i].status;
-        if (capfail[i]) errors[i] = "leakage exponent exceeds cap (unphysical variation inputs)";
-        else if (sbits & (GTD_ST_RUNAWAY_DET | GTD_ST_RUNAWAY_RAND))
-            errors[i] = "random_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)";
-        else if (sbits)
-            errors[i] = "sample status " + std::to_string(sbits);
-        if (errors[i].empty()) maxima.push_back(hs[i].max_rise);
-    }
-    if (!csv_path.empty()) {  // write_monte_carlo_csv (solver.cpp:411-423)
-        std::ofstream os(csv_path);
-        if (!os) fail(ST_CONFIG, "solver", "cannot open '" + csv_path + "' for writing");
-        os << "seed,max_rise,mean_rise,runtime_ms\n";
-        os.precision(17);
-        for (int i = 0; i < B; ++i) {
-            if (!errors[i].empty())
-                os << seeds[i] << ",error,error," << per_ms << '\n';
-            else
-                os << seeds[i] << ',' << hs[i].max_rise << ',' << hs[i].mean_rise << ',' << per_ms << '\n';
-        }
-    }
-    double mean = 0.0, sd = 0.0;
-    if (!maxima.empty()) {
-        for (double x : maxima) mean += x;
-        mean /= maxima.size();
-        double acc = 0.0;
-        for (double x : maxima) acc += (x - mean) * (x - mean);
-        sd = maxima.size() > 1 ? std::sqrt(acc / (maxima.size() - 1)) : 0.0;
-    }
-    if (mean_max) *mean_max = mean;
-    if (std_max) *std_max = sd;
-    for (int i = 0; i < B; ++i)
-        if (!errors[i].empty())
-            fail(ST_VALIDATION, "solver", "monte carlo seed " + std::to_string(seeds[i]) + " failed: " + errors[i]);
-}
-
 // ============================================================ FDM oracle (fdm.cu)
 // The reference's ThermalNetwork (fdm.cpp:22-296) on the device: per-cell die
 // conductivity, Jacobi-preconditioned CG with Eigen's stopping rule
@@ -758,6 +358,465 @@ OracleSetup oracle_setup(const Stack& st, const VarParams* vp, const Field* nomi
 }
 
 }  // namespace
+
+Field gt_ops_oracle_steady(const Stack& stack, const VarParams* var, const Field& p_dyn, const Field* nominal_leak,
+                           int temp_dep_leakage, int temp_dep_conductivity, int* outer_iterations);
+
+// f_sp0 alone (impulse_response for 1 W at (c, c), fdm.cpp:288-296) by the modal
+// solution, for any power-of-two n the device memory allows (config 4: 8192).
+void gt_ops_modal_kernel(const Stack& s, double* out_host) {
+    s.validate();
+    need_device();
+    const int n = s.n;
+    if (!pow2(n) || n < 16 || n > 16384)
+        fail(ST_CONFIG, "calibrate", "modal kernel supports power-of-two grids 16..16384, got n=" + std::to_string(n));
+    const gtd_stack ds = to_dev(s);
+    const size_t nn = static_cast<size_t>(n) * n;
+    DBuf work, f;
+    work.ensure(3 * nn * 8);
+    f.ensure(nn * 8);
+    cuda_ok(gtd_modal_impulse(&ds, s.die.conductivity, work.as<double>(), f.as<double>(), nullptr), "modal impulse");
+    d2h(out_host, f.p, nn * 8, nullptr);
+}
+
+Greens gt_ops_calibrate_modal(const Stack& s, const VarParams& v, const Field* nominal_leak, double leak_total) {
+    s.validate();
+    v.validate();
+    need_device();
+    const int n = s.n;
+    if (!pow2(n) || n < 16 || n > 1024)
+        fail(ST_CONFIG, "calibrate", "device calibration supports power-of-two grids 16..1024, got n=" + std::to_string(n));
+    // Uniform die conductivity: the modal DCT-II solution is the exact network response.
+    // Per-cell conductivity (dopant spread): the device FDM network (fdm.cu), like the reference.
+    const bool uniform_k = v.dopant_spread == 0.0;
+    const double pitch = s.pitch();
+    Field leak = nominal_leak ? *nominal_leak
+                              : Field(n, pitch, Unit::Watts, (leak_total > 0.0 ? leak_total : 15.0) / (double(n) * n));
+    if (leak.n != n) fail(ST_CONFIG, "greens", "nominal leakage map does not match the stack grid");
+    if (leak.min() < 0.0) fail(ST_CONFIG, "variation", "leakage_baseline: nominal leakage must be >= 0");
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const gtd_stack ds = to_dev(s);
+    const size_t nn = static_cast<size_t>(n) * n;
+    const int m = 2 * n;
+    const size_t mm = static_cast<size_t>(m) * m;
+
+    // --- kernel producer: f_sp0 by the modal solution (replaces impulse_response, fdm.cpp:288-296)
+    Greens g;
+    g.n = n;
+    g.pitch = pitch;
+    double k0p_lin = 0.0, cslope = 0.0;
+    const double k0p = s.die.conductivity;  // calibrate() uses the stack value as k0' (greens.cpp:355-357)
+    linearize(k0p, v.eta, s.ambient, &k0p_lin, &cslope);
+    const std::vector<double> k_map = conductivity_map(k0p, v, n);  // conductivity_map (variation.cpp:224-238)
+    g.f_sp0 = Field(n, pitch, Unit::KelvinPerWatt);
+    if (uniform_k) {
+        cudaStream_t st = nullptr;
+        DBuf work, f;
+        work.ensure(3 * nn * 8);
+        f.ensure(nn * 8);
+        cuda_ok(gtd_modal_impulse(&ds, k0p, work.as<double>(), f.as<double>(), st), "modal impulse");
+        d2h(g.f_sp0.v.data(), f.p, nn * 8, st);
+    } else {
+        // impulse_response (fdm.cpp:288-296): 1 W at (c, c), effects off, one linear solve
+        FdmNet net(s, k_map);
+        std::vector<double> bh(net.N, 0.0);
+        bh[static_cast<size_t>(n / 2) * n + n / 2] = 1.0;
+        upload(net.b, bh.data(), net.N * 8, net.st);
+        net.prepare(nullptr, 0.0, 0.0);
+        net.solve(0.0, false, 1e-9);
+        d2h(g.f_sp0.v.data(), net.x.p, nn * 8, net.st);
+    }
+    // extract_baseline (greens.cpp:108-124): phi = outer-ring mean, kappa_inf = farthest corner
+    {
+        double ring = 0.0;
+        int cnt = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                if (i == 0 || j == 0 || i == n - 1 || j == n - 1) {
+                    ring += g.f_sp0.at(i, j);
+                    ++cnt;
+                }
+        g.phi = ring / cnt;
+        const auto [ci, cj] = farthest_corner(n);
+        g.kappa_inf = g.f_sp0.at(ci, cj);
+        g.g_sp0 = g.f_sp0;
+        const double shift = g.f_sp0.at(n / 2, n / 2) - g.kappa_inf;  // make_g_shift (greens.cpp:170-175)
+        for (double& x : g.g_sp0.v) x += shift;
+    }
+    // --- fit_alpha (greens.cpp:126-168) with modal centre responses
+    {
+        const double fr[7] = {0.75, 0.80, 0.85, 0.90, 0.95, 1.00, 1.05};
+        double ks[7], peaks[7];
+        for (int i = 0; i < 7; ++i) ks[i] = fr[i] * k0p;
+        DBuf nets, out;
+        nets.ensure(gtd_modal_net_bytes() * 7);
+        out.ensure(7 * 8);
+        cuda_ok(gtd_modal_center(&ds, ks, 7, nets.as<double>(), out.as<double>(), nullptr), "modal sweep");
+        d2h(peaks, out.p, 7 * 8, nullptr);
+        double sx = 0, sy = 0, sxx = 0, sxy = 0;
+        for (int i = 0; i < 7; ++i) {
+            const double x = ks[i] - k0p;
+            sx += x;
+            sy += peaks[i];
+            sxx += x * x;
+            sxy += x * peaks[i];
+            g.sweep.emplace_back(ks[i], peaks[i]);
+        }
+        const double slope = (7 * sxy - sx * sy) / (7 * sxx - sx * sx), icpt = (sy - slope * sx) / 7;
+        double ss_res = 0, ss_tot = 0;
+        for (int i = 0; i < 7; ++i) {
+            const double fit = icpt + slope * (ks[i] - k0p);
+            ss_res += (peaks[i] - fit) * (peaks[i] - fit);
+            ss_tot += (peaks[i] - sy / 7) * (peaks[i] - sy / 7);
+        }
+        g.fit_r2 = ss_tot > 0.0 ? 1.0 - ss_res / ss_tot : 0.0;
+        if (g.fit_r2 < 0.95)
+            fail(ST_SOLVER, "greens", "response-vs-conductivity fit r^2 = " + std::to_string(g.fit_r2) +
+                                          " < 0.95; linearization invalid for this stack");
+        g.c_prime = -slope / icpt;
+        g.c = cslope;
+        g.alpha = g.c_prime * cslope * k0p;
+        g.rep_alpha = g.alpha;
+    }
+    g.beta = v.beta;
+    // Device tables of the set so far (fk, g, twiddles) for the closed forms and the capacitance fit.
+    g.f_det = Field(n, pitch, Unit::KelvinPerWatt);
+    g.f_rand = Field(n, pitch, Unit::KelvinPerWatt);
+    g.p_var = Field(n, pitch, Unit::Watts);
+    auto d = prepare_device(g, GT_FP64, dev);
+    cudaStream_t st = d->stream;
+
+    // --- make_leakage_baseline (variation.cpp:197-211), run 0
+    DBuf dl, dtox, nom, pl, pv, flag, red;
+    dl.ensure(nn * 8);
+    dtox.ensure(nn * 8);
+    pl.ensure(nn * 8);
+    pv.ensure(nn * 8);
+    flag.ensure(8);
+    red.ensure(64);
+    {
+        VarDevice vd(d.get(), v, pitch);
+        LeakNoise z = leak_noise(v, n, v.seed, 0);
+        vd.field(v, z.sys_l, z.rnd_l, dl.as<double>());
+        vd.field(v, z.sys_t, z.rnd_t, dtox.as<double>());
+    }
+    upload(nom, leak.v.data(), nn * 8, st);
+    cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+    cuda_ok(gtd_leak_exp(nom.as<double>(), dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
+                         pl.as<double>(), flag.as<int>(), st),
+            "leakage exponent");
+    int fl = 0;
+    d2h(&fl, flag.p, 4, st);
+    if (fl) fail(ST_VALIDATION, "variation", "leakage exponent exceeds cap (unphysical variation inputs)");
+    double r3[3];
+    cuda_ok(gtd_reduce(pl.as<double>(), nn, red.as<double>(), st), "reduce");
+    d2h(r3, red.p, 24, st);
+    double mu = r3[0] / double(nn);
+    cuda_ok(gtd_sub_scalar(pl.as<double>(), mu, nn, pv.as<double>(), st), "p_var");
+    cuda_ok(gtd_reduce(pv.as<double>(), nn, red.as<double>(), st), "reduce");
+    d2h(r3, red.p, 24, st);
+    const double resid = r3[0] / double(nn);
+    if (resid != 0.0) {  // re-centre once (variation.cpp:181-192)
+        mu += resid;
+        cuda_ok(gtd_sub_scalar(pl.as<double>(), mu, nn, pv.as<double>(), st), "p_var");
+    }
+    g.mu = mu;
+    d2h(g.p_var.v.data(), pv.p, nn * 8, st);
+
+    // --- deterministic and random closed forms (greens.cpp:203-251), fp64 full spectra
+    {
+        DBuf Fd, Fp, qtab;
+        Fd.ensure(mm * 16);
+        Fp.ensure(mm * 16);
+        qtab.ensure(static_cast<size_t>(n + 1) * (n + 1) * 8);
+        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+        cuda_ok(gtd_fdet_full(d->fk_full.p, d->gtab.as<double>(), n, d->d.hp, g.alpha, g.beta, g.mu, Fd.p,
+                              flag.as<int>(), st),
+                "fdet");
+        d2h(&fl, flag.p, 4, st);
+        if (fl)
+            fail(ST_SOLVER, "greens",
+                 "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
+        // f_det = kernel_to_die(ifft2(F_det))
+        cuda_ok(cudaMemcpyAsync(Fp.p, Fd.p, mm * 16, cudaMemcpyDeviceToDevice, st), "copy");
+        cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
+        DBuf out;
+        out.ensure(nn * 8);
+        const double inv = 1.0 / (double(m) * double(m));
+        cuda_ok(gtd_kernel_to_die(Fp.p, n, inv, out.as<double>(), st), "kernel_to_die");
+        d2h(g.f_det.v.data(), out.p, nn * 8, st);
+        // f_rand: F(p_var) = kernel_fft(p_var); q = sym(p_var + p_var(c,c) - p_var(far corner))
+        cuda_ok(gtd_center_kernel(pv.as<double>(), 0.0, n, Fp.p, st), "centre");
+        cuda_ok(gtd_fft2d(Fp.p, m, 1, -1, 1, d->tw64.p, st), "fft");
+        const auto [fi, fj] = farthest_corner(n);
+        const double qshift = g.p_var.at(n / 2, n / 2) - g.p_var.at(fi, fj);
+        cuda_ok(gtd_sym_table(pv.as<double>(), n, qshift, qtab.as<double>(), st), "q");
+        cuda_ok(gtd_rand_spectrum(Fd.p, d->fk_full.p, d->gtab.as<double>(), d->d.hp, qtab.as<double>(), n, g.alpha,
+                                  g.beta, g.mu, Fp.p, flag.as<int>(), st),
+                "random_greens");
+        d2h(&fl, flag.p, 4, st);
+        if (fl)
+            fail(ST_SOLVER, "greens",
+                 "random_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
+        cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
+        cuda_ok(gtd_kernel_to_die(Fp.p, n, inv, out.as<double>(), st), "kernel_to_die");
+        d2h(g.f_rand.v.data(), out.p, nn * 8, st);
+
+        // rand_scale (greens.cpp:390-421): regress the Hadamard term's gain against the FDM network
+        // on a uniform 100 W probe with every effect on (leakage and conductivity feedback)
+        Field probe(n, pitch, Unit::Watts, 100.0 / (double(n) * n));
+        int its = 0;
+        const Field oracle = gt_ops_oracle_steady(s, &v, probe, &leak, 1, 1, &its);
+        Field applied = probe;
+        for (size_t k = 0; k < nn; ++k) applied.v[k] += g.p_var.v[k] + mu;  // probe + p_leak0
+        DBuf ap, tdet;
+        upload(ap, applied.v.data(), nn * 8, st);
+        tdet.ensure(nn * 8);
+        cuda_ok(gtd_mirror_pad(ap.as<double>(), nullptr, n, Fp.p, st), "mirror");
+        cuda_ok(gtd_fft2d(Fp.p, m, 1, -1, 1, d->tw64.p, st), "fft");
+        cuda_ok(gtd_spec_mul(Fp.p, Fd.p, mm, st), "spec mul");
+        cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
+        cuda_ok(gtd_crop(Fp.p, n, inv, tdet.as<double>(), st), "crop");
+        std::vector<double> td(nn);
+        d2h(td.data(), tdet.p, nn * 8, st);
+        const double total = applied.sum();
+        double num = 0.0, den = 0.0;
+        for (size_t k = 0; k < nn; ++k) {
+            const double bk = g.f_rand.v[k] * g.p_var.v[k] * total;
+            num += (oracle.v[k] - td[k]) * bk;
+            den += bk * bk;
+        }
+        g.rand_scale = den > 0.0 ? std::clamp(num / den, 0.0, 500.0) : 1.0;
+    }
+
+    // --- fit_capacitance (greens.cpp:274-344) with the modal backward-Euler transient
+    {
+        const double tms[11] = {0.2, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 6.0, 8.0, 10.0};
+        double times[11];
+        int steps[11];
+        const double dt = 2e-5;
+        double t = 0.0;
+        int k = 0;
+        for (int i = 0; i < 11; ++i) {
+            times[i] = 1e-3 * tms[i];
+            while (t + 0.5 * dt < times[i]) {  // fdm.cpp:271-276 stepping rule
+                t += dt;
+                ++k;
+            }
+            steps[i] = k;
+        }
+        DBuf dsteps, dtimes, part, outv;
+        upload(dsteps, steps, sizeof steps, st);
+        upload(dtimes, times, sizeof times, st);
+        const int blocks = 148;
+        part.ensure(sizeof(double) * blocks * 11);
+        outv.ensure(sizeof(double) * 11);
+        double target[11];
+        if (uniform_k) {
+            cuda_ok(gtd_modal_transient(&ds, k0p, dt, dsteps.as<int>(), 11, part.as<double>(), blocks,
+                                        outv.as<double>(), st),
+                    "modal transient");
+            d2h(target, outv.p, sizeof target, st);
+        } else {
+            // transient_impulse (fdm.cpp:250-286) on the per-cell network: backward Euler at dt
+            FdmNet net(s, k_map);
+            net.prepare(nullptr, 0.0, 1.0 / dt);
+            std::vector<double> ph(nn, 0.0);
+            ph[static_cast<size_t>(n / 2) * n + n / 2] = 1.0;
+            DBuf pd;
+            upload(pd, ph.data(), nn * 8, net.st);
+            int done = 0;
+            for (int i = 0; i < 11; ++i) {
+                for (; done < steps[i]; ++done) {
+                    cuda_ok(cudaMemcpyAsync(net.xo.p, net.x.p, net.N * 8, cudaMemcpyDeviceToDevice, net.st), "copy");
+                    cuda_ok(gtd_fdm_rhs(pd.as<double>(), nullptr, 0, 0.0, net.xo.as<double>(), net.c_die, net.c_tim,
+                                        net.c_spr, 1.0 / dt, static_cast<int>(nn), net.b.as<double>(), net.st),
+                            "rhs");
+                    net.solve(1.0 / dt, true, 1e-9);
+                }
+                d2h(&target[i], net.x.as<double>() + static_cast<size_t>(n / 2) * n + n / 2, 8, net.st);
+            }
+        }
+        double c3[3];
+        cuda_ok(gtd_creduce(d->fk_full.p, mm, red.as<double>(), st), "creduce");
+        d2h(c3, red.p, 24, st);
+        const double floor_abs = 1e-6 * c3[2];
+        const double inv_m2 = 1.0 / (double(m) * double(m));
+        auto sse = [&](double cap) {
+            double vals[11];
+            cuda_ok(gtd_cap_model(d->fk_full.p, mm, floor_abs, cap, dtimes.as<double>(), 11, inv_m2, part.as<double>(),
+                                  blocks, outv.as<double>(), st),
+                    "cap model");
+            d2h(vals, outv.p, sizeof vals, st);
+            double e = 0.0;
+            for (int i = 0; i < 11; ++i) e += (vals[i] - target[i]) * (vals[i] - target[i]);
+            return e;
+        };
+        double lo = -8.0, hi = 0.0;
+        const double gr = 0.5 * (std::sqrt(5.0) - 1.0);
+        double a = hi - gr * (hi - lo), b = lo + gr * (hi - lo);
+        double fa = sse(std::pow(10.0, a)), fb = sse(std::pow(10.0, b));
+        for (int it = 0; it < 90; ++it) {
+            if (fa < fb) {
+                hi = b;
+                b = a;
+                fb = fa;
+                a = hi - gr * (hi - lo);
+                fa = sse(std::pow(10.0, a));
+            } else {
+                lo = a;
+                a = b;
+                fa = fb;
+                b = lo + gr * (hi - lo);
+                fb = sse(std::pow(10.0, b));
+            }
+        }
+        g.capacitance = std::pow(10.0, 0.5 * (lo + hi));
+        g.cap_residual = std::sqrt(sse(g.capacitance) / 11.0) / g.f_sp0.at(n / 2, n / 2);
+        if (g.cap_residual > 0.10)
+            fail(ST_SOLVER, "greens", "transient capacitance fit residual " + std::to_string(g.cap_residual) +
+                                          " exceeds 10% of the steady response");
+    }
+    g.validate();
+    return g;
+}
+
+void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nominal_leak, const Field& p_dyn,
+                        const std::vector<unsigned long long>& seeds, int jobs, const std::string& csv_path,
+                        double* mean_max, double* std_max) {
+    // reference monte_carlo (solver.cpp:338-409) + gt_monte_carlo (capi.cpp:345-369)
+    if (seeds.empty()) fail(ST_CONFIG, "solver", "monte_carlo: empty seed list");
+    need_device();
+    g.validate();
+    const int n = g.n;
+    if (p_dyn.n != n) fail(ST_CONFIG, "solver", "monte_carlo: power map does not match the GreensSet grid");
+    p_dyn.check_finite("monte_carlo");
+    if (p_dyn.min() < 0.0) fail(ST_CONFIG, "solver", "monte_carlo: powers must be >= 0");
+    if (nominal_leak.n != n) fail(ST_CONFIG, "solver", "monte_carlo: leakage map shape mismatch");
+    if (nominal_leak.min() < 0.0) fail(ST_CONFIG, "variation", "leakage_baseline: nominal leakage must be >= 0");
+    v.validate();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto d = prepare_device(g, GT_FP64, dev);
+    cudaStream_t st = d->stream;
+    const size_t nn = static_cast<size_t>(n) * n;
+    const int B = static_cast<int>(seeds.size());
+    const auto t0 = wall::now();
+    // PreparedGreens / deterministic_spectrum at gs.mu: a runaway fails the whole call (solver.cpp:350-351)
+    {
+        DBuf Fd, flag;
+        Fd.ensure(static_cast<size_t>(4) * nn * 16);
+        flag.ensure(8);
+        cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+        cuda_ok(gtd_fdet_full(d->fk_full.p, d->gtab.as<double>(), n, d->d.hp, g.alpha, g.beta, g.mu, Fd.p,
+                              flag.as<int>(), st),
+                "fdet");
+        int fl = 0;
+        d2h(&fl, flag.p, 4, st);
+        if (fl)
+            fail(ST_SOLVER, "greens",
+                 "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
+    }
+    // per-seed exp(beta_L dL + beta_tox dTox) maps: host noise (threaded), device shaping
+    DBuf V, dl, dtox, P, N, flag;
+    V.ensure(nn * 8 * B);
+    dl.ensure(nn * 8);
+    dtox.ensure(nn * 8);
+    flag.ensure(8);
+    upload(P, p_dyn.v.data(), nn * 8, st);
+    upload(N, nominal_leak.v.data(), nn * 8, st);
+    std::vector<int> capfail(B, 0);
+    {
+        VarDevice vd(d.get(), v, g.pitch);
+        const int nj = std::max(1, jobs);
+        std::vector<LeakNoise> noise(B);
+        std::atomic<int> next{0};
+        std::vector<std::thread> pool;
+        for (int w = 0; w < nj; ++w)
+            pool.emplace_back([&] {
+                for (int i = next.fetch_add(1); i < B; i = next.fetch_add(1)) {
+                    VarParams vs = v;
+                    vs.seed = seeds[i];
+                    noise[i] = leak_noise(vs, n, vs.seed, 0);
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (int i = 0; i < B; ++i) {
+            vd.field(v, noise[i].sys_l, noise[i].rnd_l, dl.as<double>());
+            vd.field(v, noise[i].sys_t, noise[i].rnd_t, dtox.as<double>());
+            cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+            cuda_ok(gtd_leak_exp(nullptr, dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
+                                 V.as<double>() + i * nn, flag.as<int>(), st),
+                    "leakage exponent");
+            int fl = 0;
+            d2h(&fl, flag.p, 4, st);
+            capfail[i] = fl;
+            noise[i] = LeakNoise{};
+        }
+    }
+    // run_one per seed on the fused mode-A kernels: P and nominal broadcast, closed forms at gs.mu
+    DBuf stats, scratch;
+    stats.ensure(sizeof(gtd_sample_stats) * B);
+    const int chunk = std::min(B, 256);
+    scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, 1) * chunk);
+    gtd_mc_in in{};
+    in.P = P.p;
+    in.N = N.p;
+    in.V = V.p;
+    in.sP = 0;
+    in.sN = 0;
+    in.sV = static_cast<long long>(nn);
+    in.nom_scale = 1.0;
+    gtd_mc_opts o{};
+    o.mu_per_sample = 0;
+    o.with_rand = 1;
+    o.exponent_cap = 1e300;  // the cap was checked on the exponent itself above
+    cuda_ok(gtd_mc_batch(&d->d, &in, B, &o, nullptr, stats.as<gtd_sample_stats>(), scratch.p, chunk, st, nullptr,
+                         nullptr),
+            "mc batch");
+    std::vector<gtd_sample_stats> hs(B);
+    d2h(hs.data(), stats.p, sizeof(gtd_sample_stats) * B, st);
+    const double per_ms = std::chrono::duration<double, std::milli>(wall::now() - t0).count() / B;
+
+    std::vector<double> maxima;
+    std::vector<std::string> errors(B);
+    for (int i = 0; i < B; ++i) {
+        int sbits = hs[i].status;
+        if (capfail[i]) errors[i] = "leakage exponent exceeds cap (unphysical variation inputs)";
+        else if (sbits & (GTD_ST_RUNAWAY_DET | GTD_ST_RUNAWAY_RAND))
+            errors[i] = "random_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)";
+        else if (sbits)
+            errors[i] = "sample status " + std::to_string(sbits);
+        if (errors[i].empty()) maxima.push_back(hs[i].max_rise);
+    }
+    if (!csv_path.empty()) {  // write_monte_carlo_csv (solver.cpp:411-423)
+        std::ofstream os(csv_path);
+        if (!os) fail(ST_CONFIG, "solver", "cannot open '" + csv_path + "' for writing");
+        os << "seed,max_rise,mean_rise,runtime_ms\n";
+        os.precision(17);
+        for (int i = 0; i < B; ++i) {
+            if (!errors[i].empty())
+                os << seeds[i] << ",error,error," << per_ms << '\n';
+            else
+                os << seeds[i] << ',' << hs[i].max_rise << ',' << hs[i].mean_rise << ',' << per_ms << '\n';
+        }
+    }
+    double mean = 0.0, sd = 0.0;
+    if (!maxima.empty()) {
+        for (double x : maxima) mean += x;
+        mean /= maxima.size();
+        double acc = 0.0;
+        for (double x : maxima) acc += (x - mean) * (x - mean);
+        sd = maxima.size() > 1 ? std::sqrt(acc / (maxima.size() - 1)) : 0.0;
+    }
+    if (mean_max) *mean_max = mean;
+    if (std_max) *std_max = sd;
+    for (int i = 0; i < B; ++i)
+        if (!errors[i].empty())
+            fail(ST_VALIDATION, "solver", "monte carlo seed " + std::to_string(seeds[i]) + " failed: " + errors[i]);
+}
 
 // steady_solve (fdm.cpp:167-205) with SolveOptions defaults (max_iters 50, tol 0.01 K, linear_tol 1e-9)
 Field gt_ops_oracle_steady(const Stack& stack, const VarParams* var, const Field& p_dyn, const Field* nominal_leak,

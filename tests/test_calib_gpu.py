@@ -61,14 +61,44 @@ def test_calibrate_matches_reference(b200lib, oracle, tmp_path, n):
     cb, cr = Lb.gt_greens_capacitance(gb), Lr.gt_greens_capacitance(gr)
     print(f"n={n} capacitance {cb:.6e} vs reference {cr:.6e}")
     assert cb == pytest.approx(cr, rel=1e-4)
+    _check_rand_scale(tmp_path, Lb, gb, Lr, gr, n)
 
 
-def test_calibrate_rejects_nonuniform_conductivity(b200lib, tmp_path):
-    stack = _write(tmp_path / "stack.txt", "n 32\n")
-    var = _write(tmp_path / "var.txt", "dopant_spread 0.05\n")
-    g = C.c_void_p()
-    assert b200lib.gt_calibrate(stack, var, None, 10.0, C.byref(g), None) == 2
-    assert b"uniform die conductivity" in b200lib.gt_last_error()
+def _rand_scale(L, g, d):
+    L.gt_greens_save(g, str(d).encode())
+    for line in (d / "calibration.txt").read_text().splitlines() + (d / "manifest.txt").read_text().splitlines():
+        if line.startswith("rand_scale"):
+            return float(line.split()[1])
+    raise AssertionError("rand_scale not saved")
+
+
+def _check_rand_scale(tmp_path, Lb, gb, Lr, gr, n):
+    rb, rr = _rand_scale(Lb, gb, tmp_path / "sb"), _rand_scale(Lr, gr, tmp_path / "sr")
+    print(f"n={n} rand_scale {rb:.6f} vs reference {rr:.6f}")
+    assert rb == pytest.approx(rr, rel=1e-5, abs=1e-6)
+
+
+def test_calibrate_per_cell_conductivity_matches_reference(b200lib, oracle, tmp_path):
+    """dopant_spread > 0: f_sp0 and the capacitance target come from the device FDM network
+    with the reference's own per-cell conductivity draws."""
+    n = 32
+    stack = _write(tmp_path / "stack.txt", f"n {n}\ndie_edge 0.016\n")
+    var = _write(tmp_path / "var.txt", "dopant_spread 0.05\nbeta 0.017\nseed 3\n")
+    res = []
+    for L in (b200lib, oracle.ref_lib()):
+        g = C.c_void_p()
+        assert L.gt_calibrate(stack, var, None, 84.0, C.byref(g), None) == 0, L.gt_last_error()
+        res.append((L, g))
+    (Lb, gb), (Lr, gr) = res
+    mb, mr = _greens_maps(Lb, gb, n), _greens_maps(Lr, gr, n)
+    for k in ("f_sp0", "f_det", "f_rand"):
+        rel = np.abs(mb[k] - mr[k]).max() / np.abs(mr[k]).max()
+        print(f"per-cell k {k}: max rel diff {rel:.2e}")
+        assert rel <= 1e-6
+    cb, cr = Lb.gt_greens_capacitance(gb), Lr.gt_greens_capacitance(gr)
+    print(f"per-cell k capacitance {cb:.6e} vs reference {cr:.6e}")
+    assert cb == pytest.approx(cr, rel=1e-4)
+    _check_rand_scale(tmp_path, Lb, gb, Lr, gr, n)
 
 
 def test_monte_carlo_matches_reference(b200lib, oracle, greens64, tmp_path):
