@@ -11,7 +11,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <filesystem>
 #include <fstream>
 #include <sstream>
@@ -68,7 +71,69 @@ void Field::check_finite(const char* what) const {
         if (!std::isfinite(x)) fail(ST_VALIDATION, "field", std::string(what) + ": non-finite entry");
 }
 
+// Binary sidecar "<path>.bin": the 17-digit text stays the
+// interchange format; a raw little-endian copy next to it makes re-reads of large
+// maps (one 8192^2 map is ~1.7 GB of text) a memcpy. The sidecar is used only if
+// it is at least as new as the text and records the text's byte size, so a text
+// edited by another tool falls back to parsing. GT_NO_BINARY_SIDECAR=1 disables it.
+namespace {
+struct SidecarHeader {
+    char magic[8];
+    int32_t n, unit;
+    double pitch;
+    uint64_t text_bytes;
+};
+constexpr char kMagic[8] = {'G', 'T', 'F', 'B', '1', 0, 0, 0};
+bool sidecars_enabled() {
+    const char* e = std::getenv("GT_NO_BINARY_SIDECAR");
+    return !(e && *e && *e != '0');
+}
+bool read_sidecar(const std::string& path, Field* out) {
+    namespace fs = std::filesystem;
+    const std::string bin = path + ".bin";
+    std::error_code ec;
+    if (!sidecars_enabled() || !fs::exists(bin, ec) || !fs::exists(path, ec)) return false;
+    if (fs::last_write_time(bin, ec) < fs::last_write_time(path, ec) || ec) return false;
+    std::ifstream is(bin, std::ios::binary);
+    SidecarHeader h{};
+    if (!is.read(reinterpret_cast<char*>(&h), sizeof h)) return false;
+    if (std::memcmp(h.magic, kMagic, 8) != 0 || h.n < 2 || h.unit < 0 || h.unit > 3) return false;
+    if (h.text_bytes != static_cast<uint64_t>(fs::file_size(path, ec)) || ec) return false;
+    Field f(h.n, h.pitch, static_cast<Unit>(h.unit));
+    if (!is.read(reinterpret_cast<char*>(f.v.data()), static_cast<std::streamsize>(f.v.size() * sizeof(double))))
+        return false;
+    *out = std::move(f);
+    return true;
+}
+void write_sidecar(const Field& f, const std::string& path) {
+    namespace fs = std::filesystem;
+    if (!sidecars_enabled()) return;
+    std::error_code ec;
+    SidecarHeader h{};
+    std::memcpy(h.magic, kMagic, 8);
+    h.n = f.n;
+    h.unit = static_cast<int32_t>(f.unit);
+    h.pitch = f.pitch;
+    h.text_bytes = static_cast<uint64_t>(fs::file_size(path, ec));
+    if (ec) return;
+    std::ofstream os(path + ".bin", std::ios::binary | std::ios::trunc);
+    os.write(reinterpret_cast<const char*>(&h), sizeof h);
+    os.write(reinterpret_cast<const char*>(f.v.data()), static_cast<std::streamsize>(f.v.size() * sizeof(double)));
+    if (!os) {
+        os.close();
+        fs::remove(path + ".bin", ec);  // a partial sidecar must not be picked up
+    }
+}
+}  // namespace
+
 Field read_field(const std::string& path) {
+    {
+        Field f(2, 1.0, Unit::Watts);
+        if (read_sidecar(path, &f)) {
+            f.check_finite(path.c_str());
+            return f;
+        }
+    }
     std::ifstream is(path);
     if (!is) fail(ST_CONFIG, "field-io", "cannot open '" + path + "'");
     int n = 0;
@@ -96,6 +161,8 @@ void write_field(const Field& f, const std::string& path) {
         os << '\n';
     }
     if (!os) fail(ST_CONFIG, "field-io", "write failed for '" + path + "'");
+    os.close();
+    write_sidecar(f, path);
 }
 
 // ------------------------------------------------------------------- Kv

@@ -134,3 +134,32 @@ def test_solve_without_device_fails_loudly(b200lib, greens64):
         DeviceGreens(greens64)
     assert e.value.status == 5 and e.value.stage == "device"
     assert b200lib.gt_device_count() == 0
+
+
+def test_field_binary_sidecar(b200lib, tmp_path):
+    """gt_field_save writes the reference text format plus a binary sidecar; loads prefer
+    a fresh sidecar and fall back to the text when the text no longer matches it."""
+    import ctypes as C
+    import numpy as np
+    L = b200lib
+    n = 8
+    f = C.c_void_p()
+    assert L.gt_field_create(n, 0.001, b"kelvin", C.byref(f)) == 0
+    vals = np.ctypeslib.as_array(L.gt_field_data(f), shape=(n, n))
+    vals[...] = np.arange(n * n).reshape(n, n) * 0.1 + 1e-3
+    path = tmp_path / "t.map"
+    assert L.gt_field_save(f, str(path).encode()) == 0
+    assert (tmp_path / "t.map.bin").exists()
+    g = C.c_void_p()
+    assert L.gt_field_load(str(path).encode(), C.byref(g)) == 0
+    np.testing.assert_array_equal(np.ctypeslib.as_array(L.gt_field_data(g), shape=(n, n)), vals)
+    L.gt_field_free(g)
+    # edit the text (another tool): the stale sidecar must be ignored
+    lines = path.read_text().splitlines()
+    lines[1] = " ".join(["5"] * n)
+    path.write_text("\n".join(lines) + "\n")
+    assert L.gt_field_load(str(path).encode(), C.byref(g)) == 0
+    got = np.ctypeslib.as_array(L.gt_field_data(g), shape=(n, n))
+    assert (got[0] == 5).all()
+    L.gt_field_free(g)
+    L.gt_field_free(f)
