@@ -679,6 +679,51 @@ Greens gt_ops_calibrate_modal(const Stack& s, const VarParams& v, const Field* n
             fail(ST_SOLVER, "greens", "transient capacitance fit residual " + std::to_string(g.cap_residual) +
                                           " exceeds 10% of the steady response");
     }
+    // --- tran tensor (greens.cpp:427-442): transient Green's maps at t = 10 ms * i / 100,
+    // F_det (1 - exp(-t/tau)) -> kernel_to_die -> clamp_small_negatives(1e-2)
+    {
+        DBuf Fd, Fp, out, flag2;
+        Fd.ensure(mm * 16);
+        Fp.ensure(mm * 16);
+        out.ensure(nn * 8);
+        flag2.ensure(8);
+        cuda_ok(cudaMemsetAsync(flag2.p, 0, 8, st), "memset");
+        cuda_ok(gtd_fdet_full(d->fk_full.p, d->gtab.as<double>(), n, d->d.hp, g.alpha, g.beta, g.mu, Fd.p,
+                              flag2.as<int>(), st),
+                "fdet");
+        double c3[3];
+        cuda_ok(gtd_creduce(d->fk_full.p, mm, red.as<double>(), st), "creduce");
+        d2h(c3, red.p, 24, st);
+        const double inv = 1.0 / (double(m) * double(m));
+        const int samples = 100;
+        const double horizon = 0.010;
+        g.t_samples.clear();
+        g.tran.clear();
+        for (int i = 1; i <= samples; ++i) {
+            const double t = horizon * i / samples;
+            cuda_ok(gtd_transient(d->fk_full.p, d->gtab.as<double>(), Fd.p, n, d->d.hp, g.alpha, g.capacitance,
+                                  1e-6 * c3[2], t, Fp.p, 0.0, 0, nullptr, nullptr, flag2.as<int>(), st),
+                    "transient factors");
+            cuda_ok(gtd_fft2d(Fp.p, m, 1, +1, 1, d->tw64.p, st), "ifft");
+            cuda_ok(gtd_kernel_to_die(Fp.p, n, inv, out.as<double>(), st), "kernel_to_die");
+            Field map(n, pitch, Unit::KelvinPerWatt);
+            d2h(map.v.data(), out.p, nn * 8, st);
+            int fl2 = 0;
+            d2h(&fl2, flag2.p, 4, st);
+            if (fl2 & 1)
+                fail(ST_SOLVER, "greens",
+                     "non-positive transient time constant at an energetic frequency; transient closed form is "
+                     "invalid here");
+            const double peak = map.max(), floor = -1e-2 * std::max(peak, 0.0);  // clamp_small_negatives
+            for (double& x : map.v) {
+                if (x < floor)
+                    fail(ST_VALIDATION, "greens", "tran tensor: negative value beyond spectral-ringing tolerance");
+                if (x < 0.0) x = 0.0;
+            }
+            g.t_samples.push_back(t);
+            g.tran.push_back(std::move(map));
+        }
+    }
     g.validate();
     return g;
 }

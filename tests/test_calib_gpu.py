@@ -76,6 +76,17 @@ def _check_rand_scale(tmp_path, Lb, gb, Lr, gr, n):
     rb, rr = _rand_scale(Lb, gb, tmp_path / "sb"), _rand_scale(Lr, gr, tmp_path / "sr")
     print(f"n={n} rand_scale {rb:.6f} vs reference {rr:.6f}")
     assert rb == pytest.approx(rr, rel=1e-5, abs=1e-6)
+    # the 100-map transient tensor (greens.cpp:427-442), as saved by both libraries
+    tb = sorted((tmp_path / "sb").glob("tran_*.map"))
+    tr = sorted((tmp_path / "sr").glob("tran_*.map"))
+    assert len(tb) == len(tr) == 100
+    worst = 0.0
+    for a, b in zip(tb[::9], tr[::9]):
+        ma = np.loadtxt(a, skiprows=1)
+        mb = np.loadtxt(b, skiprows=1)
+        worst = max(worst, np.abs(ma - mb).max() / np.abs(mb).max())
+    print(f"n={n} tran tensor max rel diff {worst:.2e}")
+    assert worst <= 1e-5
 
 
 def test_calibrate_per_cell_conductivity_matches_reference(b200lib, oracle, tmp_path):
