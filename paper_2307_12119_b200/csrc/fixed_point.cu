@@ -36,7 +36,11 @@ struct FPGeom {
     static constexpr int L = G::L;
     static constexpr int NT = G::NT;
     static constexpr int hp = ((h + L - 1) / L) * L;  // column tiles of L columns
-    static constexpr int LP = L + 2;
+    // tile pitch: fp32 line pairs are 16-byte loads (even pitch); fp64 pairs are two
+    // 16-byte loads, so an odd pitch pads less (M = 2048: 3 instead of 4 lines)
+    static constexpr int LP = sizeof(T) == 8 ? L + 1 : L + 2;
+    // a twiddle table of >= 32 KB is read from global (L1) so two CTAs fit an SM
+    static constexpr bool GTW = M * sizeof(cplx<T>) >= 32768;
     static constexpr int RP = n / 2;                   // die-row pairs
     static constexpr int RB = (RP + L - 1) / L;        // row-pair blocks per sample
     static constexpr int CT = hp / L;                  // column tiles per sample
@@ -83,10 +87,9 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
     constexpr int RB = Gm::RB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
-    T* tileT = reinterpret_cast<T*>(tile);
     cplx<T>* s_tw = tile + M * LP;
-    double* red = reinterpret_cast<double*>(s_tw + M);
-    load_twiddles<T, M, NT>(s_tw, g_tw);
+    if constexpr (!Gm::GTW) load_twiddles<T, M, NT>(s_tw, g_tw);
+    const cplx<T>* tw = Gm::GTW ? g_tw : s_tw;
     __syncthreads();
 
     for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
@@ -103,64 +106,103 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
         double dmax = 0.0;
         int bad = 0;
 
+        // Every global input of a stage is issued in batches of UB items ahead of
+        // its use (one exposed HBM latency per batch, not one per element).
+        constexpr int UB = 4;
         if (!FIRST) {
             // pack rows (2p, 2p+1) of the column-pass output into one Hermitian line pair
-            for (int idx = threadIdx.x; idx < L * h; idx += NT) {
-                const int l = idx / h, v = idx - l * h;
-                const int xa = 2 * (p0 + l);
-                cplx<T> y = mk<T>(T(0), T(0)), r = y;
-                if (xa < n) {
-                    y = As[static_cast<size_t>(xa) * hp + v];
-                    r = As[static_cast<size_t>(xa + 1) * hp + v];
+            constexpr int IPH = (L * h + NT - 1) / NT;
+#pragma unroll
+            for (int i0 = 0; i0 < IPH; i0 += UB) {
+                cplx<T> yv[UB], rv[UB];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int idx = threadIdx.x + (i0 + u) * NT;
+                    const int l = idx / h, v = idx - l * h;
+                    const int xa = 2 * (p0 + l);
+                    yv[u] = rv[u] = mk<T>(T(0), T(0));
+                    if (i0 + u < IPH && idx < L * h && xa < n) {
+                        yv[u] = As[static_cast<size_t>(xa) * hp + v];
+                        rv[u] = As[static_cast<size_t>(xa + 1) * hp + v];
+                    }
                 }
-                if (v == 0 || v == n) {
-                    tile[v * LP + l] = mk<T>(y.x, r.x);
-                } else {
-                    tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
-                    tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int idx = threadIdx.x + (i0 + u) * NT;
+                    if (i0 + u >= IPH || idx >= L * h) continue;
+                    const int l = idx / h, v = idx - l * h;
+                    const cplx<T> y = yv[u], r = rv[u];
+                    if (v == 0 || v == n) {
+                        tile[v * LP + l] = mk<T>(y.x, r.x);
+                    } else {
+                        tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
+                        tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+                    }
                 }
             }
             __syncthreads();
-            tile_fft<T, M, L, LP, NT, +1>(tile, s_tw);
-            // theta -> T_{k+1}; residual; write state; build next applied rows in place
-            for (int idx = threadIdx.x; idx < 2 * L * n; idx += NT) {
-                const int lr = idx / n, j = idx - lr * n;  // local row 0..2L-1
-                const int l = lr >> 1, half = lr & 1;
-                const int x = 2 * p0 + lr;
-                if (x >= n) continue;
-                const cplx<T> z = tile[j * LP + l];
-                T th = (half ? z.y : z.x) * inv;  // theta - T0
-                T t = th;
-                if (kirchhoff) {
-                    const T br = ka + kb * th;
-                    if (!(br > T(0))) bad |= GTD_ST_KIRCHHOFF;
-                    t = pow(br, kexp) - t_ambient;
-                }
-                if (!finite_val(t)) bad |= GTD_ST_NONFINITE;
-                const T old = Ts[x * n + j];
-                dmax = fmax(dmax, double(fabs(t - old)));
-                Ts[x * n + j] = t;
-            }
-            __syncthreads();
+            tile_fft<T, M, L, LP, NT, +1>(tile, tw);
         }
-        // forward: z = mirror(applied row 2p) + i mirror(applied row 2p+1)
-        for (int idx = threadIdx.x; idx < 2 * L * n; idx += NT) {
-            const int lr = idx / n, y = idx - lr * n;
-            const int l = lr >> 1, half = lr & 1;
-            const int x = 2 * p0 + lr;
-            T a = T(0);
-            if (x < n) {
-                const T dT = FIRST ? T(0) : Ts[x * n + y];
-                const T p = P[x * n + y];
-                const T lk = in.nom_scale * Nm[x * n + y] * V[x * n + y];
-                const T f = law ? T(exp(beta * dT)) : T(1) + beta * dT;
-                a = p + lk * f;
+        // theta -> T_{k+1}, residual, state write, and the next applied rows
+        // z = mirror(a_2p) + i mirror(a_2p+1), in place: a thread owns cell j of
+        // both rows of its pair, so it alone reads and rewrites tile slot j (and
+        // the mirror slot M-1-j, never read here).
+        {
+            constexpr int IPT = (L * n + NT - 1) / NT;
+#pragma unroll
+            for (int i0 = 0; i0 < IPT; i0 += UB) {
+                T told[UB][2], pv[UB][2], lv[UB][2];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int idx = threadIdx.x + (i0 + u) * NT;
+                    const int l = idx / n, j = idx - l * n;
+                    const int x = 2 * (p0 + l);
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        told[u][half] = pv[u][half] = lv[u][half] = T(0);
+                        if (i0 + u < IPT && idx < L * n && x < n) {
+                            const size_t o = static_cast<size_t>(x + half) * n + j;
+                            if (!FIRST) told[u][half] = Ts[o];
+                            pv[u][half] = P[o];
+                            lv[u][half] = in.nom_scale * Nm[o] * V[o];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int idx = threadIdx.x + (i0 + u) * NT;
+                    if (i0 + u >= IPT || idx >= L * n) continue;
+                    const int l = idx / n, j = idx - l * n;
+                    const int x = 2 * (p0 + l);
+                    T a[2] = {T(0), T(0)};
+                    if (x < n) {
+                        const cplx<T> z = FIRST ? mk<T>(T(0), T(0)) : tile[j * LP + l];
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            T t = T(0);
+                            if (!FIRST) {
+                                const T th = (half ? z.y : z.x) * inv;  // theta - T0
+                                t = th;
+                                if (kirchhoff) {
+                                    const T br = ka + kb * th;
+                                    if (!(br > T(0))) bad |= GTD_ST_KIRCHHOFF;
+                                    t = pow(br, kexp) - t_ambient;
+                                }
+                                if (!finite_val(t)) bad |= GTD_ST_NONFINITE;
+                                dmax = fmax(dmax, double(fabs(t - told[u][half])));
+                                Ts[static_cast<size_t>(x + half) * n + j] = t;
+                            }
+                            const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
+                            a[half] = pv[u][half] + lv[u][half] * f;
+                        }
+                    }
+                    tile[j * LP + l] = mk<T>(a[0], a[1]);
+                    tile[(M - 1 - j) * LP + l] = mk<T>(a[0], a[1]);
+                }
             }
-            tileT[2 * (y * LP + l) + half] = a;
-            tileT[2 * ((M - 1 - y) * LP + l) + half] = a;
         }
         __syncthreads();
-        tile_fft<T, M, L, LP, NT, -1>(tile, s_tw);
+        tile_fft<T, M, L, LP, NT, -1>(tile, tw);
         for (int idx = threadIdx.x; idx < 2 * L * hp; idx += NT) {
             const int lr = idx / hp, v = idx - lr * hp;
             const int l = lr >> 1, half = lr & 1;
@@ -566,32 +608,52 @@ __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int
 
 // per-sample max / mean of the converged maps
 template <typename T>
-__global__ void fp_stats(const T* __restrict__ Tst, int n, int sample0, double* __restrict__ mx,
-                         double* __restrict__ mean) {
+__global__ void __launch_bounds__(512) fp_stats(const T* __restrict__ Tst, int n, int sample0, double* __restrict__ mx,
+                                                double* __restrict__ mean) {
+    // one CTA per sample; each thread streams 4-element vectors with independent
+    // accumulators (fixed order: deterministic), 8 loads in flight per iteration
     const size_t sg = static_cast<size_t>(sample0) + blockIdx.x;
     const T* t = Tst + sg * n * n;
-    double m = -1.0 / 0.0, s = 0.0;
-    for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-        m = fmax(m, double(t[i]));
-        s += double(t[i]);
+    const size_t cnt = static_cast<size_t>(n) * n;  // n >= 16 even: a multiple of 8
+    double m[8], s[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        m[k] = -1.0 / 0.0;
+        s[k] = 0.0;
     }
+    for (size_t i = static_cast<size_t>(threadIdx.x) * 8; i < cnt; i += static_cast<size_t>(blockDim.x) * 8) {
+        T v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = t[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            m[k] = fmax(m[k], double(v[k]));
+            s[k] += double(v[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        m[0] = fmax(m[0], m[k]);
+        s[0] += s[k];
+    }
+    double mm = m[0], ss = s[0];
     __shared__ double rm[32], rs[32];
     for (int o = 16; o > 0; o >>= 1) {
-        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mm = fmax(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        rm[threadIdx.x >> 5] = m;
-        rs[threadIdx.x >> 5] = s;
+        rm[threadIdx.x >> 5] = mm;
+        rs[threadIdx.x >> 5] = ss;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < int(blockDim.x >> 5); ++w) {
-            m = fmax(m, rm[w]);
-            s += rs[w];
+            mm = fmax(mm, rm[w]);
+            ss += rs[w];
         }
-        if (mx) mx[sg] = m;
-        if (mean) mean[sg] = s / (double(n) * double(n));
+        if (mx) mx[sg] = mm;
+        if (mean) mean[sg] = ss / (double(n) * double(n));
     }
 }
 
@@ -599,7 +661,7 @@ template <typename T, int M>
 struct FPLaunch {
     using Gm = FPGeom<T, M>;
     using Gc = FPCGeom<T, M>;
-    static size_t smem_rows() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
+    static size_t smem_rows() { return sizeof(cplx<T>) * (M * Gm::LP + (Gm::GTW ? 0 : M)); }
     static size_t smem_rows_w() {
         if constexpr (fp_warp_rows<T, M>())
             return sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + M / 2 + FPW_WARPS * WarpFFT<T, M>::SCRATCH);
@@ -688,7 +750,7 @@ struct FPLaunch {
                     if (*counter_h == 0) break;
                 }
             }
-            fp_stats<T><<<cnt, 256, 0, st>>>(Tst, n, s0, mx, mean);
+            fp_stats<T><<<cnt, 512, 0, st>>>(Tst, n, s0, mx, mean);
             k += 1;
         }
         if (launches) *launches = k;

@@ -144,7 +144,11 @@ struct MCGeom {
     static constexpr int NT2 = (M / 8) * W > GT_P2_NT ? GT_P2_NT : (M / 8) * W;
     static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
     // pass 2 holds three lines per thread-butterfly: 128 registers (fp32) / 255 (fp64)
+#ifdef GT_P2_MINB
+    static constexpr int MINB2 = sizeof(T) == 8 ? 1 : GT_P2_MINB;  // tuning override (occupancy sweeps)
+#else
     static constexpr int MINB2 = sizeof(T) == 8 ? 1 : ((512 / NT2) < 1 ? 1 : (512 / NT2));
+#endif
 };
 
 // ------------------------------------------------------------------ pass 1

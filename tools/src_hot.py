@@ -11,7 +11,7 @@ rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 key = sys.argv[4] if len(sys.argv) > 4 else "Instructions Executed"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "--kernel-name", f"regex:{kern}"], capture_output=True, text=True).stdout
+                      "--kernel-name-base", "demangled", "--kernel-name", f"regex:{kern}"], capture_output=True, text=True).stdout
 rows, fname, hdr = [], "?", None
 for r in csv.reader(io.StringIO(out)):
     if not r:
