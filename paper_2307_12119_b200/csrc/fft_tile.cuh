@@ -288,8 +288,14 @@ __device__ __forceinline__ void stockham_stage_pairs(cplx<T>* tile, const cplx<T
 template <typename T, int M, int L, int LP, int NT, int SIGN, int R, int NS>
 __device__ __forceinline__ void stage(cplx<T>* tile, const cplx<T>* tw) {
     // pairs when the tile has enough pair-butterflies for every thread and the
-    // pitch keeps pairs 16-byte aligned
+    // pitch keeps pairs 16-byte aligned. fp32 only: a pair is one 16-byte access,
+    // while an fp64 pair is two 16-byte accesses at a 32-byte thread stride (twice
+    // the shared-memory wavefronts of the line-per-thread stage's contiguous ones)
+#ifndef GT_FP64_PAIRS
+    if constexpr (sizeof(T) == 4 && LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
+#else
     if constexpr (LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
+#endif
         stockham_stage_pairs<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);
     else
         stockham_stage<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);

@@ -57,9 +57,10 @@ struct FwdA {
         }
         return mk<T>(app[static_cast<size_t>(2 * p) * n + y] - shift, app[static_cast<size_t>(2 * p + 1) * n + y] - shift);
     }
-    __device__ void store(int p, int i1, int k2, cplx<T> v) const {
-        S1[static_cast<size_t>(p) * M + i1 + static_cast<size_t>(M1) * k2] =
-            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(i1) * k2, false));
+    using Pre = cplx<T>;  // the four-step twiddle, issued ahead of the stores
+    __device__ Pre pre(int, int i1, int k2) const { return twm<T>(tw, M, static_cast<long long>(i1) * k2, false); }
+    __device__ void store(int p, int i1, int k2, cplx<T> v, const Pre& w) const {
+        S1[static_cast<size_t>(p) * M + i1 + static_cast<size_t>(M1) * k2] = cmul<T>(v, w);
     }
 };
 
@@ -74,7 +75,9 @@ struct FwdB {
     __device__ cplx<T> load(int p, int k2, int j) const {
         return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M1) * k2];
     }
-    __device__ void store(int p, int k2, int k1, cplx<T> v) const {
+    struct Pre {};
+    __device__ Pre pre(int, int, int) const { return {}; }
+    __device__ void store(int p, int k2, int k1, cplx<T> v, const Pre&) const {
         Z[static_cast<size_t>(p) * M + k2 + static_cast<size_t>(M2) * k1] = v;
     }
 };
@@ -109,9 +112,10 @@ struct ColA {
         return (x & 1) ? mk<T>(T(0.5) * (a.y - b.y), T(-0.5) * (a.x - b.x))
                        : mk<T>(T(0.5) * (a.x + b.x), T(0.5) * (a.y + b.y));
     }
-    __device__ void store(int i1, int c, int k2, cplx<T> v) const {
-        C1[(static_cast<size_t>(i1) + static_cast<size_t>(M1) * k2) * hc + c] =
-            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(i1) * k2, false));
+    using Pre = cplx<T>;
+    __device__ Pre pre(int i1, int, int k2) const { return twm<T>(tw, M, static_cast<long long>(i1) * k2, false); }
+    __device__ void store(int i1, int c, int k2, cplx<T> v, const Pre& w) const {
+        C1[(static_cast<size_t>(i1) + static_cast<size_t>(M1) * k2) * hc + c] = cmul<T>(v, w);
     }
 };
 
@@ -129,13 +133,15 @@ struct ColB {
     __device__ cplx<T> load(int k2, int c, int j) const {
         return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
     }
-    __device__ cplx<T> mid(int k2, int c, int k1, cplx<T> v) const {
+    // the spectral factor at (u, v); zero for the padded columns v > n
+    __device__ cplx<T> midw(int k2, int c, int k1) const {
         const int u = k2 + M2 * k1, vv = c0 + c;
-        return vv < h ? cmul<T>(v, fk[static_cast<size_t>(u) * fkp + vv]) : mk<T>(T(0), T(0));
+        return vv < h ? fk[static_cast<size_t>(u) * fkp + vv] : mk<T>(T(0), T(0));
     }
-    __device__ void store(int k2, int c, int ia, cplx<T> v) const {
-        C2[(static_cast<size_t>(k2) + static_cast<size_t>(M2) * ia) * hc + c] =
-            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(ia) * k2, true));
+    using Pre = cplx<T>;
+    __device__ Pre pre(int k2, int, int ia) const { return twm<T>(tw, M, static_cast<long long>(ia) * k2, true); }
+    __device__ void store(int k2, int c, int ia, cplx<T> v, const Pre& w) const {
+        C2[(static_cast<size_t>(k2) + static_cast<size_t>(M2) * ia) * hc + c] = cmul<T>(v, w);
     }
 };
 
@@ -151,7 +157,9 @@ struct KColB {  // group k2, line c, j = i1: forward only; fk[u][v] natural orde
     __device__ cplx<T> load(int k2, int c, int j) const {
         return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
     }
-    __device__ void store(int k2, int c, int k1, cplx<T> v) const {
+    struct Pre {};
+    __device__ Pre pre(int, int, int) const { return {}; }
+    __device__ void store(int k2, int c, int k1, cplx<T> v, const Pre&) const {
         const int u = k2 + M2 * k1;
         if (u == 0 && c == 0) v.x += dc;  // baseline_kernel_spectrum: fk[0] += phi m^2 / 4 (greens.cpp:194-201)
         fk[static_cast<size_t>(u) * fkp + c] = v;
@@ -169,7 +177,9 @@ struct ColC {
     __device__ cplx<T> load(int ia, int c, int j) const {
         return C2[(static_cast<size_t>(j) + static_cast<size_t>(M2) * ia) * hc + c];
     }
-    __device__ void store(int ia, int c, int ib, cplx<T> v) const {
+    struct Pre {};
+    __device__ Pre pre(int, int, int) const { return {}; }
+    __device__ void store(int ia, int c, int ib, cplx<T> v, const Pre&) const {
         const int i = ia + M1 * ib;
         if (i < n) Y[static_cast<size_t>(i) * hc + c] = v;
     }
@@ -190,9 +200,10 @@ struct RinvA {
         if (f == 0 || f == n) return mk<T>(y.x, r.x);
         return f < n ? mk<T>(y.x - r.y, y.y + r.x) : mk<T>(y.x + r.y, r.x - y.y);
     }
-    __device__ void store(int p, int k2, int ia, cplx<T> v) const {
-        S1[static_cast<size_t>(p) * M + k2 + static_cast<size_t>(M2) * ia] =
-            cmul<T>(v, twm<T>(tw, M, static_cast<long long>(ia) * k2, true));
+    using Pre = cplx<T>;
+    __device__ Pre pre(int, int k2, int ia) const { return twm<T>(tw, M, static_cast<long long>(ia) * k2, true); }
+    __device__ void store(int p, int k2, int ia, cplx<T> v, const Pre& w) const {
+        S1[static_cast<size_t>(p) * M + k2 + static_cast<size_t>(M2) * ia] = cmul<T>(v, w);
     }
 };
 
@@ -252,12 +263,19 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
 };
 
 // ------------------------------------------------------------------ generic pass
+template <typename T, int N>
+constexpr int lg_pitch() {
+    return sizeof(T) == 8 ? TileGeom<T, N>::L + 1 : TileGeom<T, N>::L + 2;
+}
+
 // L lines of N points per work item; items = groups x ceil(nlines / L).
 template <typename T, int N, class Op, bool TWO>
 __global__ void __launch_bounds__(TileGeom<T, N>::NT, TileGeom<T, N>::MINB)
 lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines) {
     using G = TileGeom<T, N>;
-    constexpr int L = G::L, LP = L + 2, NT = G::NT;
+    // odd pitch (fp64 stages are line-per-thread, no pair alignment): the j-fast
+    // tile fills of the row ops hit distinct banks
+    constexpr int L = G::L, LP = lg_pitch<T, N>(), NT = G::NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_tw = tile + N * LP;
@@ -272,7 +290,12 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
         const int g = item / bpg, l0 = (item - g * bpg) * L;
         __syncthreads();
         // loads in groups of U elements, all issued before the shared-memory stores
-        constexpr int U = 4;
+        // (the whole item at once up to 16: one exposed HBM latency per item)
+        constexpr int EPT = (N * L + NT - 1) / NT;
+#ifndef GT_LG_U
+#define GT_LG_U 16
+#endif
+        constexpr int U = EPT < GT_LG_U ? EPT : GT_LG_U;
         for (int base = threadIdx.x; base < N * L; base += NT * U) {
             cplx<T> vals[U];
 #pragma unroll
@@ -291,32 +314,44 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
         __syncthreads();
         tile_fft<T, N, L, LP, NT, Op::SIGN>(tile, s_tw);
         if constexpr (TWO) {
-            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-                const int l = idx % L, k = idx / L;
-                if (l0 + l < nlines) tile[k * LP + l] = op.mid(g, l0 + l, k, tile[k * LP + l]);
+            // spectral factors issued in batches ahead of their use (global / L2 latency)
+            constexpr int UM = EPT < 8 ? EPT : 8;
+            for (int base = threadIdx.x; base < N * L; base += NT * UM) {
+                cplx<T> f[UM];
+#pragma unroll
+                for (int u = 0; u < UM; ++u) {
+                    const int idx = base + u * NT, l = idx % L, k = idx / L;
+                    f[u] = (idx < N * L && l0 + l < nlines) ? op.midw(g, l0 + l, k) : mk<T>(T(0), T(0));
+                }
+#pragma unroll
+                for (int u = 0; u < UM; ++u) {
+                    const int idx = base + u * NT, l = idx % L, k = idx / L;
+                    if (idx < N * L && l0 + l < nlines) tile[k * LP + l] = cmul<T>(tile[k * LP + l], f[u]);
+                }
             }
             __syncthreads();
             tile_fft<T, N, L, LP, NT, -Op::SIGN>(tile, s_tw);
         }
-        if constexpr (Op::REDUCE) {
-            constexpr int U = 4;
-            for (int base = threadIdx.x; base < N * L; base += NT * U) {
-                typename Op::Pre q[U];
+        {
+            // the store side's global inputs (twiddles, epilogue operands) in batches of US
+            constexpr int US = sizeof(typename Op::Pre) > 16 ? 4 : (EPT < 8 ? EPT : 8);
+            for (int base = threadIdx.x; base < N * L; base += NT * US) {
+                typename Op::Pre q[US];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
+                for (int u = 0; u < US; ++u) {
                     const int idx = base + u * NT, l = idx % L, k = idx / L;
                     if (idx < N * L && l0 + l < nlines) q[u] = op.pre(g, l0 + l, k);
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
+                for (int u = 0; u < US; ++u) {
                     const int idx = base + u * NT, l = idx % L, k = idx / L;
-                    if (idx < N * L && l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l], q[u], r_dmax, r_bad);
+                    if (idx < N * L && l0 + l < nlines) {
+                        if constexpr (Op::REDUCE)
+                            op.store(g, l0 + l, k, tile[k * LP + l], q[u], r_dmax, r_bad);
+                        else
+                            op.store(g, l0 + l, k, tile[k * LP + l], q[u]);
+                    }
                 }
-            }
-        } else {
-            for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-                const int l = idx % L, k = idx / L;
-                if (l0 + l < nlines) op.store(g, l0 + l, k, tile[k * LP + l]);
             }
         }
     }
@@ -345,7 +380,7 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
 
 template <typename T, int N>
 size_t lg_smem() {
-    return sizeof(cplx<T>) * (N * (TileGeom<T, N>::L + 2) + N);
+    return sizeof(cplx<T>) * (N * lg_pitch<T, N>() + N);
 }
 
 template <typename T, int N, class Op, bool TWO>
