@@ -99,57 +99,52 @@ __device__ __forceinline__ void dft4(cplx<T>* v) {
     v[3] = csub<T>(a1, b1);
 }
 
+// Odd half of the radix-8 DIF butterfly: a4..a7 are the differences v[k] - v[k+4];
+// a5 and a7 still owe their W8 factors (1 +- i)/sqrt2 and (-1 +- i)/sqrt2. The
+// 1/sqrt2 is folded into FFMAs of the last layer instead of two FMULs each.
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft8_odd(cplx<T> a4, cplx<T> a5, cplx<T> a6, cplx<T> a7, cplx<T>& o0, cplx<T>& o1,
+                                         cplx<T>& o2, cplx<T>& o3) {
+    const T r = T(0.70710678118654752440084436210485);
+    // unscaled W8^1 a5 and W8^3 a7
+    const cplx<T> A5 = SIGN < 0 ? mk<T>(a5.x + a5.y, a5.y - a5.x) : mk<T>(a5.x - a5.y, a5.y + a5.x);
+    const cplx<T> A7 = SIGN < 0 ? mk<T>(a7.y - a7.x, -(a7.x + a7.y)) : mk<T>(-(a7.x + a7.y), a7.x - a7.y);
+    a6 = mul_si<SIGN, T>(a6);
+    const cplx<T> p0 = cadd<T>(a4, a6), p1 = csub<T>(a4, a6);
+    const cplx<T> S = cadd<T>(A5, A7), D = mul_si<SIGN, T>(csub<T>(A5, A7));
+    o0 = mk<T>(fma(r, S.x, p0.x), fma(r, S.y, p0.y));
+    o2 = mk<T>(fma(-r, S.x, p0.x), fma(-r, S.y, p0.y));
+    o1 = mk<T>(fma(r, D.x, p1.x), fma(r, D.y, p1.y));
+    o3 = mk<T>(fma(-r, D.x, p1.x), fma(-r, D.y, p1.y));
+}
+
 template <int SIGN, typename T>
 __device__ __forceinline__ void dft8(cplx<T>* v) {
-    const T r = T(0.70710678118654752440084436210485);
-    // radix-2 DIF layer with W8^k twiddles
-    cplx<T> a0 = cadd<T>(v[0], v[4]), a4 = csub<T>(v[0], v[4]);
-    cplx<T> a1 = cadd<T>(v[1], v[5]), a5 = csub<T>(v[1], v[5]);
-    cplx<T> a2 = cadd<T>(v[2], v[6]), a6 = csub<T>(v[2], v[6]);
-    cplx<T> a3 = cadd<T>(v[3], v[7]), a7 = csub<T>(v[3], v[7]);
-    // W8^1 = (1 + SIGN i)/sqrt2, W8^2 = SIGN i, W8^3 = (-1 + SIGN i)/sqrt2
-    a5 = SIGN < 0 ? mk<T>((a5.x + a5.y) * r, (a5.y - a5.x) * r)
-                  : mk<T>((a5.x - a5.y) * r, (a5.y + a5.x) * r);
-    a6 = mul_si<SIGN, T>(a6);
-    a7 = SIGN < 0 ? mk<T>((a7.y - a7.x) * r, -(a7.x + a7.y) * r)
-                  : mk<T>(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);
-    // two DFT4 on (a0..a3) -> even outputs, (a4..a7) -> odd outputs
-    cplx<T> e[4] = {a0, a1, a2, a3};
-    cplx<T> o[4] = {a4, a5, a6, a7};
+    // radix-2 DIF layer, then DFT4 of the sums (even outputs) and of the twiddled
+    // differences (odd outputs)
+    cplx<T> e[4] = {cadd<T>(v[0], v[4]), cadd<T>(v[1], v[5]), cadd<T>(v[2], v[6]), cadd<T>(v[3], v[7])};
+    const cplx<T> a4 = csub<T>(v[0], v[4]), a5 = csub<T>(v[1], v[5]), a6 = csub<T>(v[2], v[6]),
+                  a7 = csub<T>(v[3], v[7]);
     dft4<SIGN, T>(e);
-    dft4<SIGN, T>(o);
+    dft8_odd<SIGN, T>(a4, a5, a6, a7, v[1], v[3], v[5], v[7]);
     v[0] = e[0];
     v[2] = e[1];
     v[4] = e[2];
     v[6] = e[3];
-    v[1] = o[0];
-    v[3] = o[1];
-    v[5] = o[2];
-    v[7] = o[3];
 }
 
 // DFT8 of an input whose slots 2..5 are zero (never read): the first radix-2
 // layer degenerates to copies / negations.
 template <int SIGN, typename T>
 __device__ __forceinline__ void dft8_outer_only(cplx<T>* v) {
-    const T r = T(0.70710678118654752440084436210485);
-    cplx<T> a0 = v[0], a4 = v[0], a1 = v[1], a5 = v[1];
-    cplx<T> a2 = v[6], a6 = mk<T>(-v[6].x, -v[6].y), a3 = v[7], a7 = mk<T>(-v[7].x, -v[7].y);
-    a5 = SIGN < 0 ? mk<T>((a5.x + a5.y) * r, (a5.y - a5.x) * r) : mk<T>((a5.x - a5.y) * r, (a5.y + a5.x) * r);
-    a6 = mul_si<SIGN, T>(a6);
-    a7 = SIGN < 0 ? mk<T>((a7.y - a7.x) * r, -(a7.x + a7.y) * r) : mk<T>(-(a7.x + a7.y) * r, (a7.x - a7.y) * r);
-    cplx<T> e[4] = {a0, a1, a2, a3};
-    cplx<T> o[4] = {a4, a5, a6, a7};
+    cplx<T> e[4] = {v[0], v[1], v[6], v[7]};
+    const cplx<T> a4 = v[0], a5 = v[1], a6 = mk<T>(-v[6].x, -v[6].y), a7 = mk<T>(-v[7].x, -v[7].y);
     dft4<SIGN, T>(e);
-    dft4<SIGN, T>(o);
+    dft8_odd<SIGN, T>(a4, a5, a6, a7, v[1], v[3], v[5], v[7]);
     v[0] = e[0];
     v[2] = e[1];
     v[4] = e[2];
     v[6] = e[3];
-    v[1] = o[0];
-    v[3] = o[1];
-    v[5] = o[2];
-    v[7] = o[3];
 }
 
 template <int R, int SIGN, typename T>
