@@ -91,7 +91,11 @@ gt_status gt_mc_batch(const gt_device_greens* d, const void* p_dyn, const void* 
 /* Device-resident batch: all pointers are device memory on the greens'
  * device; stats is batch x gt_sample_stats. Enqueued on `stream` (a
  * cudaStream_t; NULL = the library's own stream, pass cudaStreamLegacy for the
- * legacy default stream); returns without synchronising. */
+ * legacy default stream); returns without synchronising. Calls on one handle
+ * share its scratch, so each call's stream first waits for the previous
+ * call's work on the handle (whatever stream that used): calls on different
+ * streams are ordered, never overlapped. The same holds for every *_device
+ * entry point below. */
 gt_status gt_mc_batch_device(const gt_device_greens* d, const void* p_dyn, const void* var,
                              int batch, const gt_batch_opts* opts, void* t_out,
                              gt_sample_stats* stats, void* stream);

@@ -478,9 +478,11 @@ gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, cons
         in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
         in.nom_scale = opts ? opts->leak_frac : 0.3;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        d->order_in(st);
         cuda_ok(gtd_mc_batch(&d->d, &in, batch, &o, t_out, reinterpret_cast<gtd_sample_stats*>(stats),
                              d->scratch.p, chunk, st, d->profiling ? &gt_device_greens::mark : nullptr, d),
                 "mc batch launch");
+        d->order_out(st);
         d->kernels += gtd_mc_launch_count(batch, chunk);
         d->calls += 1;
     });
@@ -570,6 +572,7 @@ gt_status gt_var_model(gt_device_greens* d, double sigma_over_mu, double range_f
         work.ensure(mm * 16);
         lam.ensure(mm * 8);
         red.ensure(64);
+        d->order_in(st);  // earlier calls' generation may still read the old model
         d->var_sqlam.ensure(static_cast<size_t>(m) * gtd_var_pitch(n) * (d->fp64 ? 8 : 4));
         const double pitch = d->host.pitch;
         cuda_ok(gtd_var_model(&d->d, d->tw64.p, pitch, range_frac * pitch * n, work.p, lam.as<double>(),
@@ -596,9 +599,11 @@ gt_status gt_var_generate_device(const gt_device_greens* dc, const unsigned long
         cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
         const int chunk = std::min(batch, 1024);
+        d->order_in(st);
         d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(d->d.n, d->fp64) * chunk);
         cuda_ok(gtd_var_generate(&d->d, d->var_sqlam.p, seeds, batch, d->var_sigma, var_out, d->var_scratch.p, chunk, st),
                 "variation generation");
+        d->order_out(st);
         d->kernels += 2 * ((batch + chunk - 1) / chunk);
     });
 }
@@ -641,6 +646,7 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         // the variation scratch is shared by both slots: serialise generation across slots with an event
         cudaEvent_t gen_done[2];
         for (auto& e : gen_done) cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        for (auto& ss : d->slot_stream) d->order_in(ss);
         for (int s0 = 0, k = 0; s0 < batch; s0 += chunk, ++k) {
             const int cnt = std::min(chunk, batch - s0);
             const int s = k & 1;
@@ -730,9 +736,11 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     o.max_iters = opts->max_iters;
     o.poll = 4;
     long long launches = 0;
+    d->order_in(st);
     cuda_ok(gtd_fp_batch(&d->d, &in, batch, &o, t_out, iters, status, mx, mean, d->fp_scratch.p, d->fp_state.p,
                          d->fp_counter.as<int>(), d->fp_counter_h, chunk, st, &launches),
             "fixed point");
+    d->order_out(st);
     d->kernels += launches;
     d->calls += 1;
 }
@@ -863,6 +871,7 @@ gt_status gt_trace_batch_device(const gt_device_greens* dc, const int* blk, long
         cuda_ok(cudaMemcpyAsync(&fl, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s64), "d2h");
         cuda_ok(cudaStreamSynchronize(s64), "sync");
         if (fl & 1) fail(ST_SOLVER, "solver", "non-positive transient time constant");
+        d->order_in(s64);  // an earlier call's traces may still read the tables
         d->trace_tab.ensure(gtd_trace_table_bytes(n, d->fp64));
         cuda_ok(gtd_trace_tables(&d->d, Fd.p, r.p, rk.p, d->trace_tab.p, s64), "trace tables");
         cuda_ok(cudaStreamSynchronize(s64), "sync");
@@ -879,9 +888,11 @@ gt_status gt_trace_batch_device(const gt_device_greens* dc, const int* blk, long
         gtd_trace_in in{blk, blk_stride, sched, nblk, opts->steps, leak0, leak_stride};
         gtd_trace_opts o{k, opts->law, opts->beta, opts->out_stride};
         long long launches = 0;
+        d->order_in(st);
         cuda_ok(gtd_trace_batch(&d->d, d->trace_tab.p, &in, batch, &o, t_out, max_out, d->trace_scratch.p, chunk, st,
                                 &launches),
                 "trace batch");
+        d->order_out(st);
         d->kernels += launches;
         d->calls += 1;
     });

@@ -71,6 +71,16 @@ struct gt_device_greens {
     std::vector<cudaEvent_t> event_pool;
     size_t pool_used = 0;
     long long kernels = 0, calls = 0;
+    // Successive calls on one handle share its scratch; they may enqueue on
+    // different streams, so each call's stream waits for the previous call's work.
+    cudaEvent_t busy = nullptr;
+    void order_in(cudaStream_t st) {
+        if (!busy) cudaEventCreateWithFlags(&busy, cudaEventDisableTiming);
+        cudaStreamWaitEvent(st, busy, 0);
+    }
+    void order_out(cudaStream_t st) {
+        if (busy) cudaEventRecord(busy, st);
+    }
     static void mark(void* ctx, int point, cudaStream_t st) {
         auto* self = static_cast<gt_device_greens*>(ctx);
         if (self->pool_used == self->event_pool.size()) {
@@ -84,6 +94,7 @@ struct gt_device_greens {
     }
     ~gt_device_greens() {
         for (auto e : event_pool) cudaEventDestroy(e);
+        if (busy) cudaEventDestroy(busy);
         if (host_stats) cudaFreeHost(host_stats);
         if (fp_counter_h) cudaFreeHost(fp_counter_h);
         for (auto& s : slot_stream)

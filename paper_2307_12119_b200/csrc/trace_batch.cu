@@ -194,6 +194,27 @@ tr_cols(int b0, int count, TRBuf<T> bf, TRStep sp, const cplx<T>* __restrict__ g
                 stage_twiddle<T, M, false, K - 1, 2>(y[bb], j, s_twf);
                 dftR<RL, -1, T>(y[bb][0]);
                 dftR<RL, -1, T>(y[bb][1]);
+                // the state and table entries of this butterfly's 2 RL points, all issued
+                // before any state store (the stores to Zb would otherwise pin each load
+                // behind the previous point's store: one L2/HBM round trip per point).
+                // Each state entry is read and written by this thread only, once per
+                // launch, so the read-only path is safe.
+                // (RL > 2: 8 RL operands would not fit the register budget; per point.)
+                constexpr bool BATCH = RL <= 2;
+                constexpr int RB = BATCH ? RL : 1;
+                cplx<T> zo[2][RB], ta[2][RB], tr[2][RB], tb[2][RB];
+                if constexpr (BATCH) {
+#pragma unroll
+                    for (int col = 0; col < 2; ++col)
+#pragma unroll
+                        for (int q = 0; q < RB; ++q) {
+                            const size_t o = static_cast<size_t>(j + q * (M / RL)) * hp + v0 + g + col * GA;
+                            zo[col][q] = __ldg(&Zb[o]);
+                            ta[col][q] = tab[o];
+                            tr[col][q] = tab[plane + o];
+                            tb[col][q] = sp.has_k ? tab[2 * plane + o] : mk<T>(T(0), T(0));
+                        }
+                }
 #pragma unroll
                 for (int col = 0; col < 2; ++col) {
                     const int vv = v0 + g + col * GA;
@@ -205,8 +226,15 @@ tr_cols(int b0, int count, TRBuf<T> bf, TRStep sp, const cplx<T>* __restrict__ g
                         const cplx<T> Cz = cmul<T>(hu, y[bb][col][q]);  // C_P + i C_d
                         const cplx<T> ph = cconj<T>(cmul<T>(hu, hv));
                         const size_t o = static_cast<size_t>(u) * hp + vv;
-                        const cplx<T> a = tab[o], r = tab[plane + o], bk = tab[2 * plane + o];
-                        cplx<T> zs = cmul<T>(r, Zb[o]);
+                        const int qb = BATCH ? q : 0;
+                        if constexpr (!BATCH) {
+                            zo[col][0] = __ldg(&Zb[o]);
+                            ta[col][0] = tab[o];
+                            tr[col][0] = tab[plane + o];
+                            tb[col][0] = sp.has_k ? tab[2 * plane + o] : mk<T>(T(0), T(0));
+                        }
+                        const cplx<T> a = ta[col][qb], r = tr[col][qb], bk = tb[col][qb];
+                        cplx<T> zs = cmul<T>(r, zo[col][qb]);
                         const cplx<T> aP = cmul<T>(a, ph);
                         zs = mk<T>(zs.x + aP.x * Cz.x, zs.y + aP.y * Cz.x);
                         if (sp.has_k) {

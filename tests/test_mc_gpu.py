@@ -148,3 +148,31 @@ def test_mc_device_resident_equals_host_path(b200lib, g64, golden):
     h_out, h_mx, _, _, _ = dg.mc_batch_host(golden["p_dyn"], golden["var"], dg.opts())
     np.testing.assert_array_equal(out.cpu().numpy(), h_out)
     np.testing.assert_array_equal(st["max_rise"], h_mx)
+
+
+def test_mc_calls_on_different_streams_are_ordered(b200lib, g64, golden):
+    """Two device calls on one handle, enqueued back to back on different streams
+    without a host sync, share the handle's scratch: the second call's stream
+    waits for the first call's work, so both results equal the sequential ones."""
+    import torch
+    from paper_2307_12119_b200.api import SAMPLE_STATS_DTYPE
+    dg = _dg(g64, 0)
+    p = torch.from_numpy(golden["p_dyn"]).cuda()
+    v = torch.from_numpy(golden["var"]).cuda()
+    B = p.shape[0]
+    p2 = (p * 0.5).contiguous()
+    ref1, _, _, _, _ = dg.mc_batch_host(golden["p_dyn"], golden["var"], dg.opts())
+    ref2, _, _, _, _ = dg.mc_batch_host(p2.cpu().numpy(), golden["var"], dg.opts())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1, o2 = torch.empty_like(p), torch.empty_like(p)
+    st1 = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    st2 = torch.zeros_like(st1)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        dg.mc_batch_device(p.data_ptr(), v.data_ptr(), B, dg.opts(), o1.data_ptr(), st1.data_ptr(), s1.cuda_stream)
+        dg.mc_batch_device(p2.data_ptr(), v.data_ptr(), B, dg.opts(), o2.data_ptr(), st2.data_ptr(), s2.cuda_stream)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(o1.cpu().numpy(), ref1)
+        np.testing.assert_array_equal(o2.cpu().numpy(), ref2)
+        st1.zero_()
+        st2.zero_()

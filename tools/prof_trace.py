@@ -62,7 +62,7 @@ out = torch.zeros((B, frames, n, n), dtype=dt_t, device="cuda")
 mx = torch.zeros((B, frames), dtype=torch.float64, device="cuda")
 o = dg.trace_opts(dt=1e-5, steps=steps, window=500, law=0, beta=0.017, out_stride=stride)
 s = torch.cuda.Stream()
-for rep in range(2):
+for rep in range(int(sys.argv[5]) if len(sys.argv) > 5 else 2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     dg.trace_batch_device(blk.data_ptr(), n * n, sch.data_ptr(), nblk, leak0.data_ptr(), n * n, B, o,
