@@ -147,9 +147,51 @@ __device__ __forceinline__ void dft8_outer_only(cplx<T>* v) {
     v[6] = e[3];
 }
 
+template <int SIGN, typename T>
+__device__ __forceinline__ void dft16(cplx<T>* v) {
+    // radix-4 x radix-4 with w16 twiddles, in place: after the first layer slot
+    // n2 + 4 k1 holds a[n2][k1]; the second layer leaves X[k1 + 4 k2] in slot
+    // 4 k1 + k2, undone by a compile-time register permutation.
+    const T c1 = T(0.92387953251128675613), s1 = T(0.38268343236508977173);  // cos/sin(pi/8)
+    const T r2 = T(0.70710678118654752440);
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+        cplx<T> q[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+        dft4<SIGN, T>(q);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[n2 + 4 * k1] = q[k1];
+    }
+    const T sg = SIGN < 0 ? T(-1) : T(1);
+    v[5] = cmul<T>(v[5], mk<T>(c1, sg * s1));     // n2=1,k1=1: w^1
+    v[9] = cmul<T>(v[9], mk<T>(r2, sg * r2));     // n2=1,k1=2: w^2
+    v[13] = cmul<T>(v[13], mk<T>(s1, sg * c1));   // n2=1,k1=3: w^3
+    v[6] = cmul<T>(v[6], mk<T>(r2, sg * r2));     // n2=2,k1=1: w^2
+    v[10] = mul_si<SIGN, T>(v[10]);               // n2=2,k1=2: w^4
+    v[14] = cmul<T>(v[14], mk<T>(-r2, sg * r2));  // n2=2,k1=3: w^6
+    v[7] = cmul<T>(v[7], mk<T>(s1, sg * c1));     // n2=3,k1=1: w^3
+    v[11] = cmul<T>(v[11], mk<T>(-r2, sg * r2));  // n2=3,k1=2: w^6
+    v[15] = cmul<T>(v[15], mk<T>(-c1, -sg * s1)); // n2=3,k1=3: w^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        cplx<T> q[4] = {v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]};
+        dft4<SIGN, T>(q);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[4 * k1 + k2] = q[k2];
+    }
+    cplx<T> t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
 template <int R, int SIGN, typename T>
 __device__ __forceinline__ void dftR(cplx<T>* v) {
-    if constexpr (R == 8)
+    if constexpr (R == 16)
+        dft16<SIGN, T>(v);
+    else if constexpr (R == 8)
         dft8<SIGN, T>(v);
     else if constexpr (R == 4)
         dft4<SIGN, T>(v);
@@ -286,27 +328,32 @@ __device__ __forceinline__ void stage(cplx<T>* tile, const cplx<T>* tw) {
     // pitch keeps pairs 16-byte aligned. fp32 only: a pair is one 16-byte access,
     // while an fp64 pair is two 16-byte accesses at a 32-byte thread stride (twice
     // the shared-memory wavefronts of the line-per-thread stage's contiguous ones)
-#ifndef GT_FP64_PAIRS
-    if constexpr (sizeof(T) == 4 && LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
-#else
-    if constexpr (LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
-#endif
+    // Radix-16 stages run line-per-thread (a pair would hold 32 values).
+    if constexpr (sizeof(T) == 4 && R <= 8 && LP % 2 == 0 && ((M / R) * (L / 2)) % NT == 0)
         stockham_stage_pairs<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);
     else
         stockham_stage<T, M, L, LP, NT, SIGN, R, NS>(tile, tw);
 }
 
+// Tile plan: K = ceil(log2 M / 4) stages of radix <= 16, the larger radices first
+// (M = 128: 16 x 8; 1024: 16 x 8 x 8; 2048: 16 x 16 x 8; 512: 8 x 8 x 8): one
+// shared-memory round trip per stage, so fewer, wider stages move less data.
+template <int M>
+struct TilePlan {
+    static constexpr int LOG2M = ilog2(M);
+    static constexpr int K = (LOG2M + 3) / 4;
+    static constexpr int bits(int s) { return LOG2M / K + (s < LOG2M % K ? 1 : 0); }
+    static constexpr int R(int s) { return 1 << bits(s); }
+    static constexpr int NS(int s) { return s == 0 ? 1 : NS(s - 1) * R(s - 1); }
+};
+
 template <typename T, int M, int L, int LP, int NT, int SIGN, int S>
 struct StageRunner {
-    using G = TileGeom<T, M>;
     __device__ __forceinline__ static void run(cplx<T>* tile, const cplx<T>* tw) {
-        if constexpr (S < G::N8) {
-            constexpr int NS = 1 << (3 * S);
-            stage<T, M, L, LP, NT, SIGN, 8, NS>(tile, tw);
+        using TP = TilePlan<M>;
+        if constexpr (S < TP::K) {
+            stage<T, M, L, LP, NT, SIGN, TP::R(S), TP::NS(S)>(tile, tw);
             StageRunner<T, M, L, LP, NT, SIGN, S + 1>::run(tile, tw);
-        } else if constexpr (G::RLAST > 1) {
-            constexpr int NS = 1 << (3 * G::N8);
-            stage<T, M, L, LP, NT, SIGN, G::RLAST, NS>(tile, tw);
         }
     }
 };

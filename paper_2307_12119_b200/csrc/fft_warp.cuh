@@ -20,46 +20,6 @@
 
 namespace gtb {
 
-template <int SIGN, typename T>
-__device__ __forceinline__ void dft16(cplx<T>* v) {
-    // radix-4 x radix-4 with w16 twiddles, in place: after the first layer slot
-    // n2 + 4 k1 holds a[n2][k1]; the second layer leaves X[k1 + 4 k2] in slot
-    // 4 k1 + k2, undone by a compile-time register permutation.
-    const T c1 = T(0.92387953251128675613), s1 = T(0.38268343236508977173);  // cos/sin(pi/8)
-    const T r2 = T(0.70710678118654752440);
-#pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) {
-        cplx<T> q[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
-        dft4<SIGN, T>(q);
-#pragma unroll
-        for (int k1 = 0; k1 < 4; ++k1) v[n2 + 4 * k1] = q[k1];
-    }
-    const T sg = SIGN < 0 ? T(-1) : T(1);
-    v[5] = cmul<T>(v[5], mk<T>(c1, sg * s1));     // n2=1,k1=1: w^1
-    v[9] = cmul<T>(v[9], mk<T>(r2, sg * r2));     // n2=1,k1=2: w^2
-    v[13] = cmul<T>(v[13], mk<T>(s1, sg * c1));   // n2=1,k1=3: w^3
-    v[6] = cmul<T>(v[6], mk<T>(r2, sg * r2));     // n2=2,k1=1: w^2
-    v[10] = mul_si<SIGN, T>(v[10]);               // n2=2,k1=2: w^4
-    v[14] = cmul<T>(v[14], mk<T>(-r2, sg * r2));  // n2=2,k1=3: w^6
-    v[7] = cmul<T>(v[7], mk<T>(s1, sg * c1));     // n2=3,k1=1: w^3
-    v[11] = cmul<T>(v[11], mk<T>(-r2, sg * r2));  // n2=3,k1=2: w^6
-    v[15] = cmul<T>(v[15], mk<T>(-c1, -sg * s1)); // n2=3,k1=3: w^9
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1) {
-        cplx<T> q[4] = {v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]};
-        dft4<SIGN, T>(q);
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) v[4 * k1 + k2] = q[k2];
-    }
-    cplx<T> t[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = v[i];
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
-}
-
 // 32-point DFT in registers: radix 8 over n1 (inputs n2 + 4 n1), twiddle
 // w32^{n2 k1}, radix 4 over n2; X[k1 + 8 k2] lands in slot 4 k1 + k2 and a
 // compile-time register permutation restores natural order.
