@@ -85,14 +85,24 @@ gtd_mc_opts to_dev_opts(const gt_batch_opts* o) {
     return r;
 }
 
-int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o) {
+// Scratch budget of the automatic chunking: 40% of the device's free memory,
+// within [1.5 GiB, 32 GiB] (a 1024-sample chunk at n = 256 needs ~1.6 GB; at
+// n = 1024 a sample alone needs ~25 MB fp32 / ~50 MB fp64).
+size_t scratch_budget() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
+    const size_t lo = 1536ull << 20, hi = 32ull << 30;
+    return std::min(hi, std::max(lo, fr / 10 * 4));
+}
+
+int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1) {  // share: scratch buffers in flight
     if (o && o->chunk > 0) return std::min(o->chunk, batch);
     // Large chunks win: the passes are SM-issue bound, not HBM bound (a sweep of
     // 24..4096 pairs per chunk on B200 went 232k -> 325k solves/s; L2 residency
-    // of the intermediates at <= 48 MB bought nothing). Cap scratch at ~1.5 GB.
+    // of the intermediates at <= 48 MB bought nothing), and a chunk that leaves a
+    // small remainder runs that tail at low occupancy.
     const size_t per = gtd_mc_scratch_bytes_per_sample(n, fp64);
-    const size_t budget = 1536ull << 20;
-    int c = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, budget / per)));
+    int c = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, scratch_budget() / share / per)));
     return std::min(c, batch);
 }
 
@@ -502,7 +512,7 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         const size_t map = static_cast<size_t>(n) * n * es;
         // Pipeline chunk: large enough to amortise launches, two slots in flight.
         int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 512);
-        const int inner = auto_chunk(n, d->fp64, chunk, nullptr);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2);
         gtd_mc_opts o = to_dev_opts(opts);
         for (int s = 0; s < 2; ++s) {
             if (!d->slot_stream[s]) cuda_ok(cudaStreamCreateWithFlags(&d->slot_stream[s], cudaStreamNonBlocking), "stream");
@@ -622,7 +632,7 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         const size_t es = d->fp64 ? 8 : 4;
         const size_t map = static_cast<size_t>(n) * n * es;
         int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 512);
-        const int inner = auto_chunk(n, d->fp64, chunk, nullptr);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2);
         gtd_mc_opts o = to_dev_opts(opts);
         d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(n, d->fp64) * chunk);
         for (int s = 0; s < 2; ++s) {
@@ -713,7 +723,7 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     int chunk = opts->chunk > 0 ? std::min(opts->chunk, batch) : 0;
     if (!chunk) {
         const size_t per = gtd_fp_scratch_bytes_per_sample(n, d->fp64);
-        chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, (1024ull << 20) / per)));
+        chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, scratch_budget() / per)));
         chunk = std::min(chunk, batch);
     }
     d->fp_scratch.ensure(gtd_fp_scratch_bytes_per_sample(n, d->fp64) * chunk);
