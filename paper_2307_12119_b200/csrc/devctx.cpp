@@ -170,7 +170,8 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     d->gtab.ensure(static_cast<size_t>(n + 1) * hp * rb);
     d->fg.ensure(static_cast<size_t>(m) * hp * 4 * rb);
     cuda_ok(gtd_greens_tables(static_cast<const double*>(d->fsp0.p), static_cast<const double*>(d->gsp0.p),
-                              g.phi, n, hp, d->fp64, d->tw64.p, d->fk_full.p, d->fk.p, d->gtab.p, d->fg.p, st),
+                              g.phi, n, hp, d->fp64, d->tw64.p, d->fk_full.p, d->fk.p, d->gtab.p, d->fg.p, g.alpha,
+                              st),
             "greens tables");
     cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
     d->d.n = n;

@@ -145,9 +145,14 @@ __global__ void k_gtab(const double* __restrict__ g_sp0, int n, int hp, T* __res
     gt[du * hp + dv] = T(g_sp0[c * n + c] - 0.25 * s);
 }
 
-// Packed per-frequency table {fk.re, fk.im, g(du, v), 0} for the fused column pass.
+// Packed per-frequency table of the fused column pass (mc_pass2): one 16-byte
+// (fp32) load per (u, v) of {fk.re, fk.im, alpha g(du, v), D(u) D(v)}, derived in
+// fp64 and rounded once. D(u) = sin(pi u/2) / sin(pi u/m) is the real factor of
+// the centred die-box spectrum (k1 (x) k1 = conj(w^{u/2} w^{v/2}) D(u) D(v)).
+// Columns v > n are zero (they evaluate to 0 in the pass).
 template <typename T>
-__global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g_sp0, int n, int hp, T* __restrict__ fg) {
+__global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g_sp0, int n, int hp, double alpha,
+                     T* __restrict__ fg) {
     const int m = 2 * n, u = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= hp) return;
     T* o = fg + (static_cast<size_t>(u) * hp + v) * 4;
@@ -160,11 +165,10 @@ __global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g
     auto cl = [n](int i) { return i < 0 ? 0 : (i > n - 1 ? n - 1 : i); };
     const int ip = cl(c + du), im = cl(c - du), jp = cl(c + v), jm = cl(c - v);
     const double s = g_sp0[ip * n + jp] + g_sp0[ip * n + jm] + g_sp0[im * n + jp] + g_sp0[im * n + jm];
+    auto D = [n, m](int t) { return t == 0 ? double(n) : sinpi(0.5 * t) / sinpi(double(t) / m); };
     o[0] = T(z.x);
     o[1] = T(z.y);
-    o[2] = T(g_sp0[c * n + c] - 0.25 * s);
-    // die-box spectrum k1[u] k1[v] = conj(w^{u/2} w^{v/2}) D(u) D(v), D(u) = sin(pi u/2) / sin(pi u/m)
-    auto D = [n, m](int t) { return t == 0 ? double(n) : sinpi(0.5 * t) / sinpi(double(t) / m); };
+    o[2] = T(alpha * (g_sp0[c * n + c] - 0.25 * s));
     o[3] = T(D(u) * D(v));
 }
 
@@ -184,7 +188,7 @@ int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, 
 // receives the full fp64 baseline kernel spectrum fk (kept by the caller).
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
                       int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out, void* fg_out,
-                      cudaStream_t st) {
+                      double alpha, cudaStream_t st) {
     const int m = 2 * n;
     double2* K = static_cast<double2*>(work_d);
     k_center_kernel<<<dim3((m + 127) / 128, m), 128, 0, st>>>(f_sp0_d, phi, n, K);
@@ -198,14 +202,14 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
         k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                           static_cast<double*>(gtab_out));
         if (fg_out)
-            k_fg<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, static_cast<double*>(fg_out));
+            k_fg<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, alpha, static_cast<double*>(fg_out));
     } else {
         k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                      static_cast<float2*>(fk_out));
         k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                          static_cast<float*>(gtab_out));
         if (fg_out)
-            k_fg<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, static_cast<float*>(fg_out));
+            k_fg<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, alpha, static_cast<float*>(fg_out));
     }
     return static_cast<int>(cudaGetLastError());
 }

@@ -43,7 +43,7 @@ typedef struct gtd_greens {
     void* k1;             /* [m] complex: 1-D spectrum of the centred die box  */
     void* tw;             /* [m] complex: exp(-2 pi i t/m)                     */
     void* hs;             /* [m] complex: exp(-i pi t/m) (half-step twiddles)    */
-    void* fg;             /* [m][hp] {fk.re, fk.im, g(du,v), 0}: one vector load per frequency */
+    void* fg;             /* [m][hp] {fk.re, fk.im, alpha g(du,v), D(u)D(v)}: one vector load per frequency */
     double alpha, beta, rand_scale, mu_fixed;
 } gtd_greens;
 
@@ -98,7 +98,7 @@ int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, 
 /* GreensSet device tables from fp64 f_sp0 / g_sp0 (device n x n maps). */
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
                       int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out, void* fg_out,
-                      cudaStream_t st);
+                      double alpha, cudaStream_t st);
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "fft_tile.cuh"
 #include "col_pass.cuh"
@@ -92,6 +93,10 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 __device__ __forceinline__ void or_flags(int* dst, int flags) {
     const int w = __reduce_or_sync(0xffffffffu, flags);
     if ((threadIdx.x & 31) == 0 && w) atomicOr(dst, w);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ float fast_rcp(float x) { return __fdividef(1.0f, x); }
@@ -282,37 +287,38 @@ struct Vec4<double> {
 
 template <typename T, int M>
 struct ClosedForm {
+    using V4 = typename Vec4<T>::type;
     static constexpr int n = M / 2, c = n / 2, hp = MCGeom<T, M>::hp, W = MCGeom<T, M>::W;
-    const typename Vec4<T>::type* __restrict__ fg;  // {fk.re, fk.im, g, D(u) D(v)} per (u, v)
-    const T* s_srow;  // [n][W] row-symmetrised leakage of this column tile
-    T alpha, beta, mu_g, mus, qshift;
+    const V4* __restrict__ fg;  // {fk.re, fk.im, alpha g, D(u) D(v)} per (u, v) (fft2d.cu k_fg)
+    T mug, mb;   // mu_g, mu_g beta
+    T mus;       // sample mean leakage (F(p_var) = F(p_leak0) - mu K1)
+    T bq4, bqs;  // beta / 4, beta qshift: beta q = bq4 (S[ip] + S[im]) + bqs
+    T mn1, mn2;  // running minima of |den1|^2, |den2|^2 (runaway flags after the tile)
 
-    // At frequency (u, v): A_hat = ph C (ph = conj(w^{u/2} w^{v/2}), C the real
-    // 2-D DCT coefficient), b = F(p_leak0) on entry; returns Y = F_det A_hat
-    // and leaves R = F_rand in b. K1 = k1 (x) k1 = ph D(u) D(v).
-    __device__ __forceinline__ typename Vec4<T>::type table(int u, int v) const {
-        return fg[static_cast<size_t>(u) * hp + v];
-    }
-    __device__ __forceinline__ cplx<T> eval(T C, cplx<T>& b, cplx<T> ph, const typename Vec4<T>::type& t4, int u,
-                                            int v, int w, int& flags) const {
-        const int du = u <= M - u ? u : M - u;
-        const cplx<T> f = mk<T>(t4.x, t4.y);
-        const T g = t4.z, mk1 = mus * t4.w;
+    __device__ __forceinline__ V4 table(int u, int v) const { return fg[static_cast<size_t>(u) * hp + v]; }
+    // At frequency (u, v) (greens.cpp:203-251, one shared reciprocal):
+    //   C: real 2-D DCT coefficient of the applied map, A_hat = ph C with
+    //   ph = conj(w^{u/2} w^{v/2}); b: F(p_leak0) on entry, F_rand on return;
+    //   ssum = S[ip] + S[im] (row-symmetrised leakage); returns Y = F_det A_hat.
+    // den1 = 1 - alpha g - mu beta fk: F(mu) only touches the DC term, where
+    // g(0,0) = g_sp0(c,c) - g_sp0(c,c) = 0 (greens.cpp:186-192), so it drops out.
+    __device__ __forceinline__ cplx<T> eval(T C, cplx<T>& b, T ssum, cplx<T> ph, const V4& t4) {
+        const T fx = t4.x, fy = t4.y, ag = t4.z, mk1 = mus * t4.w;
+        const T a1 = T(1) - ag;
         const cplx<T> Bp = mk<T>(b.x - mk1 * ph.x, b.y - mk1 * ph.y);  // F(p_var) = F(p_leak0) - mu K1
-        const int ip = min(c + du, n - 1), im = max(c - du, 0);
-        const T q = T(0.25) * (s_srow[ip * W + w] + s_srow[im * W + w]) + qshift;
-        const T fmu = (u == 0 && v == 0) ? mu_g : T(0);
-        const T a1 = T(1) - alpha * g * (T(1) + fmu);
-        const cplx<T> den1 = mk<T>(a1 - mu_g * beta * f.x, -mu_g * beta * f.y);
-        const cplx<T> t1 = mk<T>(beta * q * f.x + alpha * g * Bp.x, beta * q * f.y + alpha * g * Bp.y);
+        const T bq = bq4 * ssum + bqs;
+        const cplx<T> den1 = mk<T>(a1 - mb * fx, -mb * fy);
+        const cplx<T> t1 = mk<T>(bq * fx + ag * Bp.x, bq * fy + ag * Bp.y);
         const cplx<T> den2 = mk<T>(den1.x - t1.x, den1.y - t1.y);
         const T d1 = cabs2<T>(den1), d2 = cabs2<T>(den2);
-        if (d1 < T(1e-12)) flags |= GTD_ST_RUNAWAY_DET;
-        if (d2 < T(1e-12)) flags |= GTD_ST_RUNAWAY_RAND;
-        const T rinv = fast_rcp(d1 * d2);
-        const cplx<T> fc1 = cmul<T>(f, cconj<T>(den1));
-        b = cscale<T>(cmul<T>(cmul<T>(fc1, t1), cconj<T>(den2)), rinv);
-        return cscale<T>(cmul<T>(fc1, ph), C * d2 * rinv);
+        mn1 = fmin(mn1, d1);
+        mn2 = fmin(mn2, d2);
+        const cplx<T> fr = cscale<T>(cmul<T>(mk<T>(fx, fy), cconj<T>(den1)), fast_rcp(d1 * d2));
+        b = cmul<T>(cmul<T>(fr, t1), cconj<T>(den2));
+        return cscale<T>(cmul<T>(fr, ph), C * d2);
+    }
+    __device__ __forceinline__ int flags() const {
+        return (mn1 < T(1e-12) ? GTD_ST_RUNAWAY_DET : 0) | (mn2 < T(1e-12) ? GTD_ST_RUNAWAY_RAND : 0);
     }
 };
 
@@ -462,6 +468,37 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 }
             }
         }
+#ifndef GT_P2_L2PF
+#define GT_P2_L2PF 1
+#endif
+#if GT_P2_L2PF
+        // The next item's row-spectrum tiles (A, B, S: one row segment per die row)
+        // are pulled into L2 now, so its stage-0 loads hit L2 instead of HBM.
+        {
+            const int nx = item + gridDim.x;
+            if (nx < count * CT) {
+#if GT_P2_TILE_MAJOR
+                const int tn = nx / count, sn = nx - tn * count;
+#else
+                const int sn = nx / CT, tn = nx - sn * CT;
+#endif
+                const size_t nb = static_cast<size_t>(sn) * n * hp + static_cast<size_t>(tn) * W;
+                constexpr int LA = (W * int(sizeof(T)) + 127) / 128, LB = (W * int(sizeof(cplx<T>)) + 127) / 128;
+                constexpr int PER = 2 * LA + LB;  // A and S segments, then B
+#pragma unroll
+                for (int t = threadIdx.x; t < n * PER; t += NT) {
+                    const int k = t / n, x = t - k * n;  // n: power of two
+                    const size_t o = nb + static_cast<size_t>(x) * hp;
+                    if (k < LA)
+                        prefetch_l2(reinterpret_cast<const char*>(Areal + o) + 128 * k);
+                    else if (k < 2 * LA)
+                        prefetch_l2(reinterpret_cast<const char*>(Srow + o) + 128 * (k - LA));
+                    else
+                        prefetch_l2(reinterpret_cast<const char*>(Bspec + o) + 128 * (k - 2 * LA));
+                }
+            }
+        }
+#endif
         // S rows into registers now, into shared memory after the stage-0 math (latency overlap)
         constexpr int ES = (n * W + NT - 1) / NT;
         T sv[ES];
@@ -497,21 +534,20 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
         const T* Vm = in.v(sg);
         ClosedForm<T, M> cf;
         cf.fg = reinterpret_cast<const typename Vec4<T>::type*>(fgtab);
-        cf.s_srow = s_srow;
-        cf.alpha = alpha;
-        cf.beta = beta;
-        cf.mu_g = mu_per_sample ? T(mu_s) : mu_fixed;
+        cf.mug = mu_per_sample ? T(mu_s) : mu_fixed;
+        cf.mb = cf.mug * beta;
         cf.mus = T(mu_s);
+        cf.bq4 = T(0.25) * beta;
         {
             const T pl_cc = in.nom_scale * Nm[c * n + c] * Vm[c * n + c];
             const T pl_00 = in.nom_scale * Nm[0] * Vm[0];
-            cf.qshift = T(double(pl_cc) - double(pl_00) - mu_s);  // greens.cpp:177-184
+            cf.bqs = beta * T(double(pl_cc) - double(pl_00) - mu_s);  // q shift, greens.cpp:177-184
         }
+        cf.mn1 = cf.mn2 = Real<T>::max();
         __syncthreads();
         // ---- middle forward stages
         FwdStagesAB<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
         // ---- last forward stage + closed forms + first inverse stage, in registers
-        int flags = 0;
         {
             cplx<T> y[BL][2 * CG][RL];  // Y_0, R_0, Y_1, R_1
 #pragma unroll
@@ -519,6 +555,15 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 const int id = threadIdx.x + b * NT;
                 if (UL % NT != 0 && id >= UL) break;
                 const int g = id % GA, j = id / GA;
+#ifndef GT_CF_PREFETCH
+#define GT_CF_PREFETCH 0
+#endif
+#if GT_CF_PREFETCH
+                // the first column's table entries are requested before the transform
+                typename Vec4<T>::type t0[RL];
+#pragma unroll
+                for (int q = 0; q < RL; ++q) t0[q] = cf.table(j + q * (M / RL), v0 + g);
+#endif
                 cplx<T> z[3][RL];
 #pragma unroll
                 for (int q = 0; q < RL; ++q) {
@@ -534,6 +579,12 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 // C_v + i C_v' = w^{u/2} Z[u]
 #pragma unroll
                 for (int q = 0; q < RL; ++q) z[0][q] = cmul<T>(s_hs[j + q * (M / RL)], z[0][q]);
+                // S rows ip = min(c + du, n - 1), im = max(c - du, 0) of frequency row u
+                auto s_off = [&](int u, int& sp, int& sm) {
+                    const int du = u <= M - u ? u : M - u;
+                    sp = min(c + du, n - 1) * W;
+                    sm = max(c - du, 0) * W;
+                };
 #pragma unroll
                 for (int col = 0; col < CG; ++col) {
                     const int w = g + col * GA, vv = v0 + w;
@@ -541,12 +592,18 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
 #pragma unroll
                     for (int q = 0; q < RL; ++q) {
                         const int u = j + q * (M / RL);
-                        // A_hat_v = conj(w^{u/2} w^{v/2}) C_v. Padded columns (v > n) see
-                        // an all-zero table entry and S = 0: they evaluate to 0, no flags.
+                        // Padded columns (v > n) see an all-zero table entry and S = 0:
+                        // they evaluate to 0 and raise no flags.
                         const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+                        int sp, sm;
+                        s_off(u, sp, sm);
                         cplx<T> bb = z[1 + col][q];
-                        y[b][2 * col][q] = cf.eval(col == 0 ? z[0][q].x : z[0][q].y, bb, ph, cf.table(u, vv), u,
-                                                   vv, w, flags);
+                        y[b][2 * col][q] = cf.eval(col == 0 ? z[0][q].x : z[0][q].y, bb,
+                                                   s_srow[sp + w] + s_srow[sm + w], ph,
+#if GT_CF_PREFETCH
+                                                   col == 0 ? t0[q] :
+#endif
+                                                   cf.table(u, vv));
                         y[b][2 * col + 1][q] = bb;
                     }
                     dftR<RL, +1, T>(y[b][2 * col]);
@@ -568,7 +625,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
             }
             __syncthreads();
         }
-        or_flags(&stats[sg].status, flags);
+        or_flags(&stats[sg].status, cf.flags());
         // ---- middle inverse stages
         InvStagesPairs<T, M, W, NT, 1, K - 1>::run(tile, s_twi);
         // ---- last inverse stage (radix 8, NS = M/8): keep rows [0, n) of Y, rows rho(x) of R
@@ -992,36 +1049,71 @@ struct MCLaunch {
             for (int& r : res) r = r < 1 ? 1 : r;
         }
         const size_t per = static_cast<size_t>(n) * hp;
-        cplx<T>* A = reinterpret_cast<cplx<T>*>(scratch);  // Y (pass 2 -> pass 3)
-        cplx<T>* B = A + per * chunk;                      // B (pass 1 -> 2), R (pass 2 -> 3)
-        T* S = reinterpret_cast<T*>(B + per * chunk);       // row-symmetrised leakage
-        T* Ar = S + per * chunk;                            // real DCT part of A (pass 1 -> 2)
         const cplx<T>* hs = reinterpret_cast<const cplx<T>*>(g->hs);
         const cplx<T>* tw = reinterpret_cast<const cplx<T>*>(g->tw);
         const T var_lo = T(exp(-o->exponent_cap)), var_hi = T(exp(o->exponent_cap));
-        auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
+        // Overlap (GT_MC_OVERLAP=1): the chunk's scratch is split into two slots whose
+        // sub-chunks run on two streams, every pass on a one-CTA-per-SM grid, so the
+        // SM-issue-bound column pass of one slot shares the SMs with the HBM-bound row
+        // passes of the other.
+        static int ovl = -1;
+        static cudaStream_t aux = nullptr;
+        static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (ovl < 0) {
+            const char* e = getenv("GT_MC_OVERLAP");
+            ovl = e ? atoi(e) : 0;
+            if (ovl) {
+                cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+            }
+        }
+        const int slots = (ovl && chunk >= 2) ? 2 : 1;
+        const int sub = chunk / slots;
+        const int cpsm = slots == 2 ? ovl : 0;  // CTAs per SM per pass under overlap
+        auto grid = [&](int items, int r) {
+            const int rr = cpsm > 0 && cpsm < r ? cpsm : r;
+            return items < sms * rr ? items : sms * rr;
+        };
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
-        for (int s0 = 0; s0 < batch; s0 += chunk) {
-            const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
-            if (mark) mark(ctx, 0, st);
+        if (slots == 2) {
+            cudaEventRecord(ev_fork, st);
+            cudaStreamWaitEvent(aux, ev_fork, 0);
+        }
+        for (int s0 = 0, k = 0; s0 < batch; s0 += sub, ++k) {
+            const int cnt = batch - s0 < sub ? batch - s0 : sub;
+            const int slot = k % slots;
+            cudaStream_t ss = slot == 0 ? st : aux;
+            gtd_mark_fn mk_ = slot == 0 ? mark : nullptr;
+            unsigned char* base = static_cast<unsigned char*>(scratch) +
+                                  static_cast<size_t>(slot) * sub * gtd_mc_scratch_bytes_per_sample(n, sizeof(T) == 8);
+            cplx<T>* A = reinterpret_cast<cplx<T>*>(base);  // Y (pass 2 -> pass 3)
+            cplx<T>* B = A + per * sub;                     // B (pass 1 -> 2), R (pass 2 -> 3)
+            T* S = reinterpret_cast<T*>(B + per * sub);      // row-symmetrised leakage
+            T* Ar = S + per * sub;                           // real DCT part of A (pass 1 -> 2)
+            if (mk_) mk_(ctx, 0, ss);
             if constexpr (use_warp_rows<T, M>())
-                mc_pass1w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(), st>>>(
+                mc_pass1w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(), ss>>>(
                     in, s0, cnt, Ar, B, S, stats, tw, hs, var_lo, var_hi);
             else
-                mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), st>>>(in, s0, cnt, Ar, B, S, stats, tw, hs,
+                mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), ss>>>(in, s0, cnt, Ar, B, S, stats, tw, hs,
                                                                              var_lo, var_hi);
-            if (mark) mark(ctx, 1, st);
-            mc_pass2<T, M><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), st>>>(
+            if (mk_) mk_(ctx, 1, ss);
+            mc_pass2<T, M><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), ss>>>(
                 in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fg), T(g->alpha), T(g->beta),
                 o->mu_per_sample, T(g->mu_fixed));
-            if (mark) mark(ctx, 2, st);
+            if (mk_) mk_(ctx, 2, ss);
             if constexpr (use_warp_rows<T, M>())
-                mc_pass3w<T, M><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32, smemw3(), st>>>(
+                mc_pass3w<T, M><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32, smemw3(), ss>>>(
                     in, s0, cnt, A, B, stats, tw, out, T(g->rand_scale), o->with_rand);
             else
-                mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), st>>>(in, s0, cnt, A, B, stats, tw, out,
+                mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), ss>>>(in, s0, cnt, A, B, stats, tw, out,
                                                                              T(g->rand_scale), o->with_rand);
-            if (mark) mark(ctx, 3, st);
+            if (mk_) mk_(ctx, 3, ss);
+        }
+        if (slots == 2) {
+            cudaEventRecord(ev_join, aux);
+            cudaStreamWaitEvent(st, ev_join, 0);
         }
         mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n);
         return static_cast<int>(cudaGetLastError());
