@@ -547,67 +547,24 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
         __syncthreads();
         // ---- middle forward stages
         FwdStagesAB<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
-        // ---- last forward stage + closed forms + first inverse stage, in registers
+        // ---- last forward stage + closed forms + first inverse stage, in registers.
+        // All forward inputs are read before one barrier, so each column's (Y, R)
+        // pair is stored as soon as it is transformed (two lines live, not four:
+        // the registers this frees let the table loads issue ahead of their use).
         {
-            cplx<T> y[BL][2 * CG][RL];  // Y_0, R_0, Y_1, R_1
+            cplx<T> z[BL][3][RL];
 #pragma unroll
             for (int b = 0; b < BL; ++b) {
                 const int id = threadIdx.x + b * NT;
                 if (UL % NT != 0 && id >= UL) break;
                 const int g = id % GA, j = id / GA;
-#ifndef GT_CF_PREFETCH
-#define GT_CF_PREFETCH 0
-#endif
-#if GT_CF_PREFETCH
-                // the first column's table entries are requested before the transform
-                typename Vec4<T>::type t0[RL];
-#pragma unroll
-                for (int q = 0; q < RL; ++q) t0[q] = cf.table(j + q * (M / RL), v0 + g);
-#endif
-                cplx<T> z[3][RL];
 #pragma unroll
                 for (int q = 0; q < RL; ++q) {
                     const int pr = prow<M / RL>(j, q);
-                    z[0][q] = tile[FL::pa(pr, g)];
+                    z[b][0][q] = tile[FL::pa(pr, g)];
                     const LinePair<T> p = ld_pair(&tile[FL::pb(pr, g)]);
-                    z[1][q] = p.a;
-                    z[2][q] = p.b;
-                }
-                stage_twiddle<T, M, false, K - 1, 3>(z, j, s_twf);
-#pragma unroll
-                for (int l = 0; l < 3; ++l) dftR<RL, -1, T>(z[l]);
-                // C_v + i C_v' = w^{u/2} Z[u]
-#pragma unroll
-                for (int q = 0; q < RL; ++q) z[0][q] = cmul<T>(s_hs[j + q * (M / RL)], z[0][q]);
-                // S rows ip = min(c + du, n - 1), im = max(c - du, 0) of frequency row u
-                auto s_off = [&](int u, int& sp, int& sm) {
-                    const int du = u <= M - u ? u : M - u;
-                    sp = min(c + du, n - 1) * W;
-                    sm = max(c - du, 0) * W;
-                };
-#pragma unroll
-                for (int col = 0; col < CG; ++col) {
-                    const int w = g + col * GA, vv = v0 + w;
-                    const cplx<T> hv = s_hs[vv];
-#pragma unroll
-                    for (int q = 0; q < RL; ++q) {
-                        const int u = j + q * (M / RL);
-                        // Padded columns (v > n) see an all-zero table entry and S = 0:
-                        // they evaluate to 0 and raise no flags.
-                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
-                        int sp, sm;
-                        s_off(u, sp, sm);
-                        cplx<T> bb = z[1 + col][q];
-                        y[b][2 * col][q] = cf.eval(col == 0 ? z[0][q].x : z[0][q].y, bb,
-                                                   s_srow[sp + w] + s_srow[sm + w], ph,
-#if GT_CF_PREFETCH
-                                                   col == 0 ? t0[q] :
-#endif
-                                                   cf.table(u, vv));
-                        y[b][2 * col + 1][q] = bb;
-                    }
-                    dftR<RL, +1, T>(y[b][2 * col]);
-                    dftR<RL, +1, T>(y[b][2 * col + 1]);
+                    z[b][1][q] = p.a;
+                    z[b][2][q] = p.b;
                 }
             }
             __syncthreads();
@@ -616,12 +573,36 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 const int id = threadIdx.x + b * NT;
                 if (UL % NT != 0 && id >= UL) break;
                 const int g = id % GA, j = id / GA;
+                stage_twiddle<T, M, false, K - 1, 3>(z[b], j, s_twf);
 #pragma unroll
-                for (int col = 0; col < CG; ++col)
+                for (int l = 0; l < 3; ++l) dftR<RL, -1, T>(z[b][l]);
+                // C_v + i C_v' = w^{u/2} Z[u]
+#pragma unroll
+                for (int q = 0; q < RL; ++q) z[b][0][q] = cmul<T>(s_hs[j + q * (M / RL)], z[b][0][q]);
+#pragma unroll
+                for (int col = 0; col < CG; ++col) {
+                    const int w = g + col * GA, vv = v0 + w;
+                    const cplx<T> hv = s_hs[vv];
+                    cplx<T> yr[2][RL];  // Y, R of this column
+#pragma unroll
+                    for (int q = 0; q < RL; ++q) {
+                        const int u = j + q * (M / RL);
+                        // S rows ip = min(c + du, n - 1), im = max(c - du, 0). Padded columns
+                        // (v > n) see an all-zero table entry and S = 0: they evaluate to 0.
+                        const int du = u <= M - u ? u : M - u;
+                        const int sp = min(c + du, n - 1) * W, sm = max(c - du, 0) * W;
+                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+                        cplx<T> bb = z[b][1 + col][q];
+                        yr[0][q] = cf.eval(col == 0 ? z[b][0][q].x : z[b][0][q].y, bb,
+                                           s_srow[sp + w] + s_srow[sm + w], ph, cf.table(u, vv));
+                        yr[1][q] = bb;
+                    }
+                    dftR<RL, +1, T>(yr[0]);
+                    dftR<RL, +1, T>(yr[1]);
 #pragma unroll
                     for (int r = 0; r < RL; ++r)
-                        st_pair(&tile[IL::template off<1>(j * RL, r, g + col * GA)],
-                                LinePair<T>{y[b][2 * col][r], y[b][2 * col + 1][r]});
+                        st_pair(&tile[IL::template off<1>(j * RL, r, w)], LinePair<T>{yr[0][r], yr[1][r]});
+                }
             }
             __syncthreads();
         }
