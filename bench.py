@@ -516,7 +516,7 @@ def run_b200(args, cfg):
     achieved = bps[dom] * B * args.steps / (pass_ms[dom] / 1e3) / 1e9
     peak, peak_src = peaks()
     # measured DRAM bytes of the dominant kernel (ncu --set full, committed under profiles/)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, fp32_util = None, None, None
     tf = ROOT / "profiles" / "r1_traffic.json"
     kname = ["mc_pass1w", "mc_pass2", "mc_pass3w"][dom] + f"<{'float' if es == 4 else 'double'}, {2 * n}>"
     if tf.exists():
@@ -524,6 +524,8 @@ def run_b200(args, cfg):
         if kname in tj["kernels"]:
             traffic = tj["kernels"][kname]["dram_bytes_per_pair"] * per_launch
             traffic_src = f"{kname}: {tj['source']} (scaled to {per_launch} pairs per launch)"
+            # the compute side of the same kernel (the path is SM-issue bound, not HBM bound)
+            fp32_util = tj["kernels"][kname].get("fp32")
     whole = survey_bytes_per_solve(n, es) * B / (ms / 1e3) / 1e9  # per GPU
 
     # end to end through the public host API: pinned host inputs, H2D + compute + D2H of per-pair results.
@@ -666,7 +668,8 @@ def run_b200(args, cfg):
                          "pass_ms_per_step": [x / args.steps for x in pass_ms[:3]],
                          "bytes_per_pair_per_pass": bps, "peak_source": peak_src,
                          "whole_solve_GBps_survey_model": whole,
-                         "whole_solve_frac_survey_model": whole / peak},
+                         "whole_solve_frac_survey_model": whole / peak,
+                         "fp32_pipe_ncu": fp32_util},
             "gpu_launches": int(kernels), "batch_calls": int(calls), "failed_pairs": failed,
             "fp64_residual_check": resid, "clocks": clk,
         }
