@@ -32,6 +32,7 @@
 #include "fft_tile.cuh"
 #include "col_pass.cuh"
 #include "fft_warp.cuh"
+#include "bulk_copy.cuh"
 #include "gt_device.h"
 
 namespace gtb {
@@ -743,9 +744,6 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
 #ifndef GT_W1
 #define GT_W1 16
 #endif
-#ifndef GT_P3_EARLY_NV
-#define GT_P3_EARLY_NV 1
-#endif
 #ifndef GT_W3
 #define GT_W3 8
 #endif
@@ -762,7 +760,18 @@ struct WarpMinBlocks {
     static constexpr int value = sizeof(T) == 8 ? 1 : CTAS;  // fp64 lines need 128 registers
 };
 
+// Per-warp TMA staging of pass 1's row inputs (P row, V row; N = P).
 template <typename T, int M>
+struct P1Stage {
+    static constexpr int n = M / 2;
+    static constexpr unsigned NB = n * sizeof(T), BYTES = 2 * NB;
+    static_assert(NB % 16 == 0, "bulk copy granularity");
+    static constexpr unsigned OFF =
+        ((M + n + WarpFFT<T, M>::TW1 + WARPS * WarpFFT<T, M>::SCRATCH) * sizeof(cplx<T>) + 127) / 128 * 128;
+    static constexpr size_t SMEM = OFF + WARPS * (BYTES + 8);
+};
+
+template <typename T, int M, bool TMA>
 __global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T, GT_W1_CTAS>::value)
 mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
           cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
@@ -778,18 +787,46 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
     T* st_l = reinterpret_cast<T*>(scr);
+    using SG = P1Stage<T, M>;
+    unsigned char* stage = smem_raw + SG::OFF + warp * SG::BYTES;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + SG::OFF + WARPS * SG::BYTES) + warp;
     for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
     for (int t = threadIdx.x; t < n; t += WARPS * 32) s_hs[t] = g_hs[t];
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS * 32);
+    const int stride = gridDim.x * WARPS, total = count * n;
+    auto request = [&](int item) {  // lane 0: the P and V rows of `item` into this warp's staging area
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        mbar_expect_tx(mbar, SG::BYTES);
+        bulk_g2s(stage, in.p(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+        bulk_g2s(stage + SG::NB, in.v(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+    };
+    if constexpr (TMA) {
+        if (lane == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        const int first = blockIdx.x * WARPS + warp;
+        if (lane == 0 && first < total) request(first);
+    }
     __syncthreads();
+    unsigned phase = 0;
 
-    for (int item = blockIdx.x * WARPS + warp; item < count * n; item += gridDim.x * WARPS) {
+    for (int item = blockIdx.x * WARPS + warp; item < total; item += stride) {
         const int s = item / n, x = item - s * n;
         const size_t sg = static_cast<size_t>(sample0) + s;
         const T* P_ = in.p(sg) + x * n;
         const T* N_ = in.nn(sg) + x * n;
         const T* V_ = in.v(sg) + x * n;
-        const bool n_is_p = in.N == in.P && in.sN == in.sP;
+        bool n_is_p = in.N == in.P && in.sN == in.sP;
+        if constexpr (TMA) {  // (the host selects TMA only when N = P)
+            P_ = reinterpret_cast<const T*>(stage);
+            V_ = reinterpret_cast<const T*>(stage + SG::NB);
+            n_is_p = true;
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        }
         T pv[E], nv[E], vv[E];
 #pragma unroll
         for (int t = 0; t < E; ++t) {
@@ -813,6 +850,14 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             part_l += lv[t];
             part_a += av[t];
             st_l[y] = lv[t];
+        }
+        if constexpr (TMA) {
+            // the staged rows are consumed: request the warp's next row
+            __syncwarp();
+            if (lane == 0 && item + stride < total) {
+                fence_proxy_async();
+                request(item + stride);
+            }
         }
         __syncwarp();
         // row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185)
@@ -863,13 +908,28 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     }
 }
 
+// Per-warp TMA staging of pass 3's row inputs: Y row, R row (hp complex each),
+// N row, V row (n reals each), contiguous in global memory per row.
 template <typename T, int M>
+struct P3Stage {
+    static constexpr int n = M / 2, hp = MCGeom<T, M>::hp;
+    static constexpr unsigned YB = hp * sizeof(cplx<T>), NB = n * sizeof(T);
+    static constexpr unsigned BYTES = 2 * YB + 2 * NB;  // per warp; every segment a multiple of 16 B
+    // staging offset in pass 3's shared memory: after the twiddles and the warps' scratch
+    static constexpr unsigned OFF =
+        ((M + WarpFFT<T, M>::TW1 + WARPS3 * WarpFFT<T, M>::SCRATCH) * sizeof(cplx<T>) + 127) / 128 * 128;
+    static constexpr size_t SMEM = OFF + WARPS3 * (BYTES + 8);
+    static_assert(YB % 16 == 0 && NB % 16 == 0, "bulk copy granularity");
+};
+
+template <typename T, int M, bool TMA>
 __global__ void __launch_bounds__(WARPS3 * 32, WarpMinBlocks<T, GT_W3_CTAS>::value)
 mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
           const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
           const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
     using Gm = MCGeom<T, M>;
     using WF = WarpFFT<T, M>;
+    using SG = P3Stage<T, M>;
     constexpr int n = Gm::n, c = Gm::c, hp = Gm::hp, P = WF::P;
     constexpr int E = n / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -877,29 +937,63 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx<T>* s_tw1 = s_tw + M;
     cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
+    // TMA: [WARPS3][SG::BYTES] staging after the scratch, then one mbarrier per warp
+    unsigned char* stage = smem_raw + SG::OFF + warp * SG::BYTES;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (WARPS3 - warp) * SG::BYTES) + warp;
     for (int t = threadIdx.x; t < M; t += WARPS3 * 32) s_tw[t] = g_tw[t];
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS3 * 32);
-    __syncthreads();
-    const T inv = T(1.0 / (double(M) * double(M)));
-
-    for (int item = blockIdx.x * WARPS3 + warp; item < count * n; item += gridDim.x * WARPS3) {
+    const int stride = gridDim.x * WARPS3, total = count * n;
+    // lane 0 requests the four row segments of `item` into this warp's staging area
+    auto request = [&](int item) {
         const int s = item / n, x = item - s * n;
         const size_t sg = static_cast<size_t>(sample0) + s;
-        const cplx<T>* Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
-        const cplx<T>* R_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
-#if GT_P3_EARLY_NV
+        const size_t so = (static_cast<size_t>(s) * n + x) * hp;
+        mbar_expect_tx(mbar, SG::BYTES);
+        bulk_g2s(stage, Aspec + so, SG::YB, mbar);
+        bulk_g2s(stage + SG::YB, Bspec + so, SG::YB, mbar);
+        bulk_g2s(stage + 2 * SG::YB, in.nn(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+        bulk_g2s(stage + 2 * SG::YB + SG::NB, in.v(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+    };
+    if constexpr (TMA) {
+        if (lane == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        const int first = blockIdx.x * WARPS3 + warp;
+        if (lane == 0 && first < total) request(first);
+    }
+    __syncthreads();
+    const T inv = T(1.0 / (double(M) * double(M)));
+    unsigned phase = 0;
+
+    for (int item = blockIdx.x * WARPS3 + warp; item < total; item += stride) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const cplx<T>* Y_x;
+        const cplx<T>* R_x;
+        const T* N_;
+        const T* V_;
+        if constexpr (TMA) {
+            Y_x = reinterpret_cast<const cplx<T>*>(stage);
+            R_x = reinterpret_cast<const cplx<T>*>(stage + SG::YB);
+            N_ = reinterpret_cast<const T*>(stage + 2 * SG::YB);
+            V_ = reinterpret_cast<const T*>(stage + 2 * SG::YB + SG::NB);
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        } else {
+            Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
+            R_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+            N_ = in.nn(sg) + x * n;
+            V_ = in.v(sg) + x * n;
+        }
         // epilogue inputs requested up front (one exposed round trip per row)
         T nv[E], vv[E];
-        {
-            const T* N_ = in.nn(sg) + x * n;
-            const T* V_ = in.v(sg) + x * n;
 #pragma unroll
-            for (int t = 0; t < E; ++t) {
-                nv[t] = N_[lane + 32 * t];
-                vv[t] = V_[lane + 32 * t];
-            }
+        for (int t = 0; t < E; ++t) {
+            nv[t] = N_[lane + 32 * t];
+            vv[t] = V_[lane + 32 * t];
         }
-#endif
         // Z = Y + i R over the full line from the Hermitian half spectra
         cplx<T> z[P];
 #pragma unroll
@@ -913,27 +1007,23 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
                 z[k] = mk<T>(y.x - r.y, y.y + r.x);
             else
                 z[k] = mk<T>(y.x + r.y, r.x - y.y);
-#if !GT_P3_EARLY_NV
-            // bound the loads in flight (register pressure): fence every 4 lines of the row
-            if ((k & 3) == 3) asm volatile("" ::: "memory");
-#endif
         }
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
         const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
         const T mu_t = T(mu_s);
-        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
-#if !GT_P3_EARLY_NV
-        const T* N_ = in.nn(sg) + x * n;
-        const T* V_ = in.v(sg) + x * n;
-        asm volatile("" ::: "memory");  // keep the epilogue loads below the transform (registers)
-        T nv[E], vv[E];
+        T pvs[E];  // p_var * sum(applied) * rand_scale: consumes the staged N, V rows
 #pragma unroll
-        for (int t = 0; t < E; ++t) {
-            nv[t] = N_[lane + 32 * t];
-            vv[t] = V_[lane + 32 * t];
+        for (int t = 0; t < E; ++t) pvs[t] = (in.nom_scale * nv[t] * vv[t] - mu_t) * scale;
+        if constexpr (TMA) {
+            // the staging area is free once every lane has consumed it: request the next row
+            __syncwarp();
+            if (lane == 0 && item + stride < total) {
+                fence_proxy_async();
+                request(item + stride);
+            }
         }
-#endif
+        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
         __syncwarp();
 #pragma unroll
         for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
@@ -946,8 +1036,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
             const int f = lane + 32 * t;
             const T yd = scr[f].x * inv;
             const T rd = scr[(f - c) & (M - 1)].y * inv;
-            const T pvar = in.nom_scale * nv[t] * vv[t] - mu_t;
-            T tt = yd + rd * pvar * scale;
+            T tt = yd + rd * pvs[t];
             if (!finite_(tt)) bad = GTD_ST_NONFINITE;
             tt = tt > T(0) ? tt : T(0);
             if (O_x) O_x[f] = tt;
@@ -991,15 +1080,17 @@ struct MCLaunch {
                sizeof(T) * Gm::n * Gm::W;
     }
     static size_t smem3() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
-    static size_t smemw() {
+    static size_t smemw(bool tma) {
         if constexpr (use_warp_rows<T, M>())
-            return sizeof(cplx<T>) * (M + M / 2 + WarpFFT<T, M>::TW1 + WARPS * WarpFFT<T, M>::SCRATCH);
+            return tma ? P1Stage<T, M>::SMEM
+                       : sizeof(cplx<T>) * (M + M / 2 + WarpFFT<T, M>::TW1 + WARPS * WarpFFT<T, M>::SCRATCH);
         else
             return 0;
     }
-    static size_t smemw3() {
+    static size_t smemw3(bool tma) {
         if constexpr (use_warp_rows<T, M>())
-            return sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + WARPS3 * WarpFFT<T, M>::SCRATCH);
+            return tma ? P3Stage<T, M>::SMEM
+                       : sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + WARPS3 * WarpFFT<T, M>::SCRATCH);
         else
             return 0;
     }
@@ -1019,10 +1110,18 @@ struct MCLaunch {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, Gm::NT2, smem2());
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3<T, M>, NT, smem3());
             if constexpr (use_warp_rows<T, M>()) {
-                cudaFuncSetAttribute(mc_pass1w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw()));
-                cudaFuncSetAttribute(mc_pass3w<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemw3()));
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1w<T, M>, WARPS * 32, smemw());
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3w<T, M>, WARPS3 * 32, smemw3());
+                cudaFuncSetAttribute(mc_pass1w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smemw(false)));
+                cudaFuncSetAttribute(mc_pass1w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smemw(true)));
+                cudaFuncSetAttribute(mc_pass3w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smemw3(false)));
+                cudaFuncSetAttribute(mc_pass3w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smemw3(true)));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], mc_pass1w<T, M, true>, WARPS * 32,
+                                                              smemw(true));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], mc_pass3w<T, M, true>, WARPS3 * 32,
+                                                              smemw3(true));
             }
             int dev = 0;
             cudaGetDevice(&dev);
@@ -1056,6 +1155,17 @@ struct MCLaunch {
             const int rr = cpsm > 0 && cpsm < r ? cpsm : r;
             return items < sms * rr ? items : sms * rr;
         };
+        // TMA row staging in pass 3 needs 16-byte aligned N / V rows (the spectra always are)
+        auto al16 = [](const void* p, long long stride_elems) {
+            return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((stride_elems * sizeof(T)) % 16 == 0);
+        };
+#ifndef GT_P3_TMA
+#define GT_P3_TMA 1
+#endif
+        const bool tma3 = GT_P3_TMA && al16(in.N, in.sN) && al16(in.V, in.sV) && (n * sizeof(T)) % 16 == 0;
+        // pass 1 stages P and V rows and takes N = P (the Monte-Carlo entries' nominal leakage map)
+        const bool tma1 = GT_P3_TMA && in.N == in.P && in.sN == in.sP && al16(in.P, in.sP) && al16(in.V, in.sV) &&
+                          (n * sizeof(T)) % 16 == 0;
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
         if (slots == 2) {
             cudaEventRecord(ev_fork, st);
@@ -1074,8 +1184,14 @@ struct MCLaunch {
             T* Ar = S + per * sub;                           // real DCT part of A (pass 1 -> 2)
             if (mk_) mk_(ctx, 0, ss);
             if constexpr (use_warp_rows<T, M>())
-                mc_pass1w<T, M><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(), ss>>>(
-                    in, s0, cnt, Ar, B, S, stats, tw, hs, var_lo, var_hi);
+            {
+                if (tma1)
+                    mc_pass1w<T, M, true><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(true), ss>>>(
+                        in, s0, cnt, Ar, B, S, stats, tw, hs, var_lo, var_hi);
+                else
+                    mc_pass1w<T, M, false><<<grid((cnt * n + WARPS - 1) / WARPS, res[0]), WARPS * 32, smemw(false),
+                                             ss>>>(in, s0, cnt, Ar, B, S, stats, tw, hs, var_lo, var_hi);
+            }
             else
                 mc_pass1<T, M><<<grid(cnt * RB, res[0]), NT, smem1(), ss>>>(in, s0, cnt, Ar, B, S, stats, tw, hs,
                                                                              var_lo, var_hi);
@@ -1085,8 +1201,16 @@ struct MCLaunch {
                 o->mu_per_sample, T(g->mu_fixed));
             if (mk_) mk_(ctx, 2, ss);
             if constexpr (use_warp_rows<T, M>())
-                mc_pass3w<T, M><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32, smemw3(), ss>>>(
-                    in, s0, cnt, A, B, stats, tw, out, T(g->rand_scale), o->with_rand);
+            {
+                if (tma3)
+                    mc_pass3w<T, M, true><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32,
+                                            smemw3(true), ss>>>(in, s0, cnt, A, B, stats, tw, out,
+                                                                T(g->rand_scale), o->with_rand);
+                else
+                    mc_pass3w<T, M, false><<<grid((cnt * n + WARPS3 - 1) / WARPS3, res[2]), WARPS3 * 32,
+                                             smemw3(false), ss>>>(in, s0, cnt, A, B, stats, tw, out,
+                                                                  T(g->rand_scale), o->with_rand);
+            }
             else
                 mc_pass3<T, M><<<grid(cnt * RB, res[2]), NT, smem3(), ss>>>(in, s0, cnt, A, B, stats, tw, out,
                                                                              T(g->rand_scale), o->with_rand);
