@@ -484,7 +484,7 @@ def run_b200(args, cfg):
     e1.record(stream)
     torch.cuda.synchronize()
     pass_ms, kernels, calls = dg.profile_end()
-    per_launch = min(B, args.chunk or 1024)  # pairs per pass launch (the library's auto chunk is 1024)
+    per_launch = min(B, args.chunk or 4096)  # pairs per pass launch (the library's auto chunk is up to 4096)
     if ws > 1:
         dist.barrier()
     ms_local = e0.elapsed_time(e1) / args.steps

@@ -86,7 +86,7 @@ gtd_mc_opts to_dev_opts(const gt_batch_opts* o) {
 }
 
 // Scratch budget of the automatic chunking: 40% of the device's free memory,
-// within [1.5 GiB, 32 GiB] (a 1024-sample chunk at n = 256 needs ~1.6 GB; at
+// within [1.5 GiB, 32 GiB] (a 4096-sample chunk at n = 256 needs ~6.6 GB; at
 // n = 1024 a sample alone needs ~25 MB fp32 / ~50 MB fp64).
 size_t scratch_budget() {
     size_t fr = 0, tot = 0;
@@ -99,10 +99,11 @@ int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1
     if (o && o->chunk > 0) return std::min(o->chunk, batch);
     // Large chunks win: the passes are SM-issue bound, not HBM bound (a sweep of
     // 24..4096 pairs per chunk on B200 went 232k -> 325k solves/s; L2 residency
-    // of the intermediates at <= 48 MB bought nothing), and a chunk that leaves a
-    // small remainder runs that tail at low occupancy.
+    // of the intermediates at <= 48 MB bought nothing), every launch ends in a
+    // partly idle tail (config 1 at 4096 vs 1024 pairs per chunk: +1.7%), and a
+    // chunk that leaves a small remainder runs that tail at low occupancy.
     const size_t per = gtd_mc_scratch_bytes_per_sample(n, fp64);
-    int c = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, scratch_budget() / share / per)));
+    int c = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4096, scratch_budget() / share / per)));
     return std::min(c, batch);
 }
 
