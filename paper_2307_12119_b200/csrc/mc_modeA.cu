@@ -109,6 +109,19 @@ __device__ __forceinline__ bool finite_(T v) {
 }
 
 template <typename T>
+struct BitsOf;
+template <>
+struct BitsOf<float> {
+    using U = unsigned;
+    __device__ __forceinline__ static U get(float v) { return __float_as_uint(v); }
+};
+template <>
+struct BitsOf<double> {
+    using U = unsigned long long;
+    __device__ __forceinline__ static U get(double v) { return static_cast<U>(__double_as_longlong(v)); }
+};
+
+template <typename T>
 struct MCIn {
     const T* P;
     const T* N;
@@ -786,7 +799,6 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     cplx<T>* s_tw1 = s_hs + n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
-    T* st_l = reinterpret_cast<T*>(scr);
     using SG = P1Stage<T, M>;
     unsigned char* stage = smem_raw + SG::OFF + warp * SG::BYTES;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + SG::OFF + WARPS * SG::BYTES) + warp;
@@ -838,19 +850,30 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
         T part_l = T(0), part_a = T(0);
         int bad = 0;
         T av[E], lv[E];  // applied / leakage row, element lane + 32 t
+        // Input checks on bit patterns, one integer min / max per value: a finite
+        // non-negative power has bits <= max-finite (-0.0 and anything else above
+        // that take the exact check below); 0 < var_lo <= var <= var_hi is an
+        // interval of bit patterns (negatives and NaNs fall outside it).
+        using U = typename BitsOf<T>::U;
+        U pmax = 0, vmin = ~U(0), vmax = 0;
 #pragma unroll
         for (int t = 0; t < E; ++t) {
-            const int y = lane + 32 * t;
-            // NaN fails both compares, +-inf fails one: same verdict as !(x >= 0) || !isfinite(x)
-            if (!(pv[t] >= T(0) && pv[t] <= Real<T>::max()) || !(nv[t] >= T(0) && nv[t] <= Real<T>::max()))
-                bad |= GTD_ST_BAD_POWER;
-            if (!(vv[t] >= var_lo && vv[t] <= var_hi)) bad |= GTD_ST_BAD_VAR;
+            pmax = max(pmax, BitsOf<T>::get(pv[t]));
+            if (!n_is_p) pmax = max(pmax, BitsOf<T>::get(nv[t]));
+            vmin = min(vmin, BitsOf<T>::get(vv[t]));
+            vmax = max(vmax, BitsOf<T>::get(vv[t]));
             lv[t] = in.nom_scale * nv[t] * vv[t];
             av[t] = pv[t] + lv[t];
             part_l += lv[t];
             part_a += av[t];
-            st_l[y] = lv[t];
         }
+        if (pmax > BitsOf<T>::get(Real<T>::max())) {
+#pragma unroll
+            for (int t = 0; t < E; ++t)  // NaN fails both compares, +-inf one: !(x >= 0) || !isfinite(x)
+                if (!(pv[t] >= T(0) && pv[t] <= Real<T>::max()) || !(nv[t] >= T(0) && nv[t] <= Real<T>::max()))
+                    bad |= GTD_ST_BAD_POWER;
+        }
+        if (vmin < BitsOf<T>::get(var_lo) || vmax > BitsOf<T>::get(var_hi)) bad |= GTD_ST_BAD_VAR;
         if constexpr (TMA) {
             // the staged rows are consumed: request the warp's next row
             __syncwarp();
@@ -859,13 +882,25 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
                 request(item + stride);
             }
         }
-        __syncwarp();
-        // row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185)
-        T* Srow_x = Srow + (static_cast<size_t>(s) * n + x) * hp;
-        for (int v = lane; v < hp; v += 32) {
-            T val = T(0);
-            if (v < h) val = st_l[min(c + v, n - 1)] + st_l[max(c - v, 0)];
-            Srow_x[v] = val;
+        // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185):
+        // S[dv] = L[min(c + dv, n - 1)] + L[max(c - dv, 0)], c = 16 E. For dv = lane + 32 k < c,
+        // L[c + dv] is this lane's lv[E/2 + k] and L[c - dv] is lane 32 - lane's lv[E/2 - 1 - k]
+        // (lane 0: its own lv[E/2 - k]); for dv >= c both indices clamp: L[n - 1] + L[0].
+        {
+            T* Srow_x = Srow + (static_cast<size_t>(s) * n + x) * hp;
+            const T cst = __shfl_sync(0xffffffffu, lv[E - 1], 31) + __shfl_sync(0xffffffffu, lv[0], 0);
+#pragma unroll
+            for (int k = 0; k < (hp + 31) / 32; ++k) {
+                const int v = lane + 32 * k;
+                T val;
+                if (k < E / 2) {
+                    const T mir = __shfl_sync(0xffffffffu, lv[k < E / 2 ? E / 2 - 1 - k : 0], (32 - lane) & 31);
+                    val = lv[k < E / 2 ? E / 2 + k : 0] + (lane == 0 ? lv[k < E / 2 ? E / 2 - k : 0] : mir);
+                } else {
+                    val = v < h ? cst : T(0);
+                }
+                if (v < hp) Srow_x[v] = val;
+            }
         }
         // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k,
         // from registers: mirror(i) = M-1-i = (31 - lane) + 32 (P-1-k) for k >= E
