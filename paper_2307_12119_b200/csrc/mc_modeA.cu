@@ -60,6 +60,13 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T warp_max_t(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 // Sum of `v` over the CTA, result valid in thread 0. `red` >= 32 doubles.
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -1080,7 +1087,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
         }
         or_flags(&stats[sg].status, bad);
         const double ts = warp_sum(double(part));
-        const double tm = warp_max(double(mxt));
+        const double tm = double(warp_max_t(mxt));  // max is exact in T
         if (lane == 0) {
             atomicAdd(&stats[sg].sum_rise, ts);
             atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
