@@ -148,10 +148,13 @@ struct MCGeom {
     static constexpr int h = n + 1;
     static constexpr int L = G::L;
     static constexpr int NT = G::NT;
+    // fp32 at M = 2048: 4 columns per pass-2 tile (one 512-thread CTA per SM; the
+    // default 2 give 8-16-byte row segments and 8 warps per SM: +4.5% for config 2)
+    static constexpr bool WIDE2048 = M == 2048 && sizeof(T) == 4;
 #ifdef GT_P2_W
     static constexpr int W = M >= 512 ? GT_P2_W : L / 2;  // pass-2 tile width (tuning override)
 #else
-    static constexpr int W = L / 2;  // columns per pass-2 tile
+    static constexpr int W = WIDE2048 ? 4 : L / 2;  // columns per pass-2 tile
 #endif
     static constexpr int hp = ((h + W - 1) / W) * W;
     static constexpr int LP = L + 2;  // padded pitch for row tiles (transposing I/O; even for pairs)
@@ -167,7 +170,8 @@ struct MCGeom {
 #ifndef GT_P2_CTAS
 #define GT_P2_CTAS 2
 #endif
-    static constexpr int NT2 = (M / 8) * W > GT_P2_NT ? GT_P2_NT : (M / 8) * W;
+    static constexpr int NT2C = WIDE2048 ? 512 : GT_P2_NT;
+    static constexpr int NT2 = (M / 8) * W > NT2C ? NT2C : (M / 8) * W;
     static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
     // pass 2 holds three lines per thread-butterfly: 128 registers (fp32) / 255 (fp64)
 #ifdef GT_P2_MINB
