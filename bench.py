@@ -469,6 +469,12 @@ def run_b200(args, cfg):
 
     clocks = ClockSampler(local)
     torch.cuda.synchronize()
+    # untimed clock ramp before the W warm-up steps: on a freshly idle GPU the first
+    # ~0.5 s of load can run below the boost clock (a W = 3 warm-up is ~25 ms here)
+    t_ramp = time.time()
+    while time.time() - t_ramp < 1.0:
+        step()
+        torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

@@ -79,6 +79,61 @@ __device__ __forceinline__ cplx<T> mul_si(cplx<T> a) {
     return SIGN < 0 ? mk<T>(a.y, -a.x) : mk<T>(-a.y, a.x);
 }
 
+// ---- packed FP32 (sm_100 FADD2 / FMUL2 / FFMA2): a complex float is one
+// register pair, so every complex add is ONE instruction and a complex multiply
+// three; the SASS operand swizzle (.F32x2.LO_HI) and scalar broadcast (.F32)
+// make the +-i rotations and the real scalings free inside an FFMA2. The
+// arithmetic is the scalar one (IEEE round-to-nearest per lane); only the
+// contraction of a complex multiply into FMA differs from the scalar path.
+// Off by default; a translation unit opts in by defining GT_PACKED_F32 1 before
+// including this header (mc_rows.cu: the warp row passes gain; the latency-bound
+// column pass measured slower and stays scalar).
+#ifndef GT_PACKED_F32
+#define GT_PACKED_F32 0
+#endif
+#if GT_PACKED_F32
+template <>
+__device__ __forceinline__ float2 cadd<float>(float2 a, float2 b) {
+    return __fadd2_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float2 csub<float>(float2 a, float2 b) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+// a b = (ax, ay) bx + (ay, ax) (-by, by): the pair (-by, by) is one FMUL2 of a
+// broadcast, shared by every line a twiddle multiplies (common subexpression).
+template <>
+__device__ __forceinline__ float2 cmul<float>(float2 a, float2 b) {
+    const float2 bn = __fmul2_rn(make_float2(b.y, b.y), make_float2(-1.0f, 1.0f));
+    return __ffma2_rn(make_float2(a.y, a.x), bn, __fmul2_rn(a, make_float2(b.x, b.x)));
+}
+template <>
+__device__ __forceinline__ float2 cscale<float>(float2 a, float s) {
+    return __fmul2_rn(a, make_float2(s, s));
+}
+#endif
+
+// a + s (SIGN i) d  (SIGN = -1: -i d = (d.y, -d.x); +1: i d = (-d.y, d.x))
+template <int SIGN, typename T>
+__device__ __forceinline__ cplx<T> add_rot(cplx<T> a, cplx<T> d, T s) {
+#if GT_PACKED_F32
+    if constexpr (sizeof(T) == 4)
+        return __ffma2_rn(make_float2(d.y, d.x), SIGN < 0 ? make_float2(s, -s) : make_float2(-s, s), a);
+    else
+#endif
+        return SIGN < 0 ? mk<T>(a.x + s * d.y, a.y - s * d.x) : mk<T>(a.x - s * d.y, a.y + s * d.x);
+}
+// p + s S (complex by real)
+template <typename T>
+__device__ __forceinline__ cplx<T> add_scaled(cplx<T> p, cplx<T> S, T s) {
+#if GT_PACKED_F32
+    if constexpr (sizeof(T) == 4)
+        return __ffma2_rn(S, make_float2(s, s), p);
+    else
+#endif
+        return mk<T>(fma(s, S.x, p.x), fma(s, S.y, p.y));
+}
+
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
 // ---------------------------------------------------------------- butterflies
@@ -92,11 +147,11 @@ __device__ __forceinline__ void dft2(cplx<T>* v) {
 template <int SIGN, typename T>
 __device__ __forceinline__ void dft4(cplx<T>* v) {
     cplx<T> a0 = cadd<T>(v[0], v[2]), a1 = csub<T>(v[0], v[2]);
-    cplx<T> b0 = cadd<T>(v[1], v[3]), b1 = mul_si<SIGN, T>(csub<T>(v[1], v[3]));
+    cplx<T> b0 = cadd<T>(v[1], v[3]), d = csub<T>(v[1], v[3]);
     v[0] = cadd<T>(a0, b0);
     v[2] = csub<T>(a0, b0);
-    v[1] = cadd<T>(a1, b1);
-    v[3] = csub<T>(a1, b1);
+    v[1] = add_rot<SIGN, T>(a1, d, T(1));   // a1 + (SIGN i) d
+    v[3] = add_rot<SIGN, T>(a1, d, T(-1));  // a1 - (SIGN i) d
 }
 
 // Odd half of the radix-8 DIF butterfly: a4..a7 are the differences v[k] - v[k+4];
@@ -106,16 +161,15 @@ template <int SIGN, typename T>
 __device__ __forceinline__ void dft8_odd(cplx<T> a4, cplx<T> a5, cplx<T> a6, cplx<T> a7, cplx<T>& o0, cplx<T>& o1,
                                          cplx<T>& o2, cplx<T>& o3) {
     const T r = T(0.70710678118654752440084436210485);
-    // unscaled W8^1 a5 and W8^3 a7
-    const cplx<T> A5 = SIGN < 0 ? mk<T>(a5.x + a5.y, a5.y - a5.x) : mk<T>(a5.x - a5.y, a5.y + a5.x);
-    const cplx<T> A7 = SIGN < 0 ? mk<T>(a7.y - a7.x, -(a7.x + a7.y)) : mk<T>(-(a7.x + a7.y), a7.x - a7.y);
-    a6 = mul_si<SIGN, T>(a6);
-    const cplx<T> p0 = cadd<T>(a4, a6), p1 = csub<T>(a4, a6);
-    const cplx<T> S = cadd<T>(A5, A7), D = mul_si<SIGN, T>(csub<T>(A5, A7));
-    o0 = mk<T>(fma(r, S.x, p0.x), fma(r, S.y, p0.y));
-    o2 = mk<T>(fma(-r, S.x, p0.x), fma(-r, S.y, p0.y));
-    o1 = mk<T>(fma(r, D.x, p1.x), fma(r, D.y, p1.y));
-    o3 = mk<T>(fma(-r, D.x, p1.x), fma(-r, D.y, p1.y));
+    // unscaled W8^1 a5 = (1 + SIGN i) a5 and W8^3 a7 = (-1 + SIGN i) a7
+    const cplx<T> A5 = add_rot<SIGN, T>(a5, a5, T(1));
+    const cplx<T> A7 = add_rot<SIGN, T>(mk<T>(-a7.x, -a7.y), a7, T(1));
+    const cplx<T> p0 = add_rot<SIGN, T>(a4, a6, T(1)), p1 = add_rot<SIGN, T>(a4, a6, T(-1));  // a4 +- (SIGN i) a6
+    const cplx<T> S = cadd<T>(A5, A7), Dd = csub<T>(A5, A7);  // D = (SIGN i) Dd
+    o0 = add_scaled<T>(p0, S, r);
+    o2 = add_scaled<T>(p0, S, -r);
+    o1 = add_rot<SIGN, T>(p1, Dd, r);
+    o3 = add_rot<SIGN, T>(p1, Dd, -r);
 }
 
 template <int SIGN, typename T>

@@ -1,0 +1,612 @@
+// mc_rows.cu — mode-A row passes (pass 1: row transforms of the applied and
+// leakage maps; pass 3: inverse row transforms and the epilogue), see
+// mc_modeA.cu for the algorithm. This translation unit uses the packed FP32
+// complex arithmetic of fft_tile.cuh (sm_100 FADD2 / FMUL2 / FFMA2): the warp
+// row FFTs run 32 warps per SM and gain from the halved instruction count
+// (pass 1 -2.4%, pass 3 -5%), while the column pass, at 16 warps per SM and
+// latency bound, measured 7% slower with it and stays scalar.
+#define GT_PACKED_F32 1
+#include "mc_common.cuh"
+
+namespace gtb {
+
+// ------------------------------------------------------------------ pass 1
+// The applied map enters the row transform mirror-padded, so its half spectrum
+// is A[v] = w^{-v/2} At[v] with At real (the DCT-II of the row; w = e^{-2 pi i/M}).
+// Pass 1 stores only At = Re(w^{v/2} A), A = (Z[v] + conj Z[M-v]) / 2, with
+// hs[v] = w^{v/2}; At[n] = 0 exactly.
+
+// Persistent over (sample, block of L die rows). Each die row x becomes one
+// complex line z = mirror(applied row) + i * centre-embedded(p_leak0 row).
+template <typename T, int M>
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+mc_pass1(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
+         cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
+         const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T var_lo, T var_hi) {
+    using Gm = MCGeom<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
+    constexpr int hp = Gm::hp;
+    constexpr int RB = (n + L - 1) / L;
+    constexpr int EPT = (L * n + NT - 1) / NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* tileT = reinterpret_cast<T*>(tile);
+    cplx<T>* s_tw = tile + M * LP;
+    double* red = reinterpret_cast<double*>(s_tw + M);
+
+    load_twiddles<T, M, NT>(s_tw, g_tw);
+    for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
+        const int s = item / RB;
+        const int x0 = (item - s * RB) * L;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const T* P = in.p(sg);
+        const T* Nm = in.nn(sg);
+        const T* V = in.v(sg);
+        const bool n_is_p = Nm == P;
+
+        // imaginary part outside the centre embedding is zero
+        for (int idx = threadIdx.x; idx < (M - 2 * c) * L; idx += NT) {
+            const int l = idx % L, j = c + idx / L;
+            tileT[2 * (j * LP + l) + 1] = T(0);
+        }
+        T pv[EPT], nv[EPT], vv[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, y = idx - l * n, x = x0 + l;
+            pv[k] = nv[k] = T(0);
+            vv[k] = T(1);
+            if (idx < L * n && x < n) {
+                pv[k] = P[x * n + y];
+                nv[k] = n_is_p ? pv[k] : Nm[x * n + y];
+                vv[k] = V[x * n + y];
+            }
+        }
+        T part_l = T(0), part_a = T(0);  // per-thread partials (<= EPT terms), fp64 across threads
+        int bad = 0;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= L * n) break;
+            const int l = idx / n, y = idx - l * n;
+            const T p = pv[k], nm = nv[k], vr = vv[k];
+            if (!(p >= T(0)) || !finite_(p) || !(nm >= T(0)) || !finite_(nm)) bad |= GTD_ST_BAD_POWER;
+            if (!(vr >= var_lo && vr <= var_hi)) bad |= GTD_ST_BAD_VAR;
+            const T lk = in.nom_scale * nm * vr;
+            const T a = p + lk;
+            part_l += lk;
+            part_a += a;
+            tileT[2 * (y * LP + l)] = a;
+            tileT[2 * ((M - 1 - y) * LP + l)] = a;
+            tileT[2 * (((y - c) & (M - 1)) * LP + l) + 1] = lk;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double tl = block_sum<NT>(double(part_l), red);  // (contains the barrier for the tile)
+        const double ta = block_sum<NT>(double(part_a), red);
+        if (threadIdx.x == 0) {
+            atomicAdd(&stats[sg].sum_leak, tl);
+            atomicAdd(&stats[sg].sum_applied, ta);
+        }
+        // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185),
+        // read back from the embedded imaginary part: p_leak0(l, y) at j = (y - c) mod M.
+        for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+            const int l = idx / hp, dv = idx - l * hp;
+            const int x = x0 + l;
+            if (x >= n) continue;
+            T v = T(0);
+            if (dv < h) {
+                const int jp = min(c + dv, n - 1), jm = max(c - dv, 0);
+                v = tileT[2 * (((jp - c) & (M - 1)) * LP + l) + 1] + tileT[2 * (((jm - c) & (M - 1)) * LP + l) + 1];
+            }
+            Srow[(static_cast<size_t>(s) * n + x) * hp + dv] = v;
+        }
+        __syncthreads();
+        tile_fft<T, M, L, LP, NT, -1>(tile, s_tw);
+
+        // Split Z into the two real-input half spectra and store rows.
+        for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
+            const int l = idx / hp, v = idx - l * hp;
+            const int x = x0 + l;
+            if (x >= n) continue;
+            T Ar = T(0);
+            cplx<T> B = mk<T>(T(0), T(0));
+            if (v < h) {
+                const cplx<T> Z = tile[v * LP + l];
+                const cplx<T> Zc = cconj<T>(tile[((M - v) & (M - 1)) * LP + l]);
+                if (v < n) Ar = dct_part<T>(Z, Zc, g_hs[v]);
+                const T dx = Z.x - Zc.x, dy = Z.y - Zc.y;
+                B = mk<T>(T(0.5) * dy, T(-0.5) * dx);
+            }
+            const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+            Areal[o] = Ar;
+            Bspec[o] = B;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ pass 3
+template <typename T, int M>
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
+         const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
+         const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
+    using Gm = MCGeom<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT;
+    constexpr int hp = Gm::hp;
+    constexpr int RB = (n + L - 1) / L;
+    constexpr int EPT = (L * h + NT - 1) / NT;
+    constexpr int EPO = (L * n + NT - 1) / NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + M * LP;
+    double* red = reinterpret_cast<double*>(s_tw + M);
+
+    load_twiddles<T, M, NT>(s_tw, g_tw);
+    for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
+        const int s = item / RB;
+        const int x0 = (item - s * RB) * L;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+
+        cplx<T> yv[EPT], rv[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / h, v = idx - l * h, x = x0 + l;
+            yv[k] = rv[k] = mk<T>(T(0), T(0));
+            if (idx < L * h && x < n) {
+                const size_t o = (static_cast<size_t>(s) * n + x) * hp + v;
+                yv[k] = Aspec[o];
+                rv[k] = Bspec[o];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= L * h) break;
+            const int l = idx / h, v = idx - l * h;
+            const cplx<T> y = yv[k], r = rv[k];
+            if (v == 0 || v == n) {
+                tile[v * LP + l] = mk<T>(y.x, r.x);
+            } else {
+                tile[v * LP + l] = mk<T>(y.x - r.y, y.y + r.x);
+                tile[(M - v) * LP + l] = mk<T>(y.x + r.y, r.x - y.y);
+            }
+        }
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T inv = T(1.0 / (double(M) * double(M)));
+        const T* Nm = in.nn(sg);
+        const T* V = in.v(sg);
+        __syncthreads();
+        tile_fft<T, M, L, LP, NT, +1>(tile, s_tw);
+        T nv[EPO], vv[EPO];
+#pragma unroll
+        for (int k = 0; k < EPO; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, j = idx - l * n, x = x0 + l;
+            nv[k] = vv[k] = T(0);
+            if (idx < L * n && x < n) {
+                nv[k] = Nm[x * n + j];
+                vv[k] = V[x * n + j];
+            }
+        }
+
+        T part_t = T(0), mxt = T(0);
+        int bad = 0;
+        const T mu_t = T(mu_s);
+#pragma unroll
+        for (int k = 0; k < EPO; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            const int l = idx / n, j = idx - l * n, x = x0 + l;
+            if (idx >= L * n || x >= n) continue;
+            const T yd = tile[j * LP + l].x * inv;
+            const int jr = (j - c) & (M - 1);
+            const T rd = tile[jr * LP + l].y * inv;
+            const T pvar = in.nom_scale * nv[k] * vv[k] - mu_t;
+            T t = yd + rd * pvar * scale;
+            if (!finite_(t)) bad = GTD_ST_NONFINITE;
+            t = t > T(0) ? t : T(0);
+            if (out) out[(sg * n + x) * n + j] = t;
+            part_t += t;
+            mxt = mxt > t ? mxt : t;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double ts = block_sum<NT>(double(part_t), red);
+        const double tm = block_max<NT>(double(mxt), red);
+        if (threadIdx.x == 0) {
+            atomicAdd(&stats[sg].sum_rise, ts);
+            atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
+            if (x0 == 0) stats[sg].mu = mu_s;
+        }
+    }
+}
+
+template <typename T, int M, bool TMA>
+__global__ void __launch_bounds__(WARPS * 32, WarpMinBlocks<T, GT_W1_CTAS>::value)
+mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
+          cplx<T>* __restrict__ Bspec, T* __restrict__ Srow, gtd_sample_stats* __restrict__ stats,
+          const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T var_lo, T var_hi) {
+    using Gm = MCGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, h = Gm::h, hp = Gm::hp, P = WF::P;
+    constexpr int E = n / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_hs = s_tw + M;
+    cplx<T>* s_tw1 = s_hs + n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
+    using SG = P1Stage<T, M>;
+    unsigned char* stage = smem_raw + SG::OFF + warp * SG::BYTES;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + SG::OFF + WARPS * SG::BYTES) + warp;
+    for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
+    for (int t = threadIdx.x; t < n; t += WARPS * 32) s_hs[t] = g_hs[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS * 32);
+    const int stride = gridDim.x * WARPS, total = count * n;
+    auto request = [&](int item) {  // lane 0: the P and V rows of `item` into this warp's staging area
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        mbar_expect_tx(mbar, SG::BYTES);
+        bulk_g2s(stage, in.p(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+        bulk_g2s(stage + SG::NB, in.v(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+    };
+    if constexpr (TMA) {
+        if (lane == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        const int first = blockIdx.x * WARPS + warp;
+        if (lane == 0 && first < total) request(first);
+    }
+    __syncthreads();
+    unsigned phase = 0;
+
+    for (int item = blockIdx.x * WARPS + warp; item < total; item += stride) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const T* P_ = in.p(sg) + x * n;
+        const T* N_ = in.nn(sg) + x * n;
+        const T* V_ = in.v(sg) + x * n;
+        bool n_is_p = in.N == in.P && in.sN == in.sP;
+        if constexpr (TMA) {  // (the host selects TMA only when N = P)
+            P_ = reinterpret_cast<const T*>(stage);
+            V_ = reinterpret_cast<const T*>(stage + SG::NB);
+            n_is_p = true;
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        }
+        T pv[E], nv[E], vv[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int y = lane + 32 * t;
+            pv[t] = P_[y];
+            vv[t] = V_[y];
+            nv[t] = n_is_p ? pv[t] : N_[y];
+        }
+        T part_l = T(0), part_a = T(0);
+        int bad = 0;
+        T av[E], lv[E];  // applied / leakage row, element lane + 32 t
+        // Input checks on bit patterns, one integer min / max per value: a finite
+        // non-negative power has bits <= max-finite (-0.0 and anything else above
+        // that take the exact check below); 0 < var_lo <= var <= var_hi is an
+        // interval of bit patterns (negatives and NaNs fall outside it).
+        using U = typename BitsOf<T>::U;
+        U pmax = 0, vmin = ~U(0), vmax = 0;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            pmax = max(pmax, BitsOf<T>::get(pv[t]));
+            if (!n_is_p) pmax = max(pmax, BitsOf<T>::get(nv[t]));
+            vmin = min(vmin, BitsOf<T>::get(vv[t]));
+            vmax = max(vmax, BitsOf<T>::get(vv[t]));
+            lv[t] = in.nom_scale * nv[t] * vv[t];
+            av[t] = pv[t] + lv[t];
+            part_l += lv[t];
+            part_a += av[t];
+        }
+        if (pmax > BitsOf<T>::get(Real<T>::max())) {
+#pragma unroll
+            for (int t = 0; t < E; ++t)  // NaN fails both compares, +-inf one: !(x >= 0) || !isfinite(x)
+                if (!(pv[t] >= T(0) && pv[t] <= Real<T>::max()) || !(nv[t] >= T(0) && nv[t] <= Real<T>::max()))
+                    bad |= GTD_ST_BAD_POWER;
+        }
+        if (vmin < BitsOf<T>::get(var_lo) || vmax > BitsOf<T>::get(var_hi)) bad |= GTD_ST_BAD_VAR;
+        if constexpr (TMA) {
+            // the staged rows are consumed: request the warp's next row
+            __syncwarp();
+            if (lane == 0 && item + stride < total) {
+                fence_proxy_async();
+                request(item + stride);
+            }
+        }
+        // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185):
+        // S[dv] = L[min(c + dv, n - 1)] + L[max(c - dv, 0)], c = 16 E. For dv = lane + 32 k < c,
+        // L[c + dv] is this lane's lv[E/2 + k] and L[c - dv] is lane 32 - lane's lv[E/2 - 1 - k]
+        // (lane 0: its own lv[E/2 - k]); for dv >= c both indices clamp: L[n - 1] + L[0].
+        {
+            T* Srow_x = Srow + (static_cast<size_t>(s) * n + x) * hp;
+            const T cst = __shfl_sync(0xffffffffu, lv[E - 1], 31) + __shfl_sync(0xffffffffu, lv[0], 0);
+#pragma unroll
+            for (int k = 0; k < (hp + 31) / 32; ++k) {
+                const int v = lane + 32 * k;
+                T val;
+                if (k < E / 2) {
+                    const T mir = __shfl_sync(0xffffffffu, lv[k < E / 2 ? E / 2 - 1 - k : 0], (32 - lane) & 31);
+                    val = lv[k < E / 2 ? E / 2 + k : 0] + (lane == 0 ? lv[k < E / 2 ? E / 2 - k : 0] : mir);
+                } else {
+                    val = v < h ? cst : T(0);
+                }
+                if (v < hp) Srow_x[v] = val;
+            }
+        }
+        // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k,
+        // from registers: mirror(i) = M-1-i = (31 - lane) + 32 (P-1-k) for k >= E
+        // (one shuffle); the centre embedding keeps the lane (t = k + E/2, k - 3E/2).
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const T re = k < E ? av[k] : __shfl_xor_sync(0xffffffffu, av[P - 1 - k], 31);
+            const T im = k < E / 2 ? lv[k + E / 2] : (k >= P - E / 2 ? lv[k - (P - E / 2)] : T(0));
+            z[k] = mk<T>(re, im);
+        }
+        __syncwarp();
+        WF::template run<-1>(z, scr, s_tw, s_tw1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        // split into the two real-input half spectra (A as its real DCT part)
+        T* A_x = Areal + (static_cast<size_t>(s) * n + x) * hp;
+        cplx<T>* B_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+        for (int v = lane; v < hp; v += 32) {
+            T Ar = T(0);
+            cplx<T> B = mk<T>(T(0), T(0));
+            if (v < h) {
+                const cplx<T> Z = scr[v];
+                const cplx<T> Zc = cconj<T>(scr[(M - v) & (M - 1)]);
+                if (v < n) Ar = dct_part<T>(Z, Zc, s_hs[v]);
+                B = mk<T>(T(0.5) * (Z.y - Zc.y), T(-0.5) * (Z.x - Zc.x));
+            }
+            A_x[v] = Ar;
+            B_x[v] = B;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double tl = warp_sum(double(part_l)), ta = warp_sum(double(part_a));
+        if (lane == 0) {
+            atomicAdd(&stats[sg].sum_leak, tl);
+            atomicAdd(&stats[sg].sum_applied, ta);
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, int M, bool TMA>
+__global__ void __launch_bounds__(WARPS3 * 32, WarpMinBlocks<T, GT_W3_CTAS>::value)
+mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Aspec,
+          const cplx<T>* __restrict__ Bspec, gtd_sample_stats* __restrict__ stats,
+          const cplx<T>* __restrict__ g_tw, T* __restrict__ out, T rand_scale, int with_rand) {
+    using Gm = MCGeom<T, M>;
+    using WF = WarpFFT<T, M>;
+    using SG = P3Stage<T, M>;
+    constexpr int n = Gm::n, c = Gm::c, hp = Gm::hp, P = WF::P;
+    constexpr int E = n / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s_tw = reinterpret_cast<cplx<T>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx<T>* s_tw1 = s_tw + M;
+    cplx<T>* scr = s_tw1 + WF::TW1 + warp * WF::SCRATCH;
+    // TMA: [WARPS3][SG::BYTES] staging after the scratch, then one mbarrier per warp
+    unsigned char* stage = smem_raw + SG::OFF + warp * SG::BYTES;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (WARPS3 - warp) * SG::BYTES) + warp;
+    for (int t = threadIdx.x; t < M; t += WARPS3 * 32) s_tw[t] = g_tw[t];
+    WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS3 * 32);
+    const int stride = gridDim.x * WARPS3, total = count * n;
+    // lane 0 requests the four row segments of `item` into this warp's staging area
+    auto request = [&](int item) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const size_t so = (static_cast<size_t>(s) * n + x) * hp;
+        mbar_expect_tx(mbar, SG::BYTES);
+        bulk_g2s(stage, Aspec + so, SG::YB, mbar);
+        bulk_g2s(stage + SG::YB, Bspec + so, SG::YB, mbar);
+        bulk_g2s(stage + 2 * SG::YB, in.nn(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+        bulk_g2s(stage + 2 * SG::YB + SG::NB, in.v(sg) + static_cast<size_t>(x) * n, SG::NB, mbar);
+    };
+    if constexpr (TMA) {
+        if (lane == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        const int first = blockIdx.x * WARPS3 + warp;
+        if (lane == 0 && first < total) request(first);
+    }
+    __syncthreads();
+    const T inv = T(1.0 / (double(M) * double(M)));
+    unsigned phase = 0;
+
+    for (int item = blockIdx.x * WARPS3 + warp; item < total; item += stride) {
+        const int s = item / n, x = item - s * n;
+        const size_t sg = static_cast<size_t>(sample0) + s;
+        const cplx<T>* Y_x;
+        const cplx<T>* R_x;
+        const T* N_;
+        const T* V_;
+        if constexpr (TMA) {
+            Y_x = reinterpret_cast<const cplx<T>*>(stage);
+            R_x = reinterpret_cast<const cplx<T>*>(stage + SG::YB);
+            N_ = reinterpret_cast<const T*>(stage + 2 * SG::YB);
+            V_ = reinterpret_cast<const T*>(stage + 2 * SG::YB + SG::NB);
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        } else {
+            Y_x = Aspec + (static_cast<size_t>(s) * n + x) * hp;
+            R_x = Bspec + (static_cast<size_t>(s) * n + x) * hp;
+            N_ = in.nn(sg) + x * n;
+            V_ = in.v(sg) + x * n;
+        }
+        // epilogue inputs requested up front (one exposed round trip per row)
+        T nv[E], vv[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            nv[t] = N_[lane + 32 * t];
+            vv[t] = V_[lane + 32 * t];
+        }
+        // Z = Y + i R over the full line from the Hermitian half spectra
+        cplx<T> z[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int v = lane + 32 * k;
+            const int w = v <= n ? v : M - v;
+            const cplx<T> y = Y_x[w], r = R_x[w];
+            if (v == 0 || v == n)
+                z[k] = mk<T>(y.x, r.x);
+            else if (v < n)
+                z[k] = mk<T>(y.x - r.y, y.y + r.x);
+            else
+                z[k] = mk<T>(y.x + r.y, r.x - y.y);
+        }
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T mu_t = T(mu_s);
+        T pvs[E];  // p_var * sum(applied) * rand_scale: consumes the staged N, V rows
+#pragma unroll
+        for (int t = 0; t < E; ++t) pvs[t] = (in.nom_scale * nv[t] * vv[t] - mu_t) * scale;
+        if constexpr (TMA) {
+            // the staging area is free once every lane has consumed it: request the next row
+            __syncwarp();
+            if (lane == 0 && item + stride < total) {
+                fence_proxy_async();
+                request(item + stride);
+            }
+        }
+        WF::template run<+1>(z, scr, s_tw, s_tw1, lane);
+        __syncwarp();
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) scr[WF::out_pos(lane, m1)] = z[m1];
+        __syncwarp();
+        T part = T(0), mxt = T(0);
+        int bad = 0;
+        T* O_x = out ? out + (sg * n + x) * n : nullptr;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+            const int f = lane + 32 * t;
+            const T yd = scr[f].x * inv;
+            const T rd = scr[(f - c) & (M - 1)].y * inv;
+            T tt = yd + rd * pvs[t];
+            if (!finite_(tt)) bad = GTD_ST_NONFINITE;
+            tt = tt > T(0) ? tt : T(0);
+            if (O_x) O_x[f] = tt;
+            part += tt;
+            mxt = mxt > tt ? mxt : tt;
+        }
+        or_flags(&stats[sg].status, bad);
+        const double ts = warp_sum(double(part));
+        const double tm = double(warp_max_t(mxt));  // max is exact in T
+        if (lane == 0) {
+            atomicAdd(&stats[sg].sum_rise, ts);
+            atomicMax(&stats[sg].max_bits, static_cast<unsigned long long>(__double_as_longlong(tm)));
+            if (x == 0) stats[sg].mu = mu_s;
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, int M>
+struct RowSmem {
+    using Gm = MCGeom<T, M>;
+    static size_t tile() { return sizeof(cplx<T>) * (M * Gm::LP + M) + 64 * sizeof(double); }
+    static size_t w1(bool tma) {
+        if constexpr (use_warp_rows<T, M>())
+            return tma ? P1Stage<T, M>::SMEM
+                       : sizeof(cplx<T>) * (M + M / 2 + WarpFFT<T, M>::TW1 + WARPS * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
+    static size_t w3(bool tma) {
+        if constexpr (use_warp_rows<T, M>())
+            return tma ? P3Stage<T, M>::SMEM
+                       : sizeof(cplx<T>) * (M + WarpFFT<T, M>::TW1 + WARPS3 * WarpFFT<T, M>::SCRATCH);
+        else
+            return 0;
+    }
+};
+
+template <typename T, int M>
+int mc_rows_setup(int pass) {
+    using Gm = MCGeom<T, M>;
+    using SM = RowSmem<T, M>;
+    int r = 0;
+    if constexpr (use_warp_rows<T, M>()) {
+        if (pass == 1) {
+            cudaFuncSetAttribute(mc_pass1w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::w1(false)));
+            cudaFuncSetAttribute(mc_pass1w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::w1(true)));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, mc_pass1w<T, M, true>, WARPS * 32, SM::w1(true));
+        } else {
+            cudaFuncSetAttribute(mc_pass3w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::w3(false)));
+            cudaFuncSetAttribute(mc_pass3w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::w3(true)));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, mc_pass3w<T, M, true>, WARPS3 * 32, SM::w3(true));
+        }
+    } else {
+        if (pass == 1) {
+            cudaFuncSetAttribute(mc_pass1<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::tile()));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, mc_pass1<T, M>, Gm::NT, SM::tile());
+        } else {
+            cudaFuncSetAttribute(mc_pass3<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::tile()));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, mc_pass3<T, M>, Gm::NT, SM::tile());
+        }
+    }
+    return r < 1 ? 1 : r;
+}
+
+template <typename T, int M>
+void mc_rows_launch(int pass, bool tma, int sms, int cpsm, cudaStream_t st, const MCRowArgs<T>& a) {
+    using Gm = MCGeom<T, M>;
+    using SM = RowSmem<T, M>;
+    constexpr int n = Gm::n, L = Gm::L, NT = Gm::NT, RB = (n + L - 1) / L;
+    auto grid = [&](int items) { return items < sms * cpsm ? items : sms * cpsm; };
+    if constexpr (use_warp_rows<T, M>()) {
+        if (pass == 1) {
+            const int g = grid((a.cnt * n + WARPS - 1) / WARPS);
+            if (tma)
+                mc_pass1w<T, M, true><<<g, WARPS * 32, SM::w1(true), st>>>(a.in, a.s0, a.cnt, a.Ar, a.B, a.S, a.stats,
+                                                                           a.tw, a.hs, a.var_lo, a.var_hi);
+            else
+                mc_pass1w<T, M, false><<<g, WARPS * 32, SM::w1(false), st>>>(a.in, a.s0, a.cnt, a.Ar, a.B, a.S,
+                                                                             a.stats, a.tw, a.hs, a.var_lo, a.var_hi);
+        } else {
+            const int g = grid((a.cnt * n + WARPS3 - 1) / WARPS3);
+            if (tma)
+                mc_pass3w<T, M, true><<<g, WARPS3 * 32, SM::w3(true), st>>>(a.in, a.s0, a.cnt, a.A, a.B, a.stats, a.tw,
+                                                                            a.out, a.rand_scale, a.with_rand);
+            else
+                mc_pass3w<T, M, false><<<g, WARPS3 * 32, SM::w3(false), st>>>(a.in, a.s0, a.cnt, a.A, a.B, a.stats,
+                                                                              a.tw, a.out, a.rand_scale, a.with_rand);
+        }
+    } else {
+        const int g = grid(a.cnt * RB);
+        if (pass == 1)
+            mc_pass1<T, M><<<g, NT, SM::tile(), st>>>(a.in, a.s0, a.cnt, a.Ar, a.B, a.S, a.stats, a.tw, a.hs, a.var_lo,
+                                                      a.var_hi);
+        else
+            mc_pass3<T, M><<<g, NT, SM::tile(), st>>>(a.in, a.s0, a.cnt, a.A, a.B, a.stats, a.tw, a.out, a.rand_scale,
+                                                      a.with_rand);
+    }
+}
+
+#define GT_ROWS_INST(T, M)                       \
+    template int mc_rows_setup<T, M>(int);       \
+    template void mc_rows_launch<T, M>(int, bool, int, int, cudaStream_t, const MCRowArgs<T>&);
+#define GT_ROWS_INST_M(M) GT_ROWS_INST(float, M) GT_ROWS_INST(double, M)
+GT_ROWS_INST_M(32)
+GT_ROWS_INST_M(64)
+GT_ROWS_INST_M(128)
+GT_ROWS_INST_M(256)
+GT_ROWS_INST_M(512)
+GT_ROWS_INST_M(1024)
+GT_ROWS_INST_M(2048)
+
+}  // namespace gtb
