@@ -220,6 +220,10 @@ int gt_mc_kernel_launches(int batch, int chunk);
  * (pass_ms[0..2] = row / column / row pass, pass_ms[3] = their sum), the
  * kernels launched and the batch calls made since begin. */
 gt_status gt_profile_begin(gt_device_greens* d);
+/* mode 0: as gt_profile_begin; mode 1: events around the column pass only (the
+ * dominant kernel; two events per chunk instead of four keep a timed region's
+ * launch stream lighter), pass_ms[0] = pass_ms[2] = 0. */
+gt_status gt_profile_begin_mode(gt_device_greens* d, int mode);
 gt_status gt_profile_end(gt_device_greens* d, double* pass_ms, long long* kernels, long long* calls);
 /* Kernels launched by this prepared set since the last gt_profile_begin. */
 long long gt_kernel_launches(const gt_device_greens* d);

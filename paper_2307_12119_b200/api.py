@@ -134,6 +134,7 @@ _EXT = [
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
     ("gt_large_rows_inv", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp]),
     ("gt_profile_begin", cint, [vp]),
+    ("gt_profile_begin_mode", cint, [vp, cint]),
     ("gt_profile_end", cint, [vp, pdbl, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("gt_kernel_launches", C.c_longlong, [vp]),
 ]
@@ -370,8 +371,9 @@ class DeviceGreens:
                                          C.c_void_p(leak_ptr), leak_stride, batch, C.byref(opts),
                                          C.c_void_p(out_ptr), C.c_void_p(max_ptr) if max_ptr else None, sp))
 
-    def profile_begin(self) -> None:
-        check(lib(), lib().gt_profile_begin(self._d))
+    def profile_begin(self, mode: int = 0) -> None:
+        """mode 0: events around all three passes; 1: around the column pass only."""
+        check(lib(), lib().gt_profile_begin_mode(self._d, mode))
 
     def profile_end(self):
         """-> (pass_ms[4], kernels, calls)"""

@@ -95,8 +95,13 @@ size_t scratch_budget() {
     return std::min(hi, std::max(lo, fr / 10 * 4));
 }
 
-int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1) {  // share: scratch buffers in flight
+// share: scratch buffers in flight; have: bytes of one scratch buffer already
+// allocated (a call that fits in it skips the cudaMemGetInfo query: no driver
+// round trip on the launch path of repeated calls)
+int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1, size_t have = 0) {
     if (o && o->chunk > 0) return std::min(o->chunk, batch);
+    const int want = std::min(4096, batch);
+    if (have >= gtd_mc_scratch_bytes_per_sample(n, fp64) * static_cast<size_t>(want)) return want;
     // Large chunks win: the passes are SM-issue bound, not HBM bound (a sweep of
     // 24..4096 pairs per chunk on B200 went 232k -> 325k solves/s; L2 residency
     // of the intermediates at <= 48 MB bought nothing), every launch ends in a
@@ -479,7 +484,7 @@ gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, cons
         std::lock_guard<std::mutex> lk(d->mu);
         cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
         const int n = d->d.n;
-        const int chunk = auto_chunk(n, d->fp64, batch, opts);
+        const int chunk = auto_chunk(n, d->fp64, batch, opts, 1, d->scratch.bytes);
         d->scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * chunk);
         gtd_mc_opts o = to_dev_opts(opts);
         gtd_mc_in in{};
@@ -513,7 +518,7 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         const size_t map = static_cast<size_t>(n) * n * es;
         // Pipeline chunk: large enough to amortise launches, two slots in flight.
         int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 512);
-        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         for (int s = 0; s < 2; ++s) {
             if (!d->slot_stream[s]) cuda_ok(cudaStreamCreateWithFlags(&d->slot_stream[s], cudaStreamNonBlocking), "stream");
@@ -633,7 +638,7 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         const size_t es = d->fp64 ? 8 : 4;
         const size_t map = static_cast<size_t>(n) * n * es;
         int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 512);
-        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2);
+        const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(n, d->fp64) * chunk);
         for (int s = 0; s < 2; ++s) {
@@ -954,10 +959,14 @@ gt_status gt_fp_batch(const gt_device_greens* dc, const void* p_dyn, const void*
     });
 }
 
-gt_status gt_profile_begin(gt_device_greens* d) {
+gt_status gt_profile_begin(gt_device_greens* d) { return gt_profile_begin_mode(d, 0); }
+
+gt_status gt_profile_begin_mode(gt_device_greens* d, int mode) {
     return guarded([&] {
+        if (mode != 0 && mode != 1) fail(ST_CONFIG, "profile", "profile mode must be 0 or 1");
         std::lock_guard<std::mutex> lk(d->mu);
         d->profiling = true;
+        d->profile_mode = mode;
         d->marks.clear();
         d->pool_used = 0;
         d->kernels = 0;
@@ -970,7 +979,17 @@ gt_status gt_profile_end(gt_device_greens* d, double* pass_ms, long long* kernel
         std::lock_guard<std::mutex> lk(d->mu);
         cuda_ok(cudaSetDevice(d->device), "cudaSetDevice");
         double acc[4] = {0, 0, 0, 0};
-        for (size_t i = 0; i + 3 < d->marks.size(); i += 4) {
+        if (d->profile_mode == 1) {
+            for (size_t i = 0; i + 1 < d->marks.size(); i += 2) {
+                if (d->marks[i].first != 1 || d->marks[i + 1].first != 2)
+                    fail(ST_INTERNAL, "profile", "unbalanced profiling marks");
+                cuda_ok(cudaEventSynchronize(d->marks[i + 1].second), "event sync");
+                float ms = 0.f;
+                cuda_ok(cudaEventElapsedTime(&ms, d->marks[i].second, d->marks[i + 1].second), "elapsed");
+                acc[1] += ms;
+            }
+        }
+        for (size_t i = 0; d->profile_mode == 0 && i + 3 < d->marks.size(); i += 4) {
             for (int k = 0; k < 3; ++k) {
                 if (d->marks[i + k].first != k || d->marks[i + k + 1].first != k + 1)
                     fail(ST_INTERNAL, "profile", "unbalanced profiling marks");
@@ -986,6 +1005,7 @@ gt_status gt_profile_end(gt_device_greens* d, double* pass_ms, long long* kernel
         if (kernels) *kernels = d->kernels;
         if (calls) *calls = d->calls;
         d->profiling = false;
+        d->profile_mode = 0;
         d->marks.clear();
         d->pool_used = 0;
     });

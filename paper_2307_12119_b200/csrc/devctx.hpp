@@ -81,8 +81,10 @@ struct gt_device_greens {
     void order_out(cudaStream_t st) {
         if (busy) cudaEventRecord(busy, st);
     }
+    int profile_mode = 0;  // 1: column pass only (points 1, 2)
     static void mark(void* ctx, int point, cudaStream_t st) {
         auto* self = static_cast<gt_device_greens*>(ctx);
+        if (self->profile_mode == 1 && (point == 0 || point == 3)) return;
         if (self->pool_used == self->event_pool.size()) {
             cudaEvent_t e;
             cudaEventCreate(&e);
