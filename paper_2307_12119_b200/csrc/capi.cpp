@@ -729,7 +729,11 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     int chunk = opts->chunk > 0 ? std::min(opts->chunk, batch) : 0;
     if (!chunk) {
         const size_t per = gtd_fp_scratch_bytes_per_sample(n, d->fp64);
-        chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, scratch_budget() / per)));
+        const int want = std::min(1024, batch);
+        // a repeated call whose scratch is already allocated skips the free-memory query
+        chunk = d->fp_scratch.bytes >= per * static_cast<size_t>(want)
+                    ? want
+                    : static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, scratch_budget() / per)));
         chunk = std::min(chunk, batch);
     }
     d->fp_scratch.ensure(gtd_fp_scratch_bytes_per_sample(n, d->fp64) * chunk);
