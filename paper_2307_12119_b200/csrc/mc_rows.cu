@@ -5,7 +5,10 @@
 // row FFTs run 32 warps per SM and gain from the halved instruction count
 // (pass 1 -2.4%, pass 3 -5%), while the column pass, at 16 warps per SM and
 // latency bound, measured 7% slower with it and stays scalar.
-#define GT_PACKED_F32 1
+#ifndef GT_ROWS_PACKED
+#define GT_ROWS_PACKED 1
+#endif
+#define GT_PACKED_F32 GT_ROWS_PACKED
 #include "mc_common.cuh"
 
 namespace gtb {
