@@ -207,3 +207,29 @@ def test_mc_unaligned_inputs_take_the_direct_load_path(b200lib, g64, golden):
         np.testing.assert_array_equal(a, b)
     err = np.abs(outs[0][0].astype(np.float64) - golden["t_mu_sample"]).max()
     assert err <= FP32_ATOL
+
+
+def test_profile_modes(b200lib, g64, golden):
+    """gt_profile_begin_mode: mode 0 times the three passes, mode 1 the column pass
+    only (pass_ms[0] = pass_ms[2] = 0); both count the same launches and calls."""
+    import torch
+    from paper_2307_12119_b200.api import SAMPLE_STATS_DTYPE
+    dg = _dg(g64, 0)
+    p = torch.from_numpy(golden["p_dyn"]).cuda()
+    v = torch.from_numpy(golden["var"]).cuda()
+    B = p.shape[0]
+    out = torch.empty_like(p)
+    stats = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    res = {}
+    for mode in (0, 1):
+        dg.profile_begin(mode)
+        for _ in range(3):
+            dg.mc_batch_device(p.data_ptr(), v.data_ptr(), B, dg.opts(), out.data_ptr(), stats.data_ptr(), s)
+        res[mode] = dg.profile_end()
+    (ms0, k0, c0), (ms1, k1, c1) = res[0], res[1]
+    assert all(x > 0 for x in ms0[:3]) and abs(ms0[3] - sum(ms0[:3])) < 1e-9
+    assert ms1[0] == 0 and ms1[2] == 0 and ms1[1] > 0
+    assert (k0, c0) == (k1, c1) and c0 == 3
+    with pytest.raises(Exception):
+        dg.profile_begin(2)
