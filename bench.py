@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cfg3", action="store_true", help="skip the config-3 transient-trace sub-benchmark")
     ap.add_argument("--cfg3-steps", type=int, default=2000)
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 large-grid sub-benchmark")
+    ap.add_argument("--sub-at-scale", action="store_true",
+                    help="under torchrun (N > 1) also run the mode-B / config-2/3/4 sub-benchmarks (default: "
+                         "N > 1 measures the headline and e2e only; the sub-benchmarks are N = 1 parity configs)")
     ap.add_argument("--cfg4-n", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     return ap.parse_args()
@@ -445,6 +448,8 @@ def run_b200(args, cfg):
     from paper_2307_12119_b200.api import GT_FP32, GT_FP64, SAMPLE_STATS_DTYPE, DeviceGreens
 
     ws, rank, local = dist_env()
+    if ws > 1 and not args.sub_at_scale:
+        args.no_mode_b = args.no_cfg2 = args.no_cfg3 = args.no_cfg4 = True
     if ws > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     torch.cuda.set_device(local)
