@@ -56,7 +56,8 @@ def _compile(src: Path, nvcc: str, hdr_mtime: float, objdir: Path = BUILD, extra
     obj = objdir / (src.name + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    flags = (ARCH + CU_FLAGS + list(extra)) if src.suffix == ".cu" else CXX_FLAGS
+    # variant defines (-D...) reach the host sources too
+    flags = (ARCH + CU_FLAGS + list(extra)) if src.suffix == ".cu" else CXX_FLAGS + [e for e in extra if e.startswith("-D")]
     cmd = [nvcc, *_host_compiler(), *flags, "-I", str(CSRC), "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -98,6 +98,10 @@ size_t scratch_budget() {
 // share: scratch buffers in flight; have: bytes of one scratch buffer already
 // allocated (a call that fits in it skips the cudaMemGetInfo query: no driver
 // round trip on the launch path of repeated calls)
+#ifndef GT_E2E_CHUNK
+#define GT_E2E_CHUNK 128  // pairs per chunk of the host-input pipelines
+#endif
+
 int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1, size_t have = 0) {
     if (o && o->chunk > 0) return std::min(o->chunk, batch);
     const int want = std::min(4096, batch);
@@ -519,7 +523,7 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         // Pipeline chunk: two slots in flight; small chunks shorten the exposed first
         // copy and last compute of the PCIe-bound pipeline (config 1, 4096 pairs:
         // 512 -> 128 pairs per chunk took the end-to-end rate 191k -> 204k solves/s).
-        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 128);
+        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, GT_E2E_CHUNK);
         const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         for (int s = 0; s < 2; ++s) {
@@ -639,7 +643,7 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         const int n = d->d.n;
         const size_t es = d->fp64 ? 8 : 4;
         const size_t map = static_cast<size_t>(n) * n * es;
-        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, 128);
+        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, GT_E2E_CHUNK);
         const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(n, d->fp64) * chunk);
