@@ -166,12 +166,12 @@ def cpu_reference_rate(cfg, seconds: float, threads: int, start: int = 0):
     k = max(1, threads)
     p = inputs.power_batch(cfg, start, k, np.float32)
     v = inputs.variation_batch(cfg, start, k).numpy().astype(np.float32)
-    t = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+    t = refpy.mc_batch(g, p, v, mu_per_sample=0, jobs=threads, want_maps=False)[4]
     S = int(max(k, min(4096, k * max(1.0, seconds / max(t, 1e-3)))))
     S = max(k, (S // k) * k)
     p = inputs.power_batch(cfg, start, S, np.float32)
     v = inputs.variation_batch(cfg, start, S).numpy().astype(np.float32)
-    _, _, _, st, secs = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)
+    _, _, _, st, secs = refpy.mc_batch(g, p, v, mu_per_sample=0, jobs=threads, want_maps=False)
     return {"value": S / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{S} cfg1 pairs (n=256) through the unchanged reference core "
                       f"(oracle/_ref, FFTW/Eigen shims), {threads} std::threads as in solver.cpp:376-387; "
@@ -193,15 +193,15 @@ def run_reference_arm(args, cfg):
     k = threads
     p = inputs.power_batch(cfg, 0, k, np.float32)
     v = inputs.variation_batch(cfg, 0, k).numpy().astype(np.float32)
-    t = refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+    t = refpy.mc_batch(g, p, v, mu_per_sample=0, jobs=threads, want_maps=False)[4]
     S = max(k, int(k * per_step / max(t, 1e-3)) // k * k)
     p = inputs.power_batch(cfg, 0, S, np.float32)
     v = inputs.variation_batch(cfg, 0, S).numpy().astype(np.float32)
     for _ in range(args.warmup):
-        refpy.mc_batch(g, p[:k], v[:k], jobs=threads, want_maps=False)
+        refpy.mc_batch(g, p[:k], v[:k], mu_per_sample=0, jobs=threads, want_maps=False)
     secs = 0.0
     for _ in range(args.steps):
-        secs += refpy.mc_batch(g, p, v, jobs=threads, want_maps=False)[4]
+        secs += refpy.mc_batch(g, p, v, mu_per_sample=0, jobs=threads, want_maps=False)[4]
     value = S * args.steps / secs
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
@@ -461,7 +461,8 @@ def run_b200(args, cfg):
     n = cfg.n
 
     dg = DeviceGreens(greens_cfg1(), prec, device=local)
-    opts = dg.opts(leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=args.chunk)
+    # mu_per_sample=0: the reference monte_carlo's closed forms at gs.mu (solver.cpp:350-351,361)
+    opts = dg.opts(leak_frac=0.3, mu_per_sample=0, with_rand=1, chunk=args.chunk)
     s0, s1 = shard.shard_range(rank, ws, B)
     P, V = inputs.mc_inputs(cfg, s0, s1 - s0, device=str(dev), torch_dtype=tdt)
     out = torch.empty_like(P)
@@ -506,6 +507,23 @@ def run_b200(args, cfg):
     st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=SAMPLE_STATS_DTYPE)
     failed = int((st["status"] != 0).sum())
 
+    # the other closed-form semantics: per-sample mean leakage in F_det and F_rand
+    # (mu_per_sample=1; F_det is then divided per frequency and pair)
+    opts_ps = dg.opts(leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=args.chunk)
+    dg.mc_batch_device(P.data_ptr(), V.data_ptr(), B, opts_ps, out.data_ptr(), stats.data_ptr(), stream.cuda_stream)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(max(3, args.steps // 4)):
+        dg.mc_batch_device(P.data_ptr(), V.data_ptr(), B, opts_ps, out.data_ptr(), stats.data_ptr(),
+                           stream.cuda_stream)
+    q1.record(stream)
+    torch.cuda.synchronize()
+    ms_ps = shard.max_over_ranks(q0.elapsed_time(q1) / max(3, args.steps // 4), dev)
+    per_sample_mu = {"value": ws * B / (ms_ps / 1e3), "unit": UNIT, "ms_per_step": ms_ps,
+                     "semantics": "mu_per_sample=1: closed forms at each pair's mean leakage"}
+    step()  # leave the headline semantics' outputs in out / stats
+    torch.cuda.synchronize()
+
     # fp64 residual check on a subset (BASELINE cfg1: "fp32 with fp64 residual check")
     resid = None
     if prec == GT_FP32:
@@ -514,8 +532,8 @@ def run_b200(args, cfg):
         P64, V64 = P[:k].double().contiguous(), V[:k].double().contiguous()
         o64 = torch.empty_like(P64)
         s64 = torch.zeros(k * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        dg64.mc_batch_device(P64.data_ptr(), V64.data_ptr(), k, dg64.opts(), o64.data_ptr(), s64.data_ptr(),
-                             stream.cuda_stream)
+        dg64.mc_batch_device(P64.data_ptr(), V64.data_ptr(), k, dg64.opts(mu_per_sample=0), o64.data_ptr(),
+                             s64.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
         resid = {"samples": k, "max_abs_K": float((out[:k].double() - o64).abs().max().item()),
                  "peak_K": float(o64.max().item())}
@@ -667,7 +685,8 @@ def run_b200(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if prec == GT_FP32 else "f64", "data": "synthetic",
             "config": {"workload": "cfg1 mode A: reference run_one (solver.cpp:353-374) per (power map, variation "
-                                   "map) pair, 256x256 grid, per-sample mean leakage, shift-variant term on",
+                                   "map) pair, 256x256 grid, closed forms at the GreensSet mu as the reference "
+                                   "monte_carlo (solver.cpp:350-351,361), shift-variant term on",
                        "n": n, "pairs_per_gpu": B, "precision": args.precision, "chunk": args.chunk or "auto",
                        "greens": "reference calibrate() at n=256 (tests/golden/greens_n256.npz), rand_scale 1.0",
                        "l2": "no flush: 2 x pairs x 256 KiB inputs per step (>> 126 MB L2)",
@@ -682,7 +701,7 @@ def run_b200(args, cfg):
                          "whole_solve_frac_survey_model": whole / peak,
                          "fp32_pipe_ncu": fp32_util},
             "gpu_launches": int(kernels), "batch_calls": int(calls), "failed_pairs": failed,
-            "fp64_residual_check": resid, "clocks": clk,
+            "fp64_residual_check": resid, "clocks": clk, "per_sample_mu": per_sample_mu,
         }
         if e2e:
             line["e2e"] = e2e

@@ -40,7 +40,8 @@ enum {
     GT_SAMPLE_RUNAWAY_RAND = 8,
     GT_SAMPLE_NONFINITE = 16,
     GT_SAMPLE_NOCONVERGE = 32,
-    GT_SAMPLE_KIRCHHOFF = 64
+    GT_SAMPLE_KIRCHHOFF = 64,
+    GT_SAMPLE_ILLCOND = 128
 };
 
 /* Build a GreensSet from arrays (n x n row-major doubles) instead of a
@@ -67,6 +68,11 @@ typedef struct gt_batch_opts {
     int with_rand;       /* 0 omits the shift-variant term                       */
     int chunk;           /* samples in flight per pass (0 = automatic)          */
     double exponent_cap; /* |ln var| guard, 0 = reference default 6.0            */
+    double fp64_check;   /* GT_FP32 handles: pairs whose max 1/|den2|^2 (random_greens
+                            denominator) exceeds this are re-solved in fp64 on the
+                            device (0 = default 1e4; < 0 = off). Re-solved pairs
+                            report a negative gt_sample_stats.max_rden2; pairs beyond
+                            the re-solve capacity (batch/16) get GT_SAMPLE_ILLCOND. */
 } gt_batch_opts;
 
 void gt_batch_opts_default(gt_batch_opts* o);
@@ -76,7 +82,7 @@ typedef struct gt_sample_stats {
     double sum_leak, sum_applied, sum_rise, max_rise, mean_rise, mu;
     unsigned long long max_bits;
     int status;
-    int pad_;
+    float max_rden2;  /* max over frequencies of 1/|den2|^2 (random_greens denominator): fp32 conditioning */
 } gt_sample_stats;
 
 /* End-to-end batch from host memory: p_dyn, var are batch x n x n in the

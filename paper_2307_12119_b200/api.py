@@ -16,6 +16,9 @@ _HERE = Path(__file__).resolve().parent
 _LIBNAME = "libgreentherm_b200.so"
 
 GT_FP32, GT_FP64 = 0, 1
+# per-sample status bits (include/greentherm_b200.h GT_SAMPLE_*; gt_device.h GTD_ST_*)
+(GT_SAMPLE_BAD_POWER, GT_SAMPLE_BAD_VAR, GT_SAMPLE_RUNAWAY_DET, GT_SAMPLE_RUNAWAY_RAND, GT_SAMPLE_NONFINITE,
+ GT_SAMPLE_NOCONVERGE, GT_SAMPLE_KIRCHHOFF, GT_SAMPLE_ILLCOND) = 1, 2, 4, 8, 16, 32, 64, 128
 
 vp = C.c_void_p
 pvp = C.POINTER(C.c_void_p)
@@ -81,13 +84,13 @@ CORE_SYMBOLS = [n for n, _, _ in _CORE]
 
 class BatchOpts(C.Structure):
     _fields_ = [("leak_frac", dbl), ("mu_per_sample", cint), ("with_rand", cint), ("chunk", cint),
-                ("exponent_cap", dbl)]
+                ("exponent_cap", dbl), ("fp64_check", dbl)]
 
 
 class SampleStats(C.Structure):
     _fields_ = [("sum_leak", dbl), ("sum_applied", dbl), ("sum_rise", dbl), ("max_rise", dbl),
                 ("mean_rise", dbl), ("mu", dbl), ("max_bits", C.c_ulonglong), ("status", cint),
-                ("pad_", cint)]
+                ("max_rden2", C.c_float)]
 
 
 class FPOpts(C.Structure):
@@ -97,7 +100,7 @@ class FPOpts(C.Structure):
 
 SAMPLE_STATS_DTYPE = np.dtype([("sum_leak", "f8"), ("sum_applied", "f8"), ("sum_rise", "f8"),
                                ("max_rise", "f8"), ("mean_rise", "f8"), ("mu", "f8"),
-                               ("max_bits", "u8"), ("status", "i4"), ("pad_", "i4")])
+                               ("max_bits", "u8"), ("status", "i4"), ("max_rden2", "f4")])
 
 # greentherm_b200.h
 class TraceOpts(C.Structure):
@@ -264,8 +267,10 @@ class DeviceGreens:
         except Exception:
             pass
 
-    def opts(self, leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=0, exponent_cap=6.0) -> BatchOpts:
-        return BatchOpts(leak_frac, mu_per_sample, with_rand, chunk, exponent_cap)
+    def opts(self, leak_frac=0.3, mu_per_sample=1, with_rand=1, chunk=0, exponent_cap=6.0,
+             fp64_check=0.0) -> BatchOpts:
+        """fp64_check: conditioning threshold of the fp64 re-solve (0 = default 1e4, < 0 = off)."""
+        return BatchOpts(leak_frac, mu_per_sample, with_rand, chunk, exponent_cap, fp64_check)
 
     def mc_batch_host(self, p_dyn: np.ndarray, var: np.ndarray, opts: BatchOpts | None = None,
                       want_maps: bool = True):

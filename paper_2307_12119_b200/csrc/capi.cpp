@@ -82,7 +82,40 @@ gtd_mc_opts to_dev_opts(const gt_batch_opts* o) {
     r.mu_per_sample = o ? o->mu_per_sample : 1;
     r.with_rand = o ? o->with_rand : 1;
     r.exponent_cap = (o && o->exponent_cap > 0.0) ? o->exponent_cap : 6.0;
+    r.resolve = nullptr;
     return r;
+}
+
+// The fp64 re-solve attached to an fp32 batch ("fp32 with fp64 residual check",
+// BASELINE config 1): pairs whose random_greens denominator came within
+// 1/sqrt(thr) of singular are solved again in fp64 on the device. Measured on
+// config-1 pairs (tools/diag_mf.py): every pair above 1e-3 K fp32 error had
+// max 1/|den2|^2 > 2e5, every pair below 1e4 stayed under 2.6e-4 K; 1-2% of
+// pairs exceed 1e4. Capacity: batch/16 pairs (at least 8).
+const gtd_mc_resolve* attach_resolve(gt_device_greens* d, int slot, int batch, const gt_batch_opts* o) {
+    if (d->fp64) return nullptr;
+    double thr = o ? o->fp64_check : 0.0;
+    if (thr < 0.0) return nullptr;
+    if (thr == 0.0) thr = 1e4;
+    if (!d->dev64) d->dev64 = gth::prepare_device(d->host, GT_FP64, d->device);
+    const int n = d->d.n;
+    const int cap = std::max(8, (batch + 15) / 16);
+    const size_t nn = static_cast<size_t>(n) * n;
+    auto& r = d->resolve[slot];
+    r.in.ensure(static_cast<size_t>(cap) * 3 * nn * 8);
+    r.out.ensure(static_cast<size_t>(cap) * nn * 8);
+    r.stats.ensure(static_cast<size_t>(cap) * sizeof(gtd_sample_stats));
+    r.scr.ensure(static_cast<size_t>(cap) * gtd_mc_scratch_bytes_per_sample(n, 1));
+    r.sel.ensure(static_cast<size_t>(cap + 1) * sizeof(int));
+    r.d.g64 = &d->dev64->d;
+    r.d.in64 = r.in.p;
+    r.d.out64 = r.out.p;
+    r.d.stats64 = r.stats.as<gtd_sample_stats>();
+    r.d.scratch64 = r.scr.p;
+    r.d.sel = r.sel.as<int>();
+    r.d.cap = cap;
+    r.d.thr = static_cast<float>(thr);
+    return &r.d;
 }
 
 // Scratch budget of the automatic chunking: 40% of the device's free memory,
@@ -470,6 +503,7 @@ void gt_batch_opts_default(gt_batch_opts* o) {
     o->with_rand = 1;
     o->chunk = 0;
     o->exponent_cap = 6.0;
+    o->fp64_check = 0.0;
 }
 
 size_t gt_mc_scratch_bytes(int n, int precision) { return gtd_mc_scratch_bytes_per_sample(n, precision == GT_FP64); }
@@ -491,6 +525,7 @@ gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, cons
         const int chunk = auto_chunk(n, d->fp64, batch, opts, 1, d->scratch.bytes);
         d->scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * chunk);
         gtd_mc_opts o = to_dev_opts(opts);
+        o.resolve = attach_resolve(d, 0, batch, opts);
         gtd_mc_in in{};
         in.P = p_dyn;
         in.N = p_dyn;
@@ -503,7 +538,7 @@ gt_status gt_mc_batch_device(const gt_device_greens* dc, const void* p_dyn, cons
                              d->scratch.p, chunk, st, d->profiling ? &gt_device_greens::mark : nullptr, d),
                 "mc batch launch");
         d->order_out(st);
-        d->kernels += gtd_mc_launch_count(batch, chunk);
+        d->kernels += gtd_mc_launch_count(batch, chunk) + (o.resolve ? gtd_mc_resolve_launch_count() : 0);
         d->calls += 1;
     });
 }
@@ -558,10 +593,11 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
             in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
             in.nom_scale = opts ? opts->leak_frac : 0.3;
             auto* dst = static_cast<gtd_sample_stats*>(d->slot_stats[s].p);
+            o.resolve = attach_resolve(d, 1 + s, chunk, opts);
             cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, t_out ? d->slot_out[s].p : nullptr, dst, d->slot_scr[s].p,
                                  std::min(inner, cnt), st, nullptr, nullptr),
                     "mc batch launch");
-            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt));
+            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt)) + (o.resolve ? gtd_mc_resolve_launch_count() : 0);
             if (t_out)
                 cuda_ok(cudaMemcpyAsync(static_cast<char*>(t_out) + s0 * map, d->slot_out[s].p, cnt * map,
                                         cudaMemcpyDeviceToHost, st),
@@ -690,10 +726,12 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
             in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
             in.nom_scale = opts ? opts->leak_frac : 0.3;
             auto* dst = static_cast<gtd_sample_stats*>(d->slot_stats[s].p);
+            o.resolve = attach_resolve(d, 1 + s, chunk, opts);
             cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, t_out ? d->slot_out[s].p : nullptr, dst, d->slot_scr[s].p,
                                  std::min(inner, cnt), st, nullptr, nullptr),
                     "mc batch launch");
-            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt)) + 2;
+            d->kernels += gtd_mc_launch_count(cnt, std::min(inner, cnt)) + 2 +
+                          (o.resolve ? gtd_mc_resolve_launch_count() : 0);
             if (t_out)
                 cuda_ok(cudaMemcpyAsync(static_cast<char*>(t_out) + s0 * map, d->slot_out[s].p, cnt * map,
                                         cudaMemcpyDeviceToHost, st),

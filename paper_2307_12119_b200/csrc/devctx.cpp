@@ -173,7 +173,18 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
                               g.phi, n, hp, d->fp64, d->tw64.p, d->fk_full.p, d->fk.p, d->gtab.p, d->fg.p, g.alpha,
                               st),
             "greens tables");
-    cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
+    {
+        DBuf flag;
+        flag.ensure(sizeof(int));
+        d->fgm.ensure(static_cast<size_t>(m) * hp * 4 * rb);
+        cuda_ok(gtd_greens_fgm(d->fk_full.p, static_cast<const double*>(d->gsp0.p), n, hp, d->fp64, g.alpha,
+                               g.mu * g.beta, d->fgm.p, flag.as<int>(), st),
+                "fixed-mu table");
+        int f = 0;
+        cuda_ok(cudaMemcpyAsync(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st), "flag");
+        cuda_ok(cudaStreamSynchronize(st), "greens tables sync");
+        d->d.det_flags = f ? GTD_ST_RUNAWAY_DET : 0;
+    }
     d->d.n = n;
     d->d.m = m;
     d->d.h = n + 1;
@@ -184,6 +195,7 @@ std::unique_ptr<gt_device_greens> prepare_device(const Greens& g, int precision,
     d->d.k1 = d->k1.p;
     d->d.tw = d->tw.p;
     d->d.fg = d->fg.p;
+    d->d.fgm = d->fgm.p;
     d->d.hs = d->hs.p;
     d->d.alpha = g.alpha;
     d->d.beta = g.beta;

@@ -53,7 +53,7 @@ struct gt_device_greens {
     gtd_greens d{};
     gth::Greens host;  // copy of the set the tables were built from
     cudaStream_t stream = nullptr;
-    gth::DBuf hs, fg, fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
+    gth::DBuf hs, fg, fgm, fk, gtab, k1, tw, tw64, fsp0, gsp0, work;
     // batch scratch (guarded by mu)
     std::mutex mu;
     gth::DBuf fp_scratch, fp_state, fp_counter;
@@ -81,6 +81,14 @@ struct gt_device_greens {
     void order_out(cudaStream_t st) {
         if (busy) cudaEventRecord(busy, st);
     }
+    // fp64 re-solve of ill-conditioned fp32 Monte-Carlo pairs (gtd_mc_resolve):
+    // fp64 tables of the same GreensSet, built on first use, and per-pipeline-slot
+    // buffers (0: device-resident entry, 1 / 2: the two host-pipeline slots)
+    std::unique_ptr<gt_device_greens> dev64;
+    struct Resolve {
+        gth::DBuf in, out, stats, scr, sel;
+        gtd_mc_resolve d{};
+    } resolve[3];
     int profile_mode = 0;  // 1: column pass only (points 1, 2)
     static void mark(void* ctx, int point, cudaStream_t st) {
         auto* self = static_cast<gt_device_greens*>(ctx);

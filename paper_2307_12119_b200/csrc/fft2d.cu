@@ -172,6 +172,39 @@ __global__ void k_fg(const double2* __restrict__ K, const double* __restrict__ g
     o[3] = T(D(u) * D(v));
 }
 
+// Per-frequency table of the column pass at a FIXED mu (the reference's
+// monte_carlo: deterministic_spectrum and random_greens both at gs.mu,
+// solver.cpp:350-351,361): F_det = fk / den1 is then sample-invariant, so it
+// is divided once here (fp64) instead of per pair. One 16-byte load per (u, v):
+// {F_det.re, F_det.im, fk.re, fk.im}; den1 = 1 - alpha g - mu beta fk is rebuilt
+// in the pass from the (L1-resident) alpha-multiplier table g(du, v). Padded
+// columns (v > n) are zero. *flag gets 1 if |den1|^2 < 1e-12 anywhere
+// (check_denominator, greens.cpp:32-39).
+template <typename T>
+__global__ void k_fgm(const double2* __restrict__ K, const double* __restrict__ g_sp0, int n, int hp, double alpha,
+                      double mub, T* __restrict__ fg, int* __restrict__ flag) {
+    const int m = 2 * n, u = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= hp) return;
+    T* o = fg + (static_cast<size_t>(u) * hp + v) * 4;
+    if (v > n) {
+        for (int k = 0; k < 4; ++k) o[k] = T(0);
+        return;
+    }
+    const double2 z = K[static_cast<size_t>(u) * m + v];
+    const int c = n / 2, du = u <= m - u ? u : m - u;
+    auto cl = [n](int i) { return i < 0 ? 0 : (i > n - 1 ? n - 1 : i); };
+    const int ip = cl(c + du), im = cl(c - du), jp = cl(c + v), jm = cl(c - v);
+    const double s = g_sp0[ip * n + jp] + g_sp0[ip * n + jm] + g_sp0[im * n + jp] + g_sp0[im * n + jm];
+    const double ag = alpha * (g_sp0[c * n + c] - 0.25 * s);
+    const double d1x = 1.0 - ag - mub * z.x, d1y = -mub * z.y;
+    const double dd = d1x * d1x + d1y * d1y;
+    if (dd < 1e-12) atomicOr(flag, 1);
+    o[0] = T((z.x * d1x + z.y * d1y) / dd);  // fk / den1
+    o[1] = T((z.y * d1x - z.x * d1y) / dd);
+    o[2] = T(z.x);
+    o[3] = T(z.y);
+}
+
 }  // namespace gtb
 
 using namespace gtb;
@@ -199,6 +232,7 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
     if (fp64) {
         k_fk_half<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                       static_cast<double2*>(fk_out));
+        cudaMemsetAsync(gtab_out, 0, sizeof(double) * (n + 1) * hp, st);
         k_gtab<double><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                           static_cast<double*>(gtab_out));
         if (fg_out)
@@ -206,11 +240,26 @@ int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, 
     } else {
         k_fk_half<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, m, hp,
                                                                      static_cast<float2*>(fk_out));
+        cudaMemsetAsync(gtab_out, 0, sizeof(float) * (n + 1) * hp, st);  // padded columns v > n read as 0
         k_gtab<float><<<dim3((n + 1 + 127) / 128, n + 1), 128, 0, st>>>(g_sp0_d, n, hp,
                                                                          static_cast<float*>(gtab_out));
         if (fg_out)
             k_fg<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, alpha, static_cast<float*>(fg_out));
     }
+    return static_cast<int>(cudaGetLastError());
+}
+
+int gtd_greens_fgm(const void* work_d, const double* g_sp0_d, int n, int hp, int fp64, double alpha, double mub,
+                   void* fgm_out, int* flag_d, cudaStream_t st) {
+    const int m = 2 * n;
+    const double2* K = static_cast<const double2*>(work_d);
+    cudaMemsetAsync(flag_d, 0, sizeof(int), st);
+    if (fp64)
+        k_fgm<double><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, alpha, mub,
+                                                                  static_cast<double*>(fgm_out), flag_d);
+    else
+        k_fgm<float><<<dim3((hp + 127) / 128, m), 128, 0, st>>>(K, g_sp0_d, n, hp, alpha, mub,
+                                                                 static_cast<float*>(fgm_out), flag_d);
     return static_cast<int>(cudaGetLastError());
 }
 

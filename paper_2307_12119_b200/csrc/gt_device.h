@@ -21,6 +21,7 @@ typedef struct gtd_sample_stats {
     double mu;           /* mean leakage used for p_var             */
     unsigned long long max_bits; /* double bits of max rise (rise >= 0) */
     int status;          /* bit flags, GTD_ST_*                      */
+    float max_rden2;     /* max_(u,v) 1/|den2|^2 of random_greens (conditioning of the fp32 path) */
 } gtd_sample_stats;
 
 enum {
@@ -30,7 +31,9 @@ enum {
     GTD_ST_RUNAWAY_RAND = 8,  /* |den| < 1e-6 in random_greens             */
     GTD_ST_NONFINITE = 16,    /* non-finite rise                           */
     GTD_ST_NOCONVERGE = 32,   /* fixed point hit max_iters                 */
-    GTD_ST_KIRCHHOFF = 64     /* Kirchhoff inverse left its validity range */
+    GTD_ST_KIRCHHOFF = 64,    /* Kirchhoff inverse left its validity range */
+    GTD_ST_ILLCOND = 128      /* fp32 pair above the conditioning threshold that the
+                                 fp64 re-solve could not take (capacity exceeded)    */
 };
 
 /* Device-resident prepared GreensSet (reference PreparedGreens,
@@ -45,6 +48,8 @@ typedef struct gtd_greens {
     void* hs;             /* [m] complex: exp(-i pi t/m) (half-step twiddles)    */
     void* fg;             /* [m][hp] {fk.re, fk.im, alpha g(du,v), D(u)D(v)}: one vector load per frequency */
     double alpha, beta, rand_scale, mu_fixed;
+    void* fgm;            /* [m][hp][4] fixed-mu table {F_det, fk} (k_fgm)                     */
+    int det_flags;        /* GTD_ST_RUNAWAY_DET if den1 at mu_fixed fails check_denominator  */
 } gtd_greens;
 
 /* Inputs of a Monte-Carlo batch: p_leak0 = nom_scale * N * V, applied = P + p_leak0.
@@ -57,11 +62,28 @@ typedef struct gtd_mc_in {
     double nom_scale;
 } gtd_mc_in;
 
+/* fp64 re-solve of ill-conditioned fp32 pairs ("fp32 with fp64 residual check"):
+ * after the fp32 passes, pairs whose max 1/|den2|^2 (random_greens denominator,
+ * greens.cpp:243-247) exceeds `thr` are gathered (up to `cap`), solved again by
+ * the fp64 passes with a device-side count, and their maps / stats replace the
+ * fp32 ones. All buffers are device memory owned by the caller. */
+typedef struct gtd_mc_resolve {
+    const struct gtd_greens* g64; /* fp64 tables of the same GreensSet          */
+    void* in64;                   /* [cap][3][n][n] double: P, N, V              */
+    void* out64;                  /* [cap][n][n] double                          */
+    gtd_sample_stats* stats64;    /* [cap]                                       */
+    void* scratch64;              /* cap * gtd_mc_scratch_bytes_per_sample(n, 1) */
+    int* sel;                     /* [1 + cap]: count, then sample indices       */
+    int cap;
+    float thr;
+} gtd_mc_resolve;
+
 /* Options of the Monte-Carlo batch (mode A = reference run_one semantics). */
 typedef struct gtd_mc_opts {
     int mu_per_sample;  /* 1: closed forms use the sample mean leakage; 0: gs.mu */
     int with_rand;      /* 0 drops the shift-variant term (ablation)            */
     double exponent_cap;/* |ln var| guard (variation.cpp:173-178)               */
+    const gtd_mc_resolve* resolve; /* fp32 only: NULL = no fp64 re-solve        */
 } gtd_mc_opts;
 
 /* Optional profiling hook: called on the host between launches with the
@@ -80,8 +102,10 @@ int gtd_mc_batch(const gtd_greens* g, const gtd_mc_in* in, int batch,
                  const gtd_mc_opts* opts, void* out, gtd_sample_stats* stats, void* scratch,
                  int chunk, cudaStream_t stream, gtd_mark_fn mark, void* ctx);
 
-/* Number of kernel launches gtd_mc_batch issues for a given batch/chunk. */
+/* Number of kernel launches gtd_mc_batch issues for a given batch/chunk
+ * (resolve: 1 if the fp64 re-solve is attached). */
 int gtd_mc_launch_count(int batch, int chunk);
+int gtd_mc_resolve_launch_count(void);
 
 #ifdef __cplusplus
 }
@@ -95,6 +119,10 @@ int gtd_padded_width(int n, int fp64);
 /* Batched in-place 2-D complex FFT of [batch][m][m] (sign -1 forward,
  * +1 inverse without 1/m^2); tw = m complex twiddles of the same precision. */
 int gtd_fft2d(void* data, int m, int batch, int sign, int fp64, const void* tw, cudaStream_t st);
+/* Fixed-mu column-pass table from the full fp64 fk in work_d (after gtd_greens_tables);
+ * mub = mu * beta; *flag_d = 1 if den1 fails the runaway check. */
+int gtd_greens_fgm(const void* work_d, const double* g_sp0_d, int n, int hp, int fp64, double alpha, double mub,
+                   void* fgm_out, int* flag_d, cudaStream_t st);
 /* GreensSet device tables from fp64 f_sp0 / g_sp0 (device n x n maps). */
 int gtd_greens_tables(const double* f_sp0_d, const double* g_sp0_d, double phi, int n, int hp,
                       int fp64, const void* tw64_d, void* work_d, void* fk_out, void* gtab_out, void* fg_out,

@@ -21,10 +21,12 @@ struct Real;
 template <>
 struct Real<float> {
     static constexpr float max() { return 3.402823466e38f; }
+    static constexpr float min_pos() { return 1.175494351e-38f; }
 };
 template <>
 struct Real<double> {
     static constexpr double max() { return 1.7976931348623157e308; }
+    static constexpr double min_pos() { return 1e-300; }
 };
 
 // ---------------------------------------------------------------- reductions
@@ -114,6 +116,9 @@ struct MCIn {
     const T* V;
     long long sP, sN, sV;
     T nom_scale;
+    double nom64;     // nom_scale as the caller gave it (the fp64 re-solve must not inherit its fp32 rounding)
+    const int* dcnt;  // optional device sample count (fp64 re-solve of selected pairs): min(*dcnt, count)
+    __device__ __forceinline__ int eff_count(int count) const { return dcnt ? min(*dcnt, count) : count; }
     __device__ __forceinline__ const T* p(size_t s) const { return P + s * sP; }
     __device__ __forceinline__ const T* nn(size_t s) const { return N + s * sN; }
     __device__ __forceinline__ const T* v(size_t s) const { return V + s * sV; }

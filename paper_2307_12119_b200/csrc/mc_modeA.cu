@@ -24,6 +24,8 @@
 //                     Hadamard term, clamp, per-sample max / sum.
 // F(p_var) is formed in pass 2 as F(p_leak0) - mu * K1 with K1 = k1 (x) k1 the
 // analytic spectrum of the centred die box, so pass 1 never waits for mu.
+#include <type_traits>
+
 #include "mc_common.cuh"
 
 namespace gtb {
@@ -77,6 +79,39 @@ struct ClosedForm {
     __device__ __forceinline__ int flags() const {
         return (mn1 < T(1e-12) ? GTD_ST_RUNAWAY_DET : 0) | (mn2 < T(1e-12) ? GTD_ST_RUNAWAY_RAND : 0);
     }
+};
+
+// Closed forms at a fixed mu (mu_per_sample = 0: the reference monte_carlo,
+// solver.cpp:350-351,361). F_det is a table (k_fgm), so per frequency only the
+// random part remains: with t1 = beta fk q + alpha g F(p_var) and
+// den2 = den1 - t1, F_rand = F_det t1 / den2 (greens.cpp:241-248), one
+// reciprocal; Y = F_det A_hat. F(p_var) arrives complete (the mu K1
+// correction is applied to the B row spectra in stage 0).
+template <typename T, int M>
+struct ClosedFormMF {
+    using V4 = typename Vec4<T>::type;
+    static constexpr int hp = MCGeom<T, M>::hp;
+    const V4* __restrict__ fg;  // [m][hp] {F_det, fk}
+    const T* __restrict__ gt;   // [n+1][hp] g(du, v) (alpha multiplier, zero-padded)
+    T alpha, mb;                // alpha, mu beta
+    T bq4, bqs;                 // beta q = bq4 (S[ip] + S[im]) + bqs
+    T mn2;                      // running minimum of |den2|^2
+    __device__ __forceinline__ V4 table(int u, int v) const { return fg[static_cast<size_t>(u) * hp + v]; }
+    __device__ __forceinline__ T g(int du, int v) const { return gt[du * hp + v]; }
+    // C: real DCT coefficient of the applied map (A_hat = ph C); b: F(p_var) in, F_rand out.
+    __device__ __forceinline__ cplx<T> eval(T C, cplx<T>& b, T ssum, cplx<T> ph, const V4& t, T gv) {
+        const T ag = alpha * gv;
+        const T bq = bq4 * ssum + bqs;
+        const cplx<T> t1 = mk<T>(fma(bq, t.z, ag * b.x), fma(bq, t.w, ag * b.y));
+        const cplx<T> den2 = mk<T>(fma(-mb, t.z, T(1) - ag) - t1.x, fma(-mb, t.w, -t1.y));
+        const T d2 = cabs2<T>(den2);
+        mn2 = fmin(mn2, d2);
+        const cplx<T> fd = mk<T>(t.x, t.y);
+        const cplx<T> num = cscale<T>(cmul<T>(t1, cconj<T>(den2)), fast_rcp(d2));
+        b = cmul<T>(fd, num);
+        return cscale<T>(cmul<T>(fd, ph), C);
+    }
+    __device__ __forceinline__ int flags() const { return mn2 < T(1e-12) ? GTD_ST_RUNAWAY_RAND : 0; }
 };
 
 template <typename T, int GA, int M>
@@ -152,13 +187,13 @@ struct FwdStagesAB {
 //   the address; the centre embedding leaves half the B inputs zero), the last
 //   forward stage, the closed forms and the first inverse stage run in
 //   registers, and the last inverse stage writes the kept rows to global.
-template <typename T, int M>
+template <typename T, int M, bool MF>
 __global__ void __launch_bounds__(MCGeom<T, M>::NT2, MCGeom<T, M>::MINB2)
 mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
          cplx<T>* __restrict__ Yspec, cplx<T>* __restrict__ Bspec, const T* __restrict__ Srow,
          gtd_sample_stats* __restrict__ stats, const cplx<T>* __restrict__ g_tw,
          const cplx<T>* __restrict__ g_hs, const T* __restrict__ fgtab, T alpha, T beta, int mu_per_sample,
-         T mu_fixed) {
+         T mu_fixed, const cplx<T>* __restrict__ g_k1, const T* __restrict__ g_gtab) {
     using Gm = MCGeom<T, M>;
     using Pl = Plan<M>;
     constexpr int n = Gm::n, c = Gm::c, h = Gm::h, L = Gm::L, NT = Gm::NT2, W = Gm::W;
@@ -179,6 +214,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
     constexpr int TWF = StageTw<M, false>::SIZE, TWI = StageTw<M, true>::SIZE;
     static_assert(K >= 2 && Pl::fr(0) == 8 && RI == 8, "plan");
     static_assert((M / 8) * W % NT == 0 && BPTI >= 1, "threads");
+    static_assert(NT % GA == 0, "a thread's column group is the same in every stage-0 butterfly");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
     cplx<T>* s_twf = tile + (IL::SIZE > FL::SIZE ? IL::SIZE : FL::SIZE);
@@ -189,6 +225,7 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
     build_stage_tw<T, M, false, NT>(s_twf, g_tw);
     build_stage_tw<T, M, true, NT>(s_twi, g_tw);
     load_twiddles<T, M, NT>(s_hs, g_hs);
+    count = in.eff_count(count);
     for (int item = blockIdx.x; item < count * CT; item += gridDim.x) {
         // column-tile-major order: a CTA revisits the same column tile for
         // successive samples, so that tile's closed-form table stays in L1
@@ -202,6 +239,18 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
         const size_t sbase = static_cast<size_t>(s) * n * hp;
         __syncthreads();  // previous item's readers of tile / s_srow are done (and the tables are built)
 
+        // mu K1 correction of the B rows (fixed-mu closed forms): the row spectrum
+        // of the centred p_var row is B - mu k1(v) (p_var = p_leak0 - mu on the die)
+        const double n2 = double(n) * double(n);
+        const double mu_s = stats[sg].sum_leak / n2;
+        cplx<T> k1m[CG];
+        if constexpr (MF) {
+#pragma unroll
+            for (int col = 0; col < CG; ++col) {
+                const cplx<T> k = g_k1[v0 + (threadIdx.x % GA) + col * GA];
+                k1m[col] = mk<T>(T(mu_s) * k.x, T(mu_s) * k.y);
+            }
+        }
         // ---- forward stage 0 (radix 8, NS = 1) straight from the row spectra
         cplx<T> v[B0][3][8];
 #pragma unroll
@@ -222,6 +271,10 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                     const cplx<T>* bp = Bspec + sbase + static_cast<size_t>(xb) * hp + va;
                     v[b][1][r] = bp[0];
                     v[b][2][r] = CG == 2 ? bp[GA] : mk<T>(T(0), T(0));
+                    if constexpr (MF) {
+                        v[b][1][r] = csub<T>(v[b][1][r], k1m[0]);
+                        if (CG == 2) v[b][2][r] = csub<T>(v[b][2][r], k1m[CG - 1]);
+                    }
                 }
             }
         }
@@ -285,22 +338,28 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
             if (idx < n * W) s_srow[(idx / W) * W + idx % W] = sv[k];
         }
         // Per-sample scalars (pass 1 has completed: kernel boundary).
-        const double n2 = double(n) * double(n);
-        const double mu_s = stats[sg].sum_leak / n2;
         const T* Nm = in.nn(sg);
         const T* Vm = in.v(sg);
-        ClosedForm<T, M> cf;
+        using CF = std::conditional_t<MF, ClosedFormMF<T, M>, ClosedForm<T, M>>;
+        CF cf;
         cf.fg = reinterpret_cast<const typename Vec4<T>::type*>(fgtab);
-        cf.mug = mu_per_sample ? T(mu_s) : mu_fixed;
-        cf.mb = cf.mug * beta;
-        cf.mus = T(mu_s);
+        if constexpr (MF) {
+            cf.mb = mu_fixed * beta;
+            cf.alpha = alpha;
+            cf.gt = g_gtab;
+        } else {
+            cf.mug = mu_per_sample ? T(mu_s) : mu_fixed;
+            cf.mb = cf.mug * beta;
+            cf.mus = T(mu_s);
+            cf.mn1 = Real<T>::max();
+        }
         cf.bq4 = T(0.25) * beta;
         {
             const T pl_cc = in.nom_scale * Nm[c * n + c] * Vm[c * n + c];
             const T pl_00 = in.nom_scale * Nm[0] * Vm[0];
             cf.bqs = beta * T(double(pl_cc) - double(pl_00) - mu_s);  // q shift, greens.cpp:177-184
         }
-        cf.mn1 = cf.mn2 = Real<T>::max();
+        cf.mn2 = Real<T>::max();
         __syncthreads();
         // ---- middle forward stages
         FwdStagesAB<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
@@ -348,10 +407,14 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                         // (v > n) see an all-zero table entry and S = 0: they evaluate to 0.
                         const int du = u <= M - u ? u : M - u;
                         const int sp = min(c + du, n - 1) * W, sm = max(c - du, 0) * W;
-                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
                         cplx<T> bb = z[b][1 + col][q];
-                        yr[0][q] = cf.eval(col == 0 ? z[b][0][q].x : z[b][0][q].y, bb,
-                                           s_srow[sp + w] + s_srow[sm + w], ph, cf.table(u, vv));
+                        const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+                        if constexpr (MF)
+                            yr[0][q] = cf.eval(col == 0 ? z[b][0][q].x : z[b][0][q].y, bb,
+                                               s_srow[sp + w] + s_srow[sm + w], ph, cf.table(u, vv), cf.g(du, vv));
+                        else
+                            yr[0][q] = cf.eval(col == 0 ? z[b][0][q].x : z[b][0][q].y, bb,
+                                               s_srow[sp + w] + s_srow[sm + w], ph, cf.table(u, vv));
                         yr[1][q] = bb;
                     }
                     dftR<RL, +1, T>(yr[0]);
@@ -364,6 +427,11 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
             __syncthreads();
         }
         or_flags(&stats[sg].status, cf.flags());
+        {   // conditioning: max 1/|den2|^2 (positive floats order like their bit patterns)
+            const float rd = float(T(1) / fmax(cf.mn2, Real<T>::min_pos()));
+            const float wm = warp_max_t<float>(rd);
+            if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(&stats[sg].max_rden2), __float_as_int(wm));
+        }
         // ---- middle inverse stages
         InvStagesPairs<T, M, W, NT, 1, K - 1>::run(tile, s_twi);
         // ---- last inverse stage (radix 8, NS = M/8): keep rows [0, n) of Y, rows rho(x) of R
@@ -395,12 +463,70 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
     }
 }
 
-__global__ void mc_finalize(gtd_sample_stats* stats, int sample0, int count, int n) {
+__global__ void mc_finalize(gtd_sample_stats* stats, int sample0, int count, int n, int det_flags,
+                            const int* dcnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (dcnt) count = min(*dcnt, count);
     if (i >= count) return;
     gtd_sample_stats& st = stats[sample0 + i];
+    st.status |= det_flags;  // fixed-mu den1 runaway (checked once when the table was built)
     st.max_rise = __longlong_as_double(static_cast<long long>(st.max_bits));
     st.mean_rise = st.sum_rise / (double(n) * double(n));
+}
+
+// ------------------------------------------------- fp64 re-solve of ill-conditioned pairs
+// Pairs whose fp32 closed forms met a near-singular random_greens denominator
+// (max 1/|den2|^2 > thr) amplify the fp32 rounding of their inputs beyond the
+// 1e-3 K bar; they are solved again in fp64 (BASELINE config 1: "fp32 with fp64
+// residual check"). sel[0] counts, sel[1..cap] lists the selected samples.
+__global__ void mc_resolve_select(gtd_sample_stats* __restrict__ stats, int batch, float thr, int* __restrict__ sel,
+                                  int cap) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch) return;
+    gtd_sample_stats& st = stats[i];
+    if (st.status != 0 || !(st.max_rden2 > thr)) return;  // failed pairs stay failed
+    const int slot = atomicAdd(sel, 1);
+    if (slot < cap)
+        sel[1 + slot] = i;
+    else
+        st.status |= GTD_ST_ILLCOND;
+}
+
+// fp32 inputs of the selected pairs -> fp64 [slot][P, N, V] (exact widening).
+template <typename T>
+__global__ void mc_resolve_gather(const MCIn<T> in, const int* __restrict__ sel, int cap, int n,
+                                  double* __restrict__ in64) {
+    const int slot = blockIdx.y;
+    if (slot >= min(sel[0], cap)) return;
+    const size_t s = static_cast<size_t>(sel[1 + slot]), nn = static_cast<size_t>(n) * n;
+    const T* P = in.p(s);
+    const T* N = in.nn(s);
+    const T* V = in.v(s);
+    double* o = in64 + slot * 3 * nn;
+    for (size_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += gridDim.x * blockDim.x) {
+        o[k] = double(P[k]);
+        o[nn + k] = double(N[k]);
+        o[2 * nn + k] = double(V[k]);
+    }
+}
+
+// fp64 results -> the fp32 outputs and stats of the selected pairs; a negative
+// max_rden2 marks a pair as re-solved in fp64.
+template <typename T>
+__global__ void mc_resolve_scatter(const int* __restrict__ sel, int cap, int n, const double* __restrict__ out64,
+                                   const gtd_sample_stats* __restrict__ stats64, T* __restrict__ out,
+                                   gtd_sample_stats* __restrict__ stats) {
+    const int slot = blockIdx.y;
+    if (slot >= min(sel[0], cap)) return;
+    const size_t s = static_cast<size_t>(sel[1 + slot]), nn = static_cast<size_t>(n) * n;
+    if (out)
+        for (size_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += gridDim.x * blockDim.x)
+            out[s * nn + k] = T(out64[slot * nn + k]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const float rd = stats[s].max_rden2;
+        stats[s] = stats64[slot];
+        stats[s].max_rden2 = -rd;
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -424,8 +550,12 @@ struct MCLaunch {
         if (!sms) {
             res[0] = mc_rows_setup<T, M>(1);
             res[2] = mc_rows_setup<T, M>(3);
-            cudaFuncSetAttribute(mc_pass2<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M>, Gm::NT2, smem2());
+            cudaFuncSetAttribute(mc_pass2<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
+            cudaFuncSetAttribute(mc_pass2<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M, false>, Gm::NT2, smem2());
+            int r2 = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, mc_pass2<T, M, true>, Gm::NT2, smem2());
+            res[1] = r2 < res[1] ? r2 : res[1];
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -469,6 +599,9 @@ struct MCLaunch {
         // pass 1 stages P and V rows and takes N = P (the Monte-Carlo entries' nominal leakage map)
         const bool tma1 = GT_P3_TMA && in.N == in.P && in.sN == in.sP && al16(in.P, in.sP) && al16(in.V, in.sV) &&
                           (n * sizeof(T)) % 16 == 0;
+        // fixed-mu closed forms (the reference monte_carlo's gs.mu) read the k_fgm table
+        static const int no_fgm = getenv("GT_MC_NO_FGM") ? atoi(getenv("GT_MC_NO_FGM")) : 0;  // A/B switch
+        const bool mf = !o->mu_per_sample && g->fgm != nullptr && !no_fgm;
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
         if (slots == 2) {
             cudaEventRecord(ev_fork, st);
@@ -490,9 +623,15 @@ struct MCLaunch {
             if (mk_) mk_(ctx, 0, ss);
             mc_rows_launch<T, M>(1, tma1, sms, per_sm(res[0]), ss, ra);
             if (mk_) mk_(ctx, 1, ss);
-            mc_pass2<T, M><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), ss>>>(
-                in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fg), T(g->alpha), T(g->beta),
-                o->mu_per_sample, T(g->mu_fixed));
+            const cplx<T>* k1 = static_cast<const cplx<T>*>(g->k1);
+            if (mf)
+                mc_pass2<T, M, true><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), ss>>>(
+                    in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fgm), T(g->alpha),
+                    T(g->beta), 0, T(g->mu_fixed), k1, static_cast<const T*>(g->gtab));
+            else
+                mc_pass2<T, M, false><<<grid(cnt * CT, res[1]), Gm::NT2, smem2(), ss>>>(
+                    in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fg), T(g->alpha),
+                    T(g->beta), o->mu_per_sample, T(g->mu_fixed), k1, nullptr);
             if (mk_) mk_(ctx, 2, ss);
             mc_rows_launch<T, M>(3, tma3, sms, per_sm(res[2]), ss, ra);
             if (mk_) mk_(ctx, 3, ss);
@@ -501,7 +640,33 @@ struct MCLaunch {
             cudaEventRecord(ev_join, aux);
             cudaStreamWaitEvent(st, ev_join, 0);
         }
-        mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n);
+        mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n, mf ? g->det_flags : 0, in.dcnt);
+        if constexpr (sizeof(T) == 4) {
+            if (o->resolve) {
+                const gtd_mc_resolve* r = o->resolve;
+                const size_t nn = static_cast<size_t>(n) * n;
+                cudaMemsetAsync(r->sel, 0, sizeof(int), st);
+                mc_resolve_select<<<(batch + 255) / 256, 256, 0, st>>>(stats, batch, r->thr, r->sel, r->cap);
+                mc_resolve_gather<T><<<dim3(32, r->cap), 256, 0, st>>>(in, r->sel, r->cap, n,
+                                                                         static_cast<double*>(r->in64));
+                MCIn<double> i64;
+                i64.P = static_cast<const double*>(r->in64);
+                i64.N = i64.P + nn;
+                i64.V = i64.P + 2 * nn;
+                i64.sP = i64.sN = i64.sV = static_cast<long long>(3 * nn);
+                i64.nom_scale = in.nom64;
+                i64.nom64 = in.nom64;
+                i64.dcnt = r->sel;
+                gtd_mc_opts o64 = *o;
+                o64.resolve = nullptr;
+                const int e = MCLaunch<double, M>::run(r->g64, i64, r->cap, &o64, static_cast<double*>(r->out64),
+                                                       r->stats64, r->scratch64, r->cap, st, nullptr, nullptr);
+                if (e) return e;
+                mc_resolve_scatter<T><<<dim3(32, r->cap), 256, 0, st>>>(r->sel, r->cap, n,
+                                                                          static_cast<const double*>(r->out64),
+                                                                          r->stats64, out, stats);
+            }
+        }
         return static_cast<int>(cudaGetLastError());
     }
 };
@@ -522,6 +687,8 @@ static int dispatch_mc(const gtd_greens* g, const gtd_mc_in* i, int batch, const
     in.sN = i->sN;
     in.sV = i->sV;
     in.nom_scale = T(i->nom_scale);
+    in.nom64 = i->nom_scale;
+    in.dcnt = nullptr;
     T* O = static_cast<T*>(out);
     switch (g->m) {
         case 32: return MCLaunch<T, 32>::run(g, in, batch, o, O, stats, scratch, chunk, st, mark, ctx);
@@ -559,6 +726,8 @@ size_t gtd_mc_scratch_bytes_per_sample(int n, int fp64) {
     const size_t cb = fp64 ? 16 : 8, rb = fp64 ? 8 : 4;
     return static_cast<size_t>(n) * hp * (2 * cb + 2 * rb);
 }
+
+int gtd_mc_resolve_launch_count(void) { return 3 + 4 + 1; }  // select, gather, 3 passes, finalize, scatter
 
 int gtd_mc_launch_count(int batch, int chunk) {
     const int chunks = (batch + chunk - 1) / chunk;

@@ -38,6 +38,7 @@ mc_pass1(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     double* red = reinterpret_cast<double*>(s_tw + M);
 
     load_twiddles<T, M, NT>(s_tw, g_tw);
+    count = in.eff_count(count);
     for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
         const int s = item / RB;
         const int x0 = (item - s * RB) * L;
@@ -146,6 +147,7 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
     double* red = reinterpret_cast<double*>(s_tw + M);
 
     load_twiddles<T, M, NT>(s_tw, g_tw);
+    count = in.eff_count(count);
     for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
         const int s = item / RB;
         const int x0 = (item - s * RB) * L;
@@ -247,6 +249,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
     for (int t = threadIdx.x; t < M; t += WARPS * 32) s_tw[t] = g_tw[t];
     for (int t = threadIdx.x; t < n; t += WARPS * 32) s_hs[t] = g_hs[t];
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS * 32);
+    count = in.eff_count(count);
     const int stride = gridDim.x * WARPS, total = count * n;
     auto request = [&](int item) {  // lane 0: the P and V rows of `item` into this warp's staging area
         const int s = item / n, x = item - s * n;
@@ -405,6 +408,7 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
     uint64_t* mbar = reinterpret_cast<uint64_t*>(stage + (WARPS3 - warp) * SG::BYTES) + warp;
     for (int t = threadIdx.x; t < M; t += WARPS3 * 32) s_tw[t] = g_tw[t];
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, WARPS3 * 32);
+    count = in.eff_count(count);
     const int stride = gridDim.x * WARPS3, total = count * n;
     // lane 0 requests the four row segments of `item` into this warp's staging area
     auto request = [&](int item) {

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-GT_SAMPLE_NONFINITE, GT_SAMPLE_KIRCHHOFF, GT_SAMPLE_NOCONVERGE = 0x4, 0x8, 0x10
+from .api import GT_SAMPLE_KIRCHHOFF, GT_SAMPLE_NOCONVERGE, GT_SAMPLE_NONFINITE  # noqa: F401  (header values)
 
 
 def column_ranges(h: int, world: int) -> list[tuple[int, int]]:

@@ -106,5 +106,5 @@ def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path):
     ref, _ = fixed_point_numpy(P, V, baseline_fk(f, phi), 0.3, 0.017, 0, 1e-30, 3)
     err = np.abs(res.t.cpu().numpy() - ref).max()
     print(f"large n=2048: 3 iterations, max|dT| {err:.3e} K on peak {ref.max():.2f} K")
-    assert res.iterations == 3 and res.status == slab.GT_SAMPLE_NOCONVERGE
+    assert res.iterations == 3 and res.status == slab.GT_SAMPLE_NOCONVERGE == 32
     assert err <= 1e-9 * max(1.0, ref.max())

@@ -94,6 +94,29 @@ def test_mc_config1_grid_fp32(b200lib, oracle, greens256):
         assert err <= atol
 
 
+@pytest.mark.parametrize("mu_per_sample", [0, 1])
+def test_mc_config1_grid_maps_both_mu_modes(b200lib, oracle, greens256, mu_per_sample):
+    """Maps at the headline grid for both closed-form mu semantics: 0 = the reference
+    monte_carlo (F_det and F_rand at gs.mu, solver.cpp:350-351,361: the fixed-mu
+    table kernel), 1 = per-sample mean leakage. fp32 <= 1e-3 K, fp64 <= 1e-8 K."""
+    from paper_2307_12119_b200 import inputs
+    cfg = inputs.CONFIGS["cfg1"]
+    B = 8
+    p = inputs.power_batch(cfg, 100, B, np.float32)
+    v = inputs.variation_batch(cfg, 100, B).numpy().astype(np.float32)
+    t_ref, mx_ref, mean_ref, st_ref, _ = oracle.mc_batch(greens256, p, v, mu_per_sample=mu_per_sample, jobs=8)
+    assert (st_ref == 0).all()
+    for prec, atol in ((0, FP32_ATOL), (1, FP64_ATOL)):
+        dg = _dg(greens256, prec)
+        out, mx, mean, st, _ = dg.mc_batch_host(p, v, dg.opts(mu_per_sample=mu_per_sample))
+        assert (st == 0).all()
+        err = np.abs(out.astype(np.float64) - t_ref).max()
+        print(f"n=256 mu_per_sample={mu_per_sample} prec={prec} max|dT|={err:.3e} K (peak {t_ref.max():.1f} K)")
+        assert err <= atol
+        np.testing.assert_allclose(mx, mx_ref, rtol=0, atol=atol)
+        np.testing.assert_allclose(mean, mean_ref, rtol=0, atol=atol)
+
+
 def test_mc_sample_status_isolated(b200lib, g64, golden):
     """A bad sample is flagged (check_power / exponent cap) without touching its neighbours."""
     p = golden["p_dyn"].astype(np.float64).copy()
@@ -233,3 +256,61 @@ def test_profile_modes(b200lib, g64, golden):
     assert (k0, c0) == (k1, c1) and c0 == 3
     with pytest.raises(Exception):
         dg.profile_begin(2)
+
+
+def _cfg1_pairs(idx):
+    """Config-1 pairs by global sample index, generated as bench.py does (fp32 on the device)."""
+    import torch
+    from paper_2307_12119_b200 import inputs
+    P, V = inputs.mc_inputs(inputs.CONFIGS["cfg1"], 0, max(idx) + 1, device="cuda", torch_dtype=torch.float32)
+    sel = torch.tensor(idx, device="cuda")
+    return P[sel].cpu().numpy(), V[sel].cpu().numpy()
+
+
+@pytest.mark.parametrize("mu_per_sample", [0, 1])
+def test_mc_fp64_resolve_of_ill_conditioned_pairs(b200lib, greens256, mu_per_sample):
+    """'fp32 with fp64 residual check' (BASELINE config 1): config-1 pairs whose random_greens
+    denominator comes close to singular (pairs 25, 63, 114, 454 of the bench batch: fp32 error up
+    to 1.3e-2 K without the check) are re-solved in fp64 on the device; every pair then meets
+    1e-3 K against the fp64 path, and the re-solved ones are marked by a negative max_rden2."""
+    from paper_2307_12119_b200.api import SAMPLE_STATS_DTYPE  # noqa: F401
+    idx = [25, 63, 114, 454, 0, 1, 2, 3, 270, 5, 6, 7, 8, 9, 10, 11]
+    p, v = _cfg1_pairs(idx)
+    d64 = _dg(greens256, 1)
+    ref = d64.mc_batch_host(p.astype(np.float64), v.astype(np.float64), d64.opts(mu_per_sample=mu_per_sample))
+    d32 = _dg(greens256, 0)
+    raw = d32.mc_batch_host(p, v, d32.opts(mu_per_sample=mu_per_sample, fp64_check=-1.0))
+    chk = d32.mc_batch_host(p, v, d32.opts(mu_per_sample=mu_per_sample))
+    e_raw = np.abs(raw[0].astype(np.float64) - ref[0]).reshape(len(idx), -1).max(1)
+    e_chk = np.abs(chk[0].astype(np.float64) - ref[0]).reshape(len(idx), -1).max(1)
+    print(f"mu_per_sample={mu_per_sample}: fp32 max err without check {e_raw.max():.3e} K, with {e_chk.max():.3e} K")
+    assert e_raw.max() > FP32_ATOL  # the check is needed on these pairs
+    assert (chk[3] == 0).all()
+    assert e_chk.max() <= FP32_ATOL
+    np.testing.assert_allclose(chk[1], ref[1], rtol=0, atol=FP32_ATOL)
+
+
+def test_mc_fp64_resolve_capacity(b200lib, g64, golden):
+    """Threshold below every pair: all pairs qualify, the first batch/16 (min 8) are re-solved
+    in fp64 (marked by max_rden2 < 0, results = the fp64 path) and the rest carry
+    GT_SAMPLE_ILLCOND (128) with their fp32 results."""
+    import torch
+    from paper_2307_12119_b200.api import SAMPLE_STATS_DTYPE
+    p = np.concatenate([golden["p_dyn"]] * 3)
+    v = np.concatenate([golden["var"]] * 3)
+    B = p.shape[0]
+    d64 = _dg(g64, 1)
+    ref = d64.mc_batch_host(p.astype(np.float64), v.astype(np.float64), d64.opts(mu_per_sample=0))[0]
+    d32 = _dg(g64, 0)
+    P, V = torch.from_numpy(p.astype(np.float32)).cuda(), torch.from_numpy(v.astype(np.float32)).cuda()
+    out = torch.empty_like(P)
+    stats = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    d32.mc_batch_device(P.data_ptr(), V.data_ptr(), B, d32.opts(mu_per_sample=0, fp64_check=1e-30), out.data_ptr(),
+                        stats.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=SAMPLE_STATS_DTYPE)
+    resolved = st["max_rden2"] < 0
+    assert resolved.sum() == 8 and ((st["status"] == 128) == ~resolved).all()
+    o = out.double().cpu().numpy()
+    np.testing.assert_allclose(o[resolved], ref[resolved].astype(np.float32).astype(np.float64), rtol=0, atol=1e-9)
+    assert np.abs(o[~resolved] - ref[~resolved]).max() <= FP32_ATOL
