@@ -626,8 +626,9 @@ def run_b200(args, cfg):
                            mx_d.data_ptr(), None, stream.cuda_stream)
         torch.cuda.synchronize()
         st_lit = st_d[:k].cpu().numpy()
-        lin = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4 if prec == GT_FP64 else 2e-4,
-                         max_iters=200)
+        # tol 1e-4 K (BASELINE config 0/1); an fp32 handle iterates to 5e-4 K in fp32, then
+        # finishes in fp64 warm-started from it ("fp32 with fp64 residual check")
+        lin = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4, max_iters=200)
         dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, lin, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
                            mx_d.data_ptr(), None, stream.cuda_stream)
         torch.cuda.synchronize()
@@ -651,6 +652,7 @@ def run_b200(args, cfg):
             "linear_law": {"value": ws * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
                            "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
                            "failed": int((stl != 0).sum()), "tol_K": lin.tol,
+                           "precision": "fp32 to 5e-4 K, then fp64 to 1e-4 K" if prec == GT_FP32 else "fp64",
                            "bytes_per_iteration_model": b_it,
                            "achieved_GBps_model": b_it * float(its.sum()) / (msb / 1e3) / 1e9}}
 

@@ -123,6 +123,10 @@ typedef struct gt_fp_opts {
     double beta, t_ambient, eta, tol;
     int max_iters;
     int chunk;
+    double fp32_stage_tol; /* GT_FP32 handles (BASELINE config 1: "fp32 with fp64 residual
+                              check"): the fp32 iteration stops at this tolerance, then
+                              fp64 iterations warm-started from it finish to `tol`
+                              (0 = default 5e-4; < 0 = fp32 only). Iteration counts add up. */
 } gt_fp_opts;
 
 void gt_fp_opts_default(gt_fp_opts* o);

@@ -81,7 +81,8 @@ template <typename T, int M, bool FIRST>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
 fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
         FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
-        const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient) {
+        const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient,
+        int warm) {
     using Gm = FPGeom<T, M>;
     constexpr int n = Gm::n, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT, hp = Gm::hp;
     constexpr int RB = Gm::RB;
@@ -162,7 +163,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                         told[u][half] = pv[u][half] = lv[u][half] = T(0);
                         if (i0 + u < IPT && idx < L * n && x < n) {
                             const size_t o = static_cast<size_t>(x + half) * n + j;
-                            if (!FIRST) told[u][half] = Ts[o];
+                            if (!FIRST || warm) told[u][half] = Ts[o];
                             pv[u][half] = P[o];
                             lv[u][half] = in.nom_scale * Nm[o] * V[o];
                         }
@@ -179,7 +180,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                         const cplx<T> z = FIRST ? mk<T>(T(0), T(0)) : tile[j * LP + l];
 #pragma unroll
                         for (int half = 0; half < 2; ++half) {
-                            T t = T(0);
+                            T t = FIRST ? told[u][half] : T(0);  // warm start: the caller's T_0
                             if (!FIRST) {
                                 const T th = (half ? z.y : z.x) * inv;  // theta - T0
                                 t = th;
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(FPW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
 fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec, T* __restrict__ Ar,
           T* __restrict__ Tst, FPState* __restrict__ state, int* __restrict__ status,
           const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka,
-          T kb, T kexp, T t_ambient) {
+          T kb, T kexp, T t_ambient, int warm) {
     using Gm = FPGeom<T, M>;
     using WF = WarpFFT<T, M>;
     constexpr int n = Gm::n, h = Gm::h, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
@@ -280,7 +281,7 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
 #pragma unroll
             for (int t = 0; t < E; ++t) {
                 const int j = lane + 32 * t;
-                if constexpr (!FIRST) {
+                if (!FIRST || warm) {  // warm start (FIRST): the caller's T_0 instead of 0
                     t0[t] = T0r[j];
                     t1[t] = T1r[j];
                 }
@@ -333,7 +334,7 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
                 t1[t] = b;
             }
             __syncwarp();
-        } else {
+        } else if (!warm) {
 #pragma unroll
             for (int t = 0; t < E; ++t) t0[t] = t1[t] = T(0);
         }
@@ -714,21 +715,21 @@ struct FPLaunch {
                 if (first)
                     fp_rows_w<T, M, true><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient));
+                        kexp, T(o->t_ambient), o->warm_start);
                 else
                     fp_rows_w<T, M, false><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient));
+                        kexp, T(o->t_ambient), o->warm_start);
             } else {
                 const int gr = grid(cnt * Gm::RB, res[0]);
                 if (first)
                     fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                      T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                     T(o->t_ambient));
+                                                                     T(o->t_ambient), o->warm_start);
                 else
                     fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                       T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                      T(o->t_ambient));
+                                                                      T(o->t_ambient), o->warm_start);
             }
         };
         for (int s0 = 0; s0 < batch; s0 += chunk) {
@@ -795,6 +796,22 @@ int fp_hp(int m) {
     }
 }
 
+__global__ void k_widen(const float* __restrict__ a, double* __restrict__ b, size_t count) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x)
+        b[i] = double(a[i]);
+}
+__global__ void k_narrow(const double* __restrict__ a, float* __restrict__ b, size_t count) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x)
+        b[i] = float(a[i]);
+}
+__global__ void k_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch) return;
+    const int it = iters[i] + it64[i];
+    iters[i] = it;
+    status[i] = st64[i] | (it > max_iters ? GTD_ST_NOCONVERGE : 0);
+}
+
 }  // namespace
 }  // namespace gtb
 
@@ -809,6 +826,20 @@ size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64) {
 }
 
 size_t gtd_fp_state_bytes(void) { return sizeof(FPState); }
+
+int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st) {
+    k_widen<<<1184, 256, 0, st>>>(src, dst, count);
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_narrow(const double* src, float* dst, size_t count, cudaStream_t st) {
+    k_narrow<<<1184, 256, 0, st>>>(src, dst, count);
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters,
+                   cudaStream_t st) {
+    k_fp_combine<<<(batch + 127) / 128, 128, 0, st>>>(iters, status, it64, st64, batch, max_iters);
+    return static_cast<int>(cudaGetLastError());
+}
 
 int gtd_fp_batch(const gtd_greens* g, const gtd_mc_in* in, int batch, const gtd_fp_opts* opts, void* t_state,
                  int* iters, int* status, double* max_out, double* mean_out, void* scratch, void* state,

@@ -167,7 +167,14 @@ typedef struct gtd_fp_opts {
     double beta, t_ambient, eta, tol;
     int max_iters;
     int poll;         /* host convergence poll interval in iterations (0 = 4) */
+    int warm_start;   /* 1: t_state holds T_0 on entry (else T_0 = 0)                 */
 } gtd_fp_opts;
+/* fp32 <-> fp64 copies of device maps (fp64 finish stage of an fp32 fixed point). */
+int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st);
+int gtd_narrow(const double* src, float* dst, size_t count, cudaStream_t st);
+/* iters = it32 + it64, status = st64 | NOCONVERGE if it32 + it64 > max_iters (both [batch]). */
+int gtd_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters,
+                   cudaStream_t st);
 size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64);
 
 /* ---- config 4: large-grid mode B by four-step passes (large.cu), fp64.

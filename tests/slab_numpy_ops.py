@@ -94,3 +94,31 @@ def fixed_point_numpy(P, V, fk, leak_frac, beta, law, tol, max_iters):
         if it > 1 and d < tol:
             return T, it
     return T, max_iters
+
+
+def fixed_point_torch(P, V, f_sp0, phi, leak_frac, beta, law, tol, max_iters):
+    """fixed_point_numpy on the GPU in fp64 (torch.fft, test-side checker for n = 8192):
+    T_{k+1} = crop(IRFFT2(fk . RFFT2(mirror(P + L0 f(T_k))))), fk = FFT2(center_kernel(f_sp0 - phi))
+    + phi m^2/4 at DC (greens.cpp:194-201), stop when max|dT| < tol after iteration 1."""
+    import torch
+    n = P.shape[0]
+    m, c = 2 * n, n // 2
+    dev = P.device
+    K = torch.zeros((m, m), dtype=torch.float64, device=dev)
+    x = (torch.arange(n, device=dev) - c) % m
+    K[x[:, None], x[None, :]] = f_sp0 - phi
+    fk = torch.fft.rfft2(K)
+    del K
+    fk[0, 0] += phi * m * m / 4
+    L0 = leak_frac * P * V
+    T = torch.zeros_like(P)
+    for it in range(1, max_iters + 1):
+        app = P + L0 * (1 + beta * T if law == 0 else torch.exp(beta * T))
+        mir = torch.cat([app, app.flip(0)], 0)
+        mir = torch.cat([mir, mir.flip(1)], 1)
+        th = torch.fft.irfft2(fk * torch.fft.rfft2(mir), s=(m, m))[:n, :n]
+        d = float((th - T).abs().max())
+        T = th.contiguous()
+        if it > 1 and d < tol:
+            return T, it
+    return T, max_iters

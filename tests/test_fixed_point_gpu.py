@@ -33,22 +33,19 @@ def test_fixed_point_matches_oracle(b200lib, oracle, greens64, golden, law, kirc
     t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(greens64, p, v, jobs=4, **kw)
     assert (st_ref == 0).all(), st_ref
     for prec, atol in ((1, 1e-8), (0, 1e-3)):
+        # fp32: iterations to 5e-4 K, then the fp64 finish stage to 1e-4 K (fp32_stage_tol default).
+        # (fp32 alone cannot resolve 1e-4 K with the Kirchhoff transform: its FFT noise (~1e-4 K)
+        # times dT/dtheta = (T/T0)^eta (~3.6 at 850 K) sits above the stop rule.)
         dg = _dg(greens64, prec)
-        kwp = dict(kw)
-        if prec == 0 and kirchhoff:
-            # fp32 FFT noise (~1e-4 K) times the Kirchhoff slope dT/dtheta = (T/T0)^eta (~3.6 at
-            # 850 K) sits above a 1e-4 K stop rule; the fp32 path stops at 5e-4 K.
-            kwp["tol"] = 5e-4
-            atol = 2e-3
-        out, it, st, mx, _ = dg.fp_batch_host(p, v, dg.fp_opts(**kwp))
+        out, it, st, mx, _ = dg.fp_batch_host(p, v, dg.fp_opts(**kw))
         assert (st == 0).all(), st
         err = np.abs(out.astype(np.float64) - t_ref).max()
         print(f"law={law} kirchhoff={kirchhoff} prec={prec}: iters {it.tolist()} vs ref {it_ref.tolist()}, "
               f"max|dT|={err:.3e} K, peak {t_ref.max():.1f} K")
         if prec == 1:
             np.testing.assert_array_equal(it, it_ref)
-        elif not kirchhoff:
-            assert np.abs(it - it_ref).max() <= 3  # fp32 rounding moves the 1e-4 K crossing
+        else:
+            assert np.abs(it - it_ref).max() <= 4  # fp32 rounding moves the 5e-4 K hand-over
         assert err <= atol
         np.testing.assert_allclose(mx, t_ref.reshape(len(p), -1).max(axis=1), atol=atol)
 
@@ -93,4 +90,55 @@ def test_linear_uniform_reduces_to_closed_form(b200lib, greens64):
     assert sa[0] == 0
     gap = np.abs(tb - ta).max()
     print(f"die-domain fixed point vs closed form: {gap:.3e} K on peak {ta.max():.2f} K after {it[0]} iterations")
-    assert gap <= 2e-3 * ta.max()
+    # measured 1.2e-11 K on a 26 K peak (iteration to 1e-9 K): the pin is at the stop rule's scale
+    assert gap <= 1e-8
+
+
+@pytest.mark.parametrize("law,kirchhoff,scale", [(0, 0, 1.0), (1, 0, 0.25), (1, 1, 0.15)])
+def test_fixed_point_config1_grid(b200lib, oracle, greens256, law, kirchhoff, scale):
+    """Config-1 grid (n = 256: the M = 512 warp-per-row-pair passes the bench runs) on 8
+    config-1 pairs against the fp64 restatement (reference outer loop, fdm.cpp:167-205),
+    stop rule max|dT| < 1e-4 K:
+      * fp64: the same iteration count per pair and <= 1e-8 K;
+      * fp32 with the fp64 finish stage (fp32 to 5e-4 K, then fp64 iterations warm-started
+        from it to 1e-4 K -- BASELINE config 1 "fp32 with fp64 residual check"): <= 1e-3 K."""
+    import torch
+    from paper_2307_12119_b200 import inputs
+    P, V = inputs.mc_inputs(inputs.CONFIGS["cfg1"], 0, 8, device="cuda", torch_dtype=torch.float32)
+    p = P.cpu().numpy().astype(np.float64) * scale
+    v = V.cpu().numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=law, kirchhoff=kirchhoff, tol=1e-4, max_iters=120)
+    t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(greens256, p, v, jobs=8, **kw)
+    assert (st_ref == 0).all(), st_ref
+    d64 = _dg(greens256, 1)
+    out, it, st, mx, _ = d64.fp_batch_host(p, v, d64.fp_opts(**kw))
+    assert (st == 0).all(), st
+    np.testing.assert_array_equal(it, it_ref)
+    err64 = np.abs(out - t_ref).max()
+    assert err64 <= 1e-8, err64
+    d32 = _dg(greens256, 0)
+    out32, it32, st32, mx32, _ = d32.fp_batch_host(p.astype(np.float32), v.astype(np.float32), d32.fp_opts(**kw))
+    assert (st32 == 0).all(), st32
+    err32 = np.abs(out32.astype(np.float64) - t_ref).max()
+    print(f"law={law} kirchhoff={kirchhoff} scale={scale}: ref iters {it_ref.tolist()}, fp64 {err64:.2e} K, "
+          f"fp32+fp64 finish iters {it32.tolist()} {err32:.2e} K (peak {t_ref.max():.1f} K)")
+    assert err32 <= 1e-3
+    np.testing.assert_allclose(mx32, t_ref.reshape(8, -1).max(axis=1), rtol=0, atol=1e-3)
+
+
+def test_fixed_point_fp32_only_stage_is_selectable(b200lib, greens64, golden):
+    """fp32_stage_tol < 0 keeps the whole iteration in fp32 (the round-1 behaviour); the
+    default finishes in fp64, so its result equals the fp64 path's to fp32 rounding."""
+    p = golden["p_dyn"].astype(np.float32)
+    v = golden["var"].astype(np.float32)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=80)
+    d32 = _dg(greens64, 0)
+    a = d32.fp_batch_host(p, v, d32.fp_opts(**kw))
+    b = d32.fp_batch_host(p, v, d32.fp_opts(fp32_stage_tol=-1.0, **kw))
+    d64 = _dg(greens64, 1)
+    c = d64.fp_batch_host(p.astype(np.float64), v.astype(np.float64), d64.fp_opts(**kw))
+    assert (a[2] == 0).all() and (b[2] == 0).all()
+    ea = np.abs(a[0] - c[0]).max()
+    eb = np.abs(b[0] - c[0]).max()
+    print(f"fp32+fp64 finish vs fp64: {ea:.2e} K; fp32 only: {eb:.2e} K")
+    assert ea <= 1e-4  # the fp64 finish lands within the stop tolerance of the fp64 fixed point

@@ -108,3 +108,79 @@ def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path):
     print(f"large n=2048: 3 iterations, max|dT| {err:.3e} K on peak {ref.max():.2f} K")
     assert res.iterations == 3 and res.status == slab.GT_SAMPLE_NOCONVERGE == 32
     assert err <= 1e-9 * max(1.0, ref.max())
+
+
+def _large_greens(b200lib, tmp_path, n):
+    from paper_2307_12119_b200.api import GreensArrays
+    (tmp_path / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
+    f = np.empty((n, n))
+    nn = C.c_int()
+    assert b200lib.gt_modal_kernel(str(tmp_path / "stack.txt").encode(), C.byref(nn),
+                                   f.ctypes.data_as(C.POINTER(C.c_double))) == 0, b200lib.gt_last_error()
+    phi = float(np.mean(np.concatenate([f[0], f[-1], f[1:-1, 0], f[1:-1, -1]])))
+    return f, phi, GreensArrays(n=n, pitch=0.016 / n, f_sp0=f, g_sp0=f, phi=phi, kappa_inf=float(f[0, 0]),
+                                alpha=0.0, beta=0.017, mu=0.0, rand_scale=1.0)
+
+
+def test_config4_n8192_converged_vs_fp64_restatement(b200lib, tmp_path):
+    """Config 4 at the benched size (n = 8192, m = 16384): the generator's map rescaled to
+    300 W as in bench.py, leakage loop to 1e-4 K through slab.solve_slab, against a test-side
+    fp64 restatement of the same loop with torch.fft (tests/slab_numpy_ops.fixed_point_torch):
+    same iteration count, <= 1e-8 K."""
+    import dataclasses
+    import sys
+    from pathlib import Path
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    sys.path.insert(0, str(Path(__file__).parent))
+    from slab_numpy_ops import fixed_point_torch
+    n = 8192
+    f, phi, ga = _large_greens(b200lib, tmp_path, n)
+    c4 = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n)
+    P = inputs.power_map_torch(c4, 0, device="cuda")
+    P *= 300.0 / float(P.sum())
+    V = inputs.variation_batch(c4, 0, 1, device="cuda", dtype=torch.float64)[0]
+    dg = DeviceGreens(ga, 1)
+    o = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    res = slab.solve_slab(slab.GpuLargeOps(dg), n, P, V, o)
+    torch.cuda.synchronize()
+    assert res.status == 0
+    t_dev, it_dev = res.t.cpu().numpy(), res.iterations
+    dg.close()
+    del res
+    torch.cuda.empty_cache()
+    ref, it_ref = fixed_point_torch(P, V, torch.from_numpy(f).cuda(), phi, 0.3, 0.017, 0, 1e-4, 200)
+    err = float(np.abs(t_dev - ref.cpu().numpy()).max())
+    print(f"config 4 n=8192: {it_dev} iterations vs {it_ref} (restatement), max|dT| {err:.3e} K on peak "
+          f"{float(ref.max()):.1f} K")
+    assert it_dev == it_ref
+    assert err <= 1e-8
+
+
+def test_large_grid_n1024_converged_vs_oracle(b200lib, oracle, tmp_path):
+    """The large-grid passes (four-step, m = 2048 = 32 x 64) through slab.solve_slab at
+    n = 1024, converged to 1e-4 K, against the CPU oracle (reference outer loop with the
+    reference's own baseline_kernel_spectrum convolution): same iterations, <= 1e-8 K."""
+    import dataclasses
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    n = 1024
+    f, phi, ga = _large_greens(b200lib, tmp_path, n)
+    cfg = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n, blocks=128, hotspots=16)
+    p = inputs.power_batch(cfg, 0, 1, np.float64)
+    p *= 300.0 / p.sum()
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    t_ref, it_ref, st_ref, secs = oracle.fixed_point_batch(ga, p, v, jobs=1, **kw)
+    assert st_ref[0] == 0
+    dg = DeviceGreens(ga, 1)
+    res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(p[0]).cuda(), torch.from_numpy(v[0]).cuda(),
+                          dg.fp_opts(**kw))
+    torch.cuda.synchronize()
+    err = float(np.abs(res.t.cpu().numpy() - t_ref[0]).max())
+    print(f"large n=1024: iters {res.iterations} vs {it_ref[0]}, max|dT| {err:.3e} K on peak {t_ref.max():.1f} K "
+          f"(oracle {secs:.1f} s)")
+    assert res.status == 0 and res.iterations == it_ref[0]
+    assert err <= 1e-8
