@@ -127,6 +127,11 @@ typedef struct gt_fp_opts {
                               check"): the fp32 iteration stops at this tolerance, then
                               fp64 iterations warm-started from it finish to `tol`
                               (0 = default 5e-4; < 0 = fp32 only). Iteration counts add up. */
+    int with_rand;         /* 1: combined config 2 -- every iteration adds the reference's
+                              shift-variant term h * sum(applied), h = f_rand o p_var *
+                              rand_scale with f_rand = random_greens at the GreensSet mu
+                              from the sample's leakage baseline (greens.cpp:225-251,
+                              solver.cpp:169-174), before the Kirchhoff inverse. */
 } gt_fp_opts;
 
 void gt_fp_opts_default(gt_fp_opts* o);

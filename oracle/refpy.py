@@ -78,6 +78,9 @@ def restate_lib() -> C.CDLL:
         L.ref_fixed_point_batch.restype = dbl
         L.ref_fixed_point_batch.argtypes = [C.POINTER(RefGreens), pdbl, pdbl, cint, dbl, dbl, cint, cint, dbl, dbl,
                                             dbl, cint, cint, pdbl, pint, pint]
+        L.ref_fixed_point_rand_batch.argtypes = [C.POINTER(RefGreens), pdbl, pdbl, cint, dbl, dbl, cint, cint, dbl, dbl,
+                                            dbl, cint, cint, pdbl, pint, pint]
+        L.ref_fixed_point_rand_batch.restype = dbl
         L.ref_trace_leak_batch.restype = dbl
         L.ref_trace_leak_batch.argtypes = [C.POINTER(RefGreens), C.POINTER(C.c_int), C.c_longlong, pdbl, cint, pdbl,
                                            C.c_longlong, cint, dbl, cint, cint, cint, dbl, cint, cint, pdbl, pint]
@@ -114,15 +117,17 @@ def mc_batch(g, p_dyn, var, leak_frac=0.3, mu_per_sample=1, with_rand=1, jobs=No
 
 
 def fixed_point_batch(g, p_dyn, var, leak_frac=0.3, beta=0.017, law=1, kirchhoff=0, t_ambient=318.15, eta=1.3,
-                      tol=1e-4, max_iters=50, jobs=None):
-    """Mode B restatement. Returns (maps, iters, status, seconds)."""
+                      tol=1e-4, max_iters=50, jobs=None, with_rand=0):
+    """Mode B restatement (with_rand: + the reference's shift-variant term each iteration,
+    restate.h ref_fixed_point_rand_batch). Returns (maps, iters, status, seconds)."""
     k = _Keep(g)
     p = np.ascontiguousarray(p_dyn, np.float64)
     v = np.ascontiguousarray(var, np.float64)
     B = p.shape[0]
     out = np.empty_like(p)
     it, st = np.empty(B, np.int32), np.empty(B, np.int32)
-    secs = restate_lib().ref_fixed_point_batch(C.byref(k.s), _p(p), _p(v), B, leak_frac, beta, law, kirchhoff,
+    fn = restate_lib().ref_fixed_point_rand_batch if with_rand else restate_lib().ref_fixed_point_batch
+    secs = fn(C.byref(k.s), _p(p), _p(v), B, leak_frac, beta, law, kirchhoff,
                                                t_ambient, eta, tol, max_iters, jobs or os.cpu_count() or 1, _p(out),
                                                it.ctypes.data_as(pint), st.ctypes.data_as(pint))
     return out, it, st, secs

@@ -216,14 +216,33 @@ int ref_calibrate(int n, double die_edge, double beta, double dopant_spread, dou
     }
 }
 
-double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const double* var, int batch,
-                             double leak_frac, double beta, int law, int kirchhoff, double t_ambient, double eta,
-                             double tol, int max_iters, int jobs, double* t_out, int* iters_out, int* status_out) {
+// with_rand: the combined config-2 loop -- each iteration adds the reference's
+// shift-variant Hadamard term hadamard(f_rand, p_var) * (sum(applied) * rand_scale)
+// (solver.cpp:169-174, 364-365) to the convolution before the Kirchhoff inverse, with
+// f_rand = random_greens at gs.mu (greens.cpp:225-251; F_det hoisted as monte_carlo,
+// solver.cpp:350-351) from the sample's own leakage baseline (variation.cpp:162-195;
+// p_leak0 = leak_frac P var as ref_mc_batch builds it), computed once per sample.
+static double fixed_point_impl(const ref_greens* g, const double* p_dyn, const double* var, int batch,
+                               double leak_frac, double beta, int law, int kirchhoff, double t_ambient, double eta,
+                               double tol, int max_iters, int jobs, double* t_out, int* iters_out, int* status_out,
+                               int with_rand) {
     const auto t0 = std::chrono::steady_clock::now();
     const GreensSet gs = to_greens(g);
     const int n = gs.n;
     const size_t nn = static_cast<size_t>(n) * n;
     const std::vector<cplx> fk = baseline_kernel_spectrum(gs.f_sp0, gs.phi);
+    std::vector<cplx> fdet;
+    if (with_rand) {
+        try {
+            fdet = deterministic_spectrum(gs.f_sp0, gs.phi, gs.g_sp0, gs.alpha, gs.beta, gs.mu);
+        } catch (const Error& e) {
+            for (int i = 0; i < batch; ++i)
+                if (status_out) status_out[i] = status_class(e);
+            return 0.0;
+        }
+    }
+    const FieldMap zero(n, gs.pitch, Unit::Dimensionless);
+    const double beta_l = -10.0;
     // Kirchhoff inverse for k = k_ref (T/T0)^-eta (k normalised at ambient):
     // T = [T0^(1-eta) + (1-eta)(theta-T0) T0^-eta]^(1/(1-eta)).
     const double a = std::pow(t_ambient, 1.0 - eta), b = (1.0 - eta) * std::pow(t_ambient, -eta);
@@ -233,7 +252,19 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
         try {
             const FieldMap P = to_field(p_dyn + i * nn, n, gs.pitch, Unit::Watts);
             FieldMap l0 = P;
-            for (size_t k = 0; k < nn; ++k) l0.values()[k] *= leak_frac * var[i * nn + k];
+            FieldMap hmap;  // hadamard(f_rand, p_var) when with_rand
+            if (with_rand) {
+                FieldMap nominal = P;
+                for (double& x : nominal.values()) x *= leak_frac;
+                FieldMap dl(n, gs.pitch, Unit::Dimensionless);
+                for (size_t k = 0; k < nn; ++k) dl.values()[k] = std::log(var[i * nn + k]) / beta_l;
+                LeakageBaseline leak = leakage_baseline(nominal, dl, zero, beta_l, -5.0, gs.beta);
+                l0 = leak.p_leak0;
+                FieldMap f_rand = random_greens(fdet, gs.f_sp0, gs.phi, gs.g_sp0, leak.p_var, gs.alpha, gs.beta, gs.mu);
+                hmap = hadamard(f_rand, leak.p_var);
+            } else {
+                for (size_t k = 0; k < nn; ++k) l0.values()[k] *= leak_frac * var[i * nn + k];
+            }
             for (int it = 1; it <= max_iters; ++it) {
                 FieldMap applied = P;
                 for (size_t k = 0; k < nn; ++k) {
@@ -242,6 +273,7 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
                     applied.values()[k] += l0.values()[k] * f;
                 }
                 FieldMap theta = convolve_with(fk, applied);
+                if (with_rand) theta += hmap * (applied.sum() * gs.rand_scale);
                 double delta = 0.0;
                 for (size_t k = 0; k < nn; ++k) {
                     double t = theta.values()[k];
@@ -267,6 +299,21 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
         if (status_out) status_out[i] = st;
     });
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const double* var, int batch,
+                             double leak_frac, double beta, int law, int kirchhoff, double t_ambient, double eta,
+                             double tol, int max_iters, int jobs, double* t_out, int* iters_out, int* status_out) {
+    return fixed_point_impl(g, p_dyn, var, batch, leak_frac, beta, law, kirchhoff, t_ambient, eta, tol, max_iters,
+                            jobs, t_out, iters_out, status_out, 0);
+}
+
+double ref_fixed_point_rand_batch(const ref_greens* g, const double* p_dyn, const double* var, int batch,
+                                  double leak_frac, double beta, int law, int kirchhoff, double t_ambient, double eta,
+                                  double tol, int max_iters, int jobs, double* t_out, int* iters_out,
+                                  int* status_out) {
+    return fixed_point_impl(g, p_dyn, var, batch, leak_frac, beta, law, kirchhoff, t_ambient, eta, tol, max_iters,
+                            jobs, t_out, iters_out, status_out, 1);
 }
 
 double ref_trace_leak_batch(const ref_greens* g, const int* blk, long long blk_stride, const double* sched,

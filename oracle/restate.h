@@ -66,6 +66,15 @@ double ref_fixed_point_batch(const ref_greens* g, const double* p_dyn, const dou
                              double eta, double tol, int max_iters, int jobs, double* t_out,
                              int* iters_out, int* status_out);
 
+/* Combined config 2 (north star (3) + (4)): ref_fixed_point_batch with the
+ * reference's shift-variant term in every iteration,
+ *   theta = conv(fk, applied) + hadamard(f_rand, p_var) * sum(applied) * rand_scale,
+ * f_rand = random_greens at gs.mu from the sample's leakage baseline (once per sample). */
+double ref_fixed_point_rand_batch(const ref_greens* g, const double* p_dyn, const double* var, int batch,
+                                  double leak_frac, double beta, int law, int kirchhoff, double t_ambient,
+                                  double eta, double tol, int max_iters, int jobs, double* t_out,
+                                  int* iters_out, int* status_out);
+
 /* Config 3 (north star (5) + (4)): batched power traces with the leakage
  * update every step, driven through the reference's own windowed superposition
  * time_varying_profile (solver.cpp:212-287, with_rand off), one step at a time:

@@ -760,14 +760,42 @@ void gt_fp_opts_default(gt_fp_opts* o) {
     o->max_iters = 50;
     o->chunk = 0;
     o->fp32_stage_tol = 0.0;
+    o->with_rand = 0;
 }
 
 size_t gt_fp_scratch_bytes(int n, int precision) { return gtd_fp_scratch_bytes_per_sample(n, precision == GT_FP64); }
 
 namespace {
 void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int batch, const gt_fp_opts* opts,
-                  double tol, int warm, void* t_out, int* iters, int* status, double* mx, double* mean,
+                  double tol, int warm, const void* H, void* t_out, int* iters, int* status, double* mx, double* mean,
                   cudaStream_t st);
+
+// Per-sample shift-variant maps h = f_rand o p_var * rand_scale of the combined config-2
+// loop: the mode-A passes with with_rand = 2 (closed forms at gs.mu as the reference
+// monte_carlo, the fp64 re-solve for ill-conditioned fp32 pairs). Their per-sample status
+// (bad inputs, random_greens runaway) lands in d->fp_hstats.
+void shift_variant_maps(gt_device_greens* d, const void* p_dyn, const void* var, int batch, double leak_frac,
+                        void* H, cudaStream_t st) {
+    const int n = d->d.n;
+    const int chunk = auto_chunk(n, d->fp64, batch, nullptr, 1, d->scratch.bytes);
+    d->scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, d->fp64) * chunk);
+    d->fp_hstats.ensure(sizeof(gtd_sample_stats) * batch);
+    gtd_mc_opts o{};
+    o.mu_per_sample = 0;
+    o.with_rand = 2;
+    o.exponent_cap = 6.0;
+    o.resolve = attach_resolve(d, 0, batch, nullptr);
+    gtd_mc_in in{};
+    in.P = p_dyn;
+    in.N = p_dyn;
+    in.V = var;
+    in.sP = in.sN = in.sV = static_cast<long long>(n) * n;
+    in.nom_scale = leak_frac;
+    cuda_ok(gtd_mc_batch(&d->d, &in, batch, &o, H, d->fp_hstats.as<gtd_sample_stats>(), d->scratch.p, chunk, st,
+                         nullptr, nullptr),
+            "shift-variant maps");
+    d->kernels += gtd_mc_launch_count(batch, chunk) + (o.resolve ? gtd_mc_resolve_launch_count() : 0);
+}
 
 gt_device_greens* fp64_twin(gt_device_greens* d) {
     if (!d->dev64) d->dev64 = gth::prepare_device(d->host, GT_FP64, d->device);
@@ -779,16 +807,32 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     if (!opts) fail(ST_CONFIG, "capi", "fixed point needs options");
     if (!(opts->tol > 0.0)) fail(ST_CONFIG, "oracle", "outer tolerance must be positive");
     const double stage_tol = opts->fp32_stage_tol == 0.0 ? 5e-4 : opts->fp32_stage_tol;
+    const size_t nn = static_cast<size_t>(d->d.n) * d->d.n, cnt = nn * batch;
+    const void* H = nullptr;
+    if (opts->with_rand) {
+        d->fp_h.ensure(cnt * (d->fp64 ? 8 : 4));
+        d->order_in(st);
+        shift_variant_maps(d, p_dyn, var, batch, opts->leak_frac, d->fp_h.p, st);
+        H = d->fp_h.p;
+    }
+    auto or_mode_a_status = [&] {
+        if (opts->with_rand)
+            cuda_ok(gtd_fp_or_status(status, d->fp_hstats.as<gtd_sample_stats>(), batch, st), "status");
+    };
     if (d->fp64 || stage_tol < 0.0 || opts->tol >= stage_tol) {
-        run_fp_stage(d, p_dyn, var, batch, opts, opts->tol, 0, t_out, iters, status, mx, mean, st);
+        run_fp_stage(d, p_dyn, var, batch, opts, opts->tol, 0, H, t_out, iters, status, mx, mean, st);
+        or_mode_a_status();
         return;
     }
     // "fp32 with fp64 residual check" (BASELINE config 1): the fp32 iteration runs to its
     // noise floor (stage_tol), then fp64 iterations warm-started from that iterate finish the
     // reference stop rule max|dT| < tol (fdm.cpp:190-200) on the fp64 fixed point.
-    run_fp_stage(d, p_dyn, var, batch, opts, stage_tol, 0, t_out, iters, status, nullptr, nullptr, st);
+    run_fp_stage(d, p_dyn, var, batch, opts, stage_tol, 0, H, t_out, iters, status, nullptr, nullptr, st);
     gt_device_greens* d64 = fp64_twin(d);
-    const size_t nn = static_cast<size_t>(d->d.n) * d->d.n, cnt = nn * batch;
+    if (H) {
+        d->fin_h.ensure(cnt * 8);
+        cuda_ok(gtd_widen(static_cast<const float*>(H), d->fin_h.as<double>(), cnt, st), "widen");
+    }
     d->fin_p.ensure(cnt * 8);
     d->fin_v.ensure(cnt * 8);
     d->fin_t.ensure(cnt * 8);
@@ -797,17 +841,18 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     cuda_ok(gtd_widen(static_cast<const float*>(p_dyn), d->fin_p.as<double>(), cnt, st), "widen");
     cuda_ok(gtd_widen(static_cast<const float*>(var), d->fin_v.as<double>(), cnt, st), "widen");
     cuda_ok(gtd_widen(static_cast<const float*>(t_out), d->fin_t.as<double>(), cnt, st), "widen");
-    run_fp_stage(d64, d->fin_p.p, d->fin_v.p, batch, opts, opts->tol, 1, d->fin_t.p, d->fin_it.as<int>(),
-                 d->fin_st.as<int>(), mx, mean, st);
+    run_fp_stage(d64, d->fin_p.p, d->fin_v.p, batch, opts, opts->tol, 1, H ? d->fin_h.p : nullptr, d->fin_t.p,
+                 d->fin_it.as<int>(), d->fin_st.as<int>(), mx, mean, st);
     cuda_ok(gtd_narrow(d->fin_t.as<double>(), static_cast<float*>(t_out), cnt, st), "narrow");
     cuda_ok(gtd_fp_combine(iters, status, d->fin_it.as<int>(), d->fin_st.as<int>(), batch, opts->max_iters, st),
             "combine");
+    or_mode_a_status();
     d->kernels += 5 + d64->kernels;
     d64->kernels = 0;
 }
 
 void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int batch, const gt_fp_opts* opts,
-                  double tol, int warm, void* t_out, int* iters, int* status, double* mx, double* mean,
+                  double tol, int warm, const void* H, void* t_out, int* iters, int* status, double* mx, double* mean,
                   cudaStream_t st) {
     if (!(opts->tol > 0.0)) fail(ST_CONFIG, "oracle", "outer tolerance must be positive");
     if (opts->max_iters < 1) fail(ST_CONFIG, "oracle", "max_iters must be >= 1");
@@ -842,6 +887,8 @@ void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int b
     o.max_iters = opts->max_iters;
     o.poll = 4;
     o.warm_start = warm;
+    o.H = H;
+    o.sH = static_cast<long long>(n) * n;
     long long launches = 0;
     d->order_in(st);
     cuda_ok(gtd_fp_batch(&d->d, &in, batch, &o, t_out, iters, status, mx, mean, d->fp_scratch.p, d->fp_state.p,

@@ -50,7 +50,14 @@ struct FPState {
     unsigned long long res_bits;  // max |T_{k+1} - T_k| of the current iteration (double bits)
     int iters;
     int active;
+    double sum_app[2];  // sum of the applied map of iterations k (slot k & 1): shift-variant term
 };
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
 template <typename T>
 struct FPIn {
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
 fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
         FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
         const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient,
-        int warm) {
+        int warm, const T* __restrict__ H, long long sH, int it) {
     using Gm = FPGeom<T, M>;
     constexpr int n = Gm::n, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT, hp = Gm::hp;
     constexpr int RB = Gm::RB;
@@ -104,8 +111,9 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
         T* Ts = Tst + sg * n * n;
         cplx<T>* As = A + static_cast<size_t>(s) * n * hp;
         constexpr T inv = T(1.0 / (double(M) * double(M)));
-        double dmax = 0.0;
+        double dmax = 0.0, app_part = 0.0;
         int bad = 0;
+        const T sig_prev = (!FIRST && H) ? T(state[sg].sum_app[(it - 1) & 1]) : T(0);
 
         // Every global input of a stage is issued in batches of UB items ahead of
         // its use (one exposed HBM latency per batch, not one per element).
@@ -182,7 +190,8 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                         for (int half = 0; half < 2; ++half) {
                             T t = FIRST ? told[u][half] : T(0);  // warm start: the caller's T_0
                             if (!FIRST) {
-                                const T th = (half ? z.y : z.x) * inv;  // theta - T0
+                                T th = (half ? z.y : z.x) * inv;  // theta - T0
+                                if (H) th += H[sg * sH + static_cast<size_t>(x + half) * n + j] * sig_prev;
                                 t = th;
                                 if (kirchhoff) {
                                     const T br = ka + kb * th;
@@ -195,6 +204,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                             }
                             const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
                             a[half] = pv[u][half] + lv[u][half] * f;
+                            app_part += double(a[half]);
                         }
                     }
                     tile[j * LP + l] = mk<T>(a[0], a[1]);
@@ -216,6 +226,10 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                 o = half ? dct_part_im<T>(Z, Zc, g_hs[v]) : dct_part<T>(Z, Zc, g_hs[v]);
             }
             Ar[static_cast<size_t>(s) * n * hp + static_cast<size_t>(x) * hp + v] = o;
+        }
+        if (H) {
+            app_part = warp_sum_d(app_part);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&state[sg].sum_app[it & 1], app_part);
         }
         if (!FIRST) {
             or_flags_fp(&status[sg], bad);
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(FPW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
 fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec, T* __restrict__ Ar,
           T* __restrict__ Tst, FPState* __restrict__ state, int* __restrict__ status,
           const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka,
-          T kb, T kexp, T t_ambient, int warm) {
+          T kb, T kexp, T t_ambient, int warm, const T* __restrict__ H, long long sH, int it) {
     using Gm = FPGeom<T, M>;
     using WF = WarpFFT<T, M>;
     constexpr int n = Gm::n, h = Gm::h, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
@@ -272,7 +286,8 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
         // Every global input of the item is requested up front (one exposed
         // round trip per row pair instead of three): previous T rows, P rows,
         // leakage rows L0 = nom N V.
-        T t0[E], t1[E], p0[E], p1[E], l0[E], l1[E];
+        T t0[E], t1[E], p0[E], p1[E], l0[E], l1[E], h0[E], h1[E];
+        const T sig_prev = (!FIRST && H) ? T(state[sg].sum_app[(it - 1) & 1]) : T(0);
         {
             const T* P0 = in.P + sg * in.sP + static_cast<size_t>(x0) * n;
             const T* N0 = in.N + sg * in.sN + static_cast<size_t>(x0) * n;
@@ -287,6 +302,12 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
                 }
                 p0[t] = P0[j];
                 p1[t] = P0[n + j];
+                h0[t] = h1[t] = T(0);
+                if (!FIRST && H) {
+                    const T* H0 = H + sg * sH + static_cast<size_t>(x0) * n;
+                    h0[t] = H0[j];
+                    h1[t] = H0[n + j];
+                }
                 const T n0 = n_is_p ? p0[t] : N0[j], n1 = n_is_p ? p1[t] : N0[n + j];
                 l0[t] = in.nom_scale * n0 * V0[j];
                 l1[t] = in.nom_scale * n1 * V0[n + j];
@@ -319,7 +340,7 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
             for (int t = 0; t < E; ++t) {
                 const int j = lane + 32 * t;
                 const cplx<T> th = scr[j];
-                T a = th.x * inv, b = th.y * inv;  // theta - T0 of rows x0, x0+1
+                T a = th.x * inv + h0[t] * sig_prev, b = th.y * inv + h1[t] * sig_prev;  // theta - T0, rows x0, x0+1
                 if (kirchhoff) {
                     const T ba = ka + kb * a, bb = ka + kb * b;
                     if (!(ba > T(0)) || !(bb > T(0))) bad |= GTD_ST_KIRCHHOFF;
@@ -346,6 +367,13 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
             const T f1 = law ? T(exp(beta * t1[t])) : T(1) + beta * t1[t];
             a0[t] = p0[t] + l0[t] * f0;
             a1[t] = p1[t] + l1[t] * f1;
+        }
+        if (H) {
+            double part = 0.0;
+#pragma unroll
+            for (int t = 0; t < E; ++t) part += double(a0[t]) + double(a1[t]);
+            part = warp_sum_d(part);
+            if (lane == 0) atomicAdd(&state[sg].sum_app[it & 1], part);
         }
         // z[i] = mirror(a0)[i] + i mirror(a1)[i]: mirror(i) = (31 - lane) + 32 (P-1-k) for k >= E
         cplx<T> z[P];
@@ -580,18 +608,19 @@ fp_cols_d(int sample0, int count, const T* __restrict__ Ar, cplx<T>* __restrict_
 __global__ void fp_init(FPState* st, int* status, int* iters, int sample0, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
-    st[sample0 + i] = FPState{0ull, 0, 1};
+    st[sample0 + i] = FPState{0ull, 0, 1, {0.0, 0.0}};
     status[sample0 + i] = 0;
     iters[sample0 + i] = 0;
 }
 
 // Reference stop rule (fdm.cpp:190-200): converge check first, then max_iters.
 __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int count, double tol, int max_iters,
-                          int* active_count) {
+                          int* active_count, int it) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     FPState& s = st[sample0 + i];
     if (!s.active) return;
+    s.sum_app[(it - 1) & 1] = 0.0;  // read by this iteration's row pass; the next one accumulates into it
     s.iters += 1;
     iters[sample0 + i] = s.iters;
     const double res = __longlong_as_double(static_cast<long long>(s.res_bits));
@@ -709,41 +738,41 @@ struct FPLaunch {
         auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         const int poll = o->poll > 0 ? o->poll : 4;
         long long k = 0;
-        auto rows = [&](bool first, int s0, int cnt) {
+        auto rows = [&](bool first, int s0, int cnt, int it_) {
             if constexpr (fp_warp_rows<T, M>()) {
                 const int gw = grid((cnt * RP + FPW_WARPS - 1) / FPW_WARPS, res[2]);
                 if (first)
                     fp_rows_w<T, M, true><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient), o->warm_start);
+                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
                 else
                     fp_rows_w<T, M, false><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient), o->warm_start);
+                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
             } else {
                 const int gr = grid(cnt * Gm::RB, res[0]);
                 if (first)
                     fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                      T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                     T(o->t_ambient), o->warm_start);
+                                                                     T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
                 else
                     fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                       T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                      T(o->t_ambient), o->warm_start);
+                                                                      T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
             }
         };
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
             const int gc = grid(cnt * Gc::CT, res[1]);
             fp_init<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt);
-            rows(true, s0, cnt);
+            rows(true, s0, cnt, 0);
             k += 2;
             for (int it = 1; it <= o->max_iters; ++it) {
                 fp_cols_d<T, M><<<gc, Gc::NT, smem_cols(), st>>>(s0, cnt, Ar, A, state, tw, hs, fk, g->hp);
-                rows(false, s0, cnt);
+                rows(false, s0, cnt, it);
                 cudaMemsetAsync(counter_d, 0, sizeof(int), st);
                 fp_update<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt, o->tol, o->max_iters,
-                                                            counter_d);
+                                                            counter_d, it);
                 k += 3;
                 if (it % poll == 0 || it == o->max_iters) {
                     cudaMemcpyAsync(counter_h, counter_d, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -804,6 +833,10 @@ __global__ void k_narrow(const double* __restrict__ a, float* __restrict__ b, si
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x)
         b[i] = float(a[i]);
 }
+__global__ void k_fp_or_status(int* status, const gtd_sample_stats* stats, int batch) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < batch) status[i] |= stats[i].status;
+}
 __global__ void k_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= batch) return;
@@ -833,6 +866,10 @@ int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st) {
 }
 int gtd_narrow(const double* src, float* dst, size_t count, cudaStream_t st) {
     k_narrow<<<1184, 256, 0, st>>>(src, dst, count);
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_fp_or_status(int* status, const gtd_sample_stats* stats, int batch, cudaStream_t st) {
+    k_fp_or_status<<<(batch + 127) / 128, 128, 0, st>>>(status, stats, batch);
     return static_cast<int>(cudaGetLastError());
 }
 int gtd_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters,

@@ -81,7 +81,9 @@ typedef struct gtd_mc_resolve {
 /* Options of the Monte-Carlo batch (mode A = reference run_one semantics). */
 typedef struct gtd_mc_opts {
     int mu_per_sample;  /* 1: closed forms use the sample mean leakage; 0: gs.mu */
-    int with_rand;      /* 0 drops the shift-variant term (ablation)            */
+    int with_rand;      /* 0 drops the shift-variant term (ablation); 2 outputs the
+                           shift-variant map f_rand o p_var * rand_scale alone (no
+                           deterministic part, no clamp: the config-2 fixed point's term) */
     double exponent_cap;/* |ln var| guard (variation.cpp:173-178)               */
     const gtd_mc_resolve* resolve; /* fp32 only: NULL = no fp64 re-solve        */
 } gtd_mc_opts;
@@ -168,6 +170,9 @@ typedef struct gtd_fp_opts {
     int max_iters;
     int poll;         /* host convergence poll interval in iterations (0 = 4) */
     int warm_start;   /* 1: t_state holds T_0 on entry (else T_0 = 0)                 */
+    const void* H;    /* optional [B][n][n] shift-variant maps h = f_rand o p_var * rand_scale:
+                         theta += h * sum(applied) each iteration (combined config 2)      */
+    long long sH;     /* sample stride of H in elements                                    */
 } gtd_fp_opts;
 /* fp32 <-> fp64 copies of device maps (fp64 finish stage of an fp32 fixed point). */
 int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st);
@@ -175,6 +180,8 @@ int gtd_narrow(const double* src, float* dst, size_t count, cudaStream_t st);
 /* iters = it32 + it64, status = st64 | NOCONVERGE if it32 + it64 > max_iters (both [batch]). */
 int gtd_fp_combine(int* iters, int* status, const int* it64, const int* st64, int batch, int max_iters,
                    cudaStream_t st);
+/* status[i] |= stats[i].status (mode-A status of the shift-variant maps). */
+int gtd_fp_or_status(int* status, const gtd_sample_stats* stats, int batch, cudaStream_t st);
 size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64);
 
 /* ---- config 4: large-grid mode B by four-step passes (large.cu), fp64.

@@ -180,7 +180,8 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
         }
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
-        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T scale = with_rand == 2 ? rand_scale : with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T ydet = with_rand == 2 ? T(0) : T(1);
         const T inv = T(1.0 / (double(M) * double(M)));
         const T* Nm = in.nn(sg);
         const T* V = in.v(sg);
@@ -206,13 +207,13 @@ mc_pass3(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ A
             const int idx = threadIdx.x + k * NT;
             const int l = idx / n, j = idx - l * n, x = x0 + l;
             if (idx >= L * n || x >= n) continue;
-            const T yd = tile[j * LP + l].x * inv;
+            const T yd = tile[j * LP + l].x * inv * ydet;
             const int jr = (j - c) & (M - 1);
             const T rd = tile[jr * LP + l].y * inv;
             const T pvar = in.nom_scale * nv[k] * vv[k] - mu_t;
             T t = yd + rd * pvar * scale;
             if (!finite_(t)) bad = GTD_ST_NONFINITE;
-            t = t > T(0) ? t : T(0);
+            if (with_rand != 2) t = t > T(0) ? t : T(0);
             if (out) out[(sg * n + x) * n + j] = t;
             part_t += t;
             mxt = mxt > t ? mxt : t;
@@ -477,7 +478,10 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
         }
         const double n2 = double(n) * double(n);
         const double mu_s = stats[sg].sum_leak / n2;
-        const T scale = with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        // with_rand 2: the shift-variant map f_rand o p_var * rand_scale alone (no deterministic
+        // part, no clamp) -- the per-sample term of the combined config-2 fixed point
+        const T scale = with_rand == 2 ? rand_scale : with_rand ? T(stats[sg].sum_applied * double(rand_scale)) : T(0);
+        const T ydet = with_rand == 2 ? T(0) : T(1);
         const T mu_t = T(mu_s);
         T pvs[E];  // p_var * sum(applied) * rand_scale: consumes the staged N, V rows
 #pragma unroll
@@ -501,11 +505,11 @@ mc_pass3w(const MCIn<T> in, int sample0, int count, const cplx<T>* __restrict__ 
 #pragma unroll
         for (int t = 0; t < E; ++t) {
             const int f = lane + 32 * t;
-            const T yd = scr[f].x * inv;
+            const T yd = scr[f].x * inv * ydet;
             const T rd = scr[(f - c) & (M - 1)].y * inv;
             T tt = yd + rd * pvs[t];
             if (!finite_(tt)) bad = GTD_ST_NONFINITE;
-            tt = tt > T(0) ? tt : T(0);
+            if (with_rand != 2) tt = tt > T(0) ? tt : T(0);
             if (O_x) O_x[f] = tt;
             part += tt;
             mxt = mxt > tt ? mxt : tt;
