@@ -93,8 +93,10 @@ struct VarDevice {
         noise.ensure(mm * 8);
         sys.ensure(nn * 8);
     }
-    // out = sigma_sys * shaped(sys_noise) + rnd_noise (either part may be absent)
-    void field(const VarParams& v, const std::vector<double>& sysn, const std::vector<double>& rndn, double* out) {
+    // out = sigma_sys * shaped(sys_noise) + rnd_noise (either part may be absent). With
+    // sync = false the host noise vectors must stay alive until the stream reaches this work.
+    void field(const VarParams& v, const std::vector<double>& sysn, const std::vector<double>& rndn, double* out,
+               bool sync = true) {
         cudaStream_t st = stream;
         cuda_ok(cudaMemsetAsync(out, 0, nn * 8, st), "memset");
         if (!sysn.empty()) {
@@ -106,7 +108,7 @@ struct VarDevice {
             cuda_ok(cudaMemcpyAsync(sys.p, rndn.data(), nn * 8, cudaMemcpyHostToDevice, st), "h2d");
             cuda_ok(gtd_add_maps(out, sys.as<double>(), nn, out, st), "add");
         }
-        cuda_ok(cudaStreamSynchronize(st), "sync");  // host noise buffers are reused by the caller
+        if (sync) cuda_ok(cudaStreamSynchronize(st), "sync");  // host noise buffers are reused by the caller
     }
 };
 
@@ -764,65 +766,76 @@ void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nomina
             fail(ST_SOLVER, "greens",
                  "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
     }
-    // per-seed exp(beta_L dL + beta_tox dTox) maps: host noise (threaded), device shaping
-    DBuf V, dl, dtox, P, N, flag;
-    V.ensure(nn * 8 * B);
+    // Seeds stream through in chunks (the reference runs them one per worker thread with
+    // per-thread memory, solver.cpp:376-387): per chunk, the libstdc++ noise of the next
+    // chunk is drawn on `jobs` host threads while the device shapes this chunk's maps
+    // (exp(beta_L dL + beta_tox dTox), variation.cpp:162-195) and runs the fused mode-A
+    // passes on them; one stream synchronisation per chunk, none per seed.
+    const size_t per_seed_host = (v.sigma_sys != 0.0 ? 2 * 4 * nn : 0) + (v.sigma_rand != 0.0 ? 2 * nn : 0);
+    int chunk = std::max(1, std::min(256, static_cast<int>((512ull << 20) / std::max<size_t>(1, per_seed_host * 8))));
+    if (const char* e = getenv("GT_MC_SEED_CHUNK")) chunk = std::max(1, atoi(e));  // tests: force several chunks
+    DBuf V, dl, dtox, P, N, flags, stats, scratch;
+    V.ensure(nn * 8 * chunk);
     dl.ensure(nn * 8);
     dtox.ensure(nn * 8);
-    flag.ensure(8);
+    flags.ensure(sizeof(int) * chunk);
+    stats.ensure(sizeof(gtd_sample_stats) * chunk);
+    scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, 1) * chunk);
     upload(P, p_dyn.v.data(), nn * 8, st);
     upload(N, nominal_leak.v.data(), nn * 8, st);
     std::vector<int> capfail(B, 0);
-    {
-        VarDevice vd(d.get(), v, g.pitch);
-        const int nj = std::max(1, jobs);
-        std::vector<LeakNoise> noise(B);
+    std::vector<gtd_sample_stats> hs(B);
+    VarDevice vd(d.get(), v, g.pitch);
+    const int nj = std::max(1, jobs);
+    auto draw = [&](std::vector<LeakNoise>& buf, int s0, int cnt) {
+        buf.assign(cnt, LeakNoise{});
         std::atomic<int> next{0};
         std::vector<std::thread> pool;
-        for (int w = 0; w < nj; ++w)
+        for (int w = 0; w < std::min(nj, cnt); ++w)
             pool.emplace_back([&] {
-                for (int i = next.fetch_add(1); i < B; i = next.fetch_add(1)) {
+                for (int i = next.fetch_add(1); i < cnt; i = next.fetch_add(1)) {
                     VarParams vs = v;
-                    vs.seed = seeds[i];
-                    noise[i] = leak_noise(vs, n, vs.seed, 0);
+                    vs.seed = seeds[s0 + i];
+                    buf[i] = leak_noise(vs, n, vs.seed, 0);
                 }
             });
         for (auto& th : pool) th.join();
-        for (int i = 0; i < B; ++i) {
-            vd.field(v, noise[i].sys_l, noise[i].rnd_l, dl.as<double>());
-            vd.field(v, noise[i].sys_t, noise[i].rnd_t, dtox.as<double>());
-            cuda_ok(cudaMemsetAsync(flag.p, 0, 8, st), "memset");
+    };
+    std::vector<LeakNoise> cur, nxt;
+    std::vector<int> hflags(chunk);
+    draw(cur, 0, std::min(chunk, B));
+    for (int s0 = 0; s0 < B; s0 += chunk) {
+        const int cnt = std::min(chunk, B - s0);
+        cuda_ok(cudaMemsetAsync(flags.p, 0, sizeof(int) * cnt, st), "memset");
+        for (int i = 0; i < cnt; ++i) {
+            vd.field(v, cur[i].sys_l, cur[i].rnd_l, dl.as<double>(), false);
+            vd.field(v, cur[i].sys_t, cur[i].rnd_t, dtox.as<double>(), false);
             cuda_ok(gtd_leak_exp(nullptr, dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
-                                 V.as<double>() + i * nn, flag.as<int>(), st),
+                                 V.as<double>() + i * nn, flags.as<int>() + i, st),
                     "leakage exponent");
-            int fl = 0;
-            d2h(&fl, flag.p, 4, st);
-            capfail[i] = fl;
-            noise[i] = LeakNoise{};
         }
+        // run_one per seed on the fused mode-A kernels: P and nominal broadcast, closed forms at gs.mu
+        gtd_mc_in in{};
+        in.P = P.p;
+        in.N = N.p;
+        in.V = V.p;
+        in.sP = 0;
+        in.sN = 0;
+        in.sV = static_cast<long long>(nn);
+        in.nom_scale = 1.0;
+        gtd_mc_opts o{};
+        o.mu_per_sample = 0;
+        o.with_rand = 1;
+        o.exponent_cap = 1e300;  // the cap was checked on the exponent itself above
+        cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, nullptr, stats.as<gtd_sample_stats>(), scratch.p, cnt, st, nullptr,
+                             nullptr),
+                "mc batch");
+        if (s0 + cnt < B) draw(nxt, s0 + cnt, std::min(chunk, B - s0 - cnt));  // host, while the device runs
+        d2h(hs.data() + s0, stats.p, sizeof(gtd_sample_stats) * cnt, st);  // synchronises: cur is free again
+        d2h(hflags.data(), flags.p, sizeof(int) * cnt, st);
+        for (int i = 0; i < cnt; ++i) capfail[s0 + i] = hflags[i];
+        std::swap(cur, nxt);
     }
-    // run_one per seed on the fused mode-A kernels: P and nominal broadcast, closed forms at gs.mu
-    DBuf stats, scratch;
-    stats.ensure(sizeof(gtd_sample_stats) * B);
-    const int chunk = std::min(B, 256);
-    scratch.ensure(gtd_mc_scratch_bytes_per_sample(n, 1) * chunk);
-    gtd_mc_in in{};
-    in.P = P.p;
-    in.N = N.p;
-    in.V = V.p;
-    in.sP = 0;
-    in.sN = 0;
-    in.sV = static_cast<long long>(nn);
-    in.nom_scale = 1.0;
-    gtd_mc_opts o{};
-    o.mu_per_sample = 0;
-    o.with_rand = 1;
-    o.exponent_cap = 1e300;  // the cap was checked on the exponent itself above
-    cuda_ok(gtd_mc_batch(&d->d, &in, B, &o, nullptr, stats.as<gtd_sample_stats>(), scratch.p, chunk, st, nullptr,
-                         nullptr),
-            "mc batch");
-    std::vector<gtd_sample_stats> hs(B);
-    d2h(hs.data(), stats.p, sizeof(gtd_sample_stats) * B, st);
     const double per_ms = std::chrono::duration<double, std::milli>(wall::now() - t0).count() / B;
 
     std::vector<double> maxima;

@@ -65,6 +65,7 @@ struct gt_field {
 };
 struct gt_greens {
     Greens g;
+    mutable GtSolveSlot slot;  // prepared device set, built by the first gt_solve_* call
 };
 struct gt_result {
     std::vector<Field> rise;
@@ -291,7 +292,7 @@ gt_status gt_solve_steady(const gt_greens* g, const gt_field* p_dyn, int with_ra
                           double* online_ms) {
     return guarded([&] {
         double ms = 0.0;
-        Field f = gt_ops_steady(g->g, p_dyn->f, with_rand != 0, &ms);
+        Field f = gt_ops_steady(g->g, g->slot, p_dyn->f, with_rand != 0, &ms);
         if (online_ms) *online_ms = ms;
         *out = new gt_field{std::move(f)};
     });
@@ -304,7 +305,7 @@ gt_status gt_solve_step(const gt_greens* g, const gt_field* p_dyn, const double*
         double ms = 0.0;
         std::vector<double> tv(times, times + n_times);
         auto r = std::make_unique<gt_result>();
-        r->rise = gt_ops_step(g->g, p_dyn->f, tv, with_rand != 0, &ms);
+        r->rise = gt_ops_step(g->g, g->slot, p_dyn->f, tv, with_rand != 0, &ms);
         r->times = tv;
         if (online_ms) *online_ms = ms;
         *out = r.release();
@@ -361,7 +362,7 @@ gt_status gt_solve_trace(const gt_greens* g, const gt_trace* trace, int window, 
     return guarded([&] {
         double ms = 0.0;
         auto r = std::make_unique<gt_result>();
-        r->rise = gt_ops_trace(g->g, trace->dt, trace->frames, window, with_rand != 0, &r->times, &ms);
+        r->rise = gt_ops_trace(g->g, g->slot, trace->dt, trace->frames, window, with_rand != 0, &r->times, &ms);
         if (online_ms) *online_ms = ms;
         *out = r.release();
     });

@@ -42,8 +42,9 @@ struct Solve {
     int n, m;
     size_t mm, nn;
     cudaStream_t st;
-    DBuf Fd, X, flag, red, fr, pv, rnd_scale;
+    DBuf Fd, X, flag, red, fr, pv, rnd_scale, cnt, P, T, P0, Sp;  // the last four: per-call working maps
     double fk_max = 0.0, re_sum_F = 0.0;
+    bool rand_uploaded = false;  // f_rand / p_var of the (immutable) GreensSet are on the device
 
     explicit Solve(const Greens& g) {
         g.validate();
@@ -100,8 +101,10 @@ struct Solve {
         cuda_ok(gtd_crop(in, n, 1.0 / (double(m) * double(m)), out, st), "crop");
     }
     void upload_rand(const Greens& g) {
+        if (rand_uploaded) return;
         upload(fr, g.f_rand.v.data(), nn * 8, st);
         upload(pv, g.p_var.v.data(), nn * 8, st);
+        rand_uploaded = true;
     }
     // clamp_negatives over `maps` maps with one shared peak (solver.cpp:33-46)
     void clamp(double* T, size_t count, double peak, double tol, double vmin) {
@@ -111,7 +114,6 @@ struct Solve {
             std::snprintf(b, sizeof b, "%f", vmin);
             fail(ST_VALIDATION, "solver", std::string("negative temperature rise beyond tolerance: ") + b + " K");
         }
-        DBuf cnt;
         cnt.ensure(8);
         cuda_ok(cudaMemsetAsync(cnt.p, 0, 8, st), "memset");
         cuda_ok(gtd_clamp(T, count, static_cast<unsigned long long*>(cnt.p), st), "clamp");
@@ -127,6 +129,25 @@ Field download(const double* src, int n, double pitch, cudaStream_t st) {
 
 }  // namespace
 
+struct GtSolveCache {
+    int device;
+    Solve s;
+    GtSolveCache(const Greens& g, int dev) : device(dev), s(g) {}
+};
+
+namespace {
+// The handle's prepared set on the current device (built on first use; rebuilt if the
+// caller moved to another device). The caller holds slot.mu.
+Solve& prepared(const Greens& g, GtSolveSlot& slot) {
+    const int dev = current_device();
+    if (!slot.cache || slot.cache->device != dev) {
+        slot.cache.reset();
+        slot.cache = std::make_shared<GtSolveCache>(g, dev);
+    }
+    return slot.cache->s;
+}
+}  // namespace
+
 void gt_ops_check_trace(double dt, const std::vector<Field>& frames) {
     // reference solver.cpp:74-83
     if (frames.empty()) fail(ST_CONFIG, "solver", "power trace is empty");
@@ -138,12 +159,14 @@ void gt_ops_check_trace(double dt, const std::vector<Field>& frames) {
     }
 }
 
-Field gt_ops_steady(const Greens& g, const Field& p_dyn, bool with_rand, double* online_ms) {
+Field gt_ops_steady(const Greens& g, GtSolveSlot& slot, const Field& p_dyn, bool with_rand, double* online_ms) {
     need_device();
-    Solve S(g);
+    std::lock_guard<std::mutex> lk(slot.mu);
+    Solve& S = prepared(g, slot);
     auto t0 = wall::now();
     check_power(p_dyn, g.n, "steady_profile");
-    DBuf P, T;
+    DBuf& P = S.P;
+    DBuf& T = S.T;
     upload(P, p_dyn.v.data(), S.nn * 8, S.st);
     T.ensure(S.nn * 8);
     S.padded_fft(P.as<double>(), nullptr, S.X.p);
@@ -170,15 +193,16 @@ Field gt_ops_steady(const Greens& g, const Field& p_dyn, bool with_rand, double*
     return out;
 }
 
-std::vector<Field> gt_ops_step(const Greens& g, const Field& p_dyn, const std::vector<double>& times, bool with_rand,
-                               double* online_ms) {
+std::vector<Field> gt_ops_step(const Greens& g, GtSolveSlot& slot, const Field& p_dyn,
+                               const std::vector<double>& times, bool with_rand, double* online_ms) {
     need_device();
-    Solve S(g);
+    std::lock_guard<std::mutex> lk(slot.mu);
+    Solve& S = prepared(g, slot);
     auto t0 = wall::now();
     check_power(p_dyn, g.n, "step_response");
     for (double t : times)
         if (t < 0.0) fail(ST_CONFIG, "solver", "step_response: negative time");
-    DBuf P, P0, Sp, T;
+    DBuf &P = S.P, &P0 = S.P0, &Sp = S.Sp, &T = S.T;
     upload(P, p_dyn.v.data(), S.nn * 8, S.st);
     P0.ensure(S.mm * 16);
     Sp.ensure(S.mm * 16);
@@ -221,10 +245,11 @@ std::vector<Field> gt_ops_step(const Greens& g, const Field& p_dyn, const std::v
     return out;
 }
 
-std::vector<Field> gt_ops_trace(const Greens& g, double dt, const std::vector<Field>& frames, int window,
-                                bool with_rand, std::vector<double>* times, double* online_ms) {
+std::vector<Field> gt_ops_trace(const Greens& g, GtSolveSlot& slot, double dt, const std::vector<Field>& frames,
+                                int window, bool with_rand, std::vector<double>* times, double* online_ms) {
     need_device();
-    Solve S(g);
+    std::lock_guard<std::mutex> lk(slot.mu);
+    Solve& S = prepared(g, slot);
     auto t0 = wall::now();
     gt_ops_check_trace(dt, frames);
     if (frames.front().n != g.n) fail(ST_CONFIG, "solver", "trace frames do not match the GreensSet grid");

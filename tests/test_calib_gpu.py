@@ -112,7 +112,12 @@ def test_calibrate_per_cell_conductivity_matches_reference(b200lib, oracle, tmp_
     _check_rand_scale(tmp_path, Lb, gb, Lr, gr, n)
 
 
-def test_monte_carlo_matches_reference(b200lib, oracle, greens64, tmp_path):
+@pytest.mark.parametrize("seed_chunk", [None, "4"])
+def test_monte_carlo_matches_reference(b200lib, oracle, greens64, tmp_path, monkeypatch, seed_chunk):
+    """gt_monte_carlo (capi.cpp:345-369) against the reference library, seed for seed. The
+    seeds stream through in chunks (GT_MC_SEED_CHUNK=4 forces two chunks of 6 seeds)."""
+    if seed_chunk:
+        monkeypatch.setenv("GT_MC_SEED_CHUNK", seed_chunk)
     gdir = tmp_path / "g"
     oracle.save_greens_dir(greens64, gdir)
     var = _write(tmp_path / "var.txt", "beta 0.017\nseed 7\n")
