@@ -40,7 +40,7 @@ UNIT = "solves/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=150)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1")
@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64-line", action="store_true", help="skip the fp64 mode-A line")
     ap.add_argument("--no-mode-b", action="store_true")
     ap.add_argument("--no-cfg2", action="store_true", help="skip the config-2 (n=1024, Kirchhoff) sub-benchmark")
     ap.add_argument("--no-cfg3", action="store_true", help="skip the config-3 transient-trace sub-benchmark")
@@ -215,6 +216,160 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def host_info(threads: int) -> dict:
+    """CPU model / cores of this host and whether a CPU FFTW is installed."""
+    import ctypes.util
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = next((l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")), None)
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "threads_used": threads,
+            "cpu_fftw": ctypes.util.find_library("fftw3"),
+            "fft_in_oracle": "radix-2 fp64 shim (oracle/shim/fftw_shim.cpp; no CPU FFTW on this host)"}
+
+
+def _gt_call(L, st):
+    if st:
+        raise RuntimeError(L.gt_last_error().decode())
+
+
+def dropin_line(threads: int) -> dict:
+    """The reference's own C-ABI entry points, timed on both libraries with the same files:
+    gt_solve_steady (capi.cpp:193-204) on a config-1 power map and gt_monte_carlo
+    (capi.cpp:345-369) over seeds (libstdc++ noise, bit-identical draws on both sides)."""
+    import ctypes as C
+    from oracle import refpy
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import lib
+    res = {}
+    if not refpy.build_if_possible():
+        return {"unavailable": "oracle/_ref not built"}
+    d = Path(tempfile.mkdtemp())
+    g = greens_cfg1()
+    L = lib()
+    h = g.to_handle(L)
+    _gt_call(L, L.gt_greens_save(h, str(d / "g").encode()))
+    L.gt_greens_free(h)
+    (d / "var.txt").write_text("beta 0.017\nseed 7\n")
+    p = inputs.power_batch(inputs.CONFIGS["cfg1"], 0, 1, np.float64)[0]
+    for name, lb, reps, nseeds in (("b200", L, 20, 512), ("reference", refpy.ref_lib(), 3, 32)):
+        gh = C.c_void_p()
+        _gt_call(lb, lb.gt_greens_load(str(d / "g").encode(), C.byref(gh)))
+        f = C.c_void_p()
+        _gt_call(lb, lb.gt_field_create(256, g.pitch, b"watts", C.byref(f)))
+        np.ctypeslib.as_array(lb.gt_field_data(f), shape=(256, 256))[...] = p
+        out = C.c_void_p()
+        ms = C.c_double()
+        _gt_call(lb, lb.gt_solve_steady(gh, f, 1, C.byref(out), C.byref(ms)))  # first call: preparation
+        lb.gt_field_free(out)
+        t0 = time.perf_counter()
+        online = 0.0
+        for _ in range(reps):
+            _gt_call(lb, lb.gt_solve_steady(gh, f, 1, C.byref(out), C.byref(ms)))
+            online += ms.value
+            lb.gt_field_free(out)
+        wall = (time.perf_counter() - t0) / reps
+        seeds = (C.c_ulonglong * nseeds)(*range(1, nseeds + 1))
+        mean, sd = C.c_double(), C.c_double()
+        t0 = time.perf_counter()
+        _gt_call(lb, lb.gt_monte_carlo(gh, str(d / "var.txt").encode(), None, 84.0, f, seeds, nseeds, threads, None,
+                                       C.byref(mean), C.byref(sd)))
+        mc_s = time.perf_counter() - t0
+        res[name] = {"steady_ms_per_call": 1e3 * wall, "steady_online_ms": online / reps,
+                     "monte_carlo_seeds_per_s": nseeds / mc_s, "monte_carlo_seeds": nseeds,
+                     "monte_carlo_mean_max_K": mean.value}
+        lb.gt_field_free(f)
+        lb.gt_greens_free(gh)
+    res["steady_speedup"] = res["reference"]["steady_ms_per_call"] / res["b200"]["steady_ms_per_call"]
+    res["monte_carlo_speedup"] = res["b200"]["monte_carlo_seeds_per_s"] / res["reference"]["monte_carlo_seeds_per_s"]
+    res["note"] = ("n=256 config-1 GreensSet saved once and loaded by both libraries; gt_solve_steady with_rand=1, "
+                   "wall time per call (host field in, host field out); gt_monte_carlo with jobs = host threads, "
+                   "uniform 84 W nominal leakage, reference defaults + beta 0.017")
+    return res
+
+
+def cpu_trace(ga, blk, sched, steps: int, window: int) -> dict:
+    """Config 3 on the reference's own trace entry: gt_solve_trace (capi.cpp:244-255 ->
+    time_varying_profile, solver.cpp:212-287; window sum O(steps k m^2), no per-step leakage:
+    the reference has none on this path) on ONE trace of `steps` steps at n = 512, single
+    threaded as the reference is; the same call on this library beside it."""
+    import ctypes as C
+    from oracle import refpy
+    from paper_2307_12119_b200.api import lib
+    if not refpy.build_if_possible():
+        return None
+    d = Path(tempfile.mkdtemp())
+    L = lib()
+    h = ga.to_handle(L)
+    _gt_call(L, L.gt_greens_save(h, str(d / "g").encode()))
+    L.gt_greens_free(h)
+    n = ga.n
+    out = {}
+    for name, lb in (("reference", refpy.ref_lib()), ("b200", L)):
+        gh, tr = C.c_void_p(), C.c_void_p()
+        _gt_call(lb, lb.gt_greens_load(str(d / "g").encode(), C.byref(gh)))
+        _gt_call(lb, lb.gt_trace_create(1e-5, C.byref(tr)))
+        for s in range(steps):
+            f = C.c_void_p()
+            _gt_call(lb, lb.gt_field_create(n, ga.pitch, b"watts", C.byref(f)))
+            np.ctypeslib.as_array(lb.gt_field_data(f), shape=(n, n))[...] = sched[s][blk]
+            _gt_call(lb, lb.gt_trace_push(tr, f))
+            lb.gt_field_free(f)
+        res, ms = C.c_void_p(), C.c_double()
+        t0 = time.perf_counter()
+        _gt_call(lb, lb.gt_solve_trace(gh, tr, min(window, steps), 0, C.byref(res), C.byref(ms)))
+        out[name] = steps / (time.perf_counter() - t0)
+        lb.gt_result_free(res)
+        lb.gt_trace_free(tr)
+        lb.gt_greens_free(gh)
+    return {"value": out["reference"], "unit": "trace-steps/s", "cores": 1, "kind": "reference",
+            "sample": f"1 config-3 trace of {steps} steps (n=512, dt 10 us, window {min(window, steps)}) through the "
+                      "reference gt_solve_trace, single threaded; no per-step leakage (the reference trace path "
+                      "has none)", "b200_same_call": out["b200"]}
+
+
+def cpu_cfg0(threads: int, dev) -> dict:
+    """Config 0 in full (n = 64, fp64): the fixed-point restatement (port) on the host cores
+    beside the GPU mode B, both at 1e-4 K. The literal exp law has no fixed point (SURVEY §0);
+    the linear law is the convergent one."""
+    import dataclasses
+    import torch
+    from oracle import refpy
+    from paper_2307_12119_b200 import inputs
+    from paper_2307_12119_b200.api import GT_FP64, DeviceGreens, GreensArrays
+    g = GreensArrays.from_npz(ROOT / "tests" / "golden" / "greens_n64.npz")
+    c0 = inputs.CONFIGS["cfg0"]
+    S = 64
+    p = inputs.power_batch(c0, 0, S, np.float64)
+    v = inputs.variation_batch(c0, 0, S).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    _, it_ref, st_ref, secs = refpy.fixed_point_batch(g, p, v, jobs=threads, **kw)
+    lit = refpy.fixed_point_batch(g, p[:8], v[:8], jobs=threads, **dict(kw, law=1, max_iters=50))[2]
+    dg = DeviceGreens(g, GT_FP64, device=dev.index or 0)
+    P, V = torch.from_numpy(p).to(dev), torch.from_numpy(v).to(dev)
+    T = torch.empty_like(P)
+    it = torch.zeros(S, dtype=torch.int32, device=dev)
+    st = torch.zeros(S, dtype=torch.int32, device=dev)
+    o = dg.fp_opts(**kw)
+    dg.fp_batch_device(P.data_ptr(), V.data_ptr(), S, o, T.data_ptr(), it.data_ptr(), st.data_ptr())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        dg.fp_batch_device(P.data_ptr(), V.data_ptr(), S, o, T.data_ptr(), it.data_ptr(), st.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    gms = e0.elapsed_time(e1) / 5
+    dg.close()
+    return {"value": S / secs, "unit": "solves/s", "cores": threads, "kind": "port",
+            "sample": f"{S} config-0 maps (n=64, fp64), linear-law fixed point to 1e-4 K (oracle restatement of "
+                      f"fdm.cpp:167-205 with the reference convolution), mean {float(it_ref.mean()):.1f} iterations",
+            "gpu_value": S / (gms / 1e3), "gpu_iterations_equal": bool((it.cpu().numpy() == it_ref).all()),
+            "literal_exp_law_failed": f"{int((lit != 0).sum())}/8 (no fixed point, SURVEY §0)"}
+
+
 # ---------------------------------------------------------------- GPU arm
 def device_calibrated_greens(n):
     """GreensSet from this library's device calibration (modal kernel producer,
@@ -334,6 +489,20 @@ def run_cfg2(args, dev, ws, rank):
                                  "ref_fixed_point_rand_batch: 2.8e-13 K fp64, 1.8e-5 K fp32+fp64)"}
     dgc.close()
     del Ps, Tb
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        # the same combined loop in the oracle restatement (reference random_greens inside the
+        # loop, restate.h ref_fixed_point_rand_batch), one pair per host thread
+        from oracle import refpy
+        if refpy.build_if_possible():
+            k = min(B, os.cpu_count() or 1)
+            pc = P[:k].double().cpu().numpy() * scale
+            vc = V[:k].double().cpu().numpy()
+            _, itc, stc, secs = refpy.fixed_point_batch(ga, pc, vc, leak_frac=0.3, beta=0.017, law=1, kirchhoff=1,
+                                                        tol=1e-4, max_iters=200, jobs=k, with_rand=1)
+            res["combined"]["cpu_baseline"] = {
+                "value": k / secs, "unit": UNIT, "cores": k, "kind": "port",
+                "sample": f"{k} config-2 pairs x{scale} (n=1024, fp64), combined loop to 1e-4 K, "
+                          f"mean {float(itc.mean()):.1f} iterations, {secs:.1f} s", "failed": int((stc != 0).sum())}
     dg.close()
     return res
 
@@ -388,7 +557,11 @@ def run_cfg3(args, dev, ws, rank):
     b_ts = 4 * es * m * h + 8 * es * n * h + 4 * es * n * n  # DESIGN.md §4 config-3 per trace-step model
     rate = ws * B * steps / (ms / 1e3)
     dg.close()
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_trace(ga, blks[0], scheds[0], min(steps, 100), k)
     return {"value": rate, "unit": "trace-steps/s", "traces_per_gpu": B, "steps": steps, "window": k,
+            "cpu_baseline": cpu,
             "dt_s": 1e-5, "out_stride": stride, "n": n, "ms": ms, "ms_per_step": ms / steps,
             "peak_K": float(mx.max().item()), "bytes_per_trace_step_model": b_ts,
             "achieved_GBps_model": b_ts * rate / ws / 1e9,
@@ -557,6 +730,31 @@ def run_b200(args, cfg):
                  "peak_K": float(o64.max().item())}
         dg64.close()
 
+    # the reference's own arithmetic precision: the same batch in fp64 (BASELINE config 1
+    # computes in fp32 with the fp64 residual check; this line is the like-for-like fp64 rate)
+    fp64_line = None
+    if prec == GT_FP32 and not args.no_fp64_line:
+        dgd = DeviceGreens(greens_cfg1(), GT_FP64, device=local)
+        Pd, Vd = P.double(), V.double()
+        od = torch.empty_like(Pd)
+        sd = torch.zeros(B * SAMPLE_STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        od_opts = dgd.opts(leak_frac=0.3, mu_per_sample=0, with_rand=1, chunk=args.chunk)
+        dgd.mc_batch_device(Pd.data_ptr(), Vd.data_ptr(), B, od_opts, od.data_ptr(), sd.data_ptr(), stream.cuda_stream)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        r0.record(stream)
+        for _ in range(reps):
+            dgd.mc_batch_device(Pd.data_ptr(), Vd.data_ptr(), B, od_opts, od.data_ptr(), sd.data_ptr(),
+                                stream.cuda_stream)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        ms64 = shard.max_over_ranks(r0.elapsed_time(r1) / reps, dev)
+        fp64_line = {"value": ws * B / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64, "dtype": "f64",
+                     "whole_solve_GBps_survey_model": survey_bytes_per_solve(n, 8) * B / (ms64 / 1e3) / 1e9,
+                     "max_abs_vs_fp32_K": float((out.double() - od).abs().max().item())}
+        dgd.close()
+        del Pd, Vd, od
+
     # roofline of the dominant pass (CUDA events around each pass on the launching stream)
     bps = bytes_per_sample(n, es)
     dom = int(np.argmax(pass_ms[:3]))
@@ -696,8 +894,16 @@ def run_b200(args, cfg):
             cfg4 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
+    others = {}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_rate(cfg, args.cpu_seconds, os.cpu_count() or 1)
+        cpu.update(host_info(os.cpu_count() or 1))
+        for key, fn in (("cfg0", lambda: cpu_cfg0(os.cpu_count() or 1, dev)),
+                        ("dropin_api", lambda: dropin_line(os.cpu_count() or 1))):
+            try:
+                others[key] = fn()
+            except Exception as e:
+                others[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank == 0:
         line = {
@@ -735,6 +941,10 @@ def run_b200(args, cfg):
             line["cfg4"] = cfg4
         if cpu:
             line["cpu_baseline"] = cpu
+        if fp64_line:
+            line["fp64_mode_a"] = fp64_line
+        for key, val in others.items():
+            line[key] = val
         print(json.dumps(line), flush=True)
     dg.close()
     if ws > 1:
