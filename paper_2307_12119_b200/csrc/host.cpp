@@ -74,16 +74,37 @@ void Field::check_finite(const char* what) const {
 // Binary sidecar "<path>.bin": the 17-digit text stays the
 // interchange format; a raw little-endian copy next to it makes re-reads of large
 // maps (one 8192^2 map is ~1.7 GB of text) a memcpy. The sidecar is used only if
-// it is at least as new as the text and records the text's byte size, so a text
-// edited by another tool falls back to parsing. GT_NO_BINARY_SIDECAR=1 disables it.
+// it is at least as new as the text and records the text's byte size and a
+// fingerprint of its content (FNV-1a over the first and last 4 KiB: the header line
+// and the last rows), so a text rewritten by another tool -- same size, same
+// timestamp granularity, or mtimes copied by cp -p / rsync / tar -- falls back to
+// parsing. GT_NO_BINARY_SIDECAR=1 disables it.
 namespace {
 struct SidecarHeader {
     char magic[8];
     int32_t n, unit;
     double pitch;
     uint64_t text_bytes;
+    uint64_t text_hash;
 };
-constexpr char kMagic[8] = {'G', 'T', 'F', 'B', '1', 0, 0, 0};
+constexpr char kMagic[8] = {'G', 'T', 'F', 'B', '2', 0, 0, 0};
+uint64_t text_fingerprint(const std::string& path, uint64_t size) {
+    std::ifstream is(path, std::ios::binary);
+    uint64_t h = 1469598103934665603ull ^ size;
+    auto mix = [&](const char* p, std::streamsize k) {
+        for (std::streamsize i = 0; i < k; ++i) h = (h ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
+    };
+    char buf[4096];
+    is.read(buf, sizeof buf);
+    mix(buf, is.gcount());
+    if (size > 2 * sizeof buf) {
+        is.clear();
+        is.seekg(static_cast<std::streamoff>(size - sizeof buf));
+        is.read(buf, sizeof buf);
+        mix(buf, is.gcount());
+    }
+    return h;
+}
 bool sidecars_enabled() {
     const char* e = std::getenv("GT_NO_BINARY_SIDECAR");
     return !(e && *e && *e != '0');
@@ -98,7 +119,8 @@ bool read_sidecar(const std::string& path, Field* out) {
     SidecarHeader h{};
     if (!is.read(reinterpret_cast<char*>(&h), sizeof h)) return false;
     if (std::memcmp(h.magic, kMagic, 8) != 0 || h.n < 2 || h.unit < 0 || h.unit > 3) return false;
-    if (h.text_bytes != static_cast<uint64_t>(fs::file_size(path, ec)) || ec) return false;
+    const uint64_t size = static_cast<uint64_t>(fs::file_size(path, ec));
+    if (ec || h.text_bytes != size || h.text_hash != text_fingerprint(path, size)) return false;
     Field f(h.n, h.pitch, static_cast<Unit>(h.unit));
     if (!is.read(reinterpret_cast<char*>(f.v.data()), static_cast<std::streamsize>(f.v.size() * sizeof(double))))
         return false;
@@ -116,6 +138,7 @@ void write_sidecar(const Field& f, const std::string& path) {
     h.pitch = f.pitch;
     h.text_bytes = static_cast<uint64_t>(fs::file_size(path, ec));
     if (ec) return;
+    h.text_hash = text_fingerprint(path, h.text_bytes);
     std::ofstream os(path + ".bin", std::ios::binary | std::ios::trunc);
     os.write(reinterpret_cast<const char*>(&h), sizeof h);
     os.write(reinterpret_cast<const char*>(f.v.data()), static_cast<std::streamsize>(f.v.size() * sizeof(double)));

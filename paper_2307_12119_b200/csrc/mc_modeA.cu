@@ -28,6 +28,10 @@
 
 #include "mc_common.cuh"
 
+#ifndef GT_P2_ABL
+#define GT_P2_ABL 0  // timing ablations of the column pass (tools/var_time.sh); 0 = the product
+#endif
+
 namespace gtb {
 
 // ------------------------------------------------------------------ pass 2
@@ -264,6 +268,15 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 const int i = j + r * (M / 8);
                 const int xa = i < n ? i : M - 1 - i;  // mirror_pad
                 const int xb = (i + c) & (M - 1);      // centre_kernel: row i holds die row x
+#if GT_P2_ABL == 5  // timing ablation: no stage-0 global loads
+                v[b][0][r] = mk<T>(T(xa), T(va));
+                if (r < 2 || r >= 6) {
+                    v[b][1][r] = mk<T>(T(xb), T(r));
+                    v[b][2][r] = mk<T>(T(r), T(xb));
+                }
+                continue;
+#endif
+                // columns va and va + GA are adjacent in A's rows (a_col): one 8-byte load
                 const T* ar = Areal + sbase + static_cast<size_t>(xa) * hp + va;
                 v[b][0][r] = mk<T>(ar[0], CG == 2 ? ar[GA] : T(0));
                 // the centre embedding fills rows [0, M/4) u [3M/4, M): r in {0,1,6,7} only
@@ -293,6 +306,8 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                 const int sn = nx / CT, tn = nx - sn * CT;
 #endif
                 const size_t nb = static_cast<size_t>(sn) * n * hp + static_cast<size_t>(tn) * W;
+                // S: tiles beyond column c read column c's segment (see the S loads below)
+                const size_t nbS = static_cast<size_t>(sn) * n * hp + static_cast<size_t>(min(tn * W, (c / W) * W));
                 constexpr int LA = (W * int(sizeof(T)) + 127) / 128, LB = (W * int(sizeof(cplx<T>)) + 127) / 128;
                 constexpr int PER = 2 * LA + LB;  // A and S segments, then B
 #pragma unroll
@@ -302,7 +317,8 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                     if (k < LA)
                         prefetch_l2(reinterpret_cast<const char*>(Areal + o) + 128 * k);
                     else if (k < 2 * LA)
-                        prefetch_l2(reinterpret_cast<const char*>(Srow + o) + 128 * (k - LA));
+                        prefetch_l2(reinterpret_cast<const char*>(Srow + nbS + static_cast<size_t>(x) * hp) +
+                                    128 * (k - LA));
                     else
                         prefetch_l2(reinterpret_cast<const char*>(Bspec + o) + 128 * (k - 2 * LA));
                 }
@@ -315,7 +331,8 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
 #pragma unroll
         for (int k = 0; k < ES; ++k) {
             const int idx = threadIdx.x + k * NT;
-            sv[k] = idx < n * W ? Srow[sbase + static_cast<size_t>(idx / W) * hp + v0 + idx % W] : T(0);
+            // S columns beyond c are all equal to column c (pass 1 writes [0, c] only)
+            sv[k] = idx < n * W ? Srow[sbase + static_cast<size_t>(idx / W) * hp + min(v0 + idx % W, c)] : T(0);
         }
 #pragma unroll
         for (int b = 0; b < B0; ++b) {
@@ -362,7 +379,9 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
         cf.mn2 = Real<T>::max();
         __syncthreads();
         // ---- middle forward stages
+#if GT_P2_ABL != 4  // timing ablation 4: without the middle forward stage
         FwdStagesAB<T, M, GA, NT, 1, K - 1>::run(tile, s_twf);
+#endif
         // ---- last forward stage + closed forms + first inverse stage, in registers.
         // All forward inputs are read before one barrier, so each column's (Y, R)
         // pair is stored as soon as it is transformed (two lines live, not four:
@@ -409,6 +428,18 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
                         const int sp = min(c + du, n - 1) * W, sm = max(c - du, 0) * W;
                         cplx<T> bb = z[b][1 + col][q];
                         const cplx<T> ph = cconj<T>(cmul<T>(s_hs[u], hv));
+#if GT_P2_ABL == 1  // timing ablation: table load, no closed form
+                        if constexpr (MF) {
+                            const auto t4 = cf.table(u, vv);
+                            const T C = col == 0 ? z[b][0][q].x : z[b][0][q].y;
+                            yr[0][q] = mk<T>(C * t4.x, C * t4.y);
+                        } else
+#elif GT_P2_ABL == 2  // timing ablation: no table, no closed form
+                        if constexpr (MF) {
+                            const T C = col == 0 ? z[b][0][q].x : z[b][0][q].y;
+                            yr[0][q] = mk<T>(C * ph.x, C * ph.y);
+                        } else
+#endif
                         if constexpr (MF)
                             yr[0][q] = cf.eval(col == 0 ? z[b][0][q].x : z[b][0][q].y, bb,
                                                s_srow[sp + w] + s_srow[sm + w], ph, cf.table(u, vv), cf.g(du, vv));
@@ -433,7 +464,9 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
             if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(&stats[sg].max_rden2), __float_as_int(wm));
         }
         // ---- middle inverse stages
+#if GT_P2_ABL != 3  // timing ablation 3: without the middle inverse stage
         InvStagesPairs<T, M, W, NT, 1, K - 1>::run(tile, s_twi);
+#endif
         // ---- last inverse stage (radix 8, NS = M/8): keep rows [0, n) of Y, rows rho(x) of R
         {
 #pragma unroll
@@ -454,6 +487,10 @@ mc_pass2(const MCIn<T> in, int sample0, int count, const T* __restrict__ Areal,
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int i = j + r * (M / 8);
+#if GT_P2_ABL == 6  // timing ablation: no global stores (kept alive by an impossible condition)
+                    if (o[0][r].x == T(1.2345e-30) && o[1][r].y == T(-7.5e-31)) Yspec[0] = o[0][r];
+                    continue;
+#endif
                     if (i < n) Yspec[sbase + static_cast<size_t>(i) * hp + vv] = o[0][r];
                     const int x = (i + c) & (M - 1);
                     if (x < n) Bspec[sbase + static_cast<size_t>(x) * hp + vv] = o[1][r];
@@ -545,49 +582,35 @@ struct MCLaunch {
                    gtd_mark_fn mark, void* ctx) {
         constexpr int n = Gm::n, hp = Gm::hp, W = Gm::W;
         constexpr int CT = hp / W;
-        static int res[3] = {0, 0, 0};
-        static int sms = 0;
-        if (!sms) {
-            res[0] = mc_rows_setup<T, M>(1);
-            res[2] = mc_rows_setup<T, M>(3);
+        // Kernel attributes and resident CTAs per SM, set up once per (T, M) (a function-local
+        // static: thread-safe initialisation; every device of a node is the same sm_100a part).
+        struct Occ {
+            int res[3];
+            int sms;
+        };
+        static const Occ occ = [] {
+            Occ r{{0, 0, 0}, 0};
+            r.res[0] = mc_rows_setup<T, M>(1);
+            r.res[2] = mc_rows_setup<T, M>(3);
             cudaFuncSetAttribute(mc_pass2<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
             cudaFuncSetAttribute(mc_pass2<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2()));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], mc_pass2<T, M, false>, Gm::NT2, smem2());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r.res[1], mc_pass2<T, M, false>, Gm::NT2, smem2());
             int r2 = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, mc_pass2<T, M, true>, Gm::NT2, smem2());
-            res[1] = r2 < res[1] ? r2 : res[1];
+            r.res[1] = r2 < r.res[1] ? r2 : r.res[1];
             int dev = 0;
             cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            for (int& r : res) r = r < 1 ? 1 : r;
-        }
+            cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, dev);
+            for (int& x : r.res) x = x < 1 ? 1 : x;
+            return r;
+        }();
+        const int* res = occ.res;
+        const int sms = occ.sms;
         const size_t per = static_cast<size_t>(n) * hp;
         const cplx<T>* hs = reinterpret_cast<const cplx<T>*>(g->hs);
         const cplx<T>* tw = reinterpret_cast<const cplx<T>*>(g->tw);
         const T var_lo = T(exp(-o->exponent_cap)), var_hi = T(exp(o->exponent_cap));
-        // Overlap (GT_MC_OVERLAP=1): the chunk's scratch is split into two slots whose
-        // sub-chunks run on two streams, every pass on a one-CTA-per-SM grid, so the
-        // SM-issue-bound column pass of one slot shares the SMs with the HBM-bound row
-        // passes of the other.
-        static int ovl = -1;
-        static cudaStream_t aux = nullptr;
-        static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-        if (ovl < 0) {
-            const char* e = getenv("GT_MC_OVERLAP");
-            ovl = e ? atoi(e) : 0;
-            if (ovl) {
-                cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
-                cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
-                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
-            }
-        }
-        const int slots = (ovl && chunk >= 2) ? 2 : 1;
-        const int sub = chunk / slots;
-        const int cpsm = slots == 2 ? ovl : 0;  // CTAs per SM per pass under overlap
-        auto grid = [&](int items, int r) {
-            const int rr = cpsm > 0 && cpsm < r ? cpsm : r;
-            return items < sms * rr ? items : sms * rr;
-        };
+        auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         // TMA row staging in pass 3 needs 16-byte aligned N / V rows (the spectra always are)
         auto al16 = [](const void* p, long long stride_elems) {
             return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((stride_elems * sizeof(T)) % 16 == 0);
@@ -603,25 +626,17 @@ struct MCLaunch {
         static const int no_fgm = getenv("GT_MC_NO_FGM") ? atoi(getenv("GT_MC_NO_FGM")) : 0;  // A/B switch
         const bool mf = !o->mu_per_sample && g->fgm != nullptr && !no_fgm;
         cudaMemsetAsync(stats, 0, sizeof(gtd_sample_stats) * batch, st);
-        if (slots == 2) {
-            cudaEventRecord(ev_fork, st);
-            cudaStreamWaitEvent(aux, ev_fork, 0);
-        }
-        for (int s0 = 0, k = 0; s0 < batch; s0 += sub, ++k) {
-            const int cnt = batch - s0 < sub ? batch - s0 : sub;
-            const int slot = k % slots;
-            cudaStream_t ss = slot == 0 ? st : aux;
-            gtd_mark_fn mk_ = slot == 0 ? mark : nullptr;
-            unsigned char* base = static_cast<unsigned char*>(scratch) +
-                                  static_cast<size_t>(slot) * sub * gtd_mc_scratch_bytes_per_sample(n, sizeof(T) == 8);
-            cplx<T>* A = reinterpret_cast<cplx<T>*>(base);  // Y (pass 2 -> pass 3)
-            cplx<T>* B = A + per * sub;                     // B (pass 1 -> 2), R (pass 2 -> 3)
-            T* S = reinterpret_cast<T*>(B + per * sub);      // row-symmetrised leakage
-            T* Ar = S + per * sub;                           // real DCT part of A (pass 1 -> 2)
+        for (int s0 = 0; s0 < batch; s0 += chunk) {
+            const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
+            cudaStream_t ss = st;
+            gtd_mark_fn mk_ = mark;
+            cplx<T>* A = static_cast<cplx<T>*>(scratch);  // Y (pass 2 -> pass 3)
+            cplx<T>* B = A + per * chunk;                  // B (pass 1 -> 2), R (pass 2 -> 3)
+            T* S = reinterpret_cast<T*>(B + per * chunk);   // row-symmetrised leakage
+            T* Ar = S + per * chunk;                        // real DCT part of A (pass 1 -> 2)
             MCRowArgs<T> ra{in, s0, cnt, Ar, A, B, S, stats, tw, hs, var_lo, var_hi, out, T(g->rand_scale), o->with_rand};
-            auto per_sm = [&](int r) { return cpsm > 0 && cpsm < r ? cpsm : r; };
             if (mk_) mk_(ctx, 0, ss);
-            mc_rows_launch<T, M>(1, tma1, sms, per_sm(res[0]), ss, ra);
+            mc_rows_launch<T, M>(1, tma1, sms, res[0], ss, ra);
             if (mk_) mk_(ctx, 1, ss);
             const cplx<T>* k1 = static_cast<const cplx<T>*>(g->k1);
             if (mf)
@@ -633,12 +648,8 @@ struct MCLaunch {
                     in, s0, cnt, Ar, A, B, S, stats, tw, hs, static_cast<const T*>(g->fg), T(g->alpha),
                     T(g->beta), o->mu_per_sample, T(g->mu_fixed), k1, nullptr);
             if (mk_) mk_(ctx, 2, ss);
-            mc_rows_launch<T, M>(3, tma3, sms, per_sm(res[2]), ss, ra);
+            mc_rows_launch<T, M>(3, tma3, sms, res[2], ss, ra);
             if (mk_) mk_(ctx, 3, ss);
-        }
-        if (slots == 2) {
-            cudaEventRecord(ev_join, aux);
-            cudaStreamWaitEvent(st, ev_join, 0);
         }
         mc_finalize<<<(batch + 127) / 128, 128, 0, st>>>(stats, 0, batch, n, mf ? g->det_flags : 0, in.dcnt);
         if constexpr (sizeof(T) == 4) {

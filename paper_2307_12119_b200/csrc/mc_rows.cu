@@ -93,8 +93,10 @@ mc_pass1(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
         }
         // Row-symmetrised leakage for q (symmetric_multiplier, spectral.cpp:167-185),
         // read back from the embedded imaginary part: p_leak0(l, y) at j = (y - c) mod M.
-        for (int idx = threadIdx.x; idx < L * hp; idx += NT) {
-            const int l = idx / hp, dv = idx - l * hp;
+        // Columns dv >= c all hold L[n-1] + L[0] (both indices clamp): only [0, c] is
+        // written and the column pass reads column min(dv, c) (mc_pass2).
+        for (int idx = threadIdx.x; idx < L * (c + 1); idx += NT) {
+            const int l = idx / (c + 1), dv = idx - l * (c + 1);
             const int x = x0 + l;
             if (x >= n) continue;
             T v = T(0);
@@ -336,7 +338,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
             T* Srow_x = Srow + (static_cast<size_t>(s) * n + x) * hp;
             const T cst = __shfl_sync(0xffffffffu, lv[E - 1], 31) + __shfl_sync(0xffffffffu, lv[0], 0);
 #pragma unroll
-            for (int k = 0; k < (hp + 31) / 32; ++k) {
+            for (int k = 0; k < (c + 32) / 32; ++k) {
                 const int v = lane + 32 * k;
                 T val;
                 if (k < E / 2) {
@@ -345,7 +347,7 @@ mc_pass1w(const MCIn<T> in, int sample0, int count, T* __restrict__ Areal,
                 } else {
                     val = v < h ? cst : T(0);
                 }
-                if (v < hp) Srow_x[v] = val;
+                if (v <= c) Srow_x[v] = val;  // columns beyond c equal column c (read as min(v, c))
             }
         }
         // z[i] = mirror(applied)[i] + i * centre-embedded(p_leak0)[i], i = lane + 32 k,

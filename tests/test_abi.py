@@ -163,3 +163,65 @@ def test_field_binary_sidecar(b200lib, tmp_path):
     assert (got[0] == 5).all()
     L.gt_field_free(g)
     L.gt_field_free(f)
+
+
+def test_field_sidecar_same_size_rewrite_with_copied_mtime(b200lib, tmp_path):
+    """A text rewritten to the SAME byte size whose mtime is then set back (cp -p / rsync /
+    tar keep mtimes) must not be served from the stale sidecar: the sidecar records a
+    content fingerprint of the text, not only its size and age."""
+    import ctypes as C
+    import os
+    import numpy as np
+    L = b200lib
+    n = 8
+    f = C.c_void_p()
+    assert L.gt_field_create(n, 0.001, b"kelvin", C.byref(f)) == 0
+    vals = np.ctypeslib.as_array(L.gt_field_data(f), shape=(n, n))
+    vals[...] = 1.25
+    path = tmp_path / "t.map"
+    assert L.gt_field_save(f, str(path).encode()) == 0
+    st = os.stat(path)
+    text = path.read_text()
+    edited = text.replace("1.25", "2.25", 3)  # same length, different values
+    assert len(edited) == len(text) and edited != text
+    path.write_text(edited)
+    os.utime(path, ns=(st.st_atime_ns, st.st_mtime_ns - 10**9))  # older than the sidecar
+    g = C.c_void_p()
+    assert L.gt_field_load(str(path).encode(), C.byref(g)) == 0
+    got = np.ctypeslib.as_array(L.gt_field_data(g), shape=(n, n))
+    assert (got == 2.25).sum() == 3
+    L.gt_field_free(g)
+    L.gt_field_free(f)
+
+
+def test_error_metrics_match_reference_library(b200lib, oracle):
+    """gt_error_metrics (reference capi.cpp:333 -> error_metrics, solver.cpp:289-336) on
+    random fields against the reference library itself: MAE, max error, % of the
+    reference's max rise, and the hotspot hit (Chebyshev distance <= 1)."""
+    import numpy as np
+    rng = np.random.default_rng(11)
+
+    class Rep(C.Structure):
+        _fields_ = [("mae", C.c_double), ("max_err", C.c_double), ("pct", C.c_double), ("maxpct", C.c_double),
+                    ("hit", C.c_int)]
+    for trial in range(6):
+        n = int(rng.choice([4, 16, 64]))
+        a_v = rng.uniform(0, 50, (n, n))
+        b_v = a_v + rng.normal(0, 2.0, (n, n))
+        if trial % 2:
+            b_v[rng.integers(n), rng.integers(n)] += 100.0  # move the reference hotspot
+        reps = []
+        for L in (b200lib, oracle.ref_lib()):
+            a, b = C.c_void_p(), C.c_void_p()
+            assert L.gt_field_create(n, 0.001, b"kelvin", C.byref(a)) == 0
+            assert L.gt_field_create(n, 0.001, b"kelvin", C.byref(b)) == 0
+            np.ctypeslib.as_array(L.gt_field_data(a), shape=(n, n))[...] = a_v
+            np.ctypeslib.as_array(L.gt_field_data(b), shape=(n, n))[...] = b_v
+            r = Rep()
+            assert L.gt_error_metrics(a, b, C.byref(r)) == 0
+            reps.append((r.mae, r.max_err, r.pct, r.maxpct, r.hit))
+            L.gt_field_free(a)
+            L.gt_field_free(b)
+        ours, ref = reps
+        assert ours[4] == ref[4]
+        np.testing.assert_allclose(ours[:4], ref[:4], rtol=1e-12, atol=0)

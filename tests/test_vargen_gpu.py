@@ -23,18 +23,36 @@ def test_variation_statistics_and_determinism(b200lib, greens256):
     dg = DeviceGreens(greens256, 1)
     sigma, rng_frac = 0.10, 0.5
     dg.var_model(sigma, rng_frac)
-    seeds = np.arange(1, 257, dtype=np.uint64) * 0x9E3779B97F4A7C15
-    v = _gen(dg, seeds)
-    z = (v - 1.0) / sigma
-    assert abs(z.mean()) < 0.1          # 256 fields with a correlation range of half the die
-    assert abs(z.std() - 1.0) < 0.1
-    # empirical correlation at lag d (cells) vs the spherical correlogram 1 - 1.5x + 0.5x^3
+    # 2048 fields (in slices): with a correlation range of half the die a field has only a
+    # few independent degrees of freedom, so the ensemble statistics below have a sampling
+    # spread of ~0.01 (measured 3e-3 .. 8e-3); the bar is 0.03
+    seeds = np.arange(1, 2049, dtype=np.uint64) * 0x9E3779B97F4A7C15
     n = 256
     rng_cells = rng_frac * n
-    for d in (8, 32, 64):
-        c = np.mean(z[:, :, :-d] * z[:, :, d:]) / np.mean(z * z)
+    lags = (8, 32, 64)
+    s1 = s2 = 0.0
+    cross = {d: 0.0 for d in lags}
+    cnt = 0
+    for k in range(0, len(seeds), 256):
+        z = (_gen(dg, seeds[k:k + 256]) - 1.0) / sigma
+        s1 += z.sum()
+        s2 += (z * z).sum()
+        cnt += z.size
+        for d in lags:
+            cross[d] += np.mean(z[:, :, :-d] * z[:, :, d:]) * z.shape[0]
+        if k == 0:
+            v = z * sigma + 1.0
+    mean = s1 / cnt
+    std = np.sqrt(s2 / cnt - mean ** 2)
+    print(f"mean {mean:.4f}, std {std:.4f}")
+    assert abs(mean) < 0.03
+    assert abs(std - 1.0) < 0.03
+    # empirical correlation at lag d (cells) vs the spherical correlogram 1 - 1.5x + 0.5x^3
+    for d in lags:
+        c = cross[d] / len(seeds) / (s2 / cnt)
         x = d / rng_cells
-        assert abs(c - (1 - 1.5 * x + 0.5 * x ** 3)) < 0.1, (d, c)
+        print(f"lag {d}: {c:.4f} vs {1 - 1.5 * x + 0.5 * x ** 3:.4f}")
+        assert abs(c - (1 - 1.5 * x + 0.5 * x ** 3)) < 0.03, (d, c)
     # determinism: a sample depends only on its seed (not on batch size / position)
     v2 = _gen(dg, seeds[[17, 3, 200]])
     np.testing.assert_array_equal(v2, v[[17, 3, 200]])
