@@ -132,6 +132,11 @@ typedef struct gt_fp_opts {
                               rand_scale with f_rand = random_greens at the GreensSet mu
                               from the sample's leakage baseline (greens.cpp:225-251,
                               solver.cpp:169-174), before the Kirchhoff inverse. */
+    int accel;             /* 0: plain Picard iteration (the reference outer loop,
+                              fdm.cpp:167-205: iteration counts match it); k0 > 0:
+                              Chebyshev semi-iteration from iteration k0 on, with the
+                              contraction rate estimated per sample from the residual
+                              ratio there; same stop rule on max|G(T) - T|. */
 } gt_fp_opts;
 
 void gt_fp_opts_default(gt_fp_opts* o);

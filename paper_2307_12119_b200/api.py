@@ -96,7 +96,7 @@ class SampleStats(C.Structure):
 class FPOpts(C.Structure):
     _fields_ = [("leak_frac", dbl), ("law", cint), ("kirchhoff", cint), ("beta", dbl), ("t_ambient", dbl),
                 ("eta", dbl), ("tol", dbl), ("max_iters", cint), ("chunk", cint), ("fp32_stage_tol", dbl),
-                ("with_rand", cint)]
+                ("with_rand", cint), ("accel", cint)]
 
 
 SAMPLE_STATS_DTYPE = np.dtype([("sum_leak", "f8"), ("sum_applied", "f8"), ("sum_rise", "f8"),

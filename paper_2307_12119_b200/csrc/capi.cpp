@@ -762,6 +762,7 @@ void gt_fp_opts_default(gt_fp_opts* o) {
     o->chunk = 0;
     o->fp32_stage_tol = 0.0;
     o->with_rand = 0;
+    o->accel = 0;
 }
 
 size_t gt_fp_scratch_bytes(int n, int precision) { return gtd_fp_scratch_bytes_per_sample(n, precision == GT_FP64); }
@@ -890,6 +891,14 @@ void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int b
     o.warm_start = warm;
     o.H = H;
     o.sH = static_cast<long long>(n) * n;
+    o.accel = opts->accel > 0 ? opts->accel : 0;
+    o.Tprev = o.Yout = nullptr;
+    if (o.accel) {
+        d->fp_tprev.ensure(static_cast<size_t>(n) * n * batch * (d->fp64 ? 8 : 4));
+        d->fp_yout.ensure(static_cast<size_t>(n) * n * batch * (d->fp64 ? 8 : 4));
+        o.Tprev = d->fp_tprev.p;
+        o.Yout = d->fp_yout.p;
+    }
     long long launches = 0;
     d->order_in(st);
     cuda_ok(gtd_fp_batch(&d->d, &in, batch, &o, t_out, iters, status, mx, mean, d->fp_scratch.p, d->fp_state.p,

@@ -51,6 +51,10 @@ struct FPState {
     int iters;
     int active;
     double sum_app[2];  // sum of the applied map of iterations k (slot k & 1): shift-variant term
+    // Chebyshev acceleration (gtd_fp_opts.accel): x_{k+1} = omega (gamma G(x_k) + (1 - gamma) x_k
+    // - x_{k-1}) + x_{k-1}; omega = 0 runs plain Picard (the reference outer loop).
+    double res_prev;    // residual of the previous iteration
+    double omega, gamma, sigma2;
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
 fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
         FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
         const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient,
-        int warm, const T* __restrict__ H, long long sH, int it) {
+        int warm, const T* __restrict__ H, long long sH, int it, T* __restrict__ Tprev, T* __restrict__ Yout) {
     using Gm = FPGeom<T, M>;
     constexpr int n = Gm::n, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT, hp = Gm::hp;
     constexpr int RB = Gm::RB;
@@ -114,6 +118,9 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
         double dmax = 0.0, app_part = 0.0;
         int bad = 0;
         const T sig_prev = (!FIRST && H) ? T(state[sg].sum_app[(it - 1) & 1]) : T(0);
+        const double om = (!FIRST && Tprev) ? state[sg].omega : 0.0;  // Chebyshev acceleration
+        const T omt = T(om), gmt = T(om > 0.0 ? state[sg].gamma : 1.0);
+        T* Qs = Tprev ? Tprev + sg * n * n : nullptr;
 
         // Every global input of a stage is issued in batches of UB items ahead of
         // its use (one exposed HBM latency per batch, not one per element).
@@ -200,7 +207,14 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                                 }
                                 if (!finite_val(t)) bad |= GTD_ST_NONFINITE;
                                 dmax = fmax(dmax, double(fabs(t - told[u][half])));
-                                Ts[static_cast<size_t>(x + half) * n + j] = t;
+                                const size_t oq = static_cast<size_t>(x + half) * n + j;
+                                if (Qs) {
+                                    const T xprev = om > 0.0 ? Qs[oq] : T(0);
+                                    Qs[oq] = told[u][half];
+                                    Yout[sg * n * n + oq] = t;
+                                    if (om > 0.0) t = omt * (gmt * t + (T(1) - gmt) * told[u][half] - xprev) + xprev;
+                                }
+                                Ts[oq] = t;
                             }
                             const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
                             a[half] = pv[u][half] + lv[u][half] * f;
@@ -261,7 +275,8 @@ __global__ void __launch_bounds__(FPW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
 fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec, T* __restrict__ Ar,
           T* __restrict__ Tst, FPState* __restrict__ state, int* __restrict__ status,
           const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka,
-          T kb, T kexp, T t_ambient, int warm, const T* __restrict__ H, long long sH, int it) {
+          T kb, T kexp, T t_ambient, int warm, const T* __restrict__ H, long long sH, int it,
+          T* __restrict__ Tprev, T* __restrict__ Yout) {
     using Gm = FPGeom<T, M>;
     using WF = WarpFFT<T, M>;
     constexpr int n = Gm::n, h = Gm::h, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
@@ -286,8 +301,12 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
         // Every global input of the item is requested up front (one exposed
         // round trip per row pair instead of three): previous T rows, P rows,
         // leakage rows L0 = nom N V.
-        T t0[E], t1[E], p0[E], p1[E], l0[E], l1[E], h0[E], h1[E];
+        T t0[E], t1[E], p0[E], p1[E], l0[E], l1[E], h0[E], h1[E], q0[E], q1[E];
         const T sig_prev = (!FIRST && H) ? T(state[sg].sum_app[(it - 1) & 1]) : T(0);
+        // Chebyshev acceleration state (omega > 0: x_{k+1} from G(x_k), x_k and x_{k-1})
+        const double om = (!FIRST && Tprev) ? state[sg].omega : 0.0;
+        const T omt = T(om), gmt = T(om > 0.0 ? state[sg].gamma : 1.0);
+        T* Q0r = Tprev ? Tprev + sg * n * n + static_cast<size_t>(x0) * n : nullptr;
         {
             const T* P0 = in.P + sg * in.sP + static_cast<size_t>(x0) * n;
             const T* N0 = in.N + sg * in.sN + static_cast<size_t>(x0) * n;
@@ -302,7 +321,11 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
                 }
                 p0[t] = P0[j];
                 p1[t] = P0[n + j];
-                h0[t] = h1[t] = T(0);
+                h0[t] = h1[t] = q0[t] = q1[t] = T(0);
+                if (om > 0.0) {
+                    q0[t] = Q0r[j];
+                    q1[t] = Q0r[n + j];
+                }
                 if (!FIRST && H) {
                     const T* H0 = H + sg * sH + static_cast<size_t>(x0) * n;
                     h0[t] = H0[j];
@@ -349,6 +372,17 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
                 }
                 if (!finite_val(a) || !finite_val(b)) bad |= GTD_ST_NONFINITE;
                 dmax = fmax(dmax, fmax(double(fabs(a - t0[t])), double(fabs(b - t1[t]))));
+                if (Tprev) {  // keep x_k for the next accelerated step and G(x_k) as the result
+                    Q0r[j] = t0[t];
+                    Q0r[n + j] = t1[t];
+                    T* Y0r = Yout + sg * n * n + static_cast<size_t>(x0) * n;
+                    Y0r[j] = a;
+                    Y0r[n + j] = b;
+                }
+                if (om > 0.0) {  // x_{k+1} = omega (gamma G(x_k) + (1 - gamma) x_k - x_{k-1}) + x_{k-1}
+                    a = omt * (gmt * a + (T(1) - gmt) * t0[t] - q0[t]) + q0[t];
+                    b = omt * (gmt * b + (T(1) - gmt) * t1[t] - q1[t]) + q1[t];
+                }
                 T0r[j] = a;
                 T1r[j] = b;
                 t0[t] = a;
@@ -608,14 +642,21 @@ fp_cols_d(int sample0, int count, const T* __restrict__ Ar, cplx<T>* __restrict_
 __global__ void fp_init(FPState* st, int* status, int* iters, int sample0, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
-    st[sample0 + i] = FPState{0ull, 0, 1, {0.0, 0.0}};
+    st[sample0 + i] = FPState{0ull, 0, 1, {0.0, 0.0}, 0.0, 0.0, 1.0, 0.0};
     status[sample0 + i] = 0;
     iters[sample0 + i] = 0;
 }
 
 // Reference stop rule (fdm.cpp:190-200): converge check first, then max_iters.
+// Chebyshev semi-iteration on the Picard map G (opt-in, gtd_fp_opts.accel = k0 > 0): for
+// x = J x + b with the spectrum of the Jacobian J in [0, rho] (a positive kernel times a
+// positive leakage: L0^1/2 K L0^1/2 is symmetric positive), gamma = 2 / (2 - rho) maps it to
+// [-sigma, sigma], sigma = rho / (2 - rho), and omega_1 = 1, omega_2 = 2 / (2 - sigma^2),
+// omega_{k+1} = 1 / (1 - sigma^2 omega_k / 4) give the optimal polynomial error reduction.
+// rho is estimated per sample from the Picard residual ratio at iteration k0; a residual
+// that grows by 2x under acceleration drops the sample back to plain Picard.
 __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int count, double tol, int max_iters,
-                          int* active_count, int it) {
+                          int* active_count, int it, int accel) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     FPState& s = st[sample0 + i];
@@ -625,6 +666,22 @@ __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int
     iters[sample0 + i] = s.iters;
     const double res = __longlong_as_double(static_cast<long long>(s.res_bits));
     s.res_bits = 0ull;
+    if (accel > 0) {
+        if (s.omega > 0.0) {
+            if (res > 2.0 * s.res_prev) {
+                s.omega = -1.0;  // diverging under acceleration: plain Picard from here on
+                s.gamma = 1.0;
+            } else {
+                s.omega = s.omega == 1.0 ? 2.0 / (2.0 - s.sigma2) : 1.0 / (1.0 - 0.25 * s.sigma2 * s.omega);
+            }
+        } else if (s.omega == 0.0 && s.iters == accel && s.res_prev > 0.0) {
+            const double rho = fmin(0.97, fmax(0.0, 1.02 * res / s.res_prev));
+            s.gamma = 2.0 / (2.0 - rho);
+            s.sigma2 = (rho / (2.0 - rho)) * (rho / (2.0 - rho));
+            s.omega = 1.0;
+        }
+        s.res_prev = res;
+    }
     if (status[sample0 + i]) {
         s.active = 0;
     } else if (s.iters > 1 && res < tol) {
@@ -744,21 +801,25 @@ struct FPLaunch {
                 if (first)
                     fp_rows_w<T, M, true><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
+                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
+                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
                 else
                     fp_rows_w<T, M, false><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
-                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
+                        kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
+                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
             } else {
                 const int gr = grid(cnt * Gm::RB, res[0]);
                 if (first)
                     fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                      T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                     T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
+                                                                     T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
+                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
                 else
                     fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
                                                                       T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                      T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_);
+                                                                      T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
+                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
             }
         };
         for (int s0 = 0; s0 < batch; s0 += chunk) {
@@ -772,7 +833,7 @@ struct FPLaunch {
                 rows(false, s0, cnt, it);
                 cudaMemsetAsync(counter_d, 0, sizeof(int), st);
                 fp_update<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt, o->tol, o->max_iters,
-                                                            counter_d, it);
+                                                            counter_d, it, o->accel);
                 k += 3;
                 if (it % poll == 0 || it == o->max_iters) {
                     cudaMemcpyAsync(counter_h, counter_d, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -780,6 +841,10 @@ struct FPLaunch {
                     if (*counter_h == 0) break;
                 }
             }
+            if (o->Tprev)  // accelerated: the result is G(x_k) of the last iteration (its error
+                           // bound is the reference stop rule's, not that of the extrapolated x_{k+1})
+                cudaMemcpyAsync(Tst + static_cast<size_t>(s0) * n * n, static_cast<T*>(o->Yout) + static_cast<size_t>(s0) * n * n,
+                                sizeof(T) * n * n * cnt, cudaMemcpyDeviceToDevice, st);
             fp_stats<T><<<cnt, 512, 0, st>>>(Tst, n, s0, mx, mean);
             k += 1;
         }

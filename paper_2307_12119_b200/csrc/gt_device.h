@@ -173,6 +173,10 @@ typedef struct gtd_fp_opts {
     const void* H;    /* optional [B][n][n] shift-variant maps h = f_rand o p_var * rand_scale:
                          theta += h * sum(applied) each iteration (combined config 2)      */
     long long sH;     /* sample stride of H in elements                                    */
+    int accel;        /* 0: Picard (reference outer loop); k0 > 0: Chebyshev semi-iteration
+                         from iteration k0 on, rho from the residual ratio there              */
+    void* Tprev;      /* [B][n][n] x_{k-1} state of the acceleration (required if accel)   */
+    void* Yout;       /* [B][n][n] G(x_k) of the last iteration: the result (required if accel) */
 } gtd_fp_opts;
 /* fp32 <-> fp64 copies of device maps (fp64 finish stage of an fp32 fixed point). */
 int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st);

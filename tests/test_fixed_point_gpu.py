@@ -142,3 +142,30 @@ def test_fixed_point_fp32_only_stage_is_selectable(b200lib, greens64, golden):
     eb = np.abs(b[0] - c[0]).max()
     print(f"fp32+fp64 finish vs fp64: {ea:.2e} K; fp32 only: {eb:.2e} K")
     assert ea <= 1e-4  # the fp64 finish lands within the stop tolerance of the fp64 fixed point
+
+
+@pytest.mark.parametrize("law,kirchhoff,scale", [(0, 0, 1.0), (1, 0, 0.25), (1, 1, 0.15)])
+def test_accelerated_fixed_point(b200lib, oracle, greens256, law, kirchhoff, scale):
+    """Chebyshev-accelerated iteration (gt_fp_opts.accel = 4): the same fixed point as the
+    reference outer loop (oracle, Picard to 1e-4 K) to <= 1e-3 K in fewer iterations."""
+    import torch
+    from paper_2307_12119_b200 import inputs
+    P, V = inputs.mc_inputs(inputs.CONFIGS["cfg1"], 0, 8, device="cuda", torch_dtype=torch.float32)
+    p = P.cpu().numpy().astype(np.float64) * scale
+    v = V.cpu().numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=law, kirchhoff=kirchhoff, tol=1e-4, max_iters=120)
+    t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(greens256, p, v, jobs=8, **kw)
+    assert (st_ref == 0).all()
+    for prec in (1, 0):
+        dg = _dg(greens256, prec)
+        dt = np.float64 if prec else np.float32
+        out, it, st, _, _ = dg.fp_batch_host(p.astype(dt), v.astype(dt), dg.fp_opts(accel=4, **kw))
+        assert (st == 0).all(), st
+        err = np.abs(out.astype(np.float64) - t_ref).max()
+        print(f"accel law={law} kirchhoff={kirchhoff} prec={prec}: iters {it.tolist()} vs Picard "
+              f"{it_ref.tolist()}, max|dT| {err:.2e} K")
+        assert err <= 1e-3
+        if prec == 1:
+            assert it.mean() < it_ref.mean()
+        else:  # + the fp64 finish stage's iterations (>= 2 after the 5e-4 K hand-over)
+            assert it.mean() < it_ref.mean() + 2
