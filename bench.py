@@ -59,6 +59,7 @@ def parse():
                     help="under torchrun (N > 1) also run the mode-B / config-2/3/4 sub-benchmarks (default: "
                          "N > 1 measures the headline and e2e only; the sub-benchmarks are N = 1 parity configs)")
     ap.add_argument("--cfg4-n", type=int, default=8192)
+    ap.add_argument("--cfg4-timeout", type=float, default=240.0, help="config-4 watchdog (seconds)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -640,7 +641,9 @@ def run_b200(args, cfg):
 
     ws, rank, local = dist_env()
     if ws > 1 and not args.sub_at_scale:
-        args.no_mode_b = args.no_cfg2 = args.no_cfg3 = args.no_cfg4 = True
+        # the other sub-benchmarks are N = 1 parity configs; config 4 is the one that
+        # exercises the multi-GPU exchange (slab all-to-all), so it stays on (watchdog below)
+        args.no_mode_b = args.no_cfg2 = args.no_cfg3 = True
     if ws > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     torch.cuda.set_device(local)
@@ -908,12 +911,6 @@ def run_b200(args, cfg):
             cfg3 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cfg4 = None
-    if not args.no_cfg4:
-        try:
-            cfg4 = run_cfg4(args, dev, ws, rank)
-        except Exception as e:
-            cfg4 = {"error": f"{type(e).__name__}: {e}"[:300]}
-
     cpu = None
     others = {}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -958,14 +955,33 @@ def run_b200(args, cfg):
             line["cfg2"] = cfg2
         if cfg3:
             line["cfg3"] = cfg3
-        if cfg4:
-            line["cfg4"] = cfg4
         if cpu:
             line["cpu_baseline"] = cpu
         if fp64_line:
             line["fp64_mode_a"] = fp64_line
         for key, val in others.items():
             line[key] = val
+    # Config 4 last, under a watchdog: a stuck exchange must not cost the headline line
+    # (rank 0 prints it with a timeout note and every rank exits).
+    if not args.no_cfg4:
+        import threading
+
+        def on_timeout():
+            if rank == 0:
+                line["cfg4"] = {"error": f"timeout after {args.cfg4_timeout:.0f} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+        wd = threading.Timer(args.cfg4_timeout, on_timeout)
+        wd.daemon = True
+        wd.start()
+        try:
+            cfg4 = run_cfg4(args, dev, ws, rank)
+        except Exception as e:
+            cfg4 = {"error": f"{type(e).__name__}: {e}"[:300]}
+        wd.cancel()
+        if rank == 0:
+            line["cfg4"] = cfg4
+    if rank == 0:
         print(json.dumps(line), flush=True)
     dg.close()
     if ws > 1:

@@ -116,7 +116,23 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
     if world > 1:
         zrecv = torch.empty((world, P, 2 * hc), dtype=cd, device=dev)
         yrow = torch.empty((rows, h), dtype=cd, device=dev)
-        mir = [torch.remainder(m - cq - torch.arange(hq, device=dev), m) for cq, hq in ranges]
+        # Per-destination send blocks as ONE gather from the row spectra z [P][m]: block q holds,
+        # for every local row pair, the columns rank q owns and their mirrors m - v (compact
+        # layout of gt_large_cols). The index maps are built once; each iteration is a single
+        # index_select into a preallocated buffer (no per-iteration concatenation).
+        cols = []
+        for cq, hq in ranges:
+            own = torch.arange(cq, cq + hq, device=dev)
+            blk = torch.cat([own, torch.remainder(m - own, m)])
+            cols.append((torch.arange(P, device=dev)[:, None] * m + blk[None, :]).reshape(-1))
+        send_idx = torch.cat(cols)
+        send = torch.empty(send_idx.numel(), dtype=cd, device=dev)
+        # receive side of the second exchange: source q's block [rows][hq] lands in columns
+        # [cq, cq + hq) of yrow -- one index_copy with a precomputed destination map
+        dst = [(torch.arange(rows, device=dev)[:, None] * h + torch.arange(cq, cq + hq, device=dev)[None, :])
+               .reshape(-1) for cq, hq in ranges]
+        recv_dst = torch.cat(dst)
+        recv = torch.empty(recv_dst.numel(), dtype=cd, device=dev)
     it, res, st = 0, float("inf"), 0
     for it in range(1, opts.max_iters + 1):
         ops.rows_fwd(app, P, s1, z, stream)
@@ -124,21 +140,16 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
             ops.cols(z, False, c0, hc, c1, c2, ycol, stream)
             yrow_t, hy = ycol, h
         else:
-            send = torch.cat([torch.cat([z[:, cq:cq + hq], z[:, mir[q]]], dim=1).reshape(-1)
-                              for q, (cq, hq) in enumerate(ranges)])
+            torch.index_select(z.view(-1), 0, send_idx, out=send)
             # output splits: what each source sends me; input splits: what I send each rank.
             # Complex blocks travel as their float64 (re, im) view (NCCL has no complex type).
             exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
                      [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
             ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, c1, c2, ycol, stream)
-            send = ycol.reshape(world, rows, hc).reshape(-1).contiguous()
-            recv = torch.empty(sum(rows * hq for _, hq in ranges), dtype=cd, device=dev)
-            exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
+            # ycol [n][hc] is already [world][rows][hc]: rank q's rows are a contiguous block
+            exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(ycol).view(-1),
                      [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)
-            off = 0
-            for q, (cq, hq) in enumerate(ranges):
-                yrow[:, cq:cq + hq] = recv[off:off + rows * hq].view(rows, hq)
-                off += rows * hq
+            yrow.view(-1).index_copy_(0, recv_dst, recv)
             yrow_t, hy = yrow, h
         res_bits.zero_()
         ops.rows_inv(yrow_t, hy, P, s1, t, app, p_local, l0, opts, res_bits, status, stream)
