@@ -765,7 +765,7 @@ def run_b200(args, cfg):
     peak, peak_src = peaks()
     # measured DRAM bytes of the dominant kernel (ncu --set full, committed under profiles/)
     traffic, traffic_src, fp32_util = None, None, None
-    tf = ROOT / "profiles" / "r1_traffic.json"
+    tf = ROOT / "profiles" / "r2_traffic.json"
     kname = ["mc_pass1w", "mc_pass2", "mc_pass3w"][dom] + f"<{'float' if es == 4 else 'double'}, {2 * n}>"
     if tf.exists():
         tj = json.loads(tf.read_text())
