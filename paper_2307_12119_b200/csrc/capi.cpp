@@ -133,8 +133,44 @@ size_t scratch_budget() {
 // allocated (a call that fits in it skips the cudaMemGetInfo query: no driver
 // round trip on the launch path of repeated calls)
 #ifndef GT_E2E_CHUNK
-#define GT_E2E_CHUNK 128  // pairs per chunk of the host-input pipelines
+#define GT_E2E_CHUNK 128  // first / last chunk of the host-input pipelines (pairs)
 #endif
+#ifndef GT_E2E_BIG
+#define GT_E2E_BIG 256    // steady-state chunk of the host-input pipelines (pairs)
+#endif
+
+// Chunk sizes of the host-input pipelines (two slots in flight). On the B200 hosts a
+// pinned H2D copy of 32 MiB runs at ~44 GB/s and one of >= 256 MiB at ~55 GB/s
+// (tools/h2d_bw.py: a ~0.15 ms fixed cost per copy), while a small first chunk shortens
+// the exposed first copy and a small last chunk the exposed last compute. So chunks ramp
+// up from GT_E2E_CHUNK to GT_E2E_BIG by doublings and back down at the end. Measured on
+// config 1 (4096 pairs, gt_mc_batch_seeded, tools/e2e_var.sh): uniform 128: 183k solves/s;
+// ramp 128 -> 512: 183k; 128 -> 1024: 152k; 64 -> 128: 164k; 128 -> 256: 195k (the
+// default: 21.0 ms per step against ~19.5 ms of pure PCIe time for its 1 GiB). A
+// caller-set chunk (gt_batch_opts.chunk) is used as is.
+std::vector<int> pipeline_chunks(int batch, const gt_batch_opts* o) {
+    std::vector<int> out;
+    if (o && o->chunk > 0) {
+        for (int s0 = 0; s0 < batch; s0 += o->chunk) out.push_back(std::min(o->chunk, batch - s0));
+        return out;
+    }
+    std::vector<int> up;
+    for (int c = GT_E2E_CHUNK; c < GT_E2E_BIG; c *= 2) up.push_back(c);
+    int ramp = 0;
+    for (int c : up) ramp += 2 * c;
+    if (batch <= ramp + GT_E2E_BIG) {
+        for (int s0 = 0; s0 < batch; s0 += GT_E2E_CHUNK) out.push_back(std::min(GT_E2E_CHUNK, batch - s0));
+        return out;
+    }
+    out = up;
+    int mid = batch - ramp;
+    while (mid > 0) {
+        out.push_back(std::min(GT_E2E_BIG, mid));
+        mid -= GT_E2E_BIG;
+    }
+    out.insert(out.end(), up.rbegin(), up.rend());
+    return out;
+}
 
 int auto_chunk(int n, int fp64, int batch, const gt_batch_opts* o, int share = 1, size_t have = 0) {
     if (o && o->chunk > 0) return std::min(o->chunk, batch);
@@ -556,10 +592,9 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         const int n = d->d.n;
         const size_t es = d->fp64 ? 8 : 4;
         const size_t map = static_cast<size_t>(n) * n * es;
-        // Pipeline chunk: two slots in flight; small chunks shorten the exposed first
-        // copy and last compute of the PCIe-bound pipeline (config 1, 4096 pairs:
-        // 512 -> 128 pairs per chunk took the end-to-end rate 191k -> 204k solves/s).
-        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, GT_E2E_CHUNK);
+        // Pipeline chunks: two slots in flight, sizes ramping up and down (pipeline_chunks)
+        const std::vector<int> chunks = pipeline_chunks(batch, opts);
+        const int chunk = *std::max_element(chunks.begin(), chunks.end());
         const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         for (int s = 0; s < 2; ++s) {
@@ -580,8 +615,8 @@ gt_status gt_mc_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         auto* hs = static_cast<gtd_sample_stats*>(d->host_stats);
         const char* P = static_cast<const char*>(p_dyn);
         const char* V = static_cast<const char*>(var);
-        for (int s0 = 0, k = 0; s0 < batch; s0 += chunk, ++k) {
-            const int cnt = std::min(chunk, batch - s0);
+        for (int s0 = 0, k = 0; k < static_cast<int>(chunks.size()); s0 += chunks[k], ++k) {
+            const int cnt = chunks[k];
             const int s = k & 1;
             cudaStream_t st = d->slot_stream[s];
             char* din = static_cast<char*>(d->slot_in[s].p);
@@ -680,7 +715,8 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         const int n = d->d.n;
         const size_t es = d->fp64 ? 8 : 4;
         const size_t map = static_cast<size_t>(n) * n * es;
-        int chunk = opts && opts->chunk > 0 ? std::min(opts->chunk, batch) : std::min(batch, GT_E2E_CHUNK);
+        const std::vector<int> chunks = pipeline_chunks(batch, opts);
+        const int chunk = *std::max_element(chunks.begin(), chunks.end());
         const int inner = auto_chunk(n, d->fp64, chunk, nullptr, 2, d->slot_scr[1].bytes);
         gtd_mc_opts o = to_dev_opts(opts);
         d->var_scratch.ensure(gtd_var_scratch_bytes_per_sample(n, d->fp64) * chunk);
@@ -706,8 +742,8 @@ gt_status gt_mc_batch_seeded(const gt_device_greens* dc, const void* p_dyn, cons
         cudaEvent_t gen_done[2];
         for (auto& e : gen_done) cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         for (auto& ss : d->slot_stream) d->order_in(ss);
-        for (int s0 = 0, k = 0; s0 < batch; s0 += chunk, ++k) {
-            const int cnt = std::min(chunk, batch - s0);
+        for (int s0 = 0, k = 0; k < static_cast<int>(chunks.size()); s0 += chunks[k], ++k) {
+            const int cnt = chunks[k];
             const int s = k & 1;
             cudaStream_t st = d->slot_stream[s];
             char* din = static_cast<char*>(d->slot_in[s].p);
