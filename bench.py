@@ -185,7 +185,7 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    per_step = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    per_step = max(0.5, 150.0 / max(1, args.steps + args.warmup))  # whole run ~150 s
     from oracle import refpy
     from paper_2307_12119_b200 import inputs
     if not refpy.build_if_possible():
