@@ -471,6 +471,16 @@ def run_cfg2(args, dev, ws, rank):
     msb = timed(lambda: dgc.fp_batch_device(Ps.data_ptr(), V.data_ptr(), B, fo, Tb.data_ptr(), it_d.data_ptr(),
                                             st_d.data_ptr(), mx_d.data_ptr(), None, stream.cuda_stream), 2)
     its = it_d.cpu().numpy()
+    Tpic = Tb.clone()
+    # the same solve with the Chebyshev-accelerated loop (gt_fp_opts.accel = 3)
+    fa = dgc.fp_opts(leak_frac=0.3, beta=0.017, law=1, kirchhoff=1, with_rand=1, tol=1e-4, max_iters=200, accel=3)
+    msa = timed(lambda: dgc.fp_batch_device(Ps.data_ptr(), V.data_ptr(), B, fa, Tb.data_ptr(), it_d.data_ptr(),
+                                            st_d.data_ptr(), mx_d.data_ptr(), None, stream.cuda_stream), 2)
+    its_a = it_d.cpu().numpy()
+    acc_line = {"value": ws * B / (msa / 1e3), "unit": UNIT, "ms_per_step": msa,
+                "mean_iterations": float(its_a.mean()), "max_iterations": int(its_a.max()),
+                "failed": int((st_d.cpu().numpy() != 0).sum()),
+                "max_abs_vs_picard_K": float((Tb.double() - Tpic.double()).abs().max().item())}
     h = n + 1
     b_it = 5 * es * n * n + 8 * es * n * h  # SURVEY §8(d) B_it (fp32: 54.56 MB at n = 1024)
     res["combined"] = {"value": ws * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
@@ -487,7 +497,8 @@ def run_cfg2(args, dev, ws, rank):
                        "achieved_GBps_model": (b_it * float(its.sum()) + survey_bytes_per_solve(n, es) * B)
                                               / (msb / 1e3) / 1e9,
                        "oracle": "tests/test_config2_gpu.py::test_config2_combined_matches_oracle (restate.h "
-                                 "ref_fixed_point_rand_batch: 2.8e-13 K fp64, 1.8e-5 K fp32+fp64)"}
+                                 "ref_fixed_point_rand_batch: 2.8e-13 K fp64, 1.8e-5 K fp32+fp64)",
+                       "accelerated": acc_line}
     dgc.close()
     del Ps, Tb
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -25,6 +25,10 @@
 #include "fft_warp.cuh"
 #include "gt_device.h"
 
+#ifndef GT_FP_UB
+#define GT_FP_UB 4  // global loads issued ahead per thread in the tile row pass (tuning)
+#endif
+
 namespace gtb {
 namespace {
 
@@ -88,8 +92,19 @@ __device__ __forceinline__ bool finite_val(T v) {
 }
 
 // ----------------------------------------------------------------- rows
+// Register budget of the tile row pass: the tile engine's 64 (fp32) leaves the M >= 1024
+// epilogue (theta -> T, Kirchhoff, shift-variant term, Chebyshev state) spilling; those
+// grids take one 512-thread CTA per SM with 128 registers instead (GT_FP_ROWS_MINB).
+#ifndef GT_FP_ROWS_MINB
+#define GT_FP_ROWS_MINB 0
+#endif
+template <typename T, int M>
+struct FPRowsMinB {
+    static constexpr int value = GT_FP_ROWS_MINB > 0 ? GT_FP_ROWS_MINB : TileGeom<T, M>::MINB;
+};
+
 template <typename T, int M, bool FIRST>
-__global__ void __launch_bounds__(TileGeom<T, M>::NT, TileGeom<T, M>::MINB)
+__global__ void __launch_bounds__(TileGeom<T, M>::NT, FPRowsMinB<T, M>::value)
 fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
         FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
         const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient,
@@ -124,7 +139,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
 
         // Every global input of a stage is issued in batches of UB items ahead of
         // its use (one exposed HBM latency per batch, not one per element).
-        constexpr int UB = 4;
+        constexpr int UB = GT_FP_UB;
         if (!FIRST) {
             // pack rows (2p, 2p+1) of the column-pass output into one Hermitian line pair
             constexpr int IPH = (L * h + NT - 1) / NT;
