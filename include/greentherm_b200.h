@@ -137,6 +137,9 @@ typedef struct gt_fp_opts {
                               Chebyshev semi-iteration from iteration k0 on, with the
                               contraction rate estimated per sample from the residual
                               ratio there; same stop rule on max|G(T) - T|. */
+    int warm_start;        /* 1: the t_out map holds the initial temperature rise T_0 on
+                              entry (device entry; e.g. the mode-A closed-form solution of
+                              the same pair), 0: T_0 = 0 as the reference loop starts. */
 } gt_fp_opts;
 
 void gt_fp_opts_default(gt_fp_opts* o);

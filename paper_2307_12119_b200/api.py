@@ -96,7 +96,7 @@ class SampleStats(C.Structure):
 class FPOpts(C.Structure):
     _fields_ = [("leak_frac", dbl), ("law", cint), ("kirchhoff", cint), ("beta", dbl), ("t_ambient", dbl),
                 ("eta", dbl), ("tol", dbl), ("max_iters", cint), ("chunk", cint), ("fp32_stage_tol", dbl),
-                ("with_rand", cint), ("accel", cint)]
+                ("with_rand", cint), ("accel", cint), ("warm_start", cint)]
 
 
 SAMPLE_STATS_DTYPE = np.dtype([("sum_leak", "f8"), ("sum_applied", "f8"), ("sum_rise", "f8"),
@@ -334,19 +334,19 @@ class DeviceGreens:
             setattr(o, k, v)
         return o
 
-    def fp_batch_host(self, p_dyn: np.ndarray, var: np.ndarray, opts: "FPOpts | None" = None):
-        """Mode B from host arrays -> (maps, iters, status, max, ms)."""
+    def fp_batch_host(self, p_dyn: np.ndarray, var: np.ndarray, opts: "FPOpts | None" = None, t0=None):
+        """Mode B from host arrays -> (maps, iters, status, max, ms); t0: initial maps (opts.warm_start)."""
         L = lib()
         dt = np.float64 if self.precision == GT_FP64 else np.float32
         p = np.ascontiguousarray(p_dyn, dtype=dt)
         v = np.ascontiguousarray(var, dtype=dt)
         B = p.shape[0]
-        out = np.empty_like(p)
+        o = opts or self.fp_opts()
+        out = np.empty_like(p) if not o.warm_start else np.ascontiguousarray(t0, dtype=dt).copy()
         it = np.empty(B, np.int32)
         st = np.empty(B, np.int32)
         mx = np.empty(B)
         ms = C.c_double()
-        o = opts or self.fp_opts()
         check(L, L.gt_fp_batch(self._d, p.ctypes.data_as(vp), v.ctypes.data_as(vp), B, C.byref(o),
                                out.ctypes.data_as(vp), it.ctypes.data_as(C.POINTER(cint)),
                                st.ctypes.data_as(C.POINTER(cint)), mx.ctypes.data_as(pdbl), C.byref(ms)))

@@ -799,6 +799,7 @@ void gt_fp_opts_default(gt_fp_opts* o) {
     o->fp32_stage_tol = 0.0;
     o->with_rand = 0;
     o->accel = 0;
+    o->warm_start = 0;
 }
 
 size_t gt_fp_scratch_bytes(int n, int precision) { return gtd_fp_scratch_bytes_per_sample(n, precision == GT_FP64); }
@@ -858,14 +859,15 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
             cuda_ok(gtd_fp_or_status(status, d->fp_hstats.as<gtd_sample_stats>(), batch, st), "status");
     };
     if (d->fp64 || stage_tol < 0.0 || opts->tol >= stage_tol) {
-        run_fp_stage(d, p_dyn, var, batch, opts, opts->tol, 0, H, t_out, iters, status, mx, mean, st);
+        run_fp_stage(d, p_dyn, var, batch, opts, opts->tol, opts->warm_start, H, t_out, iters, status, mx, mean, st);
         or_mode_a_status();
         return;
     }
     // "fp32 with fp64 residual check" (BASELINE config 1): the fp32 iteration runs to its
     // noise floor (stage_tol), then fp64 iterations warm-started from that iterate finish the
     // reference stop rule max|dT| < tol (fdm.cpp:190-200) on the fp64 fixed point.
-    run_fp_stage(d, p_dyn, var, batch, opts, stage_tol, 0, H, t_out, iters, status, nullptr, nullptr, st);
+    run_fp_stage(d, p_dyn, var, batch, opts, stage_tol, opts->warm_start, H, t_out, iters, status, nullptr, nullptr,
+                 st);
     gt_device_greens* d64 = fp64_twin(d);
     if (H) {
         d->fin_h.ensure(cnt * 8);
@@ -1133,6 +1135,10 @@ gt_status gt_fp_batch(const gt_device_greens* dc, const void* p_dyn, const void*
         cudaStream_t s = d->stream;
         cuda_ok(cudaMemcpyAsync(P.p, p_dyn, map * batch, cudaMemcpyHostToDevice, s), "h2d");
         cuda_ok(cudaMemcpyAsync(V.p, var, map * batch, cudaMemcpyHostToDevice, s), "h2d");
+        if (opts && opts->warm_start) {
+            if (!t_out) fail(ST_CONFIG, "capi", "warm_start needs the initial maps in t_out");
+            cuda_ok(cudaMemcpyAsync(T.p, t_out, map * batch, cudaMemcpyHostToDevice, s), "h2d");
+        }
         run_fp(d, P.p, V.p, batch, opts, T.p, it.as<int>(), st.as<int>(), mx.as<double>(), nullptr, s);
         if (t_out) cuda_ok(cudaMemcpyAsync(t_out, T.p, map * batch, cudaMemcpyDeviceToHost, s), "d2h");
         if (iters_out) cuda_ok(cudaMemcpyAsync(iters_out, it.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, s), "d2h");
