@@ -470,10 +470,29 @@ tr_rows_inv_w(int b0, int count, TRBuf<T> bf, TRStep sp, int nframes, int law, T
         const T* L0 = bf.leak0 + static_cast<size_t>(bg) * bf.leak_stride;
         T* O = sp.frame >= 0 ? out + (static_cast<size_t>(bg) * nframes + sp.frame) * nn : nullptr;
         T mx = T(0);
+        // next power rows: the block ids and leakage of both rows are requested together,
+        // then the schedule gathers -- two exposed round trips per row pair instead of a
+        // dependent blk -> sched chain per element (the pass was 84% long-scoreboard stalls)
+        int bk[2][E];
+        T lv[2][E], sv[2][E];
+        if (Pnext) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half)
+#pragma unroll
+                for (int t = 0; t < E; ++t) {
+                    const size_t o = static_cast<size_t>(x0 + half) * n + lane + 32 * t;
+                    bk[half][t] = blk[o];
+                    lv[half][t] = L0[o];
+                }
+#pragma unroll
+            for (int half = 0; half < 2; ++half)
+#pragma unroll
+                for (int t = 0; t < E; ++t) sv[half][t] = sch[bk[half][t]];
+        }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             const size_t rowo = static_cast<size_t>(x0 + half) * n;
-#pragma unroll 4
+#pragma unroll
             for (int t = 0; t < E; ++t) {
                 const int j = lane + 32 * t;
                 const cplx<T> zz = scr[j];
@@ -483,7 +502,7 @@ tr_rows_inv_w(int b0, int count, TRBuf<T> bf, TRStep sp, int nframes, int law, T
                 mx = mx > tv ? mx : tv;
                 if (Pnext) {
                     const T f = law ? T(exp(beta * tv)) : T(1) + beta * tv;
-                    Pnext[rowo + j] = sch[blk[rowo + j]] + L0[rowo + j] * f;
+                    Pnext[rowo + j] = sv[half][t] + lv[half][t] * f;
                 }
             }
         }
