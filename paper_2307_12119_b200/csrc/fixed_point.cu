@@ -182,7 +182,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
             constexpr int IPT = (L * n + NT - 1) / NT;
 #pragma unroll
             for (int i0 = 0; i0 < IPT; i0 += UB) {
-                T told[UB][2], pv[UB][2], lv[UB][2];
+                T told[UB][2], pv[UB][2], lv[UB][2], hv[UB][2], qv[UB][2];
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
                     const int idx = threadIdx.x + (i0 + u) * NT;
@@ -190,12 +190,15 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                     const int x = 2 * (p0 + l);
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
-                        told[u][half] = pv[u][half] = lv[u][half] = T(0);
+                        told[u][half] = pv[u][half] = lv[u][half] = hv[u][half] = qv[u][half] = T(0);
                         if (i0 + u < IPT && idx < L * n && x < n) {
                             const size_t o = static_cast<size_t>(x + half) * n + j;
                             if (!FIRST || warm) told[u][half] = Ts[o];
                             pv[u][half] = P[o];
                             lv[u][half] = in.nom_scale * Nm[o] * V[o];
+                            // the shift-variant map and the Chebyshev x_{k-1} join the same batch
+                            if (!FIRST && H) hv[u][half] = H[sg * sH + o];
+                            if (om > 0.0) qv[u][half] = Qs[o];
                         }
                     }
                 }
@@ -213,7 +216,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                             T t = FIRST ? told[u][half] : T(0);  // warm start: the caller's T_0
                             if (!FIRST) {
                                 T th = (half ? z.y : z.x) * inv;  // theta - T0
-                                if (H) th += H[sg * sH + static_cast<size_t>(x + half) * n + j] * sig_prev;
+                                if (H) th += hv[u][half] * sig_prev;
                                 t = th;
                                 if (kirchhoff) {
                                     const T br = ka + kb * th;
@@ -224,7 +227,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                                 dmax = fmax(dmax, double(fabs(t - told[u][half])));
                                 const size_t oq = static_cast<size_t>(x + half) * n + j;
                                 if (Qs) {
-                                    const T xprev = om > 0.0 ? Qs[oq] : T(0);
+                                    const T xprev = qv[u][half];
                                     Qs[oq] = told[u][half];
                                     Yout[sg * n * n + oq] = t;
                                     if (om > 0.0) t = omt * (gmt * t + (T(1) - gmt) * told[u][half] - xprev) + xprev;
