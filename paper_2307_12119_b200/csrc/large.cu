@@ -34,7 +34,11 @@ __device__ __forceinline__ cplx<T> twm(const double2* __restrict__ tw, int M, lo
     return mk<T>(T(w.x), T(inv ? -w.y : w.y));
 }
 
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // ------------------------------------------------------------------ pass ops
+// Every op: load(g, line, j) -> the element; pf(g, line, j) issues an L2 prefetch of the
+// same address(es) (lg_pass pulls the NEXT item's lines into L2 while it transforms this one).
 template <typename T>
 struct FwdA {
     static constexpr bool REDUCE = false;  // group p (row pair), line i1, j = i2
@@ -57,6 +61,18 @@ struct FwdA {
         }
         return mk<T>(app[static_cast<size_t>(2 * p) * n + y] - shift, app[static_cast<size_t>(2 * p + 1) * n + y] - shift);
     }
+    __device__ void pf(int p, int i1, int j) const {
+        const int i = i1 + M1 * j;
+        int y;
+        if (embed) {
+            y = (i + n / 2) & (M - 1);
+            if (y >= n) return;
+        } else {
+            y = i < n ? i : M - 1 - i;
+        }
+        pf_l2(app + static_cast<size_t>(2 * p) * n + y);
+        pf_l2(app + static_cast<size_t>(2 * p + 1) * n + y);
+    }
     using Pre = cplx<T>;  // the four-step twiddle, issued ahead of the stores
     __device__ Pre pre(int, int i1, int k2) const { return twm<T>(tw, M, static_cast<long long>(i1) * k2, false); }
     __device__ void store(int p, int i1, int k2, cplx<T> v, const Pre& w) const {
@@ -75,6 +91,7 @@ struct FwdB {
     __device__ cplx<T> load(int p, int k2, int j) const {
         return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M1) * k2];
     }
+    __device__ void pf(int p, int k2, int j) const { pf_l2(S1 + static_cast<size_t>(p) * M + j + static_cast<size_t>(M1) * k2); }
     struct Pre {};
     __device__ Pre pre(int, int, int) const { return {}; }
     __device__ void store(int p, int k2, int k1, cplx<T> v, const Pre&) const {
@@ -112,6 +129,19 @@ struct ColA {
         return (x & 1) ? mk<T>(T(0.5) * (a.y - b.y), T(-0.5) * (a.x - b.x))
                        : mk<T>(T(0.5) * (a.x + b.x), T(0.5) * (a.y + b.y));
     }
+    __device__ void pf(int i1, int c, int j) const {
+        const int i = i1 + M1 * j;
+        int x;
+        if (embed) {
+            x = (i + n / 2) & (M - 1);
+            if (x >= n) return;
+        } else {
+            x = i < n ? i : M - 1 - i;
+        }
+        const cplx<T>* Zp = Z + static_cast<size_t>(x >> 1) * zs;
+        pf_l2(Zp + oa + c);
+        pf_l2(Zp + ((ob + sb * c) & mask));
+    }
     using Pre = cplx<T>;
     __device__ Pre pre(int i1, int, int k2) const { return twm<T>(tw, M, static_cast<long long>(i1) * k2, false); }
     __device__ void store(int i1, int c, int k2, cplx<T> v, const Pre& w) const {
@@ -132,6 +162,9 @@ struct ColB {
     int h, M, M1, M2, c0, hc;
     __device__ cplx<T> load(int k2, int c, int j) const {
         return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
+    }
+    __device__ void pf(int k2, int c, int j) const {
+        pf_l2(C1 + (static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c);
     }
     // the spectral factor at (u, v); zero for the padded columns v > n
     __device__ cplx<T> midw(int k2, int c, int k1) const {
@@ -157,6 +190,7 @@ struct KColB {  // group k2, line c, j = i1: forward only; fk[u][v] natural orde
     __device__ cplx<T> load(int k2, int c, int j) const {
         return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
     }
+    __device__ void pf(int, int, int) const {}
     struct Pre {};
     __device__ Pre pre(int, int, int) const { return {}; }
     __device__ void store(int k2, int c, int k1, cplx<T> v, const Pre&) const {
@@ -176,6 +210,9 @@ struct ColC {
     int n, M, M1, M2, hc;
     __device__ cplx<T> load(int ia, int c, int j) const {
         return C2[(static_cast<size_t>(j) + static_cast<size_t>(M2) * ia) * hc + c];
+    }
+    __device__ void pf(int ia, int c, int j) const {
+        pf_l2(C2 + (static_cast<size_t>(j) + static_cast<size_t>(M2) * ia) * hc + c);
     }
     struct Pre {};
     __device__ Pre pre(int, int, int) const { return {}; }
@@ -199,6 +236,11 @@ struct RinvA {
         const cplx<T> y = Y[static_cast<size_t>(2 * p) * hy + w], r = Y[static_cast<size_t>(2 * p + 1) * hy + w];
         if (f == 0 || f == n) return mk<T>(y.x, r.x);
         return f < n ? mk<T>(y.x - r.y, y.y + r.x) : mk<T>(y.x + r.y, r.x - y.y);
+    }
+    __device__ void pf(int p, int k2, int j) const {
+        const int f = k2 + M2 * j, w = f <= n ? f : M - f;
+        pf_l2(Y + static_cast<size_t>(2 * p) * hy + w);
+        pf_l2(Y + static_cast<size_t>(2 * p + 1) * hy + w);
     }
     using Pre = cplx<T>;
     __device__ Pre pre(int, int k2, int ia) const { return twm<T>(tw, M, static_cast<long long>(ia) * k2, true); }
@@ -224,6 +266,7 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
     __device__ cplx<T> load(int p, int ia, int j) const {
         return S1[static_cast<size_t>(p) * M + j + static_cast<size_t>(M2) * ia];
     }
+    __device__ void pf(int p, int ia, int j) const { pf_l2(S1 + static_cast<size_t>(p) * M + j + static_cast<size_t>(M2) * ia); }
     struct Pre {
         T told[2], p[2], l0[2];
     };
@@ -309,6 +352,29 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
                 const int idx = base + u * NT;
                 const int l = Op::LINE_FAST ? idx % L : idx / N, j = Op::LINE_FAST ? idx / L : idx % N;
                 if (idx < N * L) tile[j * LP + l] = vals[u];
+            }
+        }
+#ifndef GT_LG_PF
+#define GT_LG_PF 1
+#endif
+        if (GT_LG_PF && L >= 8) {
+            // the next item's lines into L2 while this one is transformed: one prefetch per
+            // 128 bytes (8 consecutive 16-byte elements: 8 lines of a line-fast op, 8 j's otherwise)
+            const int nx = item + gridDim.x;
+            if (nx < groups * bpg) {
+                const int gn = nx / bpg, ln0 = (nx - gn * bpg) * L;
+                constexpr int LP8 = L / 8 > 0 ? L / 8 : 1, NP8 = N / 8;
+                for (int t = threadIdx.x; t < (Op::LINE_FAST ? LP8 * N : L * NP8); t += NT) {
+                    int l, j;
+                    if constexpr (Op::LINE_FAST) {
+                        l = (t % LP8) * 8;
+                        j = t / LP8;
+                    } else {
+                        l = t / NP8;
+                        j = (t % NP8) * 8;
+                    }
+                    if (ln0 + l < nlines) op.pf(gn, ln0 + l, j);
+                }
             }
         }
         __syncthreads();
