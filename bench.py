@@ -907,6 +907,7 @@ def run_b200(args, cfg):
                            "achieved_GBps_model": b_it * float(its.sum()) / (msb / 1e3) / 1e9},
             "linear_law_accelerated": accelerated}
 
+    torch.cuda.empty_cache()  # the sub-benchmarks size their batches from the free memory
     cfg2 = None
     if not args.no_cfg2:
         try:
@@ -914,6 +915,7 @@ def run_b200(args, cfg):
         except Exception as e:  # a sub-benchmark must not take the headline line down
             cfg2 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
+    torch.cuda.empty_cache()
     cfg3 = None
     if not args.no_cfg3:
         try:

@@ -1084,7 +1084,10 @@ gt_status gt_trace_batch_device(const gt_device_greens* dc, const int* blk, long
             size_t fr = 0, tot = 0;
             cuda_ok(cudaMemGetInfo(&fr, &tot), "meminfo");
             fr += d->trace_scratch.bytes;
-            chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(batch, (fr / 10 * 6) / per)));
+            const int fit = static_cast<int>(std::max<size_t>(1, std::min<size_t>(batch, (fr / 10 * 6) / per)));
+            // balanced chunks: 64 traces that fit 62 at a time run as 32 + 32, not 62 + 2
+            const int nchunks = (batch + fit - 1) / fit;
+            chunk = (batch + nchunks - 1) / nchunks;
         }
         d->trace_scratch.ensure(per * chunk);
         gtd_trace_in in{blk, blk_stride, sched, nblk, opts->steps, leak0, leak_stride};
