@@ -1,6 +1,6 @@
 """DRAM bytes per launch / per pair of the mode-A passes from an ncu --set full report.
 
-usage: python tools/traffic_json.py REP PAIRS_PER_LAUNCH SOURCE_NOTE > profiles/r1_traffic.json
+usage: python tools/traffic_json.py REP PAIRS_PER_LAUNCH SOURCE_NOTE > profiles/r2_traffic.json
 """
 import csv
 import io
