@@ -211,6 +211,15 @@ gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, i
 gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
                             double* app, const double* p, const double* l0, const gt_fp_opts* opts,
                             unsigned long long* res_bits, int* status, void* stream);
+/* rows_inv with the Chebyshev semi-iteration of gt_fp_opts.accel (slab.py drives omega /
+ * gamma from the residual history): x_prev [2 pairs][n] holds x_{k-1} on entry and x_k on
+ * exit, g_out (may be NULL) receives G(x_k); omega > 0 stores x_{k+1} =
+ * omega (gamma G(x_k) + (1 - gamma) x_k - x_{k-1}) + x_{k-1} in t (and the next applied
+ * rows from it); omega <= 0 is the plain Picard step. The residual is max|G(x_k) - x_k|. */
+gt_status gt_large_rows_inv_accel(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
+                                  double* app, const double* p, const double* l0, const gt_fp_opts* opts,
+                                  unsigned long long* res_bits, int* status, double* x_prev, double* g_out,
+                                  double omega, double gamma, void* stream);
 
 /* ---- Seeded variation maps generated on the device (n = 64, 128, 256).
  * The config-1 variation model: var = 1 + sigma_over_mu * z, z a unit-variance

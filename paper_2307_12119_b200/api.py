@@ -137,6 +137,8 @@ _EXT = [
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
     ("gt_large_rows_inv", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp]),
+    ("gt_large_rows_inv_accel", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp, vp,
+                                       C.c_double, C.c_double, vp]),
     ("gt_profile_begin", cint, [vp]),
     ("gt_profile_begin_mode", cint, [vp, cint]),
     ("gt_profile_end", cint, [vp, pdbl, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),

@@ -992,7 +992,16 @@ gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, i
 gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
                             double* app, const double* p, const double* l0, const gt_fp_opts* opts,
                             unsigned long long* res_bits, int* status, void* stream) {
+    return gt_large_rows_inv_accel(d, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, nullptr, nullptr,
+                                   0.0, 1.0, stream);
+}
+
+gt_status gt_large_rows_inv_accel(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
+                                  double* app, const double* p, const double* l0, const gt_fp_opts* opts,
+                                  unsigned long long* res_bits, int* status, double* x_prev, double* g_out,
+                                  double omega, double gamma, void* stream) {
     return guarded([&] {
+        if (omega > 0.0 && !x_prev) fail(ST_CONFIG, "capi", "large rows_inv: a Chebyshev step needs x_prev");
         if (!opts) fail(ST_CONFIG, "capi", "large rows_inv needs fixed-point options");
         const gtd_lg g = large_geom(d);
         gtd_fp_opts o{};
@@ -1001,8 +1010,8 @@ gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, in
         o.beta = opts->beta;
         o.t_ambient = opts->t_ambient;
         o.eta = opts->eta;
-        cuda_ok(gtd_lg_rows_inv(&g, y, hy, pairs, s1, t, app, p, l0, &o, res_bits, status,
-                                static_cast<cudaStream_t>(stream)),
+        cuda_ok(gtd_lg_rows_inv(&g, y, hy, pairs, s1, t, app, p, l0, &o, res_bits, status, x_prev, g_out, omega,
+                                gamma, static_cast<cudaStream_t>(stream)),
                 "large rows inv");
     });
 }

@@ -205,10 +205,11 @@ int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, voi
 int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, void* C1, void* C2, void* Y,
                 cudaStream_t st);
 /* Y [2 pairs][hy] (all columns 0..n of the slab's rows) -> theta -> T (Tst), residual (max bits),
- * status bits, next applied rows */
+ * status bits, next applied rows. Q / G (may be NULL): x_{k-1} in / x_k out, G(x_k) out; omega > 0
+ * stores the Chebyshev step x_{k+1} = omega (gamma G + (1 - gamma) x_k - x_{k-1}) + x_{k-1}. */
 int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1, double* Tst, double* app,
                     const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
-                    int* status, cudaStream_t st);
+                    int* status, double* Q, double* G, double omega, double gamma, cudaStream_t st);
 
 /* fk = FFT2(center_kernel(f_sp0 - phi)) + phi m^2/4 at DC, [m][fkp] (g->fk unused);
  * S1, Z: (n/2) x m complex scratch; C1: m x fkp complex scratch. */

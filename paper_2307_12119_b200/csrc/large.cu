@@ -259,6 +259,12 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
     T* app;        // [rows][n] next applied
     const T* P;    // [rows][n]
     const T* L0;   // [rows][n]
+    // Chebyshev semi-iteration (slab.py, accel > 0): Q holds x_{k-1} on entry and x_k on exit,
+    // G receives G(x_k) (the result once the stop rule holds); om > 0 stores
+    // x_{k+1} = om (gm G(x_k) + (1 - gm) x_k - x_{k-1}) + x_{k-1} as the state
+    T* Q = nullptr;
+    T* G = nullptr;
+    T om = T(0), gm = T(1);
     unsigned long long* res_bits;
     int* status;
     int n, M, M1, M2, law, kirchhoff;
@@ -268,7 +274,7 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
     }
     __device__ void pf(int p, int ia, int j) const { pf_l2(S1 + static_cast<size_t>(p) * M + j + static_cast<size_t>(M2) * ia); }
     struct Pre {
-        T told[2], p[2], l0[2];
+        T told[2], p[2], l0[2], q[2];
     };
     // the epilogue's global inputs, issued ahead of the stores (lg_pass batches 4 elements)
     __device__ Pre pre(int p, int ia, int ib) const {
@@ -281,6 +287,7 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
             r.told[half] = Tst[o];
             r.p[half] = P[o];
             r.l0[half] = L0[o];
+            r.q[half] = om > T(0) ? Q[o] : T(0);
         }
         return r;
     }
@@ -298,6 +305,9 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
             }
             if (!isfinite(t)) bad |= GTD_ST_NONFINITE;
             dmax = fmax(dmax, double(fabs(t - q.told[half])));
+            if (G) G[o] = t;
+            if (Q) Q[o] = q.told[half];
+            if (om > T(0)) t = om * (gm * t + (T(1) - gm) * q.told[half] - q.q[half]) + q.q[half];
             Tst[o] = t;
             const T f = law ? T(exp(beta * t)) : T(1) + beta * t;
             app[o] = q.p[half] + q.l0[half] * f;
@@ -532,7 +542,7 @@ int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, voi
 
 int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1, double* Tst, double* app,
                     const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
-                    int* status, cudaStream_t st) {
+                    int* status, double* Q, double* G, double omega, double gamma, cudaStream_t st) {
     RinvA<double> a{static_cast<const double2*>(Y), static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M2, hy};
     int e = launch<double>(g->M1, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
     if (e) return e;
@@ -542,6 +552,10 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
     b.app = app;
     b.P = P;
     b.L0 = L0;
+    b.Q = Q;
+    b.G = G;
+    b.om = omega;
+    b.gm = gamma;
     b.res_bits = res_bits;
     b.status = status;
     b.n = g->n;

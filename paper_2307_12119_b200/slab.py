@@ -17,6 +17,13 @@ max|T_{k+1} - T_k| < tol after iteration 1 (max over ranks), max_iters ->
 GT_SAMPLE_NOCONVERGE. With world = 1 no exchange happens and the column phase
 reads the row spectra in place.
 
+opts.accel = k0 > 0 runs the Chebyshev semi-iteration of gt_fp_batch (fixed_point.cu
+fp_update) on the same Picard map: plain iterations up to k0, the contraction rate
+rho from the residual ratio there (max over ranks, so every rank takes the same
+steps), then x_{k+1} = omega (gamma G(x_k) + (1 - gamma) x_k - x_{k-1}) + x_{k-1}
+in the inverse row pass; a residual that doubles falls back to Picard. The stop
+rule is unchanged (max|G(x_k) - x_k| < tol) and the result is G(x_k).
+
 The arithmetic lives in the sm_100a passes of libgreentherm_b200.so
 (`GpuLargeOps`, C ABI gt_large_*); this module only moves blocks between ranks.
 """
@@ -68,10 +75,17 @@ class GpuLargeOps:
         self._check(self.L.gt_large_cols(self.dg._d, self._p(z), int(compact), c0, hc, self._p(c1), self._p(c2),
                                          self._p(y), C.c_void_p(stream)))
 
-    def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream):
-        self._check(self.L.gt_large_rows_inv(self.dg._d, self._p(y), hy, pairs, self._p(s1), self._p(t),
-                                             self._p(app), self._p(p), self._p(l0), C.byref(opts),
-                                             self._p(res_bits), self._p(status), C.c_void_p(stream)))
+    def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream, q=None, g=None,
+                 omega=0.0, gamma=1.0):
+        if q is None:
+            self._check(self.L.gt_large_rows_inv(self.dg._d, self._p(y), hy, pairs, self._p(s1), self._p(t),
+                                                 self._p(app), self._p(p), self._p(l0), C.byref(opts),
+                                                 self._p(res_bits), self._p(status), C.c_void_p(stream)))
+        else:
+            self._check(self.L.gt_large_rows_inv_accel(
+                self.dg._d, self._p(y), hy, pairs, self._p(s1), self._p(t), self._p(app), self._p(p), self._p(l0),
+                C.byref(opts), self._p(res_bits), self._p(status), self._p(q), self._p(g), float(omega),
+                float(gamma), C.c_void_p(stream)))
 
 
 @dataclass
@@ -111,6 +125,10 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
     c1 = torch.empty((m, hc), dtype=cd, device=dev)
     c2 = torch.empty((m, hc), dtype=cd, device=dev)
     ycol = torch.empty((n, hc), dtype=cd, device=dev)
+    accel = int(getattr(opts, "accel", 0) or 0)
+    q = torch.zeros_like(p_local) if accel > 0 else None  # x_{k-1} in, x_k out
+    g = torch.empty_like(p_local) if accel > 0 else None  # G(x_k)
+    omega, gamma, sigma2, res_prev = 0.0, 1.0, 0.0, 0.0
     res_bits = torch.zeros(1, dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     if world > 1:
@@ -152,7 +170,8 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
             yrow.view(-1).index_copy_(0, recv_dst, recv)
             yrow_t, hy = yrow, h
         res_bits.zero_()
-        ops.rows_inv(yrow_t, hy, P, s1, t, app, p_local, l0, opts, res_bits, status, stream)
+        ops.rows_inv(yrow_t, hy, P, s1, t, app, p_local, l0, opts, res_bits, status, stream, q=q, g=g,
+                     omega=max(omega, 0.0), gamma=gamma)
         rs = torch.stack([res_bits.view(torch.float64)[0], status.to(torch.float64)[0]])
         if world > 1:
             flags = [torch.zeros_like(rs) for _ in range(world)]
@@ -165,8 +184,22 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
             res, st = float(rs[0]), int(rs[1])
         if st:
             break
+        if accel > 0:  # the next step's omega (fixed_point.cu fp_update)
+            if omega > 0.0:
+                if res > 2.0 * res_prev:
+                    omega, gamma = -1.0, 1.0  # diverging under acceleration: plain Picard from here on
+                else:
+                    omega = 2.0 / (2.0 - sigma2) if omega == 1.0 else 1.0 / (1.0 - 0.25 * sigma2 * omega)
+            elif omega == 0.0 and it == accel and res_prev > 0.0:
+                rho = min(0.97, max(0.0, 1.02 * res / res_prev))
+                gamma = 2.0 / (2.0 - rho)
+                sigma2 = (rho / (2.0 - rho)) ** 2
+                omega = 1.0
+            res_prev = res
         if it > 1 and res < opts.tol:
             break
         if it == opts.max_iters:
             st |= GT_SAMPLE_NOCONVERGE
+    if accel > 0:
+        t.copy_(g)  # G(x_k): its error bound is the stop rule's, not that of the extrapolated x_{k+1}
     return SlabResult(t=t, iterations=it, status=st, residual=res)

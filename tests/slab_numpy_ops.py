@@ -39,7 +39,8 @@ class NumpyLargeOps:
             out[:, c] = (np.fft.ifft(col) * m)[:n]
         y.copy_(__import__("torch").from_numpy(out))
 
-    def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream):
+    def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream, q=None, g=None,
+                 omega=0.0, gamma=1.0):
         import torch
         n, m = self.n, self.m
         Y = y.numpy()
@@ -47,19 +48,27 @@ class NumpyLargeOps:
         f = np.arange(m)
         w = np.where(f <= n, f, m - f)
         dmax = 0.0
-        for q in range(pairs):
-            r0, r1 = Y[2 * q][w], Y[2 * q + 1][w]
+        for pq in range(pairs):
+            r0, r1 = Y[2 * pq][w], Y[2 * pq + 1][w]
             r0 = np.where(f <= n, r0, np.conj(r0))
             r1 = np.where(f <= n, r1, np.conj(r1))
             line = (np.fft.ifft(r0 + 1j * r1) * m)[:n] / (m * m)
             for half, th in ((0, line.real), (1, line.imag)):
-                x = 2 * q + half
+                x = 2 * pq + half
                 tt = th
                 if opts.kirchhoff:
                     a_ = opts.t_ambient ** (1 - opts.eta)
                     b_ = (1 - opts.eta) * opts.t_ambient ** (-opts.eta)
                     tt = (a_ + b_ * th) ** (1 / (1 - opts.eta)) - opts.t_ambient
                 dmax = max(dmax, float(np.abs(tt - T[x]).max()))
+                if g is not None:
+                    g.numpy()[x] = tt
+                if q is not None:
+                    Q = q.numpy()
+                    xprev = Q[x].copy()
+                    Q[x] = T[x]
+                    if omega > 0:
+                        tt = omega * (gamma * tt + (1 - gamma) * T[x] - xprev) + xprev
                 T[x] = tt
                 fl = 1 + opts.beta * tt if opts.law == 0 else np.exp(opts.beta * tt)
                 A[x] = Pm[x] + L[x] * fl

@@ -184,3 +184,32 @@ def test_large_grid_n1024_converged_vs_oracle(b200lib, oracle, tmp_path):
           f"(oracle {secs:.1f} s)")
     assert res.status == 0 and res.iterations == it_ref[0]
     assert err <= 1e-8
+
+
+def test_large_grid_n1024_chebyshev_vs_oracle(b200lib, oracle, tmp_path):
+    """opts.accel on the large-grid path (Chebyshev steps in the inverse row pass, omega from
+    slab.py): fewer iterations than the reference loop, same stop rule, and the result
+    (G(x_k) of the last iteration) within 1e-3 K of the oracle's Picard fixed point."""
+    import dataclasses
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    n = 1024
+    f, phi, ga = _large_greens(b200lib, tmp_path, n)
+    cfg = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n, blocks=128, hotspots=16)
+    p = inputs.power_batch(cfg, 0, 1, np.float64)
+    p *= 300.0 / p.sum()
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(ga, p, v, jobs=1, **kw)
+    dg = DeviceGreens(ga, 1)
+    o = dg.fp_opts(**kw)
+    o.accel = 3
+    res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(p[0]).cuda(), torch.from_numpy(v[0]).cuda(), o)
+    torch.cuda.synchronize()
+    err = float(np.abs(res.t.cpu().numpy() - t_ref[0]).max())
+    print(f"large n=1024 Chebyshev: iters {res.iterations} vs {it_ref[0]} (Picard), max|dT| {err:.3e} K "
+          f"on peak {t_ref.max():.1f} K")
+    assert st_ref[0] == 0 and res.status == 0
+    assert res.iterations < it_ref[0]
+    assert err <= 1e-3

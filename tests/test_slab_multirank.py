@@ -19,7 +19,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, q):
+def _worker(rank, world, port, n, q, accel=0):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     import torch
@@ -40,6 +40,7 @@ def _worker(rank, world, port, n, q):
     o = FPOpts()
     o.leak_frac, o.law, o.kirchhoff, o.beta, o.tol, o.max_iters = 0.3, 0, 0, 0.017, 1e-10, 60
     o.t_ambient, o.eta = 318.15, 1.3
+    o.accel = accel
     res = slab.solve_slab(NumpyLargeOps(n, fk), n, torch.from_numpy(P[sl].copy()), torch.from_numpy(V[sl].copy()), o,
                           rank=rank, world=world)
     q.put((rank, res.t.numpy(), res.iterations, res.status))
@@ -79,3 +80,46 @@ def test_slab_exchange_matches_full_solve(world):
     assert all(g[3] == 0 for g in got)
     assert all(g[2] == it for g in got), (it, [g[2] for g in got])
     assert np.abs(T - ref).max() < 1e-9
+
+
+def _run(world, n, accel):
+    import queue
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, accel)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = []
+    while len(got) < world:
+        try:
+            got.append(q.get(timeout=5))
+        except queue.Empty:
+            assert all(p.is_alive() or p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got.sort(key=lambda g: g[0])
+    return np.concatenate([g[1] for g in got]), [g[2] for g in got], [g[3] for g in got]
+
+
+def test_slab_chebyshev_across_ranks():
+    """opts.accel: every rank takes the same Chebyshev steps (omega from the max-over-ranks
+    residual), so world 2 reproduces world 1 exactly, in fewer iterations than Picard,
+    and lands on the Picard fixed point."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from slab_numpy_ops import baseline_fk, fixed_point_numpy
+    n = 64
+    t1, it1, st1 = _run(1, n, 3)
+    t2, it2, st2 = _run(2, n, 3)
+    z = np.load(ROOT / "tests" / "golden" / "greens_n64.npz")
+    fk = baseline_fk(z["f_sp0"], float(z["phi"]))
+    rng = np.random.default_rng(3)
+    P = rng.uniform(0.0, 0.05, (n, n))
+    V = 1.0 + 0.1 * rng.standard_normal((n, n))
+    ref, it = fixed_point_numpy(P, V, fk, 0.3, 0.017, 0, 1e-10, 60)
+    assert st1 == [0] and st2 == [0, 0]
+    assert it2 == [it1[0]] * 2 and it1[0] < it, (it1, it2, it)
+    assert np.abs(t2 - t1).max() <= 1e-12
+    assert np.abs(t1 - ref).max() <= 1e-8
