@@ -657,8 +657,10 @@ def run_cfg4(args, dev, ws, rank):
             "ms_per_iteration": ms / res_it, "status": res_st, "peak_K": peak,
             "bytes_per_iteration_model": b_it, "achieved_GBps_model": b_it * res_it / (ms / 1e3) / 1e9,
             "accelerated": accel,
-            "scaling": "strong", "parallelism": f"slab over {ws} rank(s): row pairs / half-spectrum columns, "
-                                              "all-to-all transposes" if ws > 1 else "one GPU (no exchange)",
+            "scaling": "strong", "parallelism": f"slab over {ws} rank(s): row pairs / half-spectrum columns; the column "
+                                              "phase reads every rank's row spectra in place and stores into the owners' "
+                                              "row buffers over CUDA IPC peer mappings (gt_large_cols_peer, no all-to-all "
+                                              "copies)" if ws > 1 else "one GPU (no exchange)",
             "power_W": {"generated": P_total, "used": 300.0}, "prep_s": prep_s, "precision": "fp64",
             "law": "linear (1 + beta dT), beta 0.017, leak 0.3 x P x var, tol 1e-4 K"}
 

@@ -211,6 +211,22 @@ gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, i
 gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
                             double* app, const double* p, const double* l0, const gt_fp_opts* opts,
                             unsigned long long* res_bits, int* status, void* stream);
+/* cols over peer memory: the multi-GPU column phase without all-to-all copies.
+ * z_ranks / y_ranks are DEVICE arrays of `world` pointers, each mapped into this
+ * process (gt_ipc_open for other GPUs): z_ranks[r] = rank r's rows_fwd output
+ * [pairs_per_rank][m], y_ranks[r] = rank r's row buffer [2 pairs_per_rank][hy]
+ * (hy >= n + 1). The columns [c0, c0 + hc) are read from every rank's spectra in
+ * place (peer loads overlapped with the FFT work) and rows [0, n) of the result are
+ * stored straight into their owners' row buffers at columns c0.. (peer stores). The
+ * caller orders the phases across ranks (a barrier after rows_fwd and after cols). */
+gt_status gt_large_cols_peer(const gt_device_greens* d, const void* z_ranks, int world, int pairs_per_rank, int c0,
+                             int hc, void* c1, void* c2, const void* y_ranks, int hy, void* stream);
+/* CUDA IPC helpers for the peer exchange: gt_ipc_alloc returns a device buffer and its
+ * 64-byte handle; gt_ipc_open maps another process's handle (peer access enabled). */
+gt_status gt_ipc_alloc(size_t bytes, void** ptr, void* handle64);
+gt_status gt_ipc_open(const void* handle64, void** ptr);
+gt_status gt_ipc_close(void* ptr);
+gt_status gt_ipc_free(void* ptr);
 /* rows_inv with the Chebyshev semi-iteration of gt_fp_opts.accel (slab.py drives omega /
  * gamma from the residual history): x_prev [2 pairs][n] holds x_{k-1} on entry and x_k on
  * exit, g_out (may be NULL) receives G(x_k); omega > 0 stores x_{k+1} =

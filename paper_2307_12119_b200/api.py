@@ -137,6 +137,11 @@ _EXT = [
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
     ("gt_large_rows_inv", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp]),
+    ("gt_large_cols_peer", cint, [vp, vp, cint, cint, cint, cint, vp, vp, vp, cint, vp]),
+    ("gt_ipc_alloc", cint, [C.c_size_t, C.POINTER(vp), vp]),
+    ("gt_ipc_open", cint, [vp, C.POINTER(vp)]),
+    ("gt_ipc_close", cint, [vp]),
+    ("gt_ipc_free", cint, [vp]),
     ("gt_large_rows_inv_accel", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp, vp,
                                        C.c_double, C.c_double, vp]),
     ("gt_profile_begin", cint, [vp]),

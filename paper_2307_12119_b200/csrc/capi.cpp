@@ -989,6 +989,58 @@ gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, i
     });
 }
 
+gt_status gt_large_cols_peer(const gt_device_greens* d, const void* z_ranks, int world, int pairs_per_rank, int c0,
+                             int hc, void* c1, void* c2, const void* y_ranks, int hy, void* stream) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (world < 1 || pairs_per_rank < 1 || world * pairs_per_rank * 2 != g.n)
+            fail(ST_CONFIG, "capi", "large cols_peer: world * pairs_per_rank must be n / 2");
+        if (c0 < 0 || hc < 1 || c0 + hc > g.n + 1) fail(ST_CONFIG, "capi", "column range outside [0, n]");
+        if (hy < g.n + 1) fail(ST_CONFIG, "capi", "large cols_peer: row buffers need n + 1 columns");
+        if (!z_ranks || !y_ranks) fail(ST_CONFIG, "capi", "large cols_peer: null rank table");
+        cuda_ok(gtd_lg_cols_peer(&g, static_cast<const void* const*>(z_ranks), pairs_per_rank, c0, hc, c1, c2,
+                                 const_cast<void* const*>(static_cast<const void* const*>(y_ranks)), hy,
+                                 static_cast<cudaStream_t>(stream)),
+                "large cols peer");
+    });
+}
+
+/* CUDA IPC for the peer-memory exchange: a cudaMalloc'ed buffer (base == pointer, so the
+ * handle maps the buffer itself) and its 64-byte handle; another process opens it with
+ * peer access enabled. */
+gt_status gt_ipc_alloc(size_t bytes, void** ptr, void* handle64) {
+    return guarded([&] {
+        if (!ptr || !handle64 || bytes == 0) fail(ST_CONFIG, "capi", "gt_ipc_alloc: bad arguments");
+        void* p = nullptr;
+        cuda_ok(static_cast<int>(cudaMalloc(&p, bytes)), "ipc alloc");
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            cuda_ok(static_cast<int>(e), "ipc handle");
+        }
+        std::memcpy(handle64, &h, sizeof(h));
+        *ptr = p;
+    });
+}
+
+gt_status gt_ipc_open(const void* handle64, void** ptr) {
+    return guarded([&] {
+        if (!ptr || !handle64) fail(ST_CONFIG, "capi", "gt_ipc_open: bad arguments");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        cuda_ok(static_cast<int>(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess)), "ipc open");
+    });
+}
+
+gt_status gt_ipc_close(void* ptr) {
+    return guarded([&] { cuda_ok(static_cast<int>(cudaIpcCloseMemHandle(ptr)), "ipc close"); });
+}
+
+gt_status gt_ipc_free(void* ptr) {
+    return guarded([&] { cuda_ok(static_cast<int>(cudaFree(ptr)), "ipc free"); });
+}
+
 gt_status gt_large_rows_inv(const gt_device_greens* d, const void* y, int hy, int pairs, void* s1, double* t,
                             double* app, const double* p, const double* l0, const gt_fp_opts* opts,
                             unsigned long long* res_bits, int* status, void* stream) {

@@ -204,6 +204,12 @@ int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, voi
  * compact = 0: Z is [n/2][m]; 1: Z is [n/2][2 hc] = (Z_p[c0 + c], Z_p[(m - c0 - c) mod m]) per column c. */
 int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, void* C1, void* C2, void* Y,
                 cudaStream_t st);
+/* The column phase over peer memory (multi-GPU without all-to-all copies): Zr / Yr are DEVICE
+ * arrays of one mapped pointer per rank (Zr[r]: rank r's [P][m] row spectra, Yr[r]: its
+ * [2P][hy] row buffer); the columns [c0, c0+hc) are read from every rank's Z in place and the
+ * results stored into every rank's Y rows directly. */
+int gtd_lg_cols_peer(const gtd_lg* g, const void* const* Zr, int pairs_per_rank, int c0, int hc, void* C1, void* C2,
+                     void* const* Yr, int hy, cudaStream_t st);
 /* Y [2 pairs][hy] (all columns 0..n of the slab's rows) -> theta -> T (Tst), residual (max bits),
  * status bits, next applied rows. Q / G (may be NULL): x_{k-1} in / x_k out, G(x_k) out; omega > 0
  * stores the Chebyshev step x_{k+1} = omega (gamma G + (1 - gamma) x_k - x_{k-1}) + x_{k-1}. */

@@ -107,6 +107,9 @@ struct ColA {
     // Spectra of ALL row pairs: Z[p zs + oa + c] = Z_p[v], Z[p zs + ((ob + sb c) & mask)] = Z_p[m - v].
     // Full layout (one GPU): zs = m, oa = c0, ob = m - c0, sb = -1, mask = m - 1.
     // Compact layout (after the all-to-all): zs = 2 hc, oa = 0, ob = hc, sb = +1, mask = ~0.
+    // Peer layout (multi-GPU without an all-to-all, gtd_lg_cols_peer): row pair p lives in
+    // rank p / Pr's full [Pr][m] spectra, read in place through its mapped pointer Zr[p / Pr]
+    // (NVLink peer loads, one rank's row block per pointer); Z is unused then.
     const cplx<T>* Z;
     cplx<T>* C1;  // [m][hc] (row i1 + M1 k2)
     const double2* tw;
@@ -114,6 +117,15 @@ struct ColA {
     long long zs;
     int oa, ob, sb, mask;
     int embed = 0;  // rows: 0 mirror_pad, 1 center_kernel
+    const cplx<T>* const* Zr = nullptr;
+    int Pr = 0;
+    __device__ const cplx<T>* zrow(int p) const {
+        if (Zr) {
+            const int r = p / Pr;
+            return Zr[r] + static_cast<size_t>(p - r * Pr) * zs;
+        }
+        return Z + static_cast<size_t>(p) * zs;
+    }
     __device__ cplx<T> load(int i1, int c, int j) const {
         const int i = i1 + M1 * j;
         int x;
@@ -123,7 +135,7 @@ struct ColA {
         } else {
             x = i < n ? i : M - 1 - i;
         }
-        const cplx<T>* Zp = Z + static_cast<size_t>(x >> 1) * zs;
+        const cplx<T>* Zp = zrow(x >> 1);
         const cplx<T> a = Zp[oa + c], b = cconj<T>(Zp[(ob + sb * c) & mask]);
         // half spectra of the two real rows packed in Zp (x even: real part's, odd: imaginary part's)
         return (x & 1) ? mk<T>(T(0.5) * (a.y - b.y), T(-0.5) * (a.x - b.x))
@@ -138,7 +150,7 @@ struct ColA {
         } else {
             x = i < n ? i : M - 1 - i;
         }
-        const cplx<T>* Zp = Z + static_cast<size_t>(x >> 1) * zs;
+        const cplx<T>* Zp = zrow(x >> 1);
         pf_l2(Zp + oa + c);
         pf_l2(Zp + ((ob + sb * c) & mask));
     }
@@ -208,6 +220,10 @@ struct ColC {
     const cplx<T>* C2;
     cplx<T>* Y;  // [n][hc]
     int n, M, M1, M2, hc;
+    // Peer layout: die row i goes straight into its owner's row buffer Yr[i / rpr]
+    // [rpr][hy] at column c0 + c (NVLink peer stores), in place of the second all-to-all.
+    cplx<T>* const* Yr = nullptr;
+    int rpr = 0, hy = 0, c0 = 0;
     __device__ cplx<T> load(int ia, int c, int j) const {
         return C2[(static_cast<size_t>(j) + static_cast<size_t>(M2) * ia) * hc + c];
     }
@@ -218,7 +234,13 @@ struct ColC {
     __device__ Pre pre(int, int, int) const { return {}; }
     __device__ void store(int ia, int c, int ib, cplx<T> v, const Pre&) const {
         const int i = ia + M1 * ib;
-        if (i < n) Y[static_cast<size_t>(i) * hc + c] = v;
+        if (i >= n) return;
+        if (Yr) {
+            const int r = i / rpr;
+            Yr[r][static_cast<size_t>(i - r * rpr) * hy + c0 + c] = v;
+        } else {
+            Y[static_cast<size_t>(i) * hc + c] = v;
+        }
     }
 };
 
@@ -537,6 +559,30 @@ int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, voi
     e = launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2, hc, st);
     if (e) return e;
     ColC<double> c{static_cast<const double2*>(C2), static_cast<double2*>(Y), g->n, g->m, g->M1, g->M2, hc};
+    return launch<double>(g->M2, c, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
+}
+
+int gtd_lg_cols_peer(const gtd_lg* g, const void* const* Zr, int pairs_per_rank, int c0, int hc, void* C1, void* C2,
+                     void* const* Yr, int hy, cudaStream_t st) {
+    ColA<double> a{nullptr, static_cast<double2*>(C1), static_cast<const double2*>(g->tw), g->n, g->m, g->M1, c0, hc};
+    a.zs = g->m;
+    a.oa = c0;
+    a.ob = g->m - c0;
+    a.sb = -1;
+    a.mask = g->m - 1;
+    a.Zr = reinterpret_cast<const double2* const*>(Zr);
+    a.Pr = pairs_per_rank;
+    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
+    if (e) return e;
+    ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
+                   g->fkp, static_cast<const double2*>(g->tw), g->n + 1, g->m, g->M1, g->M2, c0, hc};
+    e = launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2, hc, st);
+    if (e) return e;
+    ColC<double> c{static_cast<const double2*>(C2), nullptr, g->n, g->m, g->M1, g->M2, hc};
+    c.Yr = reinterpret_cast<double2* const*>(Yr);
+    c.rpr = 2 * pairs_per_rank;
+    c.hy = hy;
+    c.c0 = c0;
     return launch<double>(g->M2, c, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
 }
 

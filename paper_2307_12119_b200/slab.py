@@ -1,16 +1,32 @@
 """Config 4: the mode-B fixed point on one large map, slab-decomposed over ranks.
 
-One process per GPU (torch.distributed, NCCL on GPUs; gloo in the CPU tests).
+One process per GPU (torch.distributed: NCCL on GPUs; gloo in the CPU tests).
 Rank r owns die-row pairs [r P, (r+1) P) (P = n / 2 / world) for the row
 phases and half-spectrum columns [c0_r, c0_r + hc_r) for the column phase
 (SURVEY §8e). Per iteration:
 
   rows_fwd (local rows)  -> Z [P][m]   spectra of the mirrored row pairs
-  all-to-all             -> every rank gets, for ALL row pairs, the columns it
-                            owns and their mirrors (compact [n/2][2 hc] layout)
-  cols (local columns)   -> Y [n][hc]  rows [0, n) of IFFT_col(fk . FFT_col)
-  all-to-all             -> every rank gets its rows for all columns
+  exchange 1             -> the column phase sees, for ALL row pairs, the
+                            columns it owns and their mirrors
+  cols (local columns)   -> rows [0, n) of IFFT_col(fk . FFT_col)
+  exchange 2             -> every rank gets its rows for all columns
   rows_inv (local rows)  -> theta -> T, residual, next applied rows
+
+Two transports for the exchanges (world > 1):
+
+  "peer" (default on GPUs): no copies. Each rank's Z and row buffer are
+      cudaMalloc'ed and mapped into every other rank by CUDA IPC (gt_ipc_*); the
+      column kernels read the other ranks' Z in place over NVLink while they
+      transform (gt_large_cols_peer: peer loads inside the FFT pass) and store
+      each result row straight into its owner's row buffer (peer stores). The
+      phases are ordered by a stream sync + barrier after rows_fwd and after cols.
+  "nccl": two all_to_all_single calls per iteration on compact per-destination
+      blocks (one index_select to pack, one index_copy to unpack). The CPU tests
+      run this path under gloo with numpy stand-in phases.
+
+`solve_slab_emulated` runs W ranks' slabs in ONE process on one GPU through the
+peer kernels (the rank table holds W same-device buffers) -- the multi-rank data
+path exercised without kernels that wait on each other.
 
 The stop rule is the reference outer loop's (fdm.cpp:190-200): converged when
 max|T_{k+1} - T_k| < tol after iteration 1 (max over ranks), max_iters ->
@@ -25,7 +41,8 @@ in the inverse row pass; a residual that doubles falls back to Picard. The stop
 rule is unchanged (max|G(x_k) - x_k| < tol) and the result is G(x_k).
 
 The arithmetic lives in the sm_100a passes of libgreentherm_b200.so
-(`GpuLargeOps`, C ABI gt_large_*); this module only moves blocks between ranks.
+(`GpuLargeOps`, C ABI gt_large_*); this module only orders phases and moves
+blocks between ranks.
 """
 from __future__ import annotations
 
@@ -75,6 +92,11 @@ class GpuLargeOps:
         self._check(self.L.gt_large_cols(self.dg._d, self._p(z), int(compact), c0, hc, self._p(c1), self._p(c2),
                                          self._p(y), C.c_void_p(stream)))
 
+    def cols_peer(self, z_table, world, pairs_per_rank, c0, hc, c1, c2, y_table, hy, stream):
+        """z_table / y_table: device int64 tensors of `world` mapped pointers."""
+        self._check(self.L.gt_large_cols_peer(self.dg._d, self._p(z_table), world, pairs_per_rank, c0, hc,
+                                              self._p(c1), self._p(c2), self._p(y_table), hy, C.c_void_p(stream)))
+
     def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream, q=None, g=None,
                  omega=0.0, gamma=1.0):
         if q is None:
@@ -88,6 +110,51 @@ class GpuLargeOps:
                 float(gamma), C.c_void_p(stream)))
 
 
+class IpcBuffer:
+    """A cudaMalloc'ed device buffer with its CUDA IPC handle (gt_ipc_alloc), viewed as a
+    torch tensor (zero copy, __cuda_array_interface__); `open_peer` maps another rank's."""
+
+    def __init__(self, shape, dtype, device):
+        import torch
+        from .api import check, lib
+        self.L = lib()
+        self.shape, self.dtype = tuple(shape), dtype
+        nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        self.ptr = C.c_void_p()
+        self.handle = (C.c_char * 64)()
+        check(self.L, self.L.gt_ipc_alloc(nbytes, C.byref(self.ptr), self.handle))
+        self.tensor = _wrap(self.ptr.value, self.shape, dtype, device)
+
+    def handle_bytes(self) -> bytes:
+        return bytes(self.handle)
+
+    def close(self):
+        if self.ptr:
+            self.tensor = None
+            self.L.gt_ipc_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def open_peer(handle: bytes) -> int:
+    from .api import check, lib
+    L = lib()
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    check(L, L.gt_ipc_open(buf, C.byref(p)))
+    return p.value
+
+
+def _wrap(ptr, shape, dtype, device):
+    """Zero-copy torch view of a raw device pointer."""
+    import torch
+    typestr = {torch.float64: "<f8", torch.complex128: "<c16", torch.int64: "<i8"}[dtype]
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Arr(), device=device)
+
+
 @dataclass
 class SlabResult:
     t: "object"          # local rows of the converged rise map [2P][n]
@@ -96,13 +163,84 @@ class SlabResult:
     residual: float
 
 
+class _Accel:
+    """Chebyshev omega / gamma schedule from the residual history (fixed_point.cu fp_update)."""
+
+    def __init__(self, k0):
+        self.k0 = k0
+        self.omega, self.gamma, self.sigma2, self.res_prev = 0.0, 1.0, 0.0, 0.0
+
+    def update(self, it, res):
+        if self.k0 <= 0:
+            return
+        if self.omega > 0.0:
+            if res > 2.0 * self.res_prev:
+                self.omega, self.gamma = -1.0, 1.0  # diverging under acceleration: plain Picard from here on
+            else:
+                self.omega = (2.0 / (2.0 - self.sigma2) if self.omega == 1.0
+                              else 1.0 / (1.0 - 0.25 * self.sigma2 * self.omega))
+        elif self.omega == 0.0 and it == self.k0 and self.res_prev > 0.0:
+            rho = min(0.97, max(0.0, 1.02 * res / self.res_prev))
+            self.gamma = 2.0 / (2.0 - rho)
+            self.sigma2 = (rho / (2.0 - rho)) ** 2
+            self.omega = 1.0
+        self.res_prev = res
+
+
+class _RankState:
+    """One rank's slab: rows [2P][n], its spectra / scratch buffers and loop state."""
+
+    def __init__(self, n, P, c0, hc, p_local, v_local, opts, z=None, yrow=None):
+        import torch
+        dev = p_local.device
+        m, h = 2 * n, n + 1
+        cd = torch.complex128
+        self.P, self.c0, self.hc = P, c0, hc
+        self.p = p_local
+        self.l0 = opts.leak_frac * p_local * v_local
+        self.app = (p_local + self.l0).contiguous()
+        self.t = torch.zeros_like(p_local)
+        self.s1 = torch.empty((P, m), dtype=cd, device=dev)
+        self.z = z if z is not None else torch.empty((P, m), dtype=cd, device=dev)
+        self.c1 = torch.empty((m, hc), dtype=cd, device=dev)
+        self.c2 = torch.empty((m, hc), dtype=cd, device=dev)
+        self.yrow = yrow  # [2P][h] row buffer (peer / nccl transports)
+        self.res_bits = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        accel = int(getattr(opts, "accel", 0) or 0)
+        self.q = torch.zeros_like(p_local) if accel > 0 else None  # x_{k-1} in, x_k out
+        self.g = torch.empty_like(p_local) if accel > 0 else None  # G(x_k)
+
+    def rows_inv(self, ops, y, hy, opts, acc, stream):
+        self.res_bits.zero_()
+        ops.rows_inv(y, hy, self.P, self.s1, self.t, self.app, self.p, self.l0, opts, self.res_bits, self.status,
+                     stream, q=self.q, g=self.g, omega=max(acc.omega, 0.0), gamma=acc.gamma)
+
+    def finish(self):
+        if self.g is not None:
+            self.t.copy_(self.g)  # G(x_k): its error bound is the stop rule's, not that of the extrapolated x_{k+1}
+
+
+def _stop(it, res, st, opts, acc):
+    """Reference stop rule after iteration `it`; returns (done, status)."""
+    if st:
+        return True, st
+    acc.update(it, res)
+    if it > 1 and res < opts.tol:
+        return True, st
+    if it == opts.max_iters:
+        return True, st | GT_SAMPLE_NOCONVERGE
+    return False, st
+
+
 def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 1, stream: int | None = None,
-               exchange=None) -> SlabResult:
+               exchange=None, transport: str | None = None) -> SlabResult:
     """Fixed point on the local slab. p_local / v_local: [2P][n] float64 tensors of
     this rank's rows; opts: api.FPOpts (leak_frac, law, kirchhoff, beta, t_ambient,
-    eta, tol, max_iters). Device work is issued on `stream` (default: torch's
-    current stream, which the NCCL exchange also uses). `exchange` (default
-    torch.distributed.all_to_all_single) is injectable for tests."""
+    eta, tol, max_iters, accel). Device work is issued on `stream` (default: torch's
+    current stream, which the NCCL exchange also uses). transport: "peer" (CUDA IPC
+    mapped buffers, default for CUDA tensors) or "nccl" (all-to-all copies; `exchange`
+    defaults to torch.distributed.all_to_all_single and is injectable for tests)."""
     import torch
     import torch.distributed as dist
     if (n // 2) % world:
@@ -113,27 +251,40 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
     rows = 2 * P
     ranges = column_ranges(h, world)
     c0, hc = ranges[rank]
-    exchange = exchange or dist.all_to_all_single
+    if transport is None:
+        transport = "peer" if (dev.type == "cuda" and exchange is None and world > 1) else "nccl"
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
     cd = torch.complex128
-    l0 = opts.leak_frac * p_local * v_local
-    app = (p_local + l0).contiguous()
-    t = torch.zeros_like(p_local)
-    s1 = torch.empty((P, m), dtype=cd, device=dev)
-    z = torch.empty((P, m), dtype=cd, device=dev)
-    c1 = torch.empty((m, hc), dtype=cd, device=dev)
-    c2 = torch.empty((m, hc), dtype=cd, device=dev)
-    ycol = torch.empty((n, hc), dtype=cd, device=dev)
-    accel = int(getattr(opts, "accel", 0) or 0)
-    q = torch.zeros_like(p_local) if accel > 0 else None  # x_{k-1} in, x_k out
-    g = torch.empty_like(p_local) if accel > 0 else None  # G(x_k)
-    omega, gamma, sigma2, res_prev = 0.0, 1.0, 0.0, 0.0
-    res_bits = torch.zeros(1, dtype=torch.int64, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    if world > 1:
+    acc = _Accel(int(getattr(opts, "accel", 0) or 0))
+    ipc = []
+    if world > 1 and transport == "peer":
+        zb = IpcBuffer((P, m), cd, dev)
+        yb = IpcBuffer((rows, h), cd, dev)
+        ipc = [zb, yb]
+        S = _RankState(n, P, c0, hc, p_local, v_local, opts, z=zb.tensor, yrow=yb.tensor)
+        handles = [None] * world
+        dist.all_gather_object(handles, (zb.handle_bytes(), yb.handle_bytes()))
+        opened = []
+        zp, yp = [], []
+        for r, (hz, hy_) in enumerate(handles):
+            if r == rank:
+                zp.append(zb.ptr.value)
+                yp.append(yb.ptr.value)
+            else:
+                a, b = open_peer(hz), open_peer(hy_)
+                opened += [a, b]
+                zp.append(a)
+                yp.append(b)
+        z_table = torch.tensor(zp, dtype=torch.int64, device=dev)
+        y_table = torch.tensor(yp, dtype=torch.int64, device=dev)
+    else:
+        S = _RankState(n, P, c0, hc, p_local, v_local, opts)
+    exchange = exchange or (dist.all_to_all_single if world > 1 else None)
+    if world > 1 and transport == "nccl":
         zrecv = torch.empty((world, P, 2 * hc), dtype=cd, device=dev)
-        yrow = torch.empty((rows, h), dtype=cd, device=dev)
+        ycol = torch.empty((n, hc), dtype=cd, device=dev)
+        S.yrow = torch.empty((rows, h), dtype=cd, device=dev)
         # Per-destination send blocks as ONE gather from the row spectra z [P][m]: block q holds,
         # for every local row pair, the columns rank q owns and their mirrors m - v (compact
         # layout of gt_large_cols). The index maps are built once; each iteration is a single
@@ -151,55 +302,106 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
                .reshape(-1) for cq, hq in ranges]
         recv_dst = torch.cat(dst)
         recv = torch.empty(recv_dst.numel(), dtype=cd, device=dev)
+    elif world == 1:
+        ycol = torch.empty((n, hc), dtype=cd, device=dev)
+
+    def phase_barrier():
+        # every rank's previous phase has completed on its GPU before any rank starts the next
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+
+    it, res, st = 0, float("inf"), 0
+    try:
+        for it in range(1, opts.max_iters + 1):
+            ops.rows_fwd(S.app, P, S.s1, S.z, stream)
+            if world == 1:
+                ops.cols(S.z, False, c0, hc, S.c1, S.c2, ycol, stream)
+                yrow_t = ycol
+            elif transport == "peer":
+                phase_barrier()  # all row spectra written
+                ops.cols_peer(z_table, world, P, c0, hc, S.c1, S.c2, y_table, h, stream)
+                phase_barrier()  # all column results stored into their owners' row buffers
+                yrow_t = S.yrow
+            else:
+                torch.index_select(S.z.view(-1), 0, send_idx, out=send)
+                # output splits: what each source sends me; input splits: what I send each rank.
+                # Complex blocks travel as their float64 (re, im) view (NCCL has no complex type).
+                exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
+                         [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
+                ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, S.c1, S.c2, ycol, stream)
+                # ycol [n][hc] is already [world][rows][hc]: rank q's rows are a contiguous block
+                exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(ycol).view(-1),
+                         [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)
+                S.yrow.view(-1).index_copy_(0, recv_dst, recv)
+                yrow_t = S.yrow
+            S.rows_inv(ops, yrow_t, h, opts, acc, stream)
+            rs = torch.stack([S.res_bits.view(torch.float64)[0], S.status.to(torch.float64)[0]])
+            if world > 1 and dist.get_backend() != "nccl":
+                rs = rs.cpu()  # gloo gathers host tensors
+            if world > 1:
+                flags = [torch.zeros_like(rs) for _ in range(world)]
+                dist.all_gather(flags, rs)
+                res = max(float(f[0]) for f in flags)
+                st = 0
+                for f in flags:
+                    st |= int(f[1])
+            else:
+                res, st = float(rs[0]), int(rs[1])
+            done, st = _stop(it, res, st, opts, acc)
+            if done:
+                break
+        S.finish()
+    finally:
+        if ipc:
+            torch.cuda.synchronize(dev)
+            dist.barrier()  # no rank still reads a buffer another rank is about to free
+            from .api import lib
+            for p in opened:
+                lib().gt_ipc_close(C.c_void_p(p))
+            S.z = S.yrow = None
+            for b in ipc:
+                b.close()
+    return SlabResult(t=S.t, iterations=it, status=st, residual=res)
+
+
+def solve_slab_emulated(ops, n: int, p_full, v_full, opts, world: int, stream: int | None = None) -> SlabResult:
+    """`world` ranks' slabs in ONE process on one GPU through the peer column kernels
+    (gt_large_cols_peer reads every rank's Z in place and stores into every rank's row
+    buffer; the rank tables hold same-device pointers). Each phase runs for all ranks
+    before the next starts, so no kernel waits on another. Returns the full map."""
+    import torch
+    if (n // 2) % world:
+        raise ValueError("world size must divide n / 2 (whole row pairs per rank)")
+    dev = p_full.device
+    m, h = 2 * n, n + 1
+    P = (n // 2) // world
+    rows = 2 * P
+    ranges = column_ranges(h, world)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    cd = torch.complex128
+    R = [_RankState(n, P, c0, hc, p_full[r * rows:(r + 1) * rows].contiguous(),
+                    v_full[r * rows:(r + 1) * rows].contiguous(), opts,
+                    yrow=torch.empty((rows, h), dtype=cd, device=dev))
+         for r, (c0, hc) in enumerate(ranges)]
+    z_table = torch.tensor([s.z.data_ptr() for s in R], dtype=torch.int64, device=dev)
+    y_table = torch.tensor([s.yrow.data_ptr() for s in R], dtype=torch.int64, device=dev)
+    acc = _Accel(int(getattr(opts, "accel", 0) or 0))
     it, res, st = 0, float("inf"), 0
     for it in range(1, opts.max_iters + 1):
-        ops.rows_fwd(app, P, s1, z, stream)
-        if world == 1:
-            ops.cols(z, False, c0, hc, c1, c2, ycol, stream)
-            yrow_t, hy = ycol, h
-        else:
-            torch.index_select(z.view(-1), 0, send_idx, out=send)
-            # output splits: what each source sends me; input splits: what I send each rank.
-            # Complex blocks travel as their float64 (re, im) view (NCCL has no complex type).
-            exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
-                     [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
-            ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, c1, c2, ycol, stream)
-            # ycol [n][hc] is already [world][rows][hc]: rank q's rows are a contiguous block
-            exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(ycol).view(-1),
-                     [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)
-            yrow.view(-1).index_copy_(0, recv_dst, recv)
-            yrow_t, hy = yrow, h
-        res_bits.zero_()
-        ops.rows_inv(yrow_t, hy, P, s1, t, app, p_local, l0, opts, res_bits, status, stream, q=q, g=g,
-                     omega=max(omega, 0.0), gamma=gamma)
-        rs = torch.stack([res_bits.view(torch.float64)[0], status.to(torch.float64)[0]])
-        if world > 1:
-            flags = [torch.zeros_like(rs) for _ in range(world)]
-            dist.all_gather(flags, rs)
-            res = max(float(f[0]) for f in flags)
-            st = 0
-            for f in flags:
-                st |= int(f[1])
-        else:
-            res, st = float(rs[0]), int(rs[1])
-        if st:
+        for s in R:
+            ops.rows_fwd(s.app, P, s.s1, s.z, stream)
+        for s in R:
+            ops.cols_peer(z_table, world, P, s.c0, s.hc, s.c1, s.c2, y_table, h, stream)
+        for s in R:
+            s.rows_inv(ops, s.yrow, h, opts, acc, stream)
+        res = max(float(s.res_bits.view(torch.float64)[0]) for s in R)
+        st = 0
+        for s in R:
+            st |= int(s.status[0])
+        done, st = _stop(it, res, st, opts, acc)
+        if done:
             break
-        if accel > 0:  # the next step's omega (fixed_point.cu fp_update)
-            if omega > 0.0:
-                if res > 2.0 * res_prev:
-                    omega, gamma = -1.0, 1.0  # diverging under acceleration: plain Picard from here on
-                else:
-                    omega = 2.0 / (2.0 - sigma2) if omega == 1.0 else 1.0 / (1.0 - 0.25 * sigma2 * omega)
-            elif omega == 0.0 and it == accel and res_prev > 0.0:
-                rho = min(0.97, max(0.0, 1.02 * res / res_prev))
-                gamma = 2.0 / (2.0 - rho)
-                sigma2 = (rho / (2.0 - rho)) ** 2
-                omega = 1.0
-            res_prev = res
-        if it > 1 and res < opts.tol:
-            break
-        if it == opts.max_iters:
-            st |= GT_SAMPLE_NOCONVERGE
-    if accel > 0:
-        t.copy_(g)  # G(x_k): its error bound is the stop rule's, not that of the extrapolated x_{k+1}
-    return SlabResult(t=t, iterations=it, status=st, residual=res)
+    for s in R:
+        s.finish()
+    return SlabResult(t=torch.cat([s.t for s in R]), iterations=it, status=st, residual=res)

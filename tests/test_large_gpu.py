@@ -213,3 +213,35 @@ def test_large_grid_n1024_chebyshev_vs_oracle(b200lib, oracle, tmp_path):
     assert st_ref[0] == 0 and res.status == 0
     assert res.iterations < it_ref[0]
     assert err <= 1e-3
+
+
+@pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3)])
+def test_large_grid_peer_ranks_emulated(b200lib, tmp_path, world, accel):
+    """The multi-GPU column phase over peer memory (gt_large_cols_peer: every rank's row
+    spectra read in place, results stored into their owners' row buffers), with `world`
+    ranks emulated in one process on one GPU (slab.solve_slab_emulated): identical to the
+    single-slab solve -- same iterations, same bits."""
+    import dataclasses
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    n = 1024
+    f, phi, ga = _large_greens(b200lib, tmp_path, n)
+    cfg = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n, blocks=128, hotspots=16)
+    p = inputs.power_batch(cfg, 0, 1, np.float64)
+    p *= 300.0 / p.sum()
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    dg = DeviceGreens(ga, 1)
+    o = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    o.accel = accel
+    ops = slab.GpuLargeOps(dg)
+    P, V = torch.from_numpy(p[0]).cuda(), torch.from_numpy(v[0]).cuda()
+    one = slab.solve_slab(ops, n, P, V, o)
+    em = slab.solve_slab_emulated(ops, n, P, V, o, world)
+    torch.cuda.synchronize()
+    d = float((em.t - one.t).abs().max())
+    print(f"peer ranks emulated world={world} accel={accel}: iters {em.iterations} vs {one.iterations}, "
+          f"max|dT| {d:.3e} K")
+    assert em.status == one.status == 0
+    assert em.iterations == one.iterations
+    assert d == 0.0
