@@ -120,12 +120,28 @@ struct WarpFFT {
         for (int t = 0; t < P; ++t) v[t] = scratch[kq * SP + h + Q * t];
         __syncwarp();
         dftP<P, SIGN, T>(v);
+        if constexpr (Q == 2) {
+            // w_32^{h m1} with h in {0, 1}: compile-time constants selected per lane (the
+            // shared-memory twiddle loads were ~13% of the row passes' shared wavefronts)
 #pragma unroll
-        for (int m1 = 1; m1 < P; ++m1) {
-            cplx<T> w = tw[h * m1 * P];  // w_32^{h m1} = w_M^{h m1 P}
-            if (SIGN > 0) w.y = -w.y;
-            v[m1] = cmul<T>(v[m1], w);
-        }
+            for (int m1 = 1; m1 < P; ++m1) {
+                constexpr double C8[9] = {1.0, 0.98078528040323044913, 0.92387953251128675613,
+                                          0.83146961230254523708, 0.70710678118654752440, 0.55557023301960222474,
+                                          0.38268343236508977173, 0.19509032201612826785, 0.0};
+                // cos / sin(2 pi m1 / 32), m1 < 16: second quadrant for m1 > 8
+                const double cw = m1 <= 8 ? C8[m1] : -C8[16 - m1];
+                const double sw = m1 <= 8 ? C8[8 - m1] : C8[m1 - 8];
+                const T wc = h ? T(cw) : T(1), ws = h ? T(SIGN < 0 ? -sw : sw) : T(0);
+                v[m1] = cmul<T>(v[m1], mk<T>(wc, ws));
+            }
+        } else if constexpr (Q > 2) {
+#pragma unroll
+            for (int m1 = 1; m1 < P; ++m1) {
+                cplx<T> w = tw[h * m1 * P];  // w_32^{h m1} = w_M^{h m1 P}
+                if (SIGN > 0) w.y = -w.y;
+                v[m1] = cmul<T>(v[m1], w);
+            }
+        }  // Q == 1 (M = 1024): h = 0, all factors are 1
         // Q-point DFT across the lanes kq + P h' (lane h keeps output g = h)
         if constexpr (Q == 2) {
             // radix-2 butterfly with the partner lane: g = 0 -> v0 + v1, g = 1 -> v0 - v1
