@@ -21,6 +21,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+
+#ifndef GT_LG_RINV_NT
+#define GT_LG_RINV_NT 1024
+#endif
+#ifndef GT_LG_R16
+#define GT_LG_R16 8
+#endif
 
 #include "fft_tile.cuh"
 #include "gt_device.h"
@@ -511,6 +519,172 @@ int launch(int N, const Op& op, const double2* tw, int M, int groups, int nlines
     }
 }
 
+
+// ------------------------------------------------------------------ one-pass inverse rows
+// The inverse row phase of one die row in ONE pass (replaces RinvA + RinvB for n <= 8192):
+// the real inverse of the Hermitian half spectrum Y[0..n] at length m = 2n is an n-point
+// complex inverse FFT of Z[k] = E[k] + i O[k], E = Y[k] + conj Y[n-k],
+// O = (Y[k] - conj Y[n-k]) w_m^{-k}, whose output z[j] = theta[2j] + i theta[2j+1] (only
+// j < n/2 is kept: the die's n samples). The whole n-point line lives in shared memory
+// (128 KB at n = 8192, one CTA per SM), the Stockham stages run in place, and the epilogue
+// (theta -> T, Kirchhoff inverse, residual, Chebyshev step, next applied row) is RinvB's.
+// One 16-byte pad every 8 elements: the stride-R stores of the first Stockham stage (R x 16 B
+// apart) land in different banks.
+__device__ __forceinline__ int lpad(int i) { return i + (i >> 3); }
+
+template <int R, int NT, int N>
+__device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* __restrict__ tw, int m) {
+    // butterfly j: inputs j + r N/R, twiddle w_{ns R}^{+k r} (inverse), outputs (j-k) R + k + r ns
+    constexpr int nb = N / R;
+    constexpr int BMAX = (nb + NT - 1) / NT;  // butterflies per thread
+    const int tid = threadIdx.x, nthr = NT;
+    cplx<double> v[BMAX][R];
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) {
+        const int j = tid + b * nthr;
+        if (j >= nb) break;
+        const int k = j % ns;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = buf[lpad(j + r * nb)];
+        if (ns > 1) {
+            // w_{ns R}^{k r} = w_m^{k r m / (ns R)}: one table load, powers by fp64 products
+            const double2 w = tw[((m / (ns * R)) * k) & (m - 1)];
+            const cplx<double> w1 = mk<double>(w.x, -w.y);
+            cplx<double> wr = w1;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                v[b][r] = cmul<double>(v[b][r], wr);
+                if (r + 1 < R) wr = cmul<double>(wr, w1);
+            }
+        }
+        dftR<R, +1, double>(v[b]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) {
+        const int j = tid + b * nthr;
+        if (j >= nb) break;
+        const int k = j % ns;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[lpad(base + r * ns)] = v[b][r];
+    }
+    __syncthreads();
+}
+
+template <int NT, int N, int NS, int REM>
+struct LineStages {
+    __device__ __forceinline__ static void run(double2* buf, const double2* __restrict__ tw, int m) {
+        if constexpr (REM > 1) {
+            constexpr int R = REM % GT_LG_R16 == 0 ? GT_LG_R16 : REM;  // radix GT_LG_R16, then the rest
+            line_stage<R, NT, N>(buf, NS, tw, m);
+            LineStages<NT, N, NS * R, REM / R>::run(buf, tw, m);
+        }
+    }
+};
+
+template <int NT, int N>
+__global__ void __launch_bounds__(NT, 1)
+lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __restrict__ tw, int m,
+            RinvB<double> op) {
+    constexpr int n = N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* buf = reinterpret_cast<double2*>(smem_raw);
+    __shared__ double s_m[NT / 32];
+    __shared__ int s_b[NT / 32];
+    double r_dmax = 0.0;
+    int r_bad = 0;
+    for (int x = blockIdx.x; x < rows; x += gridDim.x) {
+        const double2* Yx = Y + static_cast<size_t>(x) * hy;
+        __syncthreads();  // the previous row's epilogue reads of buf are done
+#pragma unroll 4
+        for (int k = threadIdx.x; k < n; k += NT) {
+            const double2 a = Yx[k], bq = Yx[n - k];  // k = 0 pairs with the Nyquist term Y[n]
+            const double2 w = tw[k];                    // w_m^{k} -> w_m^{-k} = conj
+            const double ex = a.x + bq.x, ey = a.y - bq.y;  // E = Y[k] + conj Y[n-k]
+            const double dx = a.x - bq.x, dy = a.y + bq.y;  // Y[k] - conj Y[n-k]
+            const double ox = dx * w.x + dy * w.y, oy = dy * w.x - dx * w.y;  // (..) w^{-k}
+            buf[lpad(k)] = make_double2(ex - oy, ey + ox);  // E + i O
+        }
+        __syncthreads();
+        // Stockham stages: radix 16 while 16 | the rest, then one radix-2/4/8 stage
+        LineStages<NT, N, 1, N>::run(buf, tw, m);
+        // epilogue: theta[t], t < n, from z[t / 2]
+        const double* th = reinterpret_cast<const double*>(buf);  // (re, im) pairs = theta[2j], theta[2j+1]
+#pragma unroll 1
+        for (int t = threadIdx.x; t < n; t += NT) {
+            const size_t o = static_cast<size_t>(x) * n + t;
+            const double told = op.Tst[o];
+            double tv = th[2 * lpad(t >> 1) + (t & 1)] * op.inv;
+            if (op.kirchhoff) {
+                const double br = op.ka + op.kb * tv;
+                if (!(br > 0.0)) r_bad |= GTD_ST_KIRCHHOFF;
+                tv = pow(br, op.kexp) - op.t_ambient;
+            }
+            if (!isfinite(tv)) r_bad |= GTD_ST_NONFINITE;
+            r_dmax = fmax(r_dmax, fabs(tv - told));
+            if (op.G) op.G[o] = tv;
+            if (op.Q) {
+                const double q = op.Q[o];
+                op.Q[o] = told;
+                if (op.om > 0.0) tv = op.om * (op.gm * tv + (1.0 - op.gm) * told - q) + q;
+            }
+            op.Tst[o] = tv;
+            const double f = op.law ? exp(op.beta * tv) : 1.0 + op.beta * tv;
+            op.app[o] = op.P[o] + op.L0[o] * f;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r_dmax = fmax(r_dmax, __shfl_xor_sync(0xffffffffu, r_dmax, o));
+    r_bad = __reduce_or_sync(0xffffffffu, r_bad);
+    if ((threadIdx.x & 31) == 0) {
+        s_m[threadIdx.x >> 5] = r_dmax;
+        s_b[threadIdx.x >> 5] = r_bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < NT / 32; ++w) {
+            r_dmax = fmax(r_dmax, s_m[w]);
+            r_bad |= s_b[w];
+        }
+        atomicMax(op.res_bits, static_cast<unsigned long long>(__double_as_longlong(r_dmax)));
+        if (r_bad) atomicOr(op.status, r_bad);
+    }
+}
+
+// One-pass variant (lg_rinv_c2r) of the inverse row phase for n <= 8192 (the line in shared memory).
+template <int N>
+int rows_inv_c2r_n(const gtd_lg* g, const void* Y, int hy, int pairs, const RinvB<double>& b, cudaStream_t st) {
+    constexpr int NT = N / 8 < GT_LG_RINV_NT ? N / 8 : GT_LG_RINV_NT;  // one radix-8 butterfly per thread
+    constexpr size_t smem = sizeof(double2) * (N + N / 8);
+    static int res = 0, sms = 0;
+    if (!sms) {
+        cudaFuncSetAttribute(lg_rinv_c2r<NT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_rinv_c2r<NT, N>, NT, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = res < 1 ? 1 : res;
+    }
+    const int rows = 2 * pairs;
+    const int grid = rows < sms * res ? rows : sms * res;
+    lg_rinv_c2r<NT, N><<<grid, NT, smem, st>>>(static_cast<const double2*>(Y), hy, rows,
+                                              static_cast<const double2*>(g->tw), g->m, b);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int rows_inv_c2r(const gtd_lg* g, const void* Y, int hy, int pairs, const RinvB<double>& b, cudaStream_t st) {
+    switch (g->n) {
+        case 512: return rows_inv_c2r_n<512>(g, Y, hy, pairs, b, st);
+        case 1024: return rows_inv_c2r_n<1024>(g, Y, hy, pairs, b, st);
+        case 2048: return rows_inv_c2r_n<2048>(g, Y, hy, pairs, b, st);
+        case 4096: return rows_inv_c2r_n<4096>(g, Y, hy, pairs, b, st);
+        case 8192: return rows_inv_c2r_n<8192>(g, Y, hy, pairs, b, st);
+        default: return -1;
+    }
+return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace
 }  // namespace gtb
 
@@ -589,9 +763,6 @@ int gtd_lg_cols_peer(const gtd_lg* g, const void* const* Zr, int pairs_per_rank,
 int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1, double* Tst, double* app,
                     const double* P, const double* L0, const gtd_fp_opts* o, unsigned long long* res_bits,
                     int* status, double* Q, double* G, double omega, double gamma, cudaStream_t st) {
-    RinvA<double> a{static_cast<const double2*>(Y), static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M2, hy};
-    int e = launch<double>(g->M1, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
-    if (e) return e;
     RinvB<double> b{};
     b.S1 = static_cast<const double2*>(S1);
     b.Tst = Tst;
@@ -616,8 +787,15 @@ int gtd_lg_rows_inv(const gtd_lg* g, const void* Y, int hy, int pairs, void* S1,
     b.kb = (1.0 - o->eta) * pow(o->t_ambient, -o->eta);
     b.t_ambient = o->t_ambient;
     b.inv = 1.0 / (double(g->m) * double(g->m));
+    static const int two_pass = getenv("GT_LG_RINV_2PASS") ? atoi(getenv("GT_LG_RINV_2PASS")) : 0;  // A/B switch
+    if (g->n >= 512 && g->n <= 8192 && !two_pass) return rows_inv_c2r(g, Y, hy, pairs, b, st);
+    RinvA<double> a{static_cast<const double2*>(Y), static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M2, hy};
+    int e = launch<double>(g->M1, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
+    if (e) return e;
     return launch<double>(g->M2, b, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
 }
+
+
 
 // fk = FFT2(center_kernel(f_sp0 - phi)) with fk[0] += phi m^2 / 4, half width [m][fkp]
 // (baseline_kernel_spectrum, greens.cpp:194-201), by the same four-step passes.
