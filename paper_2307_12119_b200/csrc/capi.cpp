@@ -960,6 +960,7 @@ gtd_lg large_geom(const gt_device_greens* d) {
     g.tw = d->tw64.p;
     g.fk = d->fk.p;
     g.fkp = d->d.hp;
+    g.hs = d->hs.p;
     return g;
 }
 }  // namespace

@@ -196,6 +196,7 @@ typedef struct gtd_lg {
     const void* tw; /* [m] double2 exp(-2 pi i t / m) */
     const void* fk; /* [m][fkp] double2 baseline kernel half spectrum */
     int fkp;
+    const void* hs; /* [m] double2 exp(-i pi t / m) (half steps; NULL: four-step row passes) */
 } gtd_lg;
 int gtd_lg_split(int m, int* M1, int* M2);
 /* applied rows [2 pairs][n] -> Z [pairs][m] (mirrored rows' spectra, two rows per line) */

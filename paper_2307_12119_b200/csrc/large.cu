@@ -532,7 +532,7 @@ int launch(int N, const Op& op, const double2* tw, int M, int groups, int nlines
 // apart) land in different banks.
 __device__ __forceinline__ int lpad(int i) { return i + (i >> 3); }
 
-template <int R, int NT, int N>
+template <int R, int NT, int N, int SIGN>
 __device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* __restrict__ tw, int m) {
     // butterfly j: inputs j + r N/R, twiddle w_{ns R}^{+k r} (inverse), outputs (j-k) R + k + r ns
     constexpr int nb = N / R;
@@ -549,7 +549,7 @@ __device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* 
         if (ns > 1) {
             // w_{ns R}^{k r} = w_m^{k r m / (ns R)}: one table load, powers by fp64 products
             const double2 w = tw[((m / (ns * R)) * k) & (m - 1)];
-            const cplx<double> w1 = mk<double>(w.x, -w.y);
+            const cplx<double> w1 = mk<double>(w.x, SIGN > 0 ? -w.y : w.y);
             cplx<double> wr = w1;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
@@ -557,7 +557,7 @@ __device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* 
                 if (r + 1 < R) wr = cmul<double>(wr, w1);
             }
         }
-        dftR<R, +1, double>(v[b]);
+        dftR<R, SIGN, double>(v[b]);
     }
     __syncthreads();
 #pragma unroll
@@ -572,13 +572,13 @@ __device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* 
     __syncthreads();
 }
 
-template <int NT, int N, int NS, int REM>
+template <int NT, int N, int SIGN, int NS, int REM>
 struct LineStages {
     __device__ __forceinline__ static void run(double2* buf, const double2* __restrict__ tw, int m) {
         if constexpr (REM > 1) {
             constexpr int R = REM % GT_LG_R16 == 0 ? GT_LG_R16 : REM;  // radix GT_LG_R16, then the rest
-            line_stage<R, NT, N>(buf, NS, tw, m);
-            LineStages<NT, N, NS * R, REM / R>::run(buf, tw, m);
+            line_stage<R, NT, N, SIGN>(buf, NS, tw, m);
+            LineStages<NT, N, SIGN, NS * R, REM / R>::run(buf, tw, m);
         }
     }
 };
@@ -608,7 +608,7 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
         }
         __syncthreads();
         // Stockham stages: radix 16 while 16 | the rest, then one radix-2/4/8 stage
-        LineStages<NT, N, 1, N>::run(buf, tw, m);
+        LineStages<NT, N, +1, 1, N>::run(buf, tw, m);
         // epilogue: theta[t], t < n, from z[t / 2]
         const double* th = reinterpret_cast<const double*>(buf);  // (re, im) pairs = theta[2j], theta[2j+1]
 #pragma unroll 1
@@ -653,6 +653,79 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
 }
 
 // One-pass variant (lg_rinv_c2r) of the inverse row phase for n <= 8192 (the line in shared memory).
+// One-pass forward row phase (replaces FwdA + FwdB for n <= 8192): the spectra of the
+// mirrored rows 2p, 2p+1 are their DCT-IIs, U_x[k] = conj(hs[k]) C_x[k] (hs[k] = w_m^{k/2}),
+// and the DCT-II of a real length-n row is Makhoul's n-point FFT of the reordered row
+// v[j] = x[2j], v[n-1-j] = x[2j+1]: C[k] = 2 Re(hs[k] V[k]). Both rows ride one complex line
+// (z = v_a + i v_b, separated by Hermitian symmetry), so one n-point FFT in shared memory
+// gives both rows' spectra, written straight to the packed layout the column phase reads:
+// Z[k] = U_a[k] + i U_b[k] and Z[m-k] = conj(U_a[k]) + i conj(U_b[k]).
+template <int NT, int N>
+__global__ void __launch_bounds__(NT, 1)
+lg_rfwd_dct(const double* __restrict__ app, int pairs, const double2* __restrict__ tw,
+            const double2* __restrict__ hs, double2* __restrict__ Z, int m) {
+    constexpr int n = N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* buf = reinterpret_cast<double2*>(smem_raw);
+    for (int p = blockIdx.x; p < pairs; p += gridDim.x) {
+        const double* xa = app + static_cast<size_t>(2 * p) * n;
+        const double* xb = xa + n;
+        __syncthreads();  // the previous pair's readers of buf are done
+#pragma unroll 4
+        for (int t = threadIdx.x; t < n; t += NT) {
+            const int j = (t & 1) ? n - 1 - (t >> 1) : (t >> 1);
+            buf[lpad(j)] = make_double2(xa[t], xb[t]);
+        }
+        __syncthreads();
+        LineStages<NT, N, -1, 1, N>::run(buf, tw, m);
+        double2* Zp = Z + static_cast<size_t>(p) * m;
+#pragma unroll 2
+        for (int k = threadIdx.x; k < n; k += NT) {
+            const double2 a = buf[lpad(k)], b = buf[lpad((n - k) & (n - 1))];  // Z[k], Z[n-k]
+            // V_a = (Z[k] + conj Z[n-k]) / 2, V_b = (Z[k] - conj Z[n-k]) / (2i)
+            const double vax = 0.5 * (a.x + b.x), vay = 0.5 * (a.y - b.y);
+            const double vbx = 0.5 * (a.y + b.y), vby = -0.5 * (a.x - b.x);
+            const double2 h = hs[k];
+            const double ca = 2.0 * (h.x * vax - h.y * vay), cb = 2.0 * (h.x * vbx - h.y * vby);
+            // U_x[k] = conj(h) C_x[k]
+            const double uar = h.x * ca, uai = -h.y * ca, ubr = h.x * cb, ubi = -h.y * cb;
+            Zp[k] = make_double2(uar - ubi, uai + ubr);                 // U_a + i U_b
+            if (k > 0) Zp[m - k] = make_double2(uar + ubi, ubr - uai);  // conj(U_a) + i conj(U_b)
+            else Zp[n] = make_double2(0.0, 0.0);                        // C[n] = 0: the Nyquist column
+        }
+    }
+}
+
+template <int N>
+int rows_fwd_dct_n(const gtd_lg* g, const double* app, int pairs, const void* hs, void* Z, cudaStream_t st) {
+    constexpr int NT = N / 8 < GT_LG_RINV_NT ? N / 8 : GT_LG_RINV_NT;
+    constexpr size_t smem = sizeof(double2) * (N + N / 8);
+    static int res = 0, sms = 0;
+    if (!sms) {
+        cudaFuncSetAttribute(lg_rfwd_dct<NT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_rfwd_dct<NT, N>, NT, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = res < 1 ? 1 : res;
+    }
+    const int grid = pairs < sms * res ? pairs : sms * res;
+    lg_rfwd_dct<NT, N><<<grid, NT, smem, st>>>(app, pairs, static_cast<const double2*>(g->tw),
+                                              static_cast<const double2*>(hs), static_cast<double2*>(Z), g->m);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int rows_fwd_dct(const gtd_lg* g, const double* app, int pairs, const void* hs, void* Z, cudaStream_t st) {
+    switch (g->n) {
+        case 512: return rows_fwd_dct_n<512>(g, app, pairs, hs, Z, st);
+        case 1024: return rows_fwd_dct_n<1024>(g, app, pairs, hs, Z, st);
+        case 2048: return rows_fwd_dct_n<2048>(g, app, pairs, hs, Z, st);
+        case 4096: return rows_fwd_dct_n<4096>(g, app, pairs, hs, Z, st);
+        case 8192: return rows_fwd_dct_n<8192>(g, app, pairs, hs, Z, st);
+        default: return -1;
+    }
+}
+
 template <int N>
 int rows_inv_c2r_n(const gtd_lg* g, const void* Y, int hy, int pairs, const RinvB<double>& b, cudaStream_t st) {
     constexpr int NT = N / 8 < GT_LG_RINV_NT ? N / 8 : GT_LG_RINV_NT;  // one radix-8 butterfly per thread
@@ -702,6 +775,8 @@ int gtd_lg_split(int m, int* M1, int* M2) {
 }
 
 int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st) {
+    static const int two_pass = getenv("GT_LG_RFWD_2PASS") ? atoi(getenv("GT_LG_RFWD_2PASS")) : 0;  // A/B switch
+    if (g->hs && g->n >= 512 && g->n <= 8192 && !two_pass) return rows_fwd_dct(g, app, pairs, g->hs, Z, st);
     FwdA<double> a{app, static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M1};
     int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
     if (e) return e;
