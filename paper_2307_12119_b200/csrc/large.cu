@@ -609,29 +609,44 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
         __syncthreads();
         // Stockham stages: radix 16 while 16 | the rest, then one radix-2/4/8 stage
         LineStages<NT, N, +1, 1, N>::run(buf, tw, m);
-        // epilogue: theta[t], t < n, from z[t / 2]
+        // epilogue: theta[t], t < n, from z[t / 2]; every global input of EB elements is
+        // requested before the first store (the stores may alias them for the compiler)
         const double* th = reinterpret_cast<const double*>(buf);  // (re, im) pairs = theta[2j], theta[2j+1]
+        constexpr int EB = 4;
+        const bool acc = op.Q != nullptr && op.om > 0.0;
 #pragma unroll 1
-        for (int t = threadIdx.x; t < n; t += NT) {
-            const size_t o = static_cast<size_t>(x) * n + t;
-            const double told = op.Tst[o];
-            double tv = th[2 * lpad(t >> 1) + (t & 1)] * op.inv;
-            if (op.kirchhoff) {
-                const double br = op.ka + op.kb * tv;
-                if (!(br > 0.0)) r_bad |= GTD_ST_KIRCHHOFF;
-                tv = pow(br, op.kexp) - op.t_ambient;
+        for (int t0 = threadIdx.x; t0 < n; t0 += NT * EB) {
+            double told[EB], pv[EB], lv[EB], qv[EB];
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+                const int t = t0 + e * NT;
+                if (t >= n) break;
+                const size_t o = static_cast<size_t>(x) * n + t;
+                told[e] = op.Tst[o];
+                pv[e] = op.P[o];
+                lv[e] = op.L0[o];
+                qv[e] = acc ? op.Q[o] : 0.0;
             }
-            if (!isfinite(tv)) r_bad |= GTD_ST_NONFINITE;
-            r_dmax = fmax(r_dmax, fabs(tv - told));
-            if (op.G) op.G[o] = tv;
-            if (op.Q) {
-                const double q = op.Q[o];
-                op.Q[o] = told;
-                if (op.om > 0.0) tv = op.om * (op.gm * tv + (1.0 - op.gm) * told - q) + q;
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+                const int t = t0 + e * NT;
+                if (t >= n) break;
+                const size_t o = static_cast<size_t>(x) * n + t;
+                double tv = th[2 * lpad(t >> 1) + (t & 1)] * op.inv;
+                if (op.kirchhoff) {
+                    const double br = op.ka + op.kb * tv;
+                    if (!(br > 0.0)) r_bad |= GTD_ST_KIRCHHOFF;
+                    tv = pow(br, op.kexp) - op.t_ambient;
+                }
+                if (!isfinite(tv)) r_bad |= GTD_ST_NONFINITE;
+                r_dmax = fmax(r_dmax, fabs(tv - told[e]));
+                if (op.G) op.G[o] = tv;
+                if (op.Q) op.Q[o] = told[e];
+                if (acc) tv = op.om * (op.gm * tv + (1.0 - op.gm) * told[e] - qv[e]) + qv[e];
+                op.Tst[o] = tv;
+                const double f = op.law ? exp(op.beta * tv) : 1.0 + op.beta * tv;
+                op.app[o] = pv[e] + lv[e] * f;
             }
-            op.Tst[o] = tv;
-            const double f = op.law ? exp(op.beta * tv) : 1.0 + op.beta * tv;
-            op.app[o] = op.P[o] + op.L0[o] * f;
         }
     }
 #pragma unroll
