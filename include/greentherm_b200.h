@@ -204,6 +204,12 @@ size_t gt_trace_scratch_bytes(int n, int precision, int window);
  * (the full gt_calibrate is limited to n <= 1024). Call with f_sp0_out = NULL to read n. */
 gt_status gt_modal_kernel(const char* stack_path, int* n_out, double* f_sp0_out);
 gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2);
+/* Layout of rows_fwd's output `z` (and of what cols / cols_peer read from it):
+ * dct_rows = 1 (n <= 8192): the rows' real DCT-II coefficients [2 pairs][n + 1] doubles
+ *   (the mirrored row's half spectrum is conj(exp(-i pi v / m)) C[v]); a compact cols input is
+ *   then [n][hc] doubles (columns c0.. of every die row, rank-major);
+ * dct_rows = 0 (larger n): packed row-pair spectra [pairs][m] complex, compact [n/2][2 hc]. */
+gt_status gt_large_row_layout(const gt_device_greens* d, int* dct_rows);
 gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
                             void* stream);
 gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, int c0, int hc, void* c1, void* c2,

@@ -135,6 +135,7 @@ _EXT = [
     ("gt_mc_batch_seeded", cint, [vp, vp, vp, cint, C.POINTER(BatchOpts), vp, pdbl, pdbl, C.POINTER(cint), pdbl]),
     ("gt_large_geometry", cint, [vp, C.POINTER(cint), C.POINTER(cint)]),
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
+    ("gt_large_row_layout", cint, [vp, C.POINTER(cint)]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
     ("gt_large_rows_inv", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp]),
     ("gt_large_cols_peer", cint, [vp, vp, cint, cint, cint, cint, vp, vp, vp, cint, vp]),

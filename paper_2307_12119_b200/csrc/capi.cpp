@@ -973,6 +973,13 @@ gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2) {
     });
 }
 
+gt_status gt_large_row_layout(const gt_device_greens* d, int* dct_rows) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (dct_rows) *dct_rows = gtd_lg_row_layout(&g);
+    });
+}
+
 gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
                             void* stream) {
     return guarded([&] {

@@ -199,6 +199,9 @@ typedef struct gtd_lg {
     const void* hs; /* [m] double2 exp(-i pi t / m) (half steps; NULL: four-step row passes) */
 } gtd_lg;
 int gtd_lg_split(int m, int* M1, int* M2);
+/* row-phase output layout: 1 = real DCT rows At [rows][n + 1] (n <= 8192, one-pass row kernels;
+ * the column phase reads columns c0.. of every row), 0 = packed row-pair spectra Z [pairs][m] */
+int gtd_lg_row_layout(const gtd_lg* g);
 /* applied rows [2 pairs][n] -> Z [pairs][m] (mirrored rows' spectra, two rows per line) */
 int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st);
 /* Z (all pairs) -> Y [n][hc] = rows [0,n) of IFFT_col(fk . FFT_col(mirror(A))) for columns c0..c0+hc.

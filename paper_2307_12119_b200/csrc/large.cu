@@ -127,6 +127,19 @@ struct ColA {
     int embed = 0;  // rows: 0 mirror_pad, 1 center_kernel
     const cplx<T>* const* Zr = nullptr;
     int Pr = 0;
+    // Real-DCT row layout (rows written by lg_rfwd_dct, n <= 8192): At[x][aoff + c] = C_x[v],
+    // the row's spectrum U_x[v] = conj(hs[v]) C_x[v] -- one 8-byte load per element. With a
+    // peer table (Zr set) rank r holds rows [2 Pr r, 2 Pr (r+1)) of At.
+    const T* At = nullptr;
+    int hA = 0, aoff = 0;
+    const double2* hs = nullptr;
+    __device__ T atv(int x, int c) const {
+        if (Zr) {
+            const int rpr = 2 * Pr, r = x / rpr;
+            return reinterpret_cast<const T*>(Zr[r])[static_cast<size_t>(x - r * rpr) * hA + aoff + c];
+        }
+        return At[static_cast<size_t>(x) * hA + aoff + c];
+    }
     __device__ const cplx<T>* zrow(int p) const {
         if (Zr) {
             const int r = p / Pr;
@@ -143,6 +156,11 @@ struct ColA {
         } else {
             x = i < n ? i : M - 1 - i;
         }
+        if (hs) {
+            const T a = atv(x, c);
+            const double2 h = hs[c0 + c];
+            return mk<T>(T(h.x) * a, -T(h.y) * a);
+        }
         const cplx<T>* Zp = zrow(x >> 1);
         const cplx<T> a = Zp[oa + c], b = cconj<T>(Zp[(ob + sb * c) & mask]);
         // half spectra of the two real rows packed in Zp (x even: real part's, odd: imaginary part's)
@@ -157,6 +175,10 @@ struct ColA {
             if (x >= n) return;
         } else {
             x = i < n ? i : M - 1 - i;
+        }
+        if (hs) {
+            if (!Zr) pf_l2(At + static_cast<size_t>(x) * hA + aoff + c);
+            return;
         }
         const cplx<T>* Zp = zrow(x >> 1);
         pf_l2(Zp + oa + c);
@@ -667,18 +689,18 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
     }
 }
 
-// One-pass variant (lg_rinv_c2r) of the inverse row phase for n <= 8192 (the line in shared memory).
 // One-pass forward row phase (replaces FwdA + FwdB for n <= 8192): the spectra of the
 // mirrored rows 2p, 2p+1 are their DCT-IIs, U_x[k] = conj(hs[k]) C_x[k] (hs[k] = w_m^{k/2}),
 // and the DCT-II of a real length-n row is Makhoul's n-point FFT of the reordered row
 // v[j] = x[2j], v[n-1-j] = x[2j+1]: C[k] = 2 Re(hs[k] V[k]). Both rows ride one complex line
 // (z = v_a + i v_b, separated by Hermitian symmetry), so one n-point FFT in shared memory
-// gives both rows' spectra, written straight to the packed layout the column phase reads:
-// Z[k] = U_a[k] + i U_b[k] and Z[m-k] = conj(U_a[k]) + i conj(U_b[k]).
+// gives both rows' DCT-II coefficients, stored as the real row layout At [rows][n + 1] the
+// column phase reads (ColA: U_x[v] = conj(hs[v]) At[x][v], one 8-byte load per element; the
+// packed complex spectra of the four-step path were 4x the bytes and read 4 times).
 template <int NT, int N>
 __global__ void __launch_bounds__(NT, 1)
 lg_rfwd_dct(const double* __restrict__ app, int pairs, const double2* __restrict__ tw,
-            const double2* __restrict__ hs, double2* __restrict__ Z, int m) {
+            const double2* __restrict__ hs, double* __restrict__ At, int m) {
     constexpr int n = N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* buf = reinterpret_cast<double2*>(smem_raw);
@@ -693,7 +715,6 @@ lg_rfwd_dct(const double* __restrict__ app, int pairs, const double2* __restrict
         }
         __syncthreads();
         LineStages<NT, N, -1, 1, N>::run(buf, tw, m);
-        double2* Zp = Z + static_cast<size_t>(p) * m;
 #pragma unroll 2
         for (int k = threadIdx.x; k < n; k += NT) {
             const double2 a = buf[lpad(k)], b = buf[lpad((n - k) & (n - 1))];  // Z[k], Z[n-k]
@@ -702,11 +723,14 @@ lg_rfwd_dct(const double* __restrict__ app, int pairs, const double2* __restrict
             const double vbx = 0.5 * (a.y + b.y), vby = -0.5 * (a.x - b.x);
             const double2 h = hs[k];
             const double ca = 2.0 * (h.x * vax - h.y * vay), cb = 2.0 * (h.x * vbx - h.y * vby);
-            // U_x[k] = conj(h) C_x[k]
-            const double uar = h.x * ca, uai = -h.y * ca, ubr = h.x * cb, ubi = -h.y * cb;
-            Zp[k] = make_double2(uar - ubi, uai + ubr);                 // U_a + i U_b
-            if (k > 0) Zp[m - k] = make_double2(uar + ubi, ubr - uai);  // conj(U_a) + i conj(U_b)
-            else Zp[n] = make_double2(0.0, 0.0);                        // C[n] = 0: the Nyquist column
+            // the rows' real DCT-II coefficients At [2 pairs][n + 1] (C[n] = 0)
+            double* Ar = At + static_cast<size_t>(2 * p) * (n + 1);
+            Ar[k] = ca;
+            Ar[n + 1 + k] = cb;
+            if (k == 0) {
+                Ar[n] = 0.0;
+                Ar[2 * n + 1] = 0.0;
+            }
         }
     }
 }
@@ -726,8 +750,14 @@ int rows_fwd_dct_n(const gtd_lg* g, const double* app, int pairs, const void* hs
     }
     const int grid = pairs < sms * res ? pairs : sms * res;
     lg_rfwd_dct<NT, N><<<grid, NT, smem, st>>>(app, pairs, static_cast<const double2*>(g->tw),
-                                              static_cast<const double2*>(hs), static_cast<double2*>(Z), g->m);
+                                              static_cast<const double2*>(hs), static_cast<double*>(Z), g->m);
     return static_cast<int>(cudaGetLastError());
+}
+
+// n <= 8192 with the half-step table: the one-pass row kernels and the real DCT row layout
+bool dct_rows(const gtd_lg* g) {
+    static const int two_pass = getenv("GT_LG_RFWD_2PASS") ? atoi(getenv("GT_LG_RFWD_2PASS")) : 0;  // A/B switch
+    return g->hs && g->n >= 512 && g->n <= 8192 && !two_pass;
 }
 
 int rows_fwd_dct(const gtd_lg* g, const double* app, int pairs, const void* hs, void* Z, cudaStream_t st) {
@@ -780,6 +810,8 @@ using namespace gtb;
 
 extern "C" {
 
+int gtd_lg_row_layout(const gtd_lg* g) { return dct_rows(g) ? 1 : 0; }
+
 int gtd_lg_split(int m, int* M1, int* M2) {
     int lg = 0;
     while ((1 << lg) < m) ++lg;
@@ -790,8 +822,7 @@ int gtd_lg_split(int m, int* M1, int* M2) {
 }
 
 int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st) {
-    static const int two_pass = getenv("GT_LG_RFWD_2PASS") ? atoi(getenv("GT_LG_RFWD_2PASS")) : 0;  // A/B switch
-    if (g->hs && g->n >= 512 && g->n <= 8192 && !two_pass) return rows_fwd_dct(g, app, pairs, g->hs, Z, st);
+    if (dct_rows(g)) return rows_fwd_dct(g, app, pairs, g->hs, Z, st);
     FwdA<double> a{app, static_cast<double2*>(S1), static_cast<const double2*>(g->tw), g->n, g->m, g->M1};
     int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, pairs, g->M1, st);
     if (e) return e;
@@ -816,6 +847,12 @@ int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, voi
         a.sb = -1;
         a.mask = g->m - 1;
     }
+    if (dct_rows(g)) {  // real DCT rows: full [n][n + 1] or compact [n][hc] (columns c0.. of every row)
+        a.At = static_cast<const double*>(Z);
+        a.hA = compact ? hc : g->n + 1;
+        a.aoff = compact ? 0 : c0;
+        a.hs = static_cast<const double2*>(g->hs);
+    }
     int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
     if (e) return e;
     ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
@@ -836,6 +873,11 @@ int gtd_lg_cols_peer(const gtd_lg* g, const void* const* Zr, int pairs_per_rank,
     a.mask = g->m - 1;
     a.Zr = reinterpret_cast<const double2* const*>(Zr);
     a.Pr = pairs_per_rank;
+    if (dct_rows(g)) {  // each rank's real DCT rows [2 pairs][n + 1]
+        a.hA = g->n + 1;
+        a.aoff = c0;
+        a.hs = static_cast<const double2*>(g->hs);
+    }
     int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
     if (e) return e;
     ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),

@@ -5,7 +5,8 @@ Rank r owns die-row pairs [r P, (r+1) P) (P = n / 2 / world) for the row
 phases and half-spectrum columns [c0_r, c0_r + hc_r) for the column phase
 (SURVEY §8e). Per iteration:
 
-  rows_fwd (local rows)  -> Z [P][m]   spectra of the mirrored row pairs
+  rows_fwd (local rows)  -> the rows' spectra: real DCT-II rows [2P][n+1] (n <= 8192:
+                            one-pass row kernel) or packed row-pair spectra Z [P][m]
   exchange 1             -> the column phase sees, for ALL row pairs, the
                             columns it owns and their mirrors
   cols (local columns)   -> rows [0, n) of IFFT_col(fk . FFT_col)
@@ -21,8 +22,9 @@ Two transports for the exchanges (world > 1):
       each result row straight into its owner's row buffer (peer stores). The
       phases are ordered by a stream sync + barrier after rows_fwd and after cols.
   "nccl": two all_to_all_single calls per iteration on compact per-destination
-      blocks (one index_select to pack, one index_copy to unpack). The CPU tests
-      run this path under gloo with numpy stand-in phases.
+      blocks (one index_select to pack, one index_copy to unpack): the columns a
+      rank owns of every DCT row (or of every packed line plus their mirrors). The
+      CPU tests run this path under gloo with numpy stand-in phases, both layouts.
 
 `solve_slab_emulated` runs W ranks' slabs in ONE process on one GPU through the
 peer kernels (the rank table holds W same-device buffers) -- the multi-rank data
@@ -75,6 +77,9 @@ class GpuLargeOps:
         m1, m2 = C.c_int(), C.c_int()
         self._check(self.L.gt_large_geometry(dg._d, C.byref(m1), C.byref(m2)))
         self.M1, self.M2 = m1.value, m2.value
+        lay = C.c_int()
+        self._check(self.L.gt_large_row_layout(dg._d, C.byref(lay)))
+        self.dct_rows = bool(lay.value)  # rows_fwd writes real DCT rows [2P][n+1] (else packed [P][m])
 
     def _check(self, st):
         from .api import check
@@ -281,21 +286,28 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
     else:
         S = _RankState(n, P, c0, hc, p_local, v_local, opts)
     exchange = exchange or (dist.all_to_all_single if world > 1 else None)
+    dct = bool(getattr(ops, "dct_rows", False))
     if world > 1 and transport == "nccl":
-        zrecv = torch.empty((world, P, 2 * hc), dtype=cd, device=dev)
         ycol = torch.empty((n, hc), dtype=cd, device=dev)
         S.yrow = torch.empty((rows, h), dtype=cd, device=dev)
-        # Per-destination send blocks as ONE gather from the row spectra z [P][m]: block q holds,
-        # for every local row pair, the columns rank q owns and their mirrors m - v (compact
-        # layout of gt_large_cols). The index maps are built once; each iteration is a single
+        # Per-destination send blocks as ONE gather from the row phase's output: block q holds,
+        # for every local row, the columns rank q owns (DCT rows [rows][h], real), or, packed,
+        # for every local row pair those columns and their mirrors m - v (compact layouts of
+        # gt_large_cols). The index maps are built once; each iteration is a single
         # index_select into a preallocated buffer (no per-iteration concatenation).
         cols = []
         for cq, hq in ranges:
             own = torch.arange(cq, cq + hq, device=dev)
-            blk = torch.cat([own, torch.remainder(m - own, m)])
-            cols.append((torch.arange(P, device=dev)[:, None] * m + blk[None, :]).reshape(-1))
+            if dct:
+                cols.append((torch.arange(rows, device=dev)[:, None] * h + own[None, :]).reshape(-1))
+            else:
+                blk = torch.cat([own, torch.remainder(m - own, m)])
+                cols.append((torch.arange(P, device=dev)[:, None] * m + blk[None, :]).reshape(-1))
         send_idx = torch.cat(cols)
-        send = torch.empty(send_idx.numel(), dtype=cd, device=dev)
+        zdt = torch.float64 if dct else cd
+        send = torch.empty(send_idx.numel(), dtype=zdt, device=dev)
+        zrecv = (torch.empty((world, rows, hc), dtype=zdt, device=dev) if dct
+                 else torch.empty((world, P, 2 * hc), dtype=cd, device=dev))
         # receive side of the second exchange: source q's block [rows][hq] lands in columns
         # [cq, cq + hq) of yrow -- one index_copy with a precomputed destination map
         dst = [(torch.arange(rows, device=dev)[:, None] * h + torch.arange(cq, cq + hq, device=dev)[None, :])
@@ -323,12 +335,17 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
                 phase_barrier()  # all column results stored into their owners' row buffers
                 yrow_t = S.yrow
             else:
-                torch.index_select(S.z.view(-1), 0, send_idx, out=send)
+                zsrc = S.z.view(-1).view(torch.float64)[: rows * h] if dct else S.z.view(-1)
+                torch.index_select(zsrc, 0, send_idx, out=send)
                 # output splits: what each source sends me; input splits: what I send each rank.
                 # Complex blocks travel as their float64 (re, im) view (NCCL has no complex type).
-                exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
-                         [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
-                ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, S.c1, S.c2, ycol, stream)
+                if dct:
+                    exchange(zrecv.view(-1), send, [rows * hc] * world, [rows * hq for _, hq in ranges])
+                    ops.cols(zrecv.reshape(n, hc), True, c0, hc, S.c1, S.c2, ycol, stream)
+                else:
+                    exchange(torch.view_as_real(zrecv).view(-1), torch.view_as_real(send).view(-1),
+                             [2 * P * 2 * hc] * world, [2 * P * 2 * hq for _, hq in ranges])
+                    ops.cols(zrecv.reshape(n // 2, 2 * hc), True, c0, hc, S.c1, S.c2, ycol, stream)
                 # ycol [n][hc] is already [world][rows][hc]: rank q's rows are a contiguous block
                 exchange(torch.view_as_real(recv).view(-1), torch.view_as_real(ycol).view(-1),
                          [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)

@@ -5,9 +5,13 @@ import numpy as np
 
 
 class NumpyLargeOps:
-    def __init__(self, n, fk):
+    def __init__(self, n, fk, dct_rows=False):
         self.n, self.m = n, 2 * n
         self.fk = fk  # [m][m] complex, full baseline kernel spectrum
+        # dct_rows: rows_fwd writes the rows' real DCT-II coefficients [rows][n+1] (the device
+        # layout for n <= 8192); else the packed row-pair spectra [pairs][m]
+        self.dct_rows = dct_rows
+        self.hs = np.exp(-1j * np.pi * np.arange(self.m) / self.m)
 
     def _mirror(self):
         i = np.arange(self.m)
@@ -16,6 +20,13 @@ class NumpyLargeOps:
     def rows_fwd(self, app, pairs, s1, z, stream):
         a = app.numpy()
         mi = self._mirror()
+        if self.dct_rows:
+            h = self.n + 1
+            at = z.view(-1).view(__import__("torch").float64).numpy()
+            for x in range(2 * pairs):
+                U = np.fft.fft(a[x][mi])[:h]
+                at[x * h:(x + 1) * h] = np.real(self.hs[:h] * U)
+            return
         for p in range(pairs):
             x = a[2 * p][mi] + 1j * a[2 * p + 1][mi]
             z[p] = __import__("torch").from_numpy(np.fft.fft(x))
@@ -25,15 +36,21 @@ class NumpyLargeOps:
         Z = z.numpy()
         mi = self._mirror()
         out = np.zeros((n, hc), complex)
+        if self.dct_rows:
+            At = z.numpy().reshape(n, hc) if compact else z.view(-1).view(__import__("torch").float64).numpy()[
+                : n * (n + 1)].reshape(n, n + 1)[:, c0:c0 + hc]
         for c in range(hc):
             v = c0 + c
-            if compact:
-                a, b = Z[:, c], np.conj(Z[:, hc + c])
+            if self.dct_rows:
+                A = np.conj(self.hs[v]) * At[:, c]
             else:
-                a, b = Z[:, v], np.conj(Z[:, (m - v) % m])
-            A = np.empty(n, complex)
-            A[0::2] = 0.5 * (a + b)
-            A[1::2] = -0.5j * (a - b)
+                if compact:
+                    a, b = Z[:, c], np.conj(Z[:, hc + c])
+                else:
+                    a, b = Z[:, v], np.conj(Z[:, (m - v) % m])
+                A = np.empty(n, complex)
+                A[0::2] = 0.5 * (a + b)
+                A[1::2] = -0.5j * (a - b)
             col = np.fft.fft(A[mi])
             col = col * self.fk[:, v] if v <= n else col * 0
             out[:, c] = (np.fft.ifft(col) * m)[:n]

@@ -19,7 +19,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, q, accel=0):
+def _worker(rank, world, port, n, q, accel=0, dct=False):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     import torch
@@ -41,14 +41,14 @@ def _worker(rank, world, port, n, q, accel=0):
     o.leak_frac, o.law, o.kirchhoff, o.beta, o.tol, o.max_iters = 0.3, 0, 0, 0.017, 1e-10, 60
     o.t_ambient, o.eta = 318.15, 1.3
     o.accel = accel
-    res = slab.solve_slab(NumpyLargeOps(n, fk), n, torch.from_numpy(P[sl].copy()), torch.from_numpy(V[sl].copy()), o,
+    res = slab.solve_slab(NumpyLargeOps(n, fk, dct_rows=dct), n, torch.from_numpy(P[sl].copy()), torch.from_numpy(V[sl].copy()), o,
                           rank=rank, world=world)
     q.put((rank, res.t.numpy(), res.iterations, res.status))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_slab_exchange_matches_full_solve(world):
+@pytest.mark.parametrize("world,dct", [(1, False), (2, False), (2, True)])
+def test_slab_exchange_matches_full_solve(world, dct):
     import torch.multiprocessing as mp
     sys.path.insert(0, str(ROOT / "tests"))
     from slab_numpy_ops import baseline_fk, fixed_point_numpy
@@ -56,7 +56,7 @@ def test_slab_exchange_matches_full_solve(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, 0, dct)) for r in range(world)]
     for p in procs:
         p.start()
     import queue
@@ -82,13 +82,13 @@ def test_slab_exchange_matches_full_solve(world):
     assert np.abs(T - ref).max() < 1e-9
 
 
-def _run(world, n, accel):
+def _run(world, n, accel, dct=False):
     import queue
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, accel)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, accel, dct)) for r in range(world)]
     for p in procs:
         p.start()
     got = []
@@ -112,7 +112,7 @@ def test_slab_chebyshev_across_ranks():
     from slab_numpy_ops import baseline_fk, fixed_point_numpy
     n = 64
     t1, it1, st1 = _run(1, n, 3)
-    t2, it2, st2 = _run(2, n, 3)
+    t2, it2, st2 = _run(2, n, 3, dct=True)
     z = np.load(ROOT / "tests" / "golden" / "greens_n64.npz")
     fk = baseline_fk(z["f_sp0"], float(z["phi"]))
     rng = np.random.default_rng(3)
