@@ -133,6 +133,9 @@ struct ColA {
     const T* At = nullptr;
     int hA = 0, aoff = 0;
     const double2* hs = nullptr;
+    // pack = 1 (DCT rows): line c carries the two real columns 2c, 2c+1 of the block (< hcols)
+    // as C[., 2c] + i C[., 2c+1]; their column transforms separate locally in ColB
+    int pack = 0, hcols = 0;
     __device__ T atv(int x, int c) const {
         if (Zr) {
             const int rpr = 2 * Pr, r = x / rpr;
@@ -156,6 +159,11 @@ struct ColA {
         } else {
             x = i < n ? i : M - 1 - i;
         }
+        if (pack) {
+            const T a0 = atv(x, 2 * c);
+            const T a1 = 2 * c + 1 < hcols ? atv(x, 2 * c + 1) : T(0);
+            return mk<T>(a0, a1);
+        }
         if (hs) {
             const T a = atv(x, c);
             const double2 h = hs[c0 + c];
@@ -177,7 +185,7 @@ struct ColA {
             x = i < n ? i : M - 1 - i;
         }
         if (hs) {
-            if (!Zr) pf_l2(At + static_cast<size_t>(x) * hA + aoff + c);
+            if (!Zr) pf_l2(At + static_cast<size_t>(x) * hA + aoff + (pack ? 2 * c : c));
             return;
         }
         const cplx<T>* Zp = zrow(x >> 1);
@@ -202,11 +210,51 @@ struct ColB {
     int fkp;
     const double2* tw;
     int h, M, M1, M2, c0, hc;
+    // pack = 1: C1 holds packed lines [m][hcp] (ColA pack); a 32-line item is the 16 packed
+    // lines of its 32 columns in slots 0..15 (slots 16..31 start empty), unpacked after the
+    // forward transform into column 2 cp (slot s) and 2 cp + 1 (slot s + 16):
+    //   D_a + i D_b = hs[u] Z[u] (both real: DCT-II of the mirrored columns), and the column
+    //   spectrum of U_x[v] = conj(hs[v]) C_x[v] is conj(hs[u] hs[v]) D[u].
+    int pack = 0, hcp = 0;
+    const double2* hs = nullptr;
+    __device__ int slot_col(int c) const { return 32 * (c >> 5) + 2 * (c & 15) + ((c >> 4) & 1); }
     __device__ cplx<T> load(int k2, int c, int j) const {
+        if (pack) {
+            const int s = c & 31, cp = 16 * (c >> 5) + s;
+            if (s >= 16 || cp >= hcp) return mk<T>(T(0), T(0));
+            return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hcp + cp];
+        }
         return C1[(static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c];
     }
     __device__ void pf(int k2, int c, int j) const {
+        if (pack) {
+            const int s = c & 31, cp = 16 * (c >> 5) + s;
+            if (s < 16 && cp < hcp) pf_l2(C1 + (static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hcp + cp);
+            return;
+        }
         pf_l2(C1 + (static_cast<size_t>(j) + static_cast<size_t>(M1) * k2) * hc + c);
+    }
+    // unpack slot s < 16 of frequency row k1 in place (slots s, s + 16), times the spectral factor
+    __device__ void unpack(cplx<T>* tile, int LP, int k2, int l0, int s, int k1) const {
+        const int u = k2 + M2 * k1;
+        const int cp = (l0 >> 1) + s;
+        const cplx<T> z = tile[k1 * LP + s];
+        const double2 hu = hs[u];
+        const cplx<T> d = cmul<T>(mk<T>(T(hu.x), T(hu.y)), z);  // D_a + i D_b
+        cplx<T> y0 = mk<T>(T(0), T(0)), y1 = mk<T>(T(0), T(0));
+        const int va = 2 * cp, vb = va + 1;  // local columns
+        if (va < hc && c0 + va < h) {
+            const double2 hv = hs[c0 + va];
+            const cplx<T> ph = cconj<T>(cmul<T>(mk<T>(T(hu.x), T(hu.y)), mk<T>(T(hv.x), T(hv.y))));
+            y0 = cscale<T>(cmul<T>(fk[static_cast<size_t>(u) * fkp + c0 + va], ph), d.x);
+        }
+        if (vb < hc && c0 + vb < h) {
+            const double2 hv = hs[c0 + vb];
+            const cplx<T> ph = cconj<T>(cmul<T>(mk<T>(T(hu.x), T(hu.y)), mk<T>(T(hv.x), T(hv.y))));
+            y1 = cscale<T>(cmul<T>(fk[static_cast<size_t>(u) * fkp + c0 + vb], ph), d.y);
+        }
+        tile[k1 * LP + s] = y0;
+        tile[k1 * LP + s + 16] = y1;
     }
     // the spectral factor at (u, v); zero for the padded columns v > n
     __device__ cplx<T> midw(int k2, int c, int k1) const {
@@ -216,6 +264,10 @@ struct ColB {
     using Pre = cplx<T>;
     __device__ Pre pre(int k2, int, int ia) const { return twm<T>(tw, M, static_cast<long long>(ia) * k2, true); }
     __device__ void store(int k2, int c, int ia, cplx<T> v, const Pre& w) const {
+        if (pack) {
+            c = slot_col(c);
+            if (c >= hc) return;
+        }
         C2[(static_cast<size_t>(k2) + static_cast<size_t>(M2) * ia) * hc + c] = cmul<T>(v, w);
     }
 };
@@ -442,6 +494,14 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
         __syncthreads();
         tile_fft<T, N, L, LP, NT, Op::SIGN>(tile, s_tw);
         if constexpr (TWO) {
+          if (op.pack) {
+            // packed ColB: unpack the 16 packed lines into the 32 columns (in place), times fk
+            // (32-column items: every column transform length the DCT-row path uses, M1 <= 128)
+            if constexpr (L == 32)
+                for (int idx = threadIdx.x; idx < N * 16; idx += NT) op.unpack(tile, LP, g, l0, idx % 16, idx / 16);
+            else
+                __trap();
+          } else {
             // spectral factors issued in batches ahead of their use (global / L2 latency)
             constexpr int UM = EPT < 8 ? EPT : 8;
             for (int base = threadIdx.x; base < N * L; base += NT * UM) {
@@ -457,6 +517,7 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
                     if (idx < N * L && l0 + l < nlines) tile[k * LP + l] = cmul<T>(tile[k * LP + l], f[u]);
                 }
             }
+          }
             __syncthreads();
             tile_fft<T, N, L, LP, NT, -Op::SIGN>(tile, s_tw);
         }
@@ -830,6 +891,29 @@ int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, voi
     return launch<double>(g->M1, b, static_cast<const double2*>(g->tw), g->m, pairs, g->M2, st);
 }
 
+// ColA + ColB of the column phase; with DCT rows two real columns share a line through the
+// first two sub-passes (half the ColA items and the C1 bytes), unpacked inside ColB.
+static int cols_ab(const gtd_lg* g, ColA<double>& a, int c0, int hc, void* C1, void* C2, cudaStream_t st) {
+    const bool pk = dct_rows(g) && !getenv("GT_LG_NOPACK");
+    const int hcp = (hc + 1) / 2;
+    if (pk) {
+        a.pack = 1;
+        a.hcols = hc;
+        a.hc = hcp;  // C1 pitch: packed lines
+    }
+    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, pk ? hcp : hc, st);
+    if (e) return e;
+    ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
+                   g->fkp, static_cast<const double2*>(g->tw), g->n + 1, g->m, g->M1, g->M2, c0, hc};
+    if (pk) {
+        b.pack = 1;
+        b.hcp = hcp;
+        b.hs = static_cast<const double2*>(g->hs);
+    }
+    return launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2,
+                                              pk ? (hc + 31) / 32 * 32 : hc, st);
+}
+
 int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, void* C1, void* C2, void* Y,
                 cudaStream_t st) {
     ColA<double> a{static_cast<const double2*>(Z), static_cast<double2*>(C1), static_cast<const double2*>(g->tw),
@@ -853,11 +937,7 @@ int gtd_lg_cols(const gtd_lg* g, const void* Z, int compact, int c0, int hc, voi
         a.aoff = compact ? 0 : c0;
         a.hs = static_cast<const double2*>(g->hs);
     }
-    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
-    if (e) return e;
-    ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
-                   g->fkp, static_cast<const double2*>(g->tw), g->n + 1, g->m, g->M1, g->M2, c0, hc};
-    e = launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2, hc, st);
+    int e = cols_ab(g, a, c0, hc, C1, C2, st);
     if (e) return e;
     ColC<double> c{static_cast<const double2*>(C2), static_cast<double2*>(Y), g->n, g->m, g->M1, g->M2, hc};
     return launch<double>(g->M2, c, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
@@ -878,11 +958,7 @@ int gtd_lg_cols_peer(const gtd_lg* g, const void* const* Zr, int pairs_per_rank,
         a.aoff = c0;
         a.hs = static_cast<const double2*>(g->hs);
     }
-    int e = launch<double>(g->M2, a, static_cast<const double2*>(g->tw), g->m, g->M1, hc, st);
-    if (e) return e;
-    ColB<double> b{static_cast<const double2*>(C1), static_cast<double2*>(C2), static_cast<const double2*>(g->fk),
-                   g->fkp, static_cast<const double2*>(g->tw), g->n + 1, g->m, g->M1, g->M2, c0, hc};
-    e = launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2, hc, st);
+    int e = cols_ab(g, a, c0, hc, C1, C2, st);
     if (e) return e;
     ColC<double> c{static_cast<const double2*>(C2), nullptr, g->n, g->m, g->M1, g->M2, hc};
     c.Yr = reinterpret_cast<double2* const*>(Yr);

@@ -57,13 +57,17 @@ from .api import GT_SAMPLE_KIRCHHOFF, GT_SAMPLE_NOCONVERGE, GT_SAMPLE_NONFINITE 
 
 
 def column_ranges(h: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous (c0, hc) per rank covering [0, h)."""
-    base, extra = divmod(h, world)
-    out, c0 = [], 0
+    """Contiguous (c0, hc) per rank covering [0, h), split on even columns: the column
+    phase carries columns 2k, 2k+1 on one line, so every rank packs the same pairs as a
+    single GPU does (identical bits for any world size)."""
+    pairs = (h + 1) // 2
+    base, extra = divmod(pairs, world)
+    out, p0 = [], 0
     for r in range(world):
-        hc = base + (1 if r < extra else 0)
-        out.append((c0, hc))
-        c0 += hc
+        pc = base + (1 if r < extra else 0)
+        c0, c1 = 2 * p0, min(h, 2 * (p0 + pc))
+        out.append((c0, c1 - c0))
+        p0 += pc
     return out
 
 
