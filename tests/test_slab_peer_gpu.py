@@ -1,5 +1,6 @@
-"""Config-4 peer transport across PROCESSES (CUDA IPC mapped buffers, gloo barriers):
-two ranks as two processes on one GPU. Each rank's row spectra and row buffer are
+"""Config-4 multi-rank transports across PROCESSES on one GPU: the peer transport (CUDA IPC
+mapped buffers, gloo barriers), and the copy ("nccl") transport with its all-to-all carried
+by gloo through host memory. With the peer transport each rank's row spectra and row buffer are
 cudaMalloc'ed and opened by the other rank (gt_ipc_open); the column kernels read the
 other rank's spectra and store into its row buffer directly. Phases are separated by a
 device sync + barrier on the host, so no kernel waits on another (B200_PROFILING: no
@@ -44,7 +45,16 @@ def _setup(n):
     return ga, p, v
 
 
-def _worker(rank, world, port, n, accel, q):
+def _gloo_exchange(out, inp, out_splits, in_splits):
+    """all_to_all_single for CUDA tensors over gloo (host round trip): the copy transport's
+    exchange logic with the device kernels, two processes on one GPU."""
+    import torch.distributed as dist
+    o = out.cpu()
+    dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits)
+    out.copy_(o)
+
+
+def _worker(rank, world, port, n, accel, q, transport="peer"):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -61,14 +71,15 @@ def _worker(rank, world, port, n, accel, q):
     o.accel = accel
     sl = slice(rank * rows, (rank + 1) * rows)
     res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(p[sl].copy()).cuda(),
-                          torch.from_numpy(v[sl].copy()).cuda(), o, rank=rank, world=world, transport="peer")
+                          torch.from_numpy(v[sl].copy()).cuda(), o, rank=rank, world=world, transport=transport,
+                          exchange=_gloo_exchange if transport == "nccl" else None)
     torch.cuda.synchronize()
     q.put((rank, res.t.cpu().numpy(), res.iterations, res.status))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("accel", [0, 3])
-def test_peer_transport_two_processes(b200lib, accel):
+@pytest.mark.parametrize("accel,transport", [(0, "peer"), (3, "peer"), (0, "nccl")])
+def test_peer_transport_two_processes(b200lib, accel, transport):
     import queue
     import torch
     import torch.multiprocessing as mp
@@ -78,7 +89,7 @@ def test_peer_transport_two_processes(b200lib, accel):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, accel, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, accel, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     got = []
@@ -98,7 +109,7 @@ def test_peer_transport_two_processes(b200lib, accel):
     o.accel = accel
     one = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(pm).cuda(), torch.from_numpy(vm).cuda(), o)
     d = float(np.abs(T - one.t.cpu().numpy()).max())
-    print(f"peer transport, 2 processes, accel={accel}: iters {[g[2] for g in got]} vs {one.iterations}, "
+    print(f"{transport} transport, 2 processes, accel={accel}: iters {[g[2] for g in got]} vs {one.iterations}, "
           f"max|dT| {d:.3e} K")
     assert all(g[3] == 0 for g in got) and one.status == 0
     assert all(g[2] == one.iterations for g in got)
