@@ -215,7 +215,7 @@ def test_large_grid_n1024_chebyshev_vs_oracle(b200lib, oracle, tmp_path):
     assert err <= 1e-3
 
 
-@pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3)])
+@pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3), (8, 0)])
 def test_large_grid_peer_ranks_emulated(b200lib, tmp_path, world, accel):
     """The multi-GPU column phase over peer memory (gt_large_cols_peer: every rank's row
     spectra read in place, results stored into their owners' row buffers), with `world`
