@@ -572,6 +572,120 @@ size_t lg_smem() {
     return sizeof(cplx<T>) * (N * lg_pitch<T, N>() + N);
 }
 
+// Packed ColB with 64-column items: the 32 packed lines (two real columns each) of the item
+// fill the whole tile for the forward sub-pass (no empty slots), then the item is finished in
+// two rounds of 32 columns -- packed lines 0..15 unpacked in place while 16..31 wait in
+// registers, inverse sub-pass, store; then 16..31 the same way.
+template <int N>
+__global__ void __launch_bounds__(TileGeom<double, N>::NT, TileGeom<double, N>::MINB)
+lg_colb64(ColB<double> op, const double2* __restrict__ twm_g, int M, int groups, int blocks) {
+    using T = double;
+    using G = TileGeom<T, N>;
+    constexpr int L = G::L, LP = lg_pitch<T, N>(), NT = G::NT;
+    static_assert(L == 32, "64-column items: 32 packed lines per tile");
+    constexpr int EPT = (N * L + NT - 1) / NT;
+    constexpr int ES = (N * 16 + NT - 1) / NT;  // stashed elements per thread
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* tile = reinterpret_cast<cplx<T>*>(smem_raw);
+    cplx<T>* s_tw = tile + N * LP;
+    for (int t = threadIdx.x; t < N; t += NT) {
+        const double2 w = twm_g[static_cast<size_t>(t) * (M / N)];
+        s_tw[t] = mk<T>(T(w.x), T(w.y));
+    }
+    for (int item = blockIdx.x; item < groups * blocks; item += gridDim.x) {
+        const int b = item / groups, k2 = item - b * groups;  // block-major: items of one block run together
+        const int cp0 = 32 * b;                                 // first packed line of the item
+        __syncthreads();
+        for (int base = threadIdx.x; base < N * L; base += NT * 16) {
+            cplx<T> vals[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int idx = base + u * NT, l = idx % L, j = idx / L;
+                vals[u] = (idx < N * L && cp0 + l < op.hcp)
+                              ? op.C1[(static_cast<size_t>(j) + static_cast<size_t>(op.M1) * k2) * op.hcp + cp0 + l]
+                              : mk<T>(T(0), T(0));
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int idx = base + u * NT, l = idx % L, j = idx / L;
+                if (idx < N * L) tile[j * LP + l] = vals[u];
+            }
+        }
+        __syncthreads();
+        tile_fft<T, N, L, LP, NT, -1>(tile, s_tw);
+        cplx<T> stash[ES];
+#pragma unroll
+        for (int q = 0; q < ES; ++q) {
+            const int idx = threadIdx.x + q * NT;
+            if (idx < N * 16) stash[q] = tile[(idx / 16) * LP + 16 + idx % 16];
+        }
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            if (half == 1) {
+                __syncthreads();  // round 0's stores have read the tile
+#pragma unroll
+                for (int q = 0; q < ES; ++q) {
+                    const int idx = threadIdx.x + q * NT;
+                    if (idx < N * 16) tile[(idx / 16) * LP + idx % 16] = stash[q];
+                }
+                __syncthreads();
+            }
+            // unpack packed lines cp0 + 16 half + s (slot s < 16) into slots s, s + 16 (in place)
+            for (int idx = threadIdx.x; idx < N * 16; idx += NT)
+                op.unpack(tile, LP, k2, 2 * (cp0 + 16 * half), idx % 16, idx / 16);
+            __syncthreads();
+            tile_fft<T, N, L, LP, NT, +1>(tile, s_tw);
+            // store: slot s -> local column 2 (cp0 + 16 half) + 2 (s mod 16) + (s >= 16)
+            constexpr int US = EPT < 8 ? EPT : 8;
+            for (int base = threadIdx.x; base < N * L; base += NT * US) {
+                cplx<T> w[US];
+#pragma unroll
+                for (int u = 0; u < US; ++u) {
+                    const int idx = base + u * NT, k = idx / L;
+                    w[u] = idx < N * L ? op.pre(k2, 0, k) : mk<T>(T(0), T(0));
+                }
+#pragma unroll
+                for (int u = 0; u < US; ++u) {
+                    const int idx = base + u * NT, l = idx % L, ia = idx / L;
+                    if (idx >= N * L) continue;
+                    const int c = 2 * (cp0 + 16 * half) + 2 * (l & 15) + (l >> 4);
+                    if (c < op.hc)
+                        op.C2[(static_cast<size_t>(k2) + static_cast<size_t>(op.M2) * ia) * op.hc + c] =
+                            cmul<T>(tile[ia * LP + l], w[u]);
+                }
+            }
+        }
+    }
+}
+
+template <int N>
+int launch_colb64_n(const ColB<double>& b, const double2* tw, int M, int groups, int blocks, cudaStream_t st) {
+    const size_t smem = lg_smem<double, N>();
+    static int res = 0, sms = 0;  // per N: each instantiation sets its own shared-memory attribute
+    if (!sms) {
+        cudaFuncSetAttribute(lg_colb64<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_colb64<N>, TileGeom<double, N>::NT, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = res < 1 ? 1 : res;
+    }
+    const int items = groups * blocks;
+    const int grid = items < sms * res ? items : sms * res;
+    if (grid > 0) lg_colb64<N><<<grid, TileGeom<double, N>::NT, smem, st>>>(b, tw, M, groups, blocks);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_colb64(const ColB<double>& b, const double2* tw, int M, int groups, int hcp, cudaStream_t st) {
+    const int blocks = (hcp + 31) / 32;
+    switch (b.M1) {
+        case 32: return launch_colb64_n<32>(b, tw, M, groups, blocks, st);
+        case 64: return launch_colb64_n<64>(b, tw, M, groups, blocks, st);
+        case 128: return launch_colb64_n<128>(b, tw, M, groups, blocks, st);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
 template <typename T, int N, class Op, bool TWO>
 int launch_n(const Op& op, const double2* tw, int M, int groups, int nlines, cudaStream_t st) {
     static int res = 0, sms = 0;
@@ -910,6 +1024,7 @@ static int cols_ab(const gtd_lg* g, ColA<double>& a, int c0, int hc, void* C1, v
         b.hcp = hcp;
         b.hs = static_cast<const double2*>(g->hs);
     }
+    if (pk && !getenv("GT_LG_COLB32")) return launch_colb64(b, static_cast<const double2*>(g->tw), g->m, g->M2, hcp, st);
     return launch<double, ColB<double>, true>(g->M1, b, static_cast<const double2*>(g->tw), g->m, g->M2,
                                               pk ? (hc + 31) / 32 * 32 : hc, st);
 }
