@@ -26,10 +26,8 @@
 #ifndef GT_LG_RINV_NT
 #define GT_LG_RINV_NT 1024
 #endif
-#ifndef GT_LG_R16
-#define GT_LG_R16 8
-#endif
 
+#include "fft_line.cuh"
 #include "fft_tile.cuh"
 #include "gt_device.h"
 
@@ -725,61 +723,6 @@ int launch(int N, const Op& op, const double2* tw, int M, int groups, int nlines
 // j < n/2 is kept: the die's n samples). The whole n-point line lives in shared memory
 // (128 KB at n = 8192, one CTA per SM), the Stockham stages run in place, and the epilogue
 // (theta -> T, Kirchhoff inverse, residual, Chebyshev step, next applied row) is RinvB's.
-// One 16-byte pad every 8 elements: the stride-R stores of the first Stockham stage (R x 16 B
-// apart) land in different banks.
-__device__ __forceinline__ int lpad(int i) { return i + (i >> 3); }
-
-template <int R, int NT, int N, int SIGN>
-__device__ __forceinline__ void line_stage(double2* buf, int ns, const double2* __restrict__ tw, int m) {
-    // butterfly j: inputs j + r N/R, twiddle w_{ns R}^{+k r} (inverse), outputs (j-k) R + k + r ns
-    constexpr int nb = N / R;
-    constexpr int BMAX = (nb + NT - 1) / NT;  // butterflies per thread
-    const int tid = threadIdx.x, nthr = NT;
-    cplx<double> v[BMAX][R];
-#pragma unroll
-    for (int b = 0; b < BMAX; ++b) {
-        const int j = tid + b * nthr;
-        if (j >= nb) break;
-        const int k = j % ns;
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = buf[lpad(j + r * nb)];
-        if (ns > 1) {
-            // w_{ns R}^{k r} = w_m^{k r m / (ns R)}: one table load, powers by fp64 products
-            const double2 w = tw[((m / (ns * R)) * k) & (m - 1)];
-            const cplx<double> w1 = mk<double>(w.x, SIGN > 0 ? -w.y : w.y);
-            cplx<double> wr = w1;
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-                v[b][r] = cmul<double>(v[b][r], wr);
-                if (r + 1 < R) wr = cmul<double>(wr, w1);
-            }
-        }
-        dftR<R, SIGN, double>(v[b]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < BMAX; ++b) {
-        const int j = tid + b * nthr;
-        if (j >= nb) break;
-        const int k = j % ns;
-        const int base = (j - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) buf[lpad(base + r * ns)] = v[b][r];
-    }
-    __syncthreads();
-}
-
-template <int NT, int N, int SIGN, int NS, int REM>
-struct LineStages {
-    __device__ __forceinline__ static void run(double2* buf, const double2* __restrict__ tw, int m) {
-        if constexpr (REM > 1) {
-            constexpr int R = REM % GT_LG_R16 == 0 ? GT_LG_R16 : REM;  // radix GT_LG_R16, then the rest
-            line_stage<R, NT, N, SIGN>(buf, NS, tw, m);
-            LineStages<NT, N, SIGN, NS * R, REM / R>::run(buf, tw, m);
-        }
-    }
-};
-
 template <int NT, int N>
 __global__ void __launch_bounds__(NT, 1)
 lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __restrict__ tw, int m,
@@ -805,7 +748,7 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
         }
         __syncthreads();
         // Stockham stages: radix 16 while 16 | the rest, then one radix-2/4/8 stage
-        LineStages<NT, N, +1, 1, N>::run(buf, tw, m);
+        LineStages<double, NT, N, +1, 1, N>::run(buf, tw, m);
         // epilogue: theta[t], t < n, from z[t / 2]; every global input of EB elements is
         // requested before the first store (the stores may alias them for the compiler)
         const double* th = reinterpret_cast<const double*>(buf);  // (re, im) pairs = theta[2j], theta[2j+1]
@@ -889,7 +832,7 @@ lg_rfwd_dct(const double* __restrict__ app, int pairs, const double2* __restrict
             buf[lpad(j)] = make_double2(xa[t], xb[t]);
         }
         __syncthreads();
-        LineStages<NT, N, -1, 1, N>::run(buf, tw, m);
+        LineStages<double, NT, N, -1, 1, N>::run(buf, tw, m);
 #pragma unroll 2
         for (int k = threadIdx.x; k < n; k += NT) {
             const double2 a = buf[lpad(k)], b = buf[lpad((n - k) & (n - 1))];  // Z[k], Z[n-k]
