@@ -76,17 +76,18 @@ def test_large_grid_needs_fp64(b200lib, greens512):
     assert e.value.status == 2
 
 
-def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path):
-    """n = 2048 takes the large-grid preparation (fk built by the four-step passes from
-    the modal f_sp0): three iterations against a direct numpy restatement."""
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path, n):
+    """n = 2048 / 4096 take the large-grid preparation (fk built by the four-step passes from
+    the modal f_sp0; m = 4096 = 64 x 64 and 8192 = 128 x 64 column splits): three iterations
+    against a direct numpy restatement."""
     import sys
     from pathlib import Path
     import torch
     from paper_2307_12119_b200 import slab
     from paper_2307_12119_b200.api import DeviceGreens, GreensArrays
     sys.path.insert(0, str(Path(__file__).parent))
-    from slab_numpy_ops import baseline_fk, fixed_point_numpy
-    n = 2048
+    from slab_numpy_ops import baseline_fk, fixed_point_numpy, fixed_point_torch
     (tmp_path / "stack.txt").write_text(f"n {n}\ndie_edge 0.016\n")
     f = np.empty((n, n))
     nn = C.c_int()
@@ -103,9 +104,14 @@ def test_large_grid_kernel_spectrum_n2048(b200lib, tmp_path):
     o = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-30, max_iters=3)
     res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(P).cuda(), torch.from_numpy(V).cuda(), o)
     torch.cuda.synchronize()
-    ref, _ = fixed_point_numpy(P, V, baseline_fk(f, phi), 0.3, 0.017, 0, 1e-30, 3)
+    if n <= 2048:
+        ref, _ = fixed_point_numpy(P, V, baseline_fk(f, phi), 0.3, 0.017, 0, 1e-30, 3)
+    else:  # the same restatement with torch.fft on the device (numpy would take minutes)
+        ref, _ = fixed_point_torch(torch.from_numpy(P).cuda(), torch.from_numpy(V).cuda(), torch.from_numpy(f).cuda(),
+                                   phi, 0.3, 0.017, 0, 1e-30, 3)
+        ref = ref.cpu().numpy()
     err = np.abs(res.t.cpu().numpy() - ref).max()
-    print(f"large n=2048: 3 iterations, max|dT| {err:.3e} K on peak {ref.max():.2f} K")
+    print(f"large n={n}: 3 iterations, max|dT| {err:.3e} K on peak {ref.max():.2f} K")
     assert res.iterations == 3 and res.status == slab.GT_SAMPLE_NOCONVERGE == 32
     assert err <= 1e-9 * max(1.0, ref.max())
 
