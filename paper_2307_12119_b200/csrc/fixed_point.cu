@@ -24,6 +24,7 @@
 #include "fft_tile.cuh"
 #include "fft_warp.cuh"
 #include "gt_device.h"
+#include "kirchhoff.cuh"
 
 #ifndef GT_FP_UB
 #define GT_FP_UB 4  // global loads issued ahead per thread in the tile row pass (tuning)
@@ -117,6 +118,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
     cplx<T>* s_tw = tile + M * LP;
     if constexpr (!Gm::GTW) load_twiddles<T, M, NT>(s_tw, g_tw);
     const cplx<T>* tw = Gm::GTW ? g_tw : s_tw;
+    const T kc = kb / ka;  // Kirchhoff inverse (kirchhoff.cuh)
     __syncthreads();
 
     for (int item = blockIdx.x; item < count * RB; item += gridDim.x) {
@@ -218,11 +220,7 @@ fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restri
                                 T th = (half ? z.y : z.x) * inv;  // theta - T0
                                 if (H) th += hv[u][half] * sig_prev;
                                 t = th;
-                                if (kirchhoff) {
-                                    const T br = ka + kb * th;
-                                    if (!(br > T(0))) bad |= GTD_ST_KIRCHHOFF;
-                                    t = pow(br, kexp) - t_ambient;
-                                }
+                                if (kirchhoff) t = kirchhoff_rise(th, kc, kexp, t_ambient, bad);
                                 if (!finite_val(t)) bad |= GTD_ST_NONFINITE;
                                 dmax = fmax(dmax, double(fabs(t - told[u][half])));
                                 const size_t oq = static_cast<size_t>(x + half) * n + j;
@@ -309,6 +307,7 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
     WF::build_tw1(s_tw1, g_tw, threadIdx.x, FPW_WARPS * 32);
     __syncthreads();
     constexpr T inv = T(1.0 / (double(M) * double(M)));
+    const T kc = kb / ka;  // Kirchhoff inverse (kirchhoff.cuh)
 
     for (int item = blockIdx.x * FPW_WARPS + warp; item < count * RP; item += gridDim.x * FPW_WARPS) {
         const int s = item / RP, x0 = 2 * (item - s * RP);
@@ -383,10 +382,8 @@ fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec,
                 const cplx<T> th = scr[j];
                 T a = th.x * inv + h0[t] * sig_prev, b = th.y * inv + h1[t] * sig_prev;  // theta - T0, rows x0, x0+1
                 if (kirchhoff) {
-                    const T ba = ka + kb * a, bb = ka + kb * b;
-                    if (!(ba > T(0)) || !(bb > T(0))) bad |= GTD_ST_KIRCHHOFF;
-                    a = pow(ba, kexp) - t_ambient;
-                    b = pow(bb, kexp) - t_ambient;
+                    a = kirchhoff_rise(a, kc, kexp, t_ambient, bad);
+                    b = kirchhoff_rise(b, kc, kexp, t_ambient, bad);
                 }
                 if (!finite_val(a) || !finite_val(b)) bad |= GTD_ST_NONFINITE;
                 dmax = fmax(dmax, fmax(double(fabs(a - t0[t])), double(fabs(b - t1[t]))));
@@ -484,6 +481,8 @@ struct FPCGeom {
     static constexpr int APLANE = (M + M / 8) * GA;
     static constexpr int TILE = InvLayout<GA, M>::SIZE > APLANE ? InvLayout<GA, M>::SIZE : APLANE;
     static_assert(hp % W == 0, "column tiles");
+    static constexpr size_t SMEM =
+        sizeof(cplx<T>) * (size_t(TILE) + StageTw<M, false>::SIZE + StageTw<M, true>::SIZE + M);
 };
 
 template <typename T, int M, int GA, int NT, int S>
@@ -773,9 +772,7 @@ struct FPLaunch {
         else
             return 0;
     }
-    static size_t smem_cols() {
-        return sizeof(cplx<T>) * (Gc::TILE + StageTw<M, false>::SIZE + StageTw<M, true>::SIZE + M);
-    }
+    static size_t smem_cols() { return Gc::SMEM; }
 
     static int run(const gtd_greens* g, const FPIn<T>& in, int batch, const gtd_fp_opts* o, T* Tst, int* iters,
                    int* status, double* mx, double* mean, void* scratch, FPState* state, int* counter_d,

@@ -30,6 +30,7 @@
 #include "fft_line.cuh"
 #include "fft_tile.cuh"
 #include "gt_device.h"
+#include "kirchhoff.cuh"
 
 namespace gtb {
 namespace {
@@ -400,11 +401,7 @@ struct RinvB {  // group p, line i_a, j = k2: theta -> T, residual, next applied
         for (int half = 0; half < 2; ++half) {
             const size_t o = static_cast<size_t>(2 * p + half) * n + i;
             T t = (half ? v.y : v.x) * inv;
-            if (kirchhoff) {
-                const T br = ka + kb * t;
-                if (!(br > T(0))) bad |= GTD_ST_KIRCHHOFF;
-                t = pow(br, kexp) - t_ambient;
-            }
+            if (kirchhoff) t = kirchhoff_rise(t, kb / ka, kexp, t_ambient, bad);
             if (!isfinite(t)) bad |= GTD_ST_NONFINITE;
             dmax = fmax(dmax, double(fabs(t - q.told[half])));
             if (G) G[o] = t;
@@ -773,11 +770,7 @@ lg_rinv_c2r(const double2* __restrict__ Y, int hy, int rows, const double2* __re
                 if (t >= n) break;
                 const size_t o = static_cast<size_t>(x) * n + t;
                 double tv = th[2 * lpad(t >> 1) + (t & 1)] * op.inv;
-                if (op.kirchhoff) {
-                    const double br = op.ka + op.kb * tv;
-                    if (!(br > 0.0)) r_bad |= GTD_ST_KIRCHHOFF;
-                    tv = pow(br, op.kexp) - op.t_ambient;
-                }
+                if (op.kirchhoff) tv = kirchhoff_rise(tv, op.kb / op.ka, op.kexp, op.t_ambient, r_bad);
                 if (!isfinite(tv)) r_bad |= GTD_ST_NONFINITE;
                 r_dmax = fmax(r_dmax, fabs(tv - told[e]));
                 if (op.G) op.G[o] = tv;
