@@ -6,6 +6,7 @@
 // the resulting tables in its own precision.
 #include <cuda_runtime.h>
 
+#include "launch_once.cuh"
 #include "fft_tile.cuh"
 #include "gt_device.h"
 
@@ -68,14 +69,13 @@ int run_fft2d(void* data, int batch, int sign, const void* tw, cudaStream_t st) 
     constexpr int LL = L < M ? L : M;
     const size_t sm_r = sizeof(cplx<T>) * (M * (L + 2) + M);
     const size_t sm_c = sizeof(cplx<T>) * (M * L + M);
-    static bool init = false;
-    if (!init) {
+    static DeviceOnce once_;
+    once_([&] {
         cudaFuncSetAttribute(fft_rows<T, M, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_r));
         cudaFuncSetAttribute(fft_rows<T, M, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_r));
         cudaFuncSetAttribute(fft_cols<T, M, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_c));
         cudaFuncSetAttribute(fft_cols<T, M, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_c));
-        init = true;
-    }
+    });
     cplx<T>* X = static_cast<cplx<T>*>(data);
     const cplx<T>* w = static_cast<const cplx<T>*>(tw);
     const int rows = batch * M;

@@ -20,6 +20,7 @@
 //   fp_update: per-sample iteration count / convergence / failure state.
 #include <cuda_runtime.h>
 
+#include "launch_once.cuh"
 #include "col_pass.cuh"
 #include "fft_tile.cuh"
 #include "fft_warp.cuh"
@@ -780,7 +781,8 @@ struct FPLaunch {
         constexpr int n = Gm::n, hp = Gm::hp, NT = Gm::NT;
         constexpr int RP = n / 2;
         static int res[3] = {0, 0, 0}, sms = 0;
-        if (!sms) {
+        static DeviceOnce once_;
+        once_([&] {
             cudaFuncSetAttribute(fp_rows<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
             cudaFuncSetAttribute(fp_rows<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
             cudaFuncSetAttribute(fp_cols_d<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cols()));
@@ -798,7 +800,7 @@ struct FPLaunch {
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             for (int& r : res) r = r < 1 ? 1 : r;
-        }
+        });
         const size_t per = static_cast<size_t>(n) * hp;
         cplx<T>* A = static_cast<cplx<T>*>(scratch);             // Y: column pass -> row pass
         T* Ar = reinterpret_cast<T*>(A + per * chunk);           // real DCT rows: row pass -> column pass

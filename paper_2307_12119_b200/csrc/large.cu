@@ -27,6 +27,7 @@
 #define GT_LG_RINV_NT 1024
 #endif
 
+#include "launch_once.cuh"
 #include "fft_line.cuh"
 #include "fft_tile.cuh"
 #include "gt_device.h"
@@ -657,14 +658,15 @@ template <int N>
 int launch_colb64_n(const ColB<double>& b, const double2* tw, int M, int groups, int blocks, cudaStream_t st) {
     const size_t smem = lg_smem<double, N>();
     static int res = 0, sms = 0;  // per N: each instantiation sets its own shared-memory attribute
-    if (!sms) {
+    static DeviceOnce once_;
+    once_([&] {
         cudaFuncSetAttribute(lg_colb64<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_colb64<N>, TileGeom<double, N>::NT, smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         res = res < 1 ? 1 : res;
-    }
+    });
     const int items = groups * blocks;
     const int grid = items < sms * res ? items : sms * res;
     if (grid > 0) lg_colb64<N><<<grid, TileGeom<double, N>::NT, smem, st>>>(b, tw, M, groups, blocks);
@@ -685,14 +687,15 @@ template <typename T, int N, class Op, bool TWO>
 int launch_n(const Op& op, const double2* tw, int M, int groups, int nlines, cudaStream_t st) {
     static int res = 0, sms = 0;
     auto k = lg_pass<T, N, Op, TWO>;
-    if (!sms) {
+    static DeviceOnce once_;
+    once_([&] {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lg_smem<T, N>()));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k, TileGeom<T, N>::NT, lg_smem<T, N>());
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         res = res < 1 ? 1 : res;
-    }
+    });
     const int items = groups * ((nlines + TileGeom<T, N>::L - 1) / TileGeom<T, N>::L);
     const int grid = items < sms * res ? items : sms * res;
     if (grid > 0) k<<<grid, TileGeom<T, N>::NT, lg_smem<T, N>(), st>>>(op, tw, M, groups, nlines);
@@ -851,14 +854,15 @@ int rows_fwd_dct_n(const gtd_lg* g, const double* app, int pairs, const void* hs
     constexpr int NT = N / 8 < GT_LG_RINV_NT ? N / 8 : GT_LG_RINV_NT;
     constexpr size_t smem = sizeof(double2) * (N + N / 8);
     static int res = 0, sms = 0;
-    if (!sms) {
+    static DeviceOnce once_;
+    once_([&] {
         cudaFuncSetAttribute(lg_rfwd_dct<NT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_rfwd_dct<NT, N>, NT, smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         res = res < 1 ? 1 : res;
-    }
+    });
     const int grid = pairs < sms * res ? pairs : sms * res;
     lg_rfwd_dct<NT, N><<<grid, NT, smem, st>>>(app, pairs, static_cast<const double2*>(g->tw),
                                               static_cast<const double2*>(hs), static_cast<double*>(Z), g->m);
@@ -887,14 +891,15 @@ int rows_inv_c2r_n(const gtd_lg* g, const void* Y, int hy, int pairs, const Rinv
     constexpr int NT = N / 8 < GT_LG_RINV_NT ? N / 8 : GT_LG_RINV_NT;  // one radix-8 butterfly per thread
     constexpr size_t smem = sizeof(double2) * (N + N / 8);
     static int res = 0, sms = 0;
-    if (!sms) {
+    static DeviceOnce once_;
+    once_([&] {
         cudaFuncSetAttribute(lg_rinv_c2r<NT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, lg_rinv_c2r<NT, N>, NT, smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         res = res < 1 ? 1 : res;
-    }
+    });
     const int rows = 2 * pairs;
     const int grid = rows < sms * res ? rows : sms * res;
     lg_rinv_c2r<NT, N><<<grid, NT, smem, st>>>(static_cast<const double2*>(Y), hy, rows,

@@ -26,6 +26,7 @@
 // analytic spectrum of the centred die box, so pass 1 never waits for mu.
 #include <type_traits>
 
+#include "launch_once.cuh"
 #include "mc_common.cuh"
 
 #ifndef GT_P2_ABL
@@ -582,13 +583,15 @@ struct MCLaunch {
                    gtd_mark_fn mark, void* ctx) {
         constexpr int n = Gm::n, hp = Gm::hp, W = Gm::W;
         constexpr int CT = hp / W;
-        // Kernel attributes and resident CTAs per SM, set up once per (T, M) (a function-local
-        // static: thread-safe initialisation; every device of a node is the same sm_100a part).
+        // Kernel attributes and resident CTAs per SM, set up once per (T, M) and device
+        // (launch_once.cuh; every device of a node is the same sm_100a part).
         struct Occ {
             int res[3];
             int sms;
         };
-        static const Occ occ = [] {
+        static Occ occ{{1, 1, 1}, 1};
+        static DeviceOnce once_;
+        once_([] { occ = [] {
             Occ r{{0, 0, 0}, 0};
             r.res[0] = mc_rows_setup<T, M>(1);
             r.res[2] = mc_rows_setup<T, M>(3);
@@ -603,7 +606,7 @@ struct MCLaunch {
             cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, dev);
             for (int& x : r.res) x = x < 1 ? 1 : x;
             return r;
-        }();
+        }(); });
         const int* res = occ.res;
         const int sms = occ.sms;
         const size_t per = static_cast<size_t>(n) * hp;

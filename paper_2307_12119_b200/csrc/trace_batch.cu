@@ -24,6 +24,7 @@
 
 #include <cstdint>
 
+#include "launch_once.cuh"
 #include "col_pass.cuh"
 #include "fft_tile.cuh"
 #include "fft_warp.cuh"
@@ -575,7 +576,8 @@ struct TRLaunch {
                    void* t_out, double* max_out, void* scratch, int chunk, cudaStream_t st, long long* launches) {
         constexpr int n = Gm::n, hp = Gm::hp;
         static int res[3] = {0, 0, 0}, sms = 0;
-        if (!sms) {
+        static DeviceOnce once_;
+        once_([&] {
             cudaFuncSetAttribute(tr_rows_fwd<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rf()));
             cudaFuncSetAttribute(tr_rows_inv<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_ri()));
             cudaFuncSetAttribute(tr_cols<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_c()));
@@ -595,7 +597,7 @@ struct TRLaunch {
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             for (int& r : res) r = r < 1 ? 1 : r;
-        }
+        });
         const int k = o->window, steps = ti->steps, os = o->out_stride;
         const int nframes = steps / os;
         const size_t nn = size_t(n) * n;

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 
+#include "launch_once.cuh"
 #include "fft_tile.cuh"
 #include "fft_warp.cuh"
 #include "gt_device.h"
@@ -178,7 +179,8 @@ struct VGLaunch {
     static int run(const gtd_greens* g, const void* sqlam, int hp, const unsigned long long* seeds, int batch,
                    double sigma, void* var, long long vstride, void* scratch, int chunk, cudaStream_t st) {
         static int res[2] = {0, 0}, sms = 0;
-        if (!sms) {
+        static DeviceOnce once_;
+        once_([&] {
             cudaFuncSetAttribute(vg_cols<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_c()));
             cudaFuncSetAttribute(vg_rows<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_r()));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], vg_cols<T, M>, TileGeom<T, M>::NT, smem_c());
@@ -187,7 +189,7 @@ struct VGLaunch {
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             for (int& r : res) r = r < 1 ? 1 : r;
-        }
+        });
         constexpr int n = M / 2, L = TileGeom<T, M>::L, CT = (n + 1 + L - 1) / L;
         auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         const cplx<T>* tw = static_cast<const cplx<T>*>(g->tw);
