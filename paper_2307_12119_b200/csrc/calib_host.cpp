@@ -15,6 +15,8 @@
 #include <random>
 #include <thread>
 #include <atomic>
+#include <mutex>
+#include <utility>
 
 #include "devctx.hpp"
 #include "gt_ops.h"
@@ -94,21 +96,42 @@ struct VarDevice {
         sys.ensure(nn * 8);
     }
     // out = sigma_sys * shaped(sys_noise) + rnd_noise (either part may be absent). With
-    // sync = false the host noise vectors must stay alive until the stream reaches this work.
+    // sync = false the host noise buffers must stay alive until the stream reaches this work.
     void field(const VarParams& v, const std::vector<double>& sysn, const std::vector<double>& rndn, double* out,
                bool sync = true) {
+        field(v, sysn.empty() ? nullptr : sysn.data(), rndn.empty() ? nullptr : rndn.data(), out, sync);
+    }
+    void field(const VarParams& v, const double* sysn, const double* rndn, double* out, bool sync) {
         cudaStream_t st = stream;
         cuda_ok(cudaMemsetAsync(out, 0, nn * 8, st), "memset");
-        if (!sysn.empty()) {
-            cuda_ok(cudaMemcpyAsync(noise.p, sysn.data(), mm * 8, cudaMemcpyHostToDevice, st), "h2d");
+        if (sysn) {
+            cuda_ok(cudaMemcpyAsync(noise.p, sysn, mm * 8, cudaMemcpyHostToDevice, st), "h2d");
             cuda_ok(gtd_var_shape(noise.as<double>(), sqrt_lam.as<double>(), n, v.sigma_sys, tw64, work.p, out, st),
                     "shape");
         }
-        if (!rndn.empty()) {
-            cuda_ok(cudaMemcpyAsync(sys.p, rndn.data(), nn * 8, cudaMemcpyHostToDevice, st), "h2d");
+        if (rndn) {
+            cuda_ok(cudaMemcpyAsync(sys.p, rndn, nn * 8, cudaMemcpyHostToDevice, st), "h2d");
             cuda_ok(gtd_add_maps(out, sys.as<double>(), nn, out, st), "add");
         }
         if (sync) cuda_ok(cudaStreamSynchronize(st), "sync");  // host noise buffers are reused by the caller
+    }
+};
+
+// Pinned host slab for the Monte-Carlo noise ring (kept for the life of the process: a
+// second gt_monte_carlo call does not pay the page-locking again).
+struct PinnedSlab {
+    double* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t doubles) {
+        if (doubles <= cap) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cuda_ok(cudaMallocHost(reinterpret_cast<void**>(&p), doubles * 8), "cudaMallocHost (noise ring)");
+        cap = doubles;
+    }
+    ~PinnedSlab() {
+        if (p) cudaFreeHost(p);
     }
 };
 
@@ -767,13 +790,19 @@ void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nomina
                  "deterministic_greens: spectral denominator collapsed below 1e-6 (leakage feedback gain reached unity)");
     }
     // Seeds stream through in chunks (the reference runs them one per worker thread with
-    // per-thread memory, solver.cpp:376-387): per chunk, the libstdc++ noise of the next
-    // chunk is drawn on `jobs` host threads while the device shapes this chunk's maps
-    // (exp(beta_L dL + beta_tox dTox), variation.cpp:162-195) and runs the fused mode-A
-    // passes on them; one stream synchronisation per chunk, none per seed.
-    const size_t per_seed_host = (v.sigma_sys != 0.0 ? 2 * 4 * nn : 0) + (v.sigma_rand != 0.0 ? 2 * nn : 0);
-    int chunk = std::max(1, std::min(256, static_cast<int>((512ull << 20) / std::max<size_t>(1, per_seed_host * 8))));
+    // per-thread memory, solver.cpp:376-387). The libstdc++ noise of chunk k + 1 is drawn on
+    // `jobs` host threads (one work item per (seed, noise stream), largest first) into a
+    // pinned ring while the device shapes chunk k's maps (exp(beta_L dL + beta_tox dTox),
+    // variation.cpp:162-195) and runs the fused mode-A passes on them; one stream
+    // synchronisation per chunk, none per seed. The chunk is sized so the two ring halves
+    // stay within 256 MB of pinned memory (small chunks also keep the un-overlapped first
+    // draw short).
+    const bool has_sys = v.sigma_sys != 0.0, has_rnd = v.sigma_rand != 0.0;
+    const size_t mm = 4 * nn;
+    const size_t per_seed_host = (has_sys ? 2 * mm : 0) + (has_rnd ? 2 * nn : 0);  // doubles
+    int chunk = static_cast<int>(std::min<size_t>(64, std::max<size_t>(1, (128ull << 20) / std::max<size_t>(1, per_seed_host * 8))));
     if (const char* e = getenv("GT_MC_SEED_CHUNK")) chunk = std::max(1, atoi(e));  // tests: force several chunks
+    chunk = std::min(chunk, B);
     DBuf V, dl, dtox, P, N, flags, stats, scratch;
     V.ensure(nn * 8 * chunk);
     dl.ensure(nn * 8);
@@ -787,29 +816,60 @@ void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nomina
     std::vector<gtd_sample_stats> hs(B);
     VarDevice vd(d.get(), v, g.pitch);
     const int nj = std::max(1, jobs);
-    auto draw = [&](std::vector<LeakNoise>& buf, int s0, int cnt) {
-        buf.assign(cnt, LeakNoise{});
-        std::atomic<int> next{0};
+    // noise ring: a process-wide pinned slab when free, a private one for a concurrent call
+    static PinnedSlab shared_ring;
+    static std::mutex ring_mu;
+    std::unique_lock<std::mutex> ring_lock(ring_mu, std::try_to_lock);
+    PinnedSlab own_ring;
+    PinnedSlab& ring = ring_lock.owns_lock() ? shared_ring : own_ring;
+    const size_t half = per_seed_host * chunk;
+    ring.ensure(std::max<size_t>(1, 2 * half));
+    // seed i of a half: [sys_l | sys_t | rnd_l | rnd_t]
+    auto slot = [&](int hsel, int i, int which) -> double* {
+        if ((which < 2 && !has_sys) || (which >= 2 && !has_rnd)) return nullptr;
+        double* base = ring.p + static_cast<size_t>(hsel) * half + static_cast<size_t>(i) * per_seed_host;
+        if (which < 2) return base + which * mm;
+        return base + (has_sys ? 2 * mm : 0) + (which - 2) * nn;
+    };
+    static const uint64_t purpose[4] = {GL_SYS, OX_SYS, GL_RAND, OX_RAND};
+    auto draw = [&](int hsel, int s0, int cnt) {
+        // items: the m^2 systematic streams first (4x the draws of an n^2 random stream)
+        std::vector<std::pair<int, int>> items;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i < cnt; ++i)
+                for (int w = 2 * pass; w < 2 * pass + 2; ++w)
+                    if (slot(hsel, i, w)) items.emplace_back(i, w);
+        std::atomic<size_t> next{0};
         std::vector<std::thread> pool;
-        for (int w = 0; w < std::min(nj, cnt); ++w)
+        const int nt = static_cast<int>(std::min<size_t>(nj, items.size()));
+        for (int w = 0; w < nt; ++w)
             pool.emplace_back([&] {
-                for (int i = next.fetch_add(1); i < cnt; i = next.fetch_add(1)) {
-                    VarParams vs = v;
-                    vs.seed = seeds[s0 + i];
-                    buf[i] = leak_noise(vs, n, vs.seed, 0);
+                for (size_t k = next.fetch_add(1); k < items.size(); k = next.fetch_add(1)) {
+                    const int i = items[k].first, which = items[k].second;
+                    draw_normals(derived_seed(seeds[s0 + i], purpose[which], 0), which < 2 ? 1.0 : v.sigma_rand,
+                                 which < 2 ? mm : nn, slot(hsel, i, which));
                 }
             });
         for (auto& th : pool) th.join();
     };
-    std::vector<LeakNoise> cur, nxt;
     std::vector<int> hflags(chunk);
-    draw(cur, 0, std::min(chunk, B));
-    for (int s0 = 0; s0 < B; s0 += chunk) {
+    draw(0, 0, std::min(chunk, B));
+    int hsel = 0;
+    for (int s0 = 0; s0 < B; s0 += chunk, hsel ^= 1) {
         const int cnt = std::min(chunk, B - s0);
+        // the next chunk's draws start now, on their own threads, while this thread feeds the device
+        std::thread drawer;
+        if (s0 + cnt < B) drawer = std::thread(draw, hsel ^ 1, s0 + cnt, std::min(chunk, B - s0 - cnt));
+        struct Joiner {
+            std::thread& t;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+            }
+        } joiner{drawer};
         cuda_ok(cudaMemsetAsync(flags.p, 0, sizeof(int) * cnt, st), "memset");
         for (int i = 0; i < cnt; ++i) {
-            vd.field(v, cur[i].sys_l, cur[i].rnd_l, dl.as<double>(), false);
-            vd.field(v, cur[i].sys_t, cur[i].rnd_t, dtox.as<double>(), false);
+            vd.field(v, slot(hsel, i, 0), slot(hsel, i, 2), dl.as<double>(), false);
+            vd.field(v, slot(hsel, i, 1), slot(hsel, i, 3), dtox.as<double>(), false);
             cuda_ok(gtd_leak_exp(nullptr, dl.as<double>(), dtox.as<double>(), v.beta_l, v.beta_tox, v.exponent_cap, n,
                                  V.as<double>() + i * nn, flags.as<int>() + i, st),
                     "leakage exponent");
@@ -830,11 +890,9 @@ void gt_ops_monte_carlo(const Greens& g, const VarParams& v, const Field& nomina
         cuda_ok(gtd_mc_batch(&d->d, &in, cnt, &o, nullptr, stats.as<gtd_sample_stats>(), scratch.p, cnt, st, nullptr,
                              nullptr),
                 "mc batch");
-        if (s0 + cnt < B) draw(nxt, s0 + cnt, std::min(chunk, B - s0 - cnt));  // host, while the device runs
-        d2h(hs.data() + s0, stats.p, sizeof(gtd_sample_stats) * cnt, st);  // synchronises: cur is free again
+        d2h(hs.data() + s0, stats.p, sizeof(gtd_sample_stats) * cnt, st);  // synchronises: this ring half is free again
         d2h(hflags.data(), flags.p, sizeof(int) * cnt, st);
         for (int i = 0; i < cnt; ++i) capfail[s0 + i] = hflags[i];
-        std::swap(cur, nxt);
     }
     const double per_ms = std::chrono::duration<double, std::milli>(wall::now() - t0).count() / B;
 
