@@ -929,9 +929,22 @@ void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int b
     o.warm_start = warm;
     o.H = H;
     o.sH = static_cast<long long>(n) * n;
-    o.accel = opts->accel > 0 ? opts->accel : 0;
+    o.accel = opts->accel;
     o.Tprev = o.Yout = nullptr;
-    if (o.accel) {
+    o.lm_state = nullptr;
+    o.lm_cos = nullptr;
+    if (o.accel < 0) {
+        if (o.accel < -4) fail(ST_CONFIG, "oracle", "accel < 0 selects Anderson(m) on the low modes, m = -accel <= 4");
+        d->fp_lm.ensure(gtd_fp_lowmode_bytes() * batch);
+        const size_t cb = sizeof(double) * 16 * n;
+        if (d->fp_lmcos.bytes < cb) {
+            d->fp_lmcos.ensure(cb);
+            cuda_ok(gtd_fp_lowmode_cos(n, d->fp_lmcos.as<double>(), st), "low-mode cosine table");
+        }
+        o.lm_state = d->fp_lm.p;
+        o.lm_cos = d->fp_lmcos.as<double>();
+    }
+    if (o.accel > 0) {
         d->fp_tprev.ensure(static_cast<size_t>(n) * n * batch * (d->fp64 ? 8 : 4));
         d->fp_yout.ensure(static_cast<size_t>(n) * n * batch * (d->fp64 ? 8 : 4));
         o.Tprev = d->fp_tprev.p;

@@ -60,6 +60,7 @@ struct gt_device_greens {
     gth::DBuf fin_p, fin_v, fin_t, fin_it, fin_st, fin_h;  // fp64 finish stage of an fp32 fixed point
     gth::DBuf fp_h, fp_hstats;  // shift-variant maps of the combined config-2 fixed point
     gth::DBuf fp_tprev, fp_yout;  // x_{k-1} and G(x_k) of the Chebyshev-accelerated fixed point
+    gth::DBuf fp_lm, fp_lmcos;    // low-mode Anderson state and its cosine table (accel < 0)
     gth::DBuf trace_scratch, trace_tab;
     gth::DBuf var_sqlam, var_scratch, slot_seeds[2];  // seeded variation model (gt_var_model)
     double var_sigma = 0.0;

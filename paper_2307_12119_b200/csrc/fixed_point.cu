@@ -684,6 +684,7 @@ __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int
     iters[sample0 + i] = s.iters;
     const double res = __longlong_as_double(static_cast<long long>(s.res_bits));
     s.res_bits = 0ull;
+    if (accel < 0) s.res_prev = res;
     if (accel > 0) {
         if (s.omega > 0.0) {
             if (res > 2.0 * s.res_prev) {
@@ -709,6 +710,220 @@ __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int
         s.active = 0;
     }
     if (s.active) atomicAdd(active_count, 1);
+}
+
+
+// ---------------------------------------------------------------- low-mode Anderson mixing
+// gtd_fp_opts.accel = -m: Anderson(m) acceleration of the Picard map restricted to the
+// LMK x LMK lowest cosine modes of the die field (the leakage feedback operator beta G diag(L0)
+// is a smoothing operator: its slow eigenvectors are smooth, everything else contracts in a few
+// plain iterations). It runs between the column pass and the row pass on the row spectra Y:
+//   a_pq   = low cosine coefficients of G(x_k), read from Y[x][q], q < LMK (a mirrored row with
+//            cosine content d_q has Y[q] = conj(hs_q) M^2 eps_q d_q, eps_0 = 1, eps_q = 1/2),
+//   f      = a - xlow  (xlow: the same coefficients of x_k, known by construction),
+//   gamma  = argmin |f - dF gamma| over the last m residual differences (Tikhonov-regularised
+//            normal equations in fp64), corr = -dG gamma,
+//   Y[x][q] += conj(hs_q) M^2 eps_q sum_p corr_pq cos(pi p (x + 1/2) / n):  x_{k+1} = G(x_k) + corr.
+// The fixed point is unchanged (corr -> 0 with f); the reference stop rule then applies to
+// max|x_{k+1} - x_k|. State per sample: LMState (gtd_fp_lowmode_bytes()).
+constexpr int LMK = 16, LMN = LMK * LMK, LMD = 4;
+struct LMState {
+    int calls;      // fp_lowmode calls on this sample so far
+    int nd;         // residual differences pushed so far
+    int have_x;     // xlow valid (cold start: x_0 = 0; warm start: from the second call on)
+    int have_prev;  // gprev / fprev valid
+    double rprev;   // Picard residual seen at the previous call (growth guard)
+    double xlow[LMN], gprev[LMN], fprev[LMN];
+    double dG[LMD][LMN], dF[LMD][LMN];
+};
+
+__global__ void fp_lowmode_init(LMState* lms, int sample0, int count, int warm) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count * LMN) return;
+    LMState& L = lms[sample0 + i / LMN];
+    const int t = i % LMN;
+    L.xlow[t] = 0.0;
+    if (t == 0) {
+        L.calls = 0;
+        L.nd = 0;
+        L.have_x = warm ? 0 : 1;
+        L.have_prev = 0;
+        L.rprev = 0.0;
+    }
+}
+
+__global__ void k_lowmode_cos(int n, double* table) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= LMK * n) return;
+    const int p = i / n, x = i - p * n;
+    table[i] = cospi(double(p) * (2.0 * x + 1.0) / (2.0 * n));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LMN)
+fp_lowmode(cplx<T>* __restrict__ Y, int n, int hp, int sample0, const FPState* __restrict__ state,
+           LMState* __restrict__ lms, const cplx<T>* __restrict__ g_hs, const double* __restrict__ costab, int depth) {
+    const int s = blockIdx.x;
+    const size_t sg = static_cast<size_t>(sample0) + s;
+    if (!state[sg].active) return;
+    LMState& L = lms[sg];
+    const int tid = threadIdx.x, p = tid / LMK, q = tid % LMK;
+    const double M = 2.0 * n;
+    cplx<T>* Ys = Y + static_cast<size_t>(s) * n * hp;
+    const cplx<T> hq = g_hs[q];
+    const double eq = q == 0 ? 1.0 : 0.5, ep = p == 0 ? 1.0 : 0.5;
+    // 1. projection of G(x_k) on mode (p, q)
+    double acc = 0.0;
+    {
+        const double* cp = costab + static_cast<size_t>(p) * n;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int x = 0; x < n; x += 4) {  // n: a power of two >= 16
+            const cplx<T> y0 = Ys[static_cast<size_t>(x) * hp + q], y1 = Ys[static_cast<size_t>(x + 1) * hp + q];
+            const cplx<T> y2 = Ys[static_cast<size_t>(x + 2) * hp + q], y3 = Ys[static_cast<size_t>(x + 3) * hp + q];
+            a0 += (double(hq.x) * y0.x - double(hq.y) * y0.y) * cp[x];
+            a1 += (double(hq.x) * y1.x - double(hq.y) * y1.y) * cp[x + 1];
+            a2 += (double(hq.x) * y2.x - double(hq.y) * y2.y) * cp[x + 2];
+            a3 += (double(hq.x) * y3.x - double(hq.y) * y3.y) * cp[x + 3];
+        }
+        acc = (a0 + a1) + (a2 + a3);
+    }
+    const double g = acc / (M * M * eq * double(n) * ep);
+    // 2. Anderson step on the LMN coefficients
+    __shared__ double red[LMD * (LMD + 1) / 2 + LMD][LMN / 32];
+    __shared__ double s_gamma[LMD];
+    __shared__ double s_corr[LMN];
+    __shared__ int s_k;
+    const int calls = L.calls, have_x = L.have_x, have_prev = L.have_prev;
+    int nd = L.nd;
+    // growth guard: a Picard residual that doubled since the last call drops the history
+    const double rnow = state[sg].res_prev, rprev = L.rprev;
+    const bool reset = calls > 1 && rprev > 0.0 && rnow > 2.0 * rprev;
+    if (reset) nd = 0;
+    __syncthreads();  // every thread has read the header before thread 0 rewrites it
+    const double f = g - L.xlow[tid];
+    if (have_x && have_prev && !reset) {
+        const int slot = nd % depth;
+        L.dG[slot][tid] = g - L.gprev[tid];
+        L.dF[slot][tid] = f - L.fprev[tid];
+        nd += 1;
+    }
+    L.gprev[tid] = g;
+    L.fprev[tid] = f;
+    const int k = have_x ? (nd < depth ? nd : depth) : 0;
+    double corr = 0.0;
+    if (k > 0) {
+        double df[LMD], dg[LMD];
+#pragma unroll
+        for (int i = 0; i < LMD; ++i) {
+            df[i] = i < k ? L.dF[i][tid] : 0.0;
+            dg[i] = i < k ? L.dG[i][tid] : 0.0;
+        }
+        // Gram entries (upper triangle) and right-hand side
+        int e = 0;
+#pragma unroll
+        for (int i = 0; i < LMD; ++i) {
+#pragma unroll
+            for (int j = i; j < LMD; ++j) {
+                const double v = warp_sum_d(df[i] * df[j]);
+                if ((tid & 31) == 0) red[e][tid >> 5] = v;
+                ++e;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < LMD; ++i) {
+            const double v = warp_sum_d(df[i] * f);
+            if ((tid & 31) == 0) red[e][tid >> 5] = v;
+            ++e;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double A[LMD][LMD], b[LMD];
+            int e2 = 0;
+            for (int i = 0; i < LMD; ++i)
+                for (int j = i; j < LMD; ++j) {
+                    double v = 0.0;
+                    for (int w = 0; w < LMN / 32; ++w) v += red[e2][w];
+                    A[i][j] = A[j][i] = v;
+                    ++e2;
+                }
+            for (int i = 0; i < LMD; ++i) {
+                double v = 0.0;
+                for (int w = 0; w < LMN / 32; ++w) v += red[e2][w];
+                b[i] = v;
+                ++e2;
+            }
+            double tr = 0.0;
+            for (int i = 0; i < k; ++i) tr += A[i][i];
+            const double lam = 1e-10 * tr;
+            for (int i = 0; i < k; ++i) A[i][i] += lam;
+            // Gaussian elimination with partial pivoting on the k x k system
+            int ok = tr > 0.0;
+            double gm[LMD] = {0.0, 0.0, 0.0, 0.0};
+            if (ok) {
+                int perm[LMD] = {0, 1, 2, 3};
+                for (int c = 0; c < k && ok; ++c) {
+                    int piv = c;
+                    for (int r = c + 1; r < k; ++r)
+                        if (fabs(A[perm[r]][c]) > fabs(A[perm[piv]][c])) piv = r;
+                    const int tmp = perm[c];
+                    perm[c] = perm[piv];
+                    perm[piv] = tmp;
+                    const double d = A[perm[c]][c];
+                    if (!(fabs(d) > 1e-300)) {
+                        ok = 0;
+                        break;
+                    }
+                    for (int r = c + 1; r < k; ++r) {
+                        const double m_ = A[perm[r]][c] / d;
+                        for (int cc = c; cc < k; ++cc) A[perm[r]][cc] -= m_ * A[perm[c]][cc];
+                        b[perm[r]] -= m_ * b[perm[c]];
+                    }
+                }
+                if (ok)
+                    for (int c = k - 1; c >= 0; --c) {
+                        double v = b[perm[c]];
+                        for (int cc = c + 1; cc < k; ++cc) v -= A[perm[c]][cc] * gm[cc];
+                        gm[c] = v / A[perm[c]][c];
+                    }
+                for (int i = 0; i < k; ++i)
+                    if (!isfinite(gm[i]) || fabs(gm[i]) > 1e3) ok = 0;
+            }
+            for (int i = 0; i < LMD; ++i) s_gamma[i] = ok ? gm[i] : 0.0;
+            s_k = ok;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < LMD; ++i) corr -= s_gamma[i] * dg[i];
+        if (!s_k) nd = 0;  // unusable history: start over from plain iterations
+    }
+    if (!isfinite(corr)) corr = 0.0;
+    L.xlow[tid] = g + corr;
+    s_corr[tid] = corr;
+    if (tid == 0) {
+        L.calls = calls + 1;
+        L.nd = nd;
+        L.have_prev = have_x;
+        L.have_x = 1;
+        L.rprev = rnow;
+    }
+    __syncthreads();
+    // 3. the correction's row spectra into Y (columns q < LMK of every die row)
+    if (k > 0) {
+        double cq[LMK];
+#pragma unroll
+        for (int pp = 0; pp < LMK; ++pp) cq[pp] = s_corr[pp * LMK + q];
+        const double sc = M * M * eq;
+        for (int x = p; x < n; x += LMK) {
+            double v = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < LMK; ++pp) v += cq[pp] * costab[static_cast<size_t>(pp) * n + x];
+            v *= sc;
+            cplx<T> y = Ys[static_cast<size_t>(x) * hp + q];
+            y.x += T(v * double(hq.x));   // conj(hs_q) v
+            y.y -= T(v * double(hq.y));
+            Ys[static_cast<size_t>(x) * hp + q] = y;
+        }
+    }
 }
 
 // per-sample max / mean of the converged maps
@@ -843,10 +1058,21 @@ struct FPLaunch {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
             const int gc = grid(cnt * Gc::CT, res[1]);
             fp_init<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt);
+            const bool lowmode = o->accel < 0 && o->lm_state && o->lm_cos && n >= LMK;
+            if (lowmode) {
+                fp_lowmode_init<<<(cnt * LMN + 255) / 256, 256, 0, st>>>(static_cast<LMState*>(o->lm_state), s0, cnt,
+                                                                         o->warm_start);
+                k += 1;
+            }
             rows(true, s0, cnt, 0);
             k += 2;
             for (int it = 1; it <= o->max_iters; ++it) {
                 fp_cols_d<T, M><<<gc, Gc::NT, smem_cols(), st>>>(s0, cnt, Ar, A, state, tw, hs, fk, g->hp);
+                if (lowmode) {
+                    fp_lowmode<T><<<cnt, LMN, 0, st>>>(A, n, hp, s0, state, static_cast<LMState*>(o->lm_state), hs,
+                                                       o->lm_cos, -o->accel);
+                    k += 1;
+                }
                 rows(false, s0, cnt, it);
                 cudaMemsetAsync(counter_d, 0, sizeof(int), st);
                 fp_update<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt, o->tol, o->max_iters,
@@ -941,6 +1167,11 @@ size_t gtd_fp_scratch_bytes_per_sample(int n, int fp64) {
 }
 
 size_t gtd_fp_state_bytes(void) { return sizeof(FPState); }
+size_t gtd_fp_lowmode_bytes(void) { return sizeof(LMState); }
+int gtd_fp_lowmode_cos(int n, double* table, cudaStream_t st) {
+    k_lowmode_cos<<<(LMK * n + 255) / 256, 256, 0, st>>>(n, table);
+    return static_cast<int>(cudaGetLastError());
+}
 
 int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st) {
     k_widen<<<1184, 256, 0, st>>>(src, dst, count);

@@ -177,7 +177,13 @@ typedef struct gtd_fp_opts {
                          from iteration k0 on, rho from the residual ratio there              */
     void* Tprev;      /* [B][n][n] x_{k-1} state of the acceleration (required if accel)   */
     void* Yout;       /* [B][n][n] G(x_k) of the last iteration: the result (required if accel) */
+    void* lm_state;   /* accel = -m < 0: Anderson(m <= 4) mixing on the 16 x 16 lowest cosine modes
+                         (fp_lowmode); [B] x gtd_fp_lowmode_bytes() of state, and lm_cos a
+                         [16][n] double table cos(pi p (x + 1/2) / n) (gtd_fp_lowmode_cos)      */
+    const double* lm_cos;
 } gtd_fp_opts;
+size_t gtd_fp_lowmode_bytes(void);
+int gtd_fp_lowmode_cos(int n, double* table, cudaStream_t st);
 /* fp32 <-> fp64 copies of device maps (fp64 finish stage of an fp32 fixed point). */
 int gtd_widen(const float* src, double* dst, size_t count, cudaStream_t st);
 int gtd_narrow(const double* src, float* dst, size_t count, cudaStream_t st);

@@ -196,6 +196,77 @@ class _Accel:
         self.res_prev = res
 
 
+class _LowMode:
+    """Anderson(m) mixing on the K x K lowest cosine modes of the die field (opts.accel = -m;
+    the batched path's fp_lowmode kernel, fixed_point.cu), applied to the row buffer Y between
+    the column phase and the inverse row phase. A mirrored row with cosine content d_q has
+    Y[q] = conj(hs_q) M^2 eps_q d_q (hs_q = exp(-i pi q / m), eps_0 = 1, eps_q = 1/2), so the
+    coefficients are a_pq = sum_x cos(pi p (x + 1/2) / n) Re(hs_q Y[x][q]) / (M^2 eps_q n eps_p)
+    -- partial sums over this rank's rows, all-reduced (256 doubles) -- and the correction is
+    added back to the same 16 columns. The 256-dimensional least squares runs on the host."""
+    K = 16
+
+    def __init__(self, depth, n, rows, row0, dev, world):
+        import numpy as np
+        import torch
+        self.depth, self.n, self.world = depth, n, world
+        K, m = self.K, 2 * n
+        q = torch.arange(K, device=dev, dtype=torch.float64)
+        x = torch.arange(row0, row0 + rows, device=dev, dtype=torch.float64)
+        self.cos = torch.cos(torch.pi * q[:, None] * (x[None, :] + 0.5) / n).contiguous()  # [K(p)][rows]
+        self.hs = torch.polar(torch.ones_like(q), -torch.pi * q / m)                        # [K] exp(-i pi q / m)
+        eps = torch.full((K,), 0.5, dtype=torch.float64, device=dev)
+        eps[0] = 1.0
+        self.scale_q = (float(m) * float(m)) * eps                                         # [K(q)]
+        self.norm = 1.0 / (self.scale_q[None, :] * (n * eps)[:, None])                     # [K(p)][K(q)]
+        self.xlow = np.zeros(K * K)
+        self.gprev = self.fprev = None
+        self.dG, self.dF = [], []
+        self.calls, self.rprev = 0, 0.0
+
+    def step(self, y, res_prev):
+        """y: this rank's row buffer [rows][hy] complex128, corrected in place; res_prev: the
+        residual of the previous iteration (growth guard)."""
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        K = self.K
+        d = (self.hs[None, :] * y[:, :K]).real                      # [rows][K(q)]
+        a = (self.cos @ d) * self.norm                              # [K(p)][K(q)]
+        if self.world > 1:
+            if dist.get_backend() != "nccl":
+                a = a.cpu()
+            dist.all_reduce(a)
+        g = a.detach().cpu().numpy().reshape(-1).copy()
+        if self.calls > 1 and self.rprev > 0.0 and res_prev > 2.0 * self.rprev:
+            self.dG, self.dF = [], []                               # residual doubled: drop the history
+            self.gprev = None
+        f = g - self.xlow
+        if self.gprev is not None:
+            self.dG.append(g - self.gprev)
+            self.dF.append(f - self.fprev)
+            self.dG, self.dF = self.dG[-self.depth:], self.dF[-self.depth:]
+        self.gprev, self.fprev = g, f
+        corr = np.zeros_like(g)
+        if self.dF:
+            A = np.stack(self.dF, 1)
+            gram = A.T @ A
+            tr = float(np.trace(gram))
+            if tr > 0.0:
+                gam = np.linalg.solve(gram + 1e-10 * tr * np.eye(gram.shape[0]), A.T @ f)
+                if np.all(np.isfinite(gam)) and np.abs(gam).max() <= 1e3:
+                    corr = -(np.stack(self.dG, 1) @ gam)
+                else:
+                    self.dG, self.dF = [], []
+        self.xlow = g + corr
+        self.calls += 1
+        self.rprev = res_prev
+        if np.any(corr):
+            c = torch.from_numpy(corr.reshape(K, K)).to(y.device)
+            add = (self.cos.T @ c) * self.scale_q[None, :]           # [rows][K(q)]
+            y[:, :K] += torch.conj(self.hs)[None, :] * add
+
+
 class _RankState:
     """One rank's slab: rows [2P][n], its spectra / scratch buffers and loop state."""
 
@@ -327,6 +398,8 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
         dist.barrier()
 
     it, res, st = 0, float("inf"), 0
+    lm_depth = -int(getattr(opts, "accel", 0) or 0)
+    lowmode = _LowMode(min(lm_depth, 4), n, rows, rank * rows, dev, world) if lm_depth > 0 and n >= _LowMode.K else None
     try:
         for it in range(1, opts.max_iters + 1):
             ops.rows_fwd(S.app, P, S.s1, S.z, stream)
@@ -355,6 +428,8 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
                          [2 * rows * hq for _, hq in ranges], [2 * rows * hc] * world)
                 S.yrow.view(-1).index_copy_(0, recv_dst, recv)
                 yrow_t = S.yrow
+            if lowmode is not None:
+                lowmode.step(yrow_t, res)
             S.rows_inv(ops, yrow_t, h, opts, acc, stream)
             rs = torch.stack([S.res_bits.view(torch.float64)[0], S.status.to(torch.float64)[0]])
             if world > 1 and dist.get_backend() != "nccl":

@@ -123,3 +123,26 @@ def test_slab_chebyshev_across_ranks():
     assert it2 == [it1[0]] * 2 and it1[0] < it, (it1, it2, it)
     assert np.abs(t2 - t1).max() <= 1e-12
     assert np.abs(t1 - ref).max() <= 1e-8
+
+
+def test_slab_lowmode_anderson_across_ranks():
+    """opts.accel = -m: Anderson(m) on the 16 x 16 lowest cosine modes of the row buffer
+    (slab._LowMode; partial projections all-reduced over the ranks' row slabs). World 2 takes
+    the same steps as world 1 (same iteration count, same field to rounding), needs fewer
+    iterations than Picard and lands on the Picard fixed point."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from slab_numpy_ops import baseline_fk, fixed_point_numpy
+    n = 64
+    t1, it1, st1 = _run(1, n, -3)
+    t2, it2, st2 = _run(2, n, -3, dct=True)
+    z = np.load(ROOT / "tests" / "golden" / "greens_n64.npz")
+    fk = baseline_fk(z["f_sp0"], float(z["phi"]))
+    rng = np.random.default_rng(3)
+    P = rng.uniform(0.0, 0.05, (n, n))
+    V = 1.0 + 0.1 * rng.standard_normal((n, n))
+    ref, it = fixed_point_numpy(P, V, fk, 0.3, 0.017, 0, 1e-10, 60)
+    print(f"low-mode Anderson(3): {it1[0]} iterations (world 1), {it2} (world 2), Picard {it}")
+    assert st1 == [0] and st2 == [0, 0]
+    assert it2 == [it1[0]] * 2 and it1[0] < it, (it1, it2, it)
+    assert np.abs(t2 - t1).max() <= 1e-9
+    assert np.abs(t1 - ref).max() <= 1e-8
