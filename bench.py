@@ -489,6 +489,15 @@ def run_cfg2(args, dev, ws, rank):
                 "mean_iterations": float(its_a.mean()), "max_iterations": int(its_a.max()),
                 "failed": int((st_d.cpu().numpy() != 0).sum()),
                 "max_abs_vs_picard_K": float((Tb.double() - Tpic.double()).abs().max().item())}
+    # ... and with Anderson(2) mixing on the 16 x 16 lowest cosine modes (gt_fp_opts.accel = -2)
+    fl = dgc.fp_opts(leak_frac=0.3, beta=0.017, law=1, kirchhoff=1, with_rand=1, tol=1e-4, max_iters=200, accel=-2)
+    msl = timed(lambda: dgc.fp_batch_device(Ps.data_ptr(), V.data_ptr(), B, fl, Tb.data_ptr(), it_d.data_ptr(),
+                                            st_d.data_ptr(), mx_d.data_ptr(), None, stream.cuda_stream), 2)
+    its_l = it_d.cpu().numpy()
+    low_line = {"value": ws * B / (msl / 1e3), "unit": UNIT, "ms_per_step": msl,
+                "mean_iterations": float(its_l.mean()), "max_iterations": int(its_l.max()),
+                "failed": int((st_d.cpu().numpy() != 0).sum()),
+                "max_abs_vs_picard_K": float((Tb.double() - Tpic.double()).abs().max().item())}
     h = n + 1
     b_it = 5 * es * n * n + 8 * es * n * h  # SURVEY §8(d) B_it (fp32: 54.56 MB at n = 1024)
     res["combined"] = {"value": ws * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
@@ -506,7 +515,7 @@ def run_cfg2(args, dev, ws, rank):
                                               / (msb / 1e3) / 1e9,
                        "oracle": "tests/test_config2_gpu.py::test_config2_combined_matches_oracle (restate.h "
                                  "ref_fixed_point_rand_batch: 2.8e-13 K fp64, 1.8e-5 K fp32+fp64)",
-                       "accelerated": acc_line}
+                       "accelerated": acc_line, "lowmode_anderson": low_line}
     dgc.close()
     del Ps, Tb
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -664,6 +673,10 @@ def run_cfg4(args, dev, ws, rank):
     # (opts.accel = -3: slab._LowMode; 256 all-reduced coefficients per iteration)
     ol = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
     ol.accel = -3
+    wl = dg.fp_opts(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=3)
+    wl.accel = -3
+    slab.solve_slab(ops, n, Pl, Vl, wl, rank=rank, world=ws)  # warm-up of the mixing step (cuBLAS handle, tables)
+    torch.cuda.synchronize()
     if dist.is_available() and dist.is_initialized():
         dist.barrier()
     e0.record()
@@ -939,6 +952,24 @@ def run_b200(args, cfg):
                        "max_abs_vs_picard_K": float((Tb.double() - Tp.double()).abs().max().item()),
                        "method": "Chebyshev semi-iteration on the Picard map from iteration 5 (rho from the "
                                  "residual ratio), result G(x_k) of the last iteration"}
+        # Anderson(4) mixing on the 16 x 16 lowest cosine modes (gt_fp_opts.accel = -4, fp_lowmode)
+        low = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4, max_iters=200, accel=-4)
+        dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, low, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
+                           mx_d.data_ptr(), None, stream.cuda_stream)
+        a0.record(stream)
+        for _ in range(steps_b):
+            dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, low, Tb.data_ptr(), it_d.data_ptr(), st_d.data_ptr(),
+                               mx_d.data_ptr(), None, stream.cuda_stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        msl = shard.max_over_ranks(a0.elapsed_time(a1) / steps_b, dev)
+        its_l = it_d.cpu().numpy()
+        lowmode = {"value": ws * B / (msl / 1e3), "unit": UNIT, "ms_per_step": msl,
+                   "mean_iterations": float(its_l.mean()), "max_iterations": int(its_l.max()),
+                   "failed": int((st_d.cpu().numpy() != 0).sum()), "tol_K": 1e-4,
+                   "max_abs_vs_picard_K": float((Tb.double() - Tp.double()).abs().max().item()),
+                   "method": "Anderson(4) mixing on the 16 x 16 lowest cosine modes of the die field (fp_lowmode "
+                             "kernel between the column and row passes), stop rule on max|x_{k+1} - x_k|"}
         h = n + 1
         b_it = 8 * es * n * h + 4 * es * n * n  # DESIGN.md §4 per-iteration model (32nh + 16n^2 B in fp32)
         mode_b = {
@@ -951,7 +982,8 @@ def run_b200(args, cfg):
                            "precision": "fp32 to 5e-4 K, then fp64 to 1e-4 K" if prec == GT_FP32 else "fp64",
                            "bytes_per_iteration_model": b_it,
                            "achieved_GBps_model": b_it * float(its.sum()) / (msb / 1e3) / 1e9},
-            "linear_law_accelerated": accelerated}
+            "linear_law_accelerated": accelerated,
+            "linear_law_lowmode_anderson": lowmode}
 
     torch.cuda.empty_cache()  # the sub-benchmarks size their batches from the free memory
     cfg2 = None

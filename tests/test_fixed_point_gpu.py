@@ -169,3 +169,39 @@ def test_accelerated_fixed_point(b200lib, oracle, greens256, law, kirchhoff, sca
             assert it.mean() < it_ref.mean()
         else:  # + the fp64 finish stage's iterations (>= 2 after the 5e-4 K hand-over)
             assert it.mean() < it_ref.mean() + 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("law,kirchhoff,scale", [(0, 0, 1.0), (1, 1, 0.15)])
+def test_lowmode_anderson_fixed_point(b200lib, oracle, greens256, law, kirchhoff, scale):
+    """Anderson(3) mixing on the 16 x 16 lowest cosine modes (gt_fp_opts.accel = -3, the
+    fp_lowmode kernel between the column and row passes): the same fixed point as the reference
+    outer loop (oracle, Picard to 1e-4 K) to <= 1e-3 K, in fewer iterations than Picard and
+    than the Chebyshev steps; against a tightly converged oracle run (1e-9 K) the accelerated
+    field is at the stop rule's scale."""
+    import torch
+    from paper_2307_12119_b200 import inputs
+    P, V = inputs.mc_inputs(inputs.CONFIGS["cfg1"], 0, 8, device="cuda", torch_dtype=torch.float32)
+    p = P.cpu().numpy().astype(np.float64) * scale
+    v = V.cpu().numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=law, kirchhoff=kirchhoff, tol=1e-4, max_iters=120)
+    t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(greens256, p, v, jobs=8, **kw)
+    kw9 = dict(kw, tol=1e-9, max_iters=400)
+    t_fix, _, st_fix, _ = oracle.fixed_point_batch(greens256, p, v, jobs=8, **kw9)
+    assert (st_ref == 0).all() and (st_fix == 0).all()
+    for prec in (1, 0):
+        dg = _dg(greens256, prec)
+        dt = np.float64 if prec else np.float32
+        out, it, st, _, _ = dg.fp_batch_host(p.astype(dt), v.astype(dt), dg.fp_opts(accel=-3, **kw))
+        _, itc, _, _, _ = dg.fp_batch_host(p.astype(dt), v.astype(dt), dg.fp_opts(accel=4, **kw))
+        assert (st == 0).all(), st
+        err = np.abs(out.astype(np.float64) - t_ref).max()
+        err_fix = np.abs(out.astype(np.float64) - t_fix).max()
+        print(f"low-mode Anderson law={law} kirchhoff={kirchhoff} prec={prec}: iters {it.tolist()} vs Picard "
+              f"{it_ref.tolist()} / Chebyshev {itc.tolist()}, max|dT| {err:.2e} K vs the 1e-4 K loop, "
+              f"{err_fix:.2e} K vs the fixed point")
+        assert err <= 1e-3
+        assert err_fix <= (3e-4 if prec == 1 else 1e-3)
+        assert it.mean() < itc.mean()
+        if prec == 1:
+            assert it.mean() < 0.6 * it_ref.mean() if law == 0 else it.mean() < it_ref.mean()

@@ -221,6 +221,40 @@ def test_large_grid_n1024_chebyshev_vs_oracle(b200lib, oracle, tmp_path):
     assert err <= 1e-3
 
 
+def test_large_grid_n1024_lowmode_anderson_vs_oracle(b200lib, oracle, tmp_path):
+    """opts.accel = -3 on the large-grid path (slab._LowMode: Anderson(3) on the 16 x 16 lowest
+    cosine modes of the row buffer between the column and inverse row phases): fewer
+    iterations than the Chebyshev steps and the reference loop, same stop rule, within
+    1e-3 K of the oracle's Picard fixed point."""
+    import dataclasses
+    import torch
+    from paper_2307_12119_b200 import inputs, slab
+    from paper_2307_12119_b200.api import DeviceGreens
+    n = 1024
+    f, phi, ga = _large_greens(b200lib, tmp_path, n)
+    cfg = dataclasses.replace(inputs.CONFIGS["cfg4"], n=n, blocks=128, hotspots=16)
+    p = inputs.power_batch(cfg, 0, 1, np.float64)
+    p *= 300.0 / p.sum()
+    v = inputs.variation_batch(cfg, 0, 1).numpy().astype(np.float64)
+    kw = dict(leak_frac=0.3, beta=0.017, law=0, kirchhoff=0, tol=1e-4, max_iters=200)
+    t_ref, it_ref, st_ref, _ = oracle.fixed_point_batch(ga, p, v, jobs=1, **kw)
+    dg = DeviceGreens(ga, 1)
+    its = {}
+    for accel in (3, -3):
+        o = dg.fp_opts(**kw)
+        o.accel = accel
+        res = slab.solve_slab(slab.GpuLargeOps(dg), n, torch.from_numpy(p[0]).cuda(), torch.from_numpy(v[0]).cuda(), o)
+        torch.cuda.synchronize()
+        assert res.status == 0
+        its[accel] = res.iterations
+    err = float(np.abs(res.t.cpu().numpy() - t_ref[0]).max())
+    print(f"large n=1024 low-mode Anderson: iters {its[-3]} vs {its[3]} (Chebyshev) / {it_ref[0]} (Picard), "
+          f"max|dT| {err:.3e} K on peak {t_ref.max():.1f} K")
+    assert st_ref[0] == 0
+    assert its[-3] < its[3] < it_ref[0]
+    assert err <= 1e-3
+
+
 @pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3), (8, 0)])
 def test_large_grid_peer_ranks_emulated(b200lib, tmp_path, world, accel):
     """The multi-GPU column phase over peer memory (gt_large_cols_peer: every rank's row
