@@ -136,7 +136,11 @@ typedef struct gt_fp_opts {
                               fdm.cpp:167-205: iteration counts match it); k0 > 0:
                               Chebyshev semi-iteration from iteration k0 on, with the
                               contraction rate estimated per sample from the residual
-                              ratio there; same stop rule on max|G(T) - T|. */
+                              ratio there; same stop rule on max|G(T) - T|.
+                              -m (m = 1..4): Anderson(m) mixing on the 16 x 16 lowest cosine
+                              modes of the die field between the column and row passes
+                              (fixed_point.cu fp_lowmode; slab.py on the large-grid path):
+                              the same fixed point, stop rule on max|T_{k+1} - T_k|. */
     int warm_start;        /* 1: the t_out map holds the initial temperature rise T_0 on
                               entry (device entry; e.g. the mode-A closed-form solution of
                               the same pair), 0: T_0 = 0 as the reference loop starts. */

@@ -807,7 +807,7 @@ size_t gt_fp_scratch_bytes(int n, int precision) { return gtd_fp_scratch_bytes_p
 namespace {
 void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int batch, const gt_fp_opts* opts,
                   double tol, int warm, const void* H, void* t_out, int* iters, int* status, double* mx, double* mean,
-                  cudaStream_t st);
+                  cudaStream_t st, const void* lm_src = nullptr);
 
 // Per-sample shift-variant maps h = f_rand o p_var * rand_scale of the combined config-2
 // loop: the mode-A passes with with_rand = 2 (closed forms at gs.mu as the reference
@@ -881,8 +881,8 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
     cuda_ok(gtd_widen(static_cast<const float*>(p_dyn), d->fin_p.as<double>(), cnt, st), "widen");
     cuda_ok(gtd_widen(static_cast<const float*>(var), d->fin_v.as<double>(), cnt, st), "widen");
     cuda_ok(gtd_widen(static_cast<const float*>(t_out), d->fin_t.as<double>(), cnt, st), "widen");
-    run_fp_stage(d64, d->fin_p.p, d->fin_v.p, batch, opts, opts->tol, 1, H ? d->fin_h.p : nullptr, d->fin_t.p,
-                 d->fin_it.as<int>(), d->fin_st.as<int>(), mx, mean, st);
+    run_fp_stage(d64, d->fin_p.p, d->fin_v.p, batch, opts, opts->tol, 2, H ? d->fin_h.p : nullptr, d->fin_t.p,
+                 d->fin_it.as<int>(), d->fin_st.as<int>(), mx, mean, st, opts->accel < 0 ? d->fp_lm.p : nullptr);
     cuda_ok(gtd_narrow(d->fin_t.as<double>(), static_cast<float*>(t_out), cnt, st), "narrow");
     cuda_ok(gtd_fp_combine(iters, status, d->fin_it.as<int>(), d->fin_st.as<int>(), batch, opts->max_iters, st),
             "combine");
@@ -893,7 +893,7 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
 
 void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int batch, const gt_fp_opts* opts,
                   double tol, int warm, const void* H, void* t_out, int* iters, int* status, double* mx, double* mean,
-                  cudaStream_t st) {
+                  cudaStream_t st, const void* lm_src) {
     if (!(opts->tol > 0.0)) fail(ST_CONFIG, "oracle", "outer tolerance must be positive");
     if (opts->max_iters < 1) fail(ST_CONFIG, "oracle", "max_iters must be >= 1");
     const int n = d->d.n;
@@ -926,7 +926,8 @@ void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int b
     o.tol = tol;
     o.max_iters = opts->max_iters;
     o.poll = 4;
-    o.warm_start = warm;
+    o.warm_start = warm ? 1 : 0;
+    o.min_iters = warm == 2 ? 1 : 2;  // 2: the fp64 stage continuing an fp32 iteration (run_fp)
     o.H = H;
     o.sH = static_cast<long long>(n) * n;
     o.accel = opts->accel;
@@ -943,6 +944,11 @@ void run_fp_stage(gt_device_greens* d, const void* p_dyn, const void* var, int b
         }
         o.lm_state = d->fp_lm.p;
         o.lm_cos = d->fp_lmcos.as<double>();
+        if (lm_src) {  // the fp64 stage continues the fp32 stage's mixing history (fp64 coefficients)
+            cuda_ok(cudaMemcpyAsync(d->fp_lm.p, lm_src, gtd_fp_lowmode_bytes() * batch, cudaMemcpyDeviceToDevice, st),
+                    "low-mode state");
+            o.lm_keep = 1;
+        }
     }
     if (o.accel > 0) {
         d->fp_tprev.ensure(static_cast<size_t>(n) * n * batch * (d->fp64 ? 8 : 4));

@@ -674,7 +674,7 @@ __global__ void fp_init(FPState* st, int* status, int* iters, int sample0, int c
 // rho is estimated per sample from the Picard residual ratio at iteration k0; a residual
 // that grows by 2x under acceleration drops the sample back to plain Picard.
 __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int count, double tol, int max_iters,
-                          int* active_count, int it, int accel) {
+                          int* active_count, int it, int accel, int min_iters) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     FPState& s = st[sample0 + i];
@@ -703,7 +703,7 @@ __global__ void fp_update(FPState* st, int* status, int* iters, int sample0, int
     }
     if (status[sample0 + i]) {
         s.active = 0;
-    } else if (s.iters > 1 && res < tol) {
+    } else if (s.iters >= min_iters && res < tol) {
         s.active = 0;
     } else if (s.iters >= max_iters) {
         status[sample0 + i] |= GTD_ST_NOCONVERGE;
@@ -1059,7 +1059,7 @@ struct FPLaunch {
             const int gc = grid(cnt * Gc::CT, res[1]);
             fp_init<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt);
             const bool lowmode = o->accel < 0 && o->lm_state && o->lm_cos && n >= LMK;
-            if (lowmode) {
+            if (lowmode && !o->lm_keep) {
                 fp_lowmode_init<<<(cnt * LMN + 255) / 256, 256, 0, st>>>(static_cast<LMState*>(o->lm_state), s0, cnt,
                                                                          o->warm_start);
                 k += 1;
@@ -1076,7 +1076,8 @@ struct FPLaunch {
                 rows(false, s0, cnt, it);
                 cudaMemsetAsync(counter_d, 0, sizeof(int), st);
                 fp_update<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt, o->tol, o->max_iters,
-                                                            counter_d, it, o->accel);
+                                                            counter_d, it, o->accel,
+                                                            o->min_iters > 0 ? o->min_iters : 2);
                 k += 3;
                 if (it % poll == 0 || it == o->max_iters) {
                     cudaMemcpyAsync(counter_h, counter_d, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -181,6 +181,11 @@ typedef struct gtd_fp_opts {
                          (fp_lowmode); [B] x gtd_fp_lowmode_bytes() of state, and lm_cos a
                          [16][n] double table cos(pi p (x + 1/2) / n) (gtd_fp_lowmode_cos)      */
     const double* lm_cos;
+    int lm_keep;      /* 1: lm_state continues a previous stage's history (no re-initialisation) */
+    int min_iters;    /* the stop rule may fire from this iteration on (0 = 2: the reference
+                         loop tests convergence after iteration 1, fdm.cpp:190-200); 1 for the
+                         fp64 stage that continues an fp32 iteration: its first evaluation is
+                         the fp64 residual check of the fp32 iterate                           */
 } gtd_fp_opts;
 size_t gtd_fp_lowmode_bytes(void);
 int gtd_fp_lowmode_cos(int n, double* table, cudaStream_t st);
