@@ -224,19 +224,17 @@ class _LowMode:
         self.dG, self.dF = [], []
         self.calls, self.rprev = 0, 0.0
 
-    def step(self, y, res_prev):
-        """y: this rank's row buffer [rows][hy] complex128, corrected in place; res_prev: the
-        residual of the previous iteration (growth guard)."""
-        import numpy as np
-        import torch
-        import torch.distributed as dist
+    def project(self, y):
+        """Partial coefficients [K(p)][K(q)] from this rank's rows of the row buffer."""
         K = self.K
         d = (self.hs[None, :] * y[:, :K]).real                      # [rows][K(q)]
-        a = (self.cos @ d) * self.norm                              # [K(p)][K(q)]
-        if self.world > 1:
-            if dist.get_backend() != "nccl":
-                a = a.cpu()
-            dist.all_reduce(a)
+        return (self.cos @ d) * self.norm
+
+    def mix(self, a, res_prev):
+        """Anderson step on the summed coefficients `a`; returns the correction [K][K] (numpy)
+        or None. res_prev: the residual of the previous iteration (growth guard)."""
+        import numpy as np
+        K = self.K
         g = a.detach().cpu().numpy().reshape(-1).copy()
         if self.calls > 1 and self.rprev > 0.0 and res_prev > 2.0 * self.rprev:
             self.dG, self.dF = [], []                               # residual doubled: drop the history
@@ -261,10 +259,26 @@ class _LowMode:
         self.xlow = g + corr
         self.calls += 1
         self.rprev = res_prev
-        if np.any(corr):
-            c = torch.from_numpy(corr.reshape(K, K)).to(y.device)
-            add = (self.cos.T @ c) * self.scale_q[None, :]           # [rows][K(q)]
-            y[:, :K] += torch.conj(self.hs)[None, :] * add
+        return corr.reshape(K, K) if np.any(corr) else None
+
+    def apply(self, y, corr):
+        """Add the correction's row spectra to columns q < K of this rank's rows (in place)."""
+        import torch
+        if corr is None:
+            return
+        c = torch.from_numpy(corr).to(y.device)
+        add = (self.cos.T @ c) * self.scale_q[None, :]               # [rows][K(q)]
+        y[:, :self.K] += torch.conj(self.hs)[None, :] * add
+
+    def step(self, y, res_prev):
+        """y: this rank's row buffer [rows][hy] complex128, corrected in place."""
+        import torch.distributed as dist
+        a = self.project(y)
+        if self.world > 1:
+            if dist.get_backend() != "nccl":
+                a = a.cpu()
+            dist.all_reduce(a)
+        self.apply(y, self.mix(a, res_prev))
 
 
 class _RankState:
@@ -483,12 +497,19 @@ def solve_slab_emulated(ops, n: int, p_full, v_full, opts, world: int, stream: i
     z_table = torch.tensor([s.z.data_ptr() for s in R], dtype=torch.int64, device=dev)
     y_table = torch.tensor([s.yrow.data_ptr() for s in R], dtype=torch.int64, device=dev)
     acc = _Accel(int(getattr(opts, "accel", 0) or 0))
+    lm_depth = -int(getattr(opts, "accel", 0) or 0)
+    lms = ([_LowMode(min(lm_depth, 4), n, rows, r * rows, dev, 1) for r in range(world)]
+           if lm_depth > 0 and n >= _LowMode.K else [])
     it, res, st = 0, float("inf"), 0
     for it in range(1, opts.max_iters + 1):
         for s in R:
             ops.rows_fwd(s.app, P, s.s1, s.z, stream)
         for s in R:
             ops.cols_peer(z_table, world, P, s.c0, s.hc, s.c1, s.c2, y_table, h, stream)
+        if lms:
+            corr = lms[0].mix(sum(lm.project(s.yrow) for lm, s in zip(lms, R)), res)
+            for lm, s in zip(lms, R):
+                lm.apply(s.yrow, corr)
         for s in R:
             s.rows_inv(ops, s.yrow, h, opts, acc, stream)
         res = max(float(s.res_bits.view(torch.float64)[0]) for s in R)

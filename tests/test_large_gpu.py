@@ -255,7 +255,7 @@ def test_large_grid_n1024_lowmode_anderson_vs_oracle(b200lib, oracle, tmp_path):
     assert err <= 1e-3
 
 
-@pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3), (8, 0)])
+@pytest.mark.parametrize("world,accel", [(2, 0), (4, 0), (4, 3), (4, -3), (8, 0)])
 def test_large_grid_peer_ranks_emulated(b200lib, tmp_path, world, accel):
     """The multi-GPU column phase over peer memory (gt_large_cols_peer: every rank's row
     spectra read in place, results stored into their owners' row buffers), with `world`
@@ -284,4 +284,5 @@ def test_large_grid_peer_ranks_emulated(b200lib, tmp_path, world, accel):
           f"max|dT| {d:.3e} K")
     assert em.status == one.status == 0
     assert em.iterations == one.iterations
-    assert d == 0.0
+    # low-mode mixing sums the ranks' partial projections in another order than one slab does
+    assert d == 0.0 if accel >= 0 else d <= 1e-9
