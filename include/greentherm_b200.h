@@ -126,7 +126,8 @@ typedef struct gt_fp_opts {
     double fp32_stage_tol; /* GT_FP32 handles (BASELINE config 1: "fp32 with fp64 residual
                               check"): the fp32 iteration stops at this tolerance, then
                               fp64 iterations warm-started from it finish to `tol`
-                              (0 = default 5e-4; < 0 = fp32 only). Iteration counts add up. */
+                              (0 = default: 5e-4, or 1e-2 with accel < 0 whose history the
+                              fp64 stage continues; < 0 = fp32 only). Iteration counts add up. */
     int with_rand;         /* 1: combined config 2 -- every iteration adds the reference's
                               shift-variant term h * sum(applied), h = f_rand o p_var *
                               rand_scale with f_rand = random_greens at the GreensSet mu

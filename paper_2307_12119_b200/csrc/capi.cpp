@@ -845,7 +845,10 @@ void run_fp(gt_device_greens* d, const void* p_dyn, const void* var, int batch, 
             int* iters, int* status, double* mx, double* mean, cudaStream_t st) {
     if (!opts) fail(ST_CONFIG, "capi", "fixed point needs options");
     if (!(opts->tol > 0.0)) fail(ST_CONFIG, "oracle", "outer tolerance must be positive");
-    const double stage_tol = opts->fp32_stage_tol == 0.0 ? 5e-4 : opts->fp32_stage_tol;
+    // default hand-over: the fp32 noise floor for Picard / Chebyshev (tools/fp_stage_sweep.py); with the
+    // low-mode mixing the fp64 stage continues the history, and an earlier hand-over (1e-2 K) costs
+    // fewer iterations in total (profiles/r2s4_notes.md)
+    const double stage_tol = opts->fp32_stage_tol == 0.0 ? (opts->accel < 0 ? 1e-2 : 5e-4) : opts->fp32_stage_tol;
     const size_t nn = static_cast<size_t>(d->d.n) * d->d.n, cnt = nn * batch;
     const void* H = nullptr;
     if (opts->with_rand) {

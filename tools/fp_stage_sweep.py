@@ -26,7 +26,7 @@ d64.close()
 del P64, V64
 d = DeviceGreens(greens_cfg1(), 0)
 T = torch.empty_like(P)
-for accel in (0, 5):
+for accel in ([int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else (0, 5)):
     for tol32 in [float(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("5e-4", "3e-4", "2e-4", "1.5e-4"))]:
         o = d.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4, max_iters=200, accel=accel,
                       fp32_stage_tol=tol32)
