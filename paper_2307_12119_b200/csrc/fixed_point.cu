@@ -478,7 +478,11 @@ struct FPCGeom {
     static constexpr int CT = hp / W;
     static constexpr int U8 = (M / 8) * GA;
     static constexpr int NT = U8 >= 256 ? 256 : (U8 < 32 ? 32 : U8);
-    static constexpr int MINB = sizeof(T) == 8 ? 1 : ((512 / NT) < 1 ? 1 : 512 / NT);
+#ifndef GT_FPC_MINB64
+#define GT_FPC_MINB64 2  // resident CTAs the fp64 column pass's register budget targets at M <= 512
+                         // (128 registers, no spills: +2.5% on the fp64 stage, profiles/r2s4_notes.md)
+#endif
+    static constexpr int MINB = sizeof(T) == 8 ? (M <= 512 ? GT_FPC_MINB64 : 1) : ((512 / NT) < 1 ? 1 : 512 / NT);
     static constexpr int APLANE = (M + M / 8) * GA;
     static constexpr int TILE = InvLayout<GA, M>::SIZE > APLANE ? InvLayout<GA, M>::SIZE : APLANE;
     static_assert(hp % W == 0, "column tiles");

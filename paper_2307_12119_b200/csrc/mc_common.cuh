@@ -158,10 +158,13 @@ struct MCGeom {
     static constexpr int NT2 = (M / 8) * W > NT2C ? NT2C : (M / 8) * W;
     static constexpr int REGS2 = (65536 / GT_P2_CTAS) / NT2 > 255 ? 255 : (65536 / GT_P2_CTAS) / NT2;
     // pass 2 holds three lines per thread-butterfly: 128 registers (fp32) / 255 (fp64)
+#ifndef GT_P2_MINB64
+#define GT_P2_MINB64 1  // fp64 column pass: resident CTAs the register budget targets (tuning)
+#endif
 #ifdef GT_P2_MINB
     static constexpr int MINB2 = sizeof(T) == 8 ? 1 : GT_P2_MINB;  // tuning override (occupancy sweeps)
 #else
-    static constexpr int MINB2 = sizeof(T) == 8 ? 1 : ((512 / NT2) < 1 ? 1 : (512 / NT2));
+    static constexpr int MINB2 = sizeof(T) == 8 ? (M <= 512 ? GT_P2_MINB64 : 1) : ((512 / NT2) < 1 ? 1 : (512 / NT2));
 #endif
 };
 
