@@ -205,3 +205,26 @@ def test_lowmode_anderson_fixed_point(b200lib, oracle, greens256, law, kirchhoff
         assert it.mean() < itc.mean()
         if prec == 1:
             assert it.mean() < 0.6 * it_ref.mean() if law == 0 else it.mean() < it_ref.mean()
+
+
+@pytest.mark.gpu
+def test_lowmode_anderson_runaway_pairs_fail_like_picard(b200lib, greens256):
+    """Pairs without a fixed point (the literal exp law at config-1 power) end with
+    a failure status under the low-mode mixing as they do under the plain loop: the mixing
+    step drops non-finite or oversized coefficients instead of producing a converged-looking
+    field, and pairs that do converge in the same batch are unaffected."""
+    import torch
+    from paper_2307_12119_b200 import inputs
+    P, V = inputs.mc_inputs(inputs.CONFIGS["cfg1"], 0, 4, device="cuda", torch_dtype=torch.float32)
+    p = P.cpu().numpy().astype(np.float64)
+    v = V.cpu().numpy().astype(np.float64)
+    p[2:] *= 0.15  # pairs 2, 3 converge; 0, 1 run away
+    dg = _dg(greens256, 1)
+    kw = dict(leak_frac=0.3, beta=0.017, law=1, kirchhoff=0, tol=1e-4, max_iters=60)
+    out0, it0, st0, _, _ = dg.fp_batch_host(p, v, dg.fp_opts(accel=0, **kw))
+    out3, it3, st3, _, _ = dg.fp_batch_host(p, v, dg.fp_opts(accel=-3, **kw))
+    print(f"status Picard {st0.tolist()} / low-mode {st3.tolist()}, iterations {it0.tolist()} / {it3.tolist()}")
+    assert (st0[:2] != 0).all() and (st3[:2] != 0).all()
+    assert (st0[2:] == 0).all() and (st3[2:] == 0).all()
+    assert np.abs(out3[2:] - out0[2:]).max() <= 1e-3
+    assert (it3[2:] <= it0[2:]).all()
