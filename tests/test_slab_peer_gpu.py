@@ -78,7 +78,7 @@ def _worker(rank, world, port, n, accel, q, transport="peer"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("accel,transport", [(0, "peer"), (3, "peer"), (0, "nccl")])
+@pytest.mark.parametrize("accel,transport", [(0, "peer"), (3, "peer"), (-3, "peer"), (0, "nccl")])
 def test_peer_transport_two_processes(b200lib, accel, transport):
     import queue
     import torch
@@ -113,4 +113,5 @@ def test_peer_transport_two_processes(b200lib, accel, transport):
           f"max|dT| {d:.3e} K")
     assert all(g[3] == 0 for g in got) and one.status == 0
     assert all(g[2] == one.iterations for g in got)
-    assert d == 0.0
+    # the low-mode mixing (accel < 0) all-reduces the ranks' partial projections: same steps to rounding
+    assert d == 0.0 if accel >= 0 else d <= 1e-9
