@@ -16,7 +16,8 @@ out = torch.empty_like(P)
 it = torch.zeros(B, dtype=torch.int32, device="cuda")
 st = torch.zeros(B, dtype=torch.int32, device="cuda")
 s = torch.cuda.Stream()
-lin = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=2e-4, max_iters=200)
+accel = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+lin = dg.fp_opts(leak_frac=0.3, law=0, kirchhoff=0, beta=0.017, tol=1e-4 if accel else 2e-4, max_iters=200, accel=accel)
 for _ in range(2):
     dg.fp_batch_device(P.data_ptr(), V.data_ptr(), B, lin, out.data_ptr(), it.data_ptr(), st.data_ptr(), None, None,
                        s.cuda_stream)
