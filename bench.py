@@ -371,11 +371,25 @@ def cpu_cfg0(threads: int, dev) -> dict:
     e1.record()
     torch.cuda.synchronize()
     gms = e0.elapsed_time(e1) / 5
+    it_eq = bool((it.cpu().numpy() == it_ref).all())
+    # the same maps with the low-mode Anderson mixing (gt_fp_opts.accel = -3)
+    Tp = T.clone()
+    ol = dg.fp_opts(accel=-3, **kw)
+    dg.fp_batch_device(P.data_ptr(), V.data_ptr(), S, ol, T.data_ptr(), it.data_ptr(), st.data_ptr())
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        dg.fp_batch_device(P.data_ptr(), V.data_ptr(), S, ol, T.data_ptr(), it.data_ptr(), st.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    lms = e0.elapsed_time(e1) / 5
+    low = {"gpu_value": S / (lms / 1e3), "mean_iterations": float(it.double().mean()),
+           "failed": int((st != 0).sum()), "max_abs_vs_picard_K": float((T - Tp).abs().max())}
     dg.close()
-    return {"value": S / secs, "unit": "solves/s", "cores": threads, "kind": "port",
+    return {"value": S / secs, "unit": "solves/s", "cores": threads, "kind": "port", "gpu_lowmode_anderson": low,
             "sample": f"{S} config-0 maps (n=64, fp64), linear-law fixed point to 1e-4 K (oracle restatement of "
                       f"fdm.cpp:167-205 with the reference convolution), mean {float(it_ref.mean()):.1f} iterations",
-            "gpu_value": S / (gms / 1e3), "gpu_iterations_equal": bool((it.cpu().numpy() == it_ref).all()),
+            "gpu_value": S / (gms / 1e3), "gpu_iterations_equal": it_eq,
             "literal_exp_law_failed": f"{int((lit != 0).sum())}/8 (no fixed point, SURVEY §0)"}
 
 
