@@ -20,6 +20,8 @@
 //   fp_update: per-sample iteration count / convergence / failure state.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "launch_once.cuh"
 #include "col_pass.cuh"
 #include "fft_tile.cuh"
@@ -105,12 +107,18 @@ struct FPRowsMinB {
     static constexpr int value = GT_FP_ROWS_MINB > 0 ? GT_FP_ROWS_MINB : TileGeom<T, M>::MINB;
 };
 
-template <typename T, int M, bool FIRST>
+// FEAT bit 0: shift-variant maps (H) in use; bit 1: Chebyshev state (Tprev) in use. The
+// per-thread register arrays of an unused feature vanish at compile time (FEAT = 0, the plain
+// loop and the low-mode mixing: the warp row pass drops its spills at 128 registers, +9% on
+// the config-1 loop; profiles/r2s4_notes.md).
+template <typename T, int M, bool FIRST, int FEAT>
 __global__ void __launch_bounds__(TileGeom<T, M>::NT, FPRowsMinB<T, M>::value)
 fp_rows(FPIn<T> in, int sample0, int count, cplx<T>* __restrict__ A, T* __restrict__ Ar, T* __restrict__ Tst,
         FPState* __restrict__ state, int* __restrict__ status, const cplx<T>* __restrict__ g_tw,
         const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka, T kb, T kexp, T t_ambient,
-        int warm, const T* __restrict__ H, long long sH, int it, T* __restrict__ Tprev, T* __restrict__ Yout) {
+        int warm, const T* __restrict__ H_, long long sH, int it, T* __restrict__ Tprev_, T* __restrict__ Yout) {
+    const T* const H = (FEAT & 1) ? H_ : nullptr;
+    T* const Tprev = (FEAT & 2) ? Tprev_ : nullptr;
     using Gm = FPGeom<T, M>;
     constexpr int n = Gm::n, h = Gm::h, L = Gm::L, LP = Gm::LP, NT = Gm::NT, hp = Gm::hp;
     constexpr int RB = Gm::RB;
@@ -287,13 +295,15 @@ constexpr bool fp_warp_rows() {
     return M == 128 || M == 256 || M == 512;
 }
 
-template <typename T, int M, bool FIRST>
+template <typename T, int M, bool FIRST, int FEAT>
 __global__ void __launch_bounds__(FPW_WARPS * 32, sizeof(T) == 8 ? 1 : 2)
 fp_rows_w(FPIn<T> in, int sample0, int count, const cplx<T>* __restrict__ Yspec, T* __restrict__ Ar,
           T* __restrict__ Tst, FPState* __restrict__ state, int* __restrict__ status,
           const cplx<T>* __restrict__ g_tw, const cplx<T>* __restrict__ g_hs, T beta, int law, int kirchhoff, T ka,
-          T kb, T kexp, T t_ambient, int warm, const T* __restrict__ H, long long sH, int it,
-          T* __restrict__ Tprev, T* __restrict__ Yout) {
+          T kb, T kexp, T t_ambient, int warm, const T* __restrict__ H_, long long sH, int it,
+          T* __restrict__ Tprev_, T* __restrict__ Yout) {
+    const T* const H = (FEAT & 1) ? H_ : nullptr;
+    T* const Tprev = (FEAT & 2) ? Tprev_ : nullptr;
     using Gm = FPGeom<T, M>;
     using WF = WarpFFT<T, M>;
     constexpr int n = Gm::n, h = Gm::h, hp = Gm::hp, P = WF::P, E = n / 32, RP = n / 2;
@@ -999,26 +1009,36 @@ struct FPLaunch {
                    int* counter_h, int chunk, cudaStream_t st, long long* launches) {
         constexpr int n = Gm::n, hp = Gm::hp, NT = Gm::NT;
         constexpr int RP = n / 2;
-        static int res[3] = {0, 0, 0}, sms = 0;
+        // res_r[FEAT] / res_w[FEAT]: resident CTAs per SM of the tile / warp row pass variants
+        static int res_r[4] = {0, 0, 0, 0}, res_w[4] = {0, 0, 0, 0}, res_c = 0, sms = 0;
         static DeviceOnce once_;
         once_([&] {
-            cudaFuncSetAttribute(fp_rows<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
-            cudaFuncSetAttribute(fp_rows<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
+            auto rows_attr = [&](auto feat_c) {
+                constexpr int FE = decltype(feat_c)::value;
+                cudaFuncSetAttribute(fp_rows<T, M, true, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
+                cudaFuncSetAttribute(fp_rows<T, M, false, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_rows()));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res_r[FE], fp_rows<T, M, false, FE>, NT, smem_rows());
+                if constexpr (fp_warp_rows<T, M>()) {
+                    cudaFuncSetAttribute(fp_rows_w<T, M, true, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem_rows_w()));
+                    cudaFuncSetAttribute(fp_rows_w<T, M, false, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem_rows_w()));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res_w[FE], fp_rows_w<T, M, false, FE>,
+                                                                  FPW_WARPS * 32, smem_rows_w());
+                }
+            };
+            rows_attr(std::integral_constant<int, 0>{});
+            rows_attr(std::integral_constant<int, 1>{});
+            rows_attr(std::integral_constant<int, 2>{});
+            rows_attr(std::integral_constant<int, 3>{});
             cudaFuncSetAttribute(fp_cols_d<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cols()));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[0], fp_rows<T, M, false>, NT, smem_rows());
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], fp_cols_d<T, M>, Gc::NT, smem_cols());
-            if constexpr (fp_warp_rows<T, M>()) {
-                cudaFuncSetAttribute(fp_rows_w<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem_rows_w()));
-                cudaFuncSetAttribute(fp_rows_w<T, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem_rows_w()));
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], fp_rows_w<T, M, false>, FPW_WARPS * 32,
-                                                              smem_rows_w());
-            }
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res_c, fp_cols_d<T, M>, Gc::NT, smem_cols());
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            for (int& r : res) r = r < 1 ? 1 : r;
+            for (int& r : res_r) r = r < 1 ? 1 : r;
+            for (int& r : res_w) r = r < 1 ? 1 : r;
+            res_c = res_c < 1 ? 1 : res_c;
         });
         const size_t per = static_cast<size_t>(n) * hp;
         cplx<T>* A = static_cast<cplx<T>*>(scratch);             // Y: column pass -> row pass
@@ -1031,36 +1051,39 @@ struct FPLaunch {
         auto grid = [&](int items, int r) { return items < sms * r ? items : sms * r; };
         const int poll = o->poll > 0 ? o->poll : 4;
         long long k = 0;
+        const int feat = (o->H ? 1 : 0) | (o->Tprev ? 2 : 0);
         auto rows = [&](bool first, int s0, int cnt, int it_) {
-            if constexpr (fp_warp_rows<T, M>()) {
-                const int gw = grid((cnt * RP + FPW_WARPS - 1) / FPW_WARPS, res[2]);
-                if (first)
-                    fp_rows_w<T, M, true><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
+            auto go = [&](auto first_c, auto feat_c) {
+                constexpr bool F = decltype(first_c)::value;
+                constexpr int FE = decltype(feat_c)::value;
+                if constexpr (fp_warp_rows<T, M>()) {
+                    const int gw = grid((cnt * RP + FPW_WARPS - 1) / FPW_WARPS, res_w[FE]);
+                    fp_rows_w<T, M, F, FE><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
                         kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
                         static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
-                else
-                    fp_rows_w<T, M, false><<<gw, FPW_WARPS * 32, smem_rows_w(), st>>>(
+                } else {
+                    const int gr = grid(cnt * Gm::RB, res_r[FE]);
+                    fp_rows<T, M, F, FE><<<gr, NT, smem_rows(), st>>>(
                         in, s0, cnt, A, Ar, Tst, state, status, tw, hs, T(o->beta), o->law, o->kirchhoff, ka, kb,
                         kexp, T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
                         static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
-            } else {
-                const int gr = grid(cnt * Gm::RB, res[0]);
-                if (first)
-                    fp_rows<T, M, true><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
-                                                                     T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                     T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
-                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
-                else
-                    fp_rows<T, M, false><<<gr, NT, smem_rows(), st>>>(in, s0, cnt, A, Ar, Tst, state, status, tw, hs,
-                                                                      T(o->beta), o->law, o->kirchhoff, ka, kb, kexp,
-                                                                      T(o->t_ambient), o->warm_start, static_cast<const T*>(o->H), o->sH, it_,
-                        static_cast<T*>(o->Tprev), static_cast<T*>(o->Yout));
-            }
+                }
+            };
+            auto by_feat = [&](auto first_c) {
+                switch (feat) {
+                    case 0: go(first_c, std::integral_constant<int, 0>{}); break;
+                    case 1: go(first_c, std::integral_constant<int, 1>{}); break;
+                    case 2: go(first_c, std::integral_constant<int, 2>{}); break;
+                    default: go(first_c, std::integral_constant<int, 3>{}); break;
+                }
+            };
+            if (first) by_feat(std::true_type{});
+            else by_feat(std::false_type{});
         };
         for (int s0 = 0; s0 < batch; s0 += chunk) {
             const int cnt = batch - s0 < chunk ? batch - s0 : chunk;
-            const int gc = grid(cnt * Gc::CT, res[1]);
+            const int gc = grid(cnt * Gc::CT, res_c);
             fp_init<<<(cnt + 127) / 128, 128, 0, st>>>(state, status, iters, s0, cnt);
             const bool lowmode = o->accel < 0 && o->lm_state && o->lm_cos && n >= LMK;
             if (lowmode && !o->lm_keep) {
