@@ -173,7 +173,8 @@ struct MCGeom {
 // loads and stores it coalesced straight from / to registers and transforms it
 // with the one-warp FFT (fft_warp.cuh): no CTA barriers, no transposing tile.
 #ifndef GT_W1
-#define GT_W1 16
+#define GT_W1 12  // 12 warps x 2 CTAs at 80 registers: no spills (16 warps at 64 registers spilled 40 B;
+                  // pass 1 1.51 -> 1.46 ms per 4096 pairs, profiles/r2s4_notes.md)
 #endif
 #ifndef GT_W3
 #define GT_W3 8
