@@ -215,6 +215,27 @@ gt_status gt_large_geometry(const gt_device_greens* d, int* m1, int* m2);
  *   then [n][hc] doubles (columns c0.. of every die row, rank-major);
  * dct_rows = 0 (larger n): packed row-pair spectra [pairs][m] complex, compact [n/2][2 hc]. */
 gt_status gt_large_row_layout(const gt_device_greens* d, int* dct_rows);
+
+/* Low-mode Anderson mixing of gt_fp_opts.accel = -m on the large-grid path (slab.py drives it
+ * between gt_large_cols* and gt_large_rows_inv): `y` is this rank's part [rows][hy] (complex
+ * fp64) of the row buffer, holding die rows row0 .. row0 + rows - 1.
+ *   project: coef[256] = the slab's share of the 16 x 16 lowest cosine coefficients of G(x_k)
+ *            (partial: scratch of gt_large_lowmode_partial_blocks(rows) x 256 doubles); a
+ *            multi-GPU driver all-reduces coef over the ranks (sum);
+ *   mix:     one Anderson(depth <= 4) step on the summed coefficients (state:
+ *            gt_large_lowmode_state_bytes() bytes, initialised by gt_large_lowmode_init;
+ *            res_prev: the residual of the previous iteration) -> corr[256];
+ *   apply:   the correction's row spectra added to columns [0, 16) of y.
+ * All device pointers; no host synchronisation. */
+size_t gt_large_lowmode_state_bytes(void);
+int gt_large_lowmode_partial_blocks(int rows);
+gt_status gt_large_lowmode_init(void* state, void* stream);
+gt_status gt_large_lowmode_project(const gt_device_greens* d, const void* y, int hy, int rows, int row0,
+                                   double* partial, double* coef, void* stream);
+gt_status gt_large_lowmode_mix(void* state, const double* coef, int depth, double res_prev, double* corr,
+                               void* stream);
+gt_status gt_large_lowmode_apply(const gt_device_greens* d, void* y, int hy, int rows, int row0, const double* corr,
+                                 void* stream);
 gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
                             void* stream);
 gt_status gt_large_cols(const gt_device_greens* d, const void* z, int compact, int c0, int hc, void* c1, void* c2,

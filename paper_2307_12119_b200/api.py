@@ -136,6 +136,12 @@ _EXT = [
     ("gt_large_geometry", cint, [vp, C.POINTER(cint), C.POINTER(cint)]),
     ("gt_large_rows_fwd", cint, [vp, vp, cint, vp, vp, vp]),
     ("gt_large_row_layout", cint, [vp, C.POINTER(cint)]),
+    ("gt_large_lowmode_state_bytes", C.c_size_t, []),
+    ("gt_large_lowmode_partial_blocks", cint, [cint]),
+    ("gt_large_lowmode_init", cint, [vp, vp]),
+    ("gt_large_lowmode_project", cint, [vp, vp, cint, cint, cint, vp, vp, vp]),
+    ("gt_large_lowmode_mix", cint, [vp, vp, cint, C.c_double, vp, vp]),
+    ("gt_large_lowmode_apply", cint, [vp, vp, cint, cint, cint, vp, vp]),
     ("gt_large_cols", cint, [vp, vp, cint, cint, cint, vp, vp, vp, vp]),
     ("gt_large_rows_inv", cint, [vp, vp, cint, cint, vp, vp, vp, vp, vp, C.POINTER(FPOpts), vp, vp, vp]),
     ("gt_large_cols_peer", cint, [vp, vp, cint, cint, cint, cint, vp, vp, vp, cint, vp]),

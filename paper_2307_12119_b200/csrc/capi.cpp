@@ -1002,6 +1002,48 @@ gt_status gt_large_row_layout(const gt_device_greens* d, int* dct_rows) {
     });
 }
 
+size_t gt_large_lowmode_state_bytes(void) { return gtd_lg_lowmode_state_bytes(); }
+int gt_large_lowmode_partial_blocks(int rows) { return gtd_lg_lowmode_partial_blocks(rows); }
+
+gt_status gt_large_lowmode_init(void* state, void* stream) {
+    return guarded([&] {
+        if (!state) fail(ST_CONFIG, "capi", "large lowmode: null state");
+        cuda_ok(gtd_lg_lowmode_init(state, static_cast<cudaStream_t>(stream)), "large lowmode init");
+    });
+}
+
+gt_status gt_large_lowmode_project(const gt_device_greens* d, const void* y, int hy, int rows, int row0,
+                                   double* partial, double* coef, void* stream) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (!y || !partial || !coef || rows < 1 || row0 < 0 || row0 + rows > g.n || hy < 16)
+            fail(ST_CONFIG, "capi", "large lowmode project: bad row range or buffers");
+        cuda_ok(gtd_lg_lowmode_project(&g, y, hy, rows, row0, partial, coef, static_cast<cudaStream_t>(stream)),
+                "large lowmode project");
+    });
+}
+
+gt_status gt_large_lowmode_mix(void* state, const double* coef, int depth, double res_prev, double* corr,
+                               void* stream) {
+    return guarded([&] {
+        if (!state || !coef || !corr) fail(ST_CONFIG, "capi", "large lowmode mix: null buffer");
+        if (depth < 1 || depth > 4) fail(ST_CONFIG, "capi", "large lowmode mix: depth must be 1..4");
+        cuda_ok(gtd_lg_lowmode_mix(state, coef, depth, res_prev, corr, static_cast<cudaStream_t>(stream)),
+                "large lowmode mix");
+    });
+}
+
+gt_status gt_large_lowmode_apply(const gt_device_greens* d, void* y, int hy, int rows, int row0, const double* corr,
+                                 void* stream) {
+    return guarded([&] {
+        const gtd_lg g = large_geom(d);
+        if (!y || !corr || rows < 1 || row0 < 0 || row0 + rows > g.n || hy < 16)
+            fail(ST_CONFIG, "capi", "large lowmode apply: bad row range or buffers");
+        cuda_ok(gtd_lg_lowmode_apply(&g, y, hy, rows, row0, corr, static_cast<cudaStream_t>(stream)),
+                "large lowmode apply");
+    });
+}
+
 gt_status gt_large_rows_fwd(const gt_device_greens* d, const double* app, int pairs, void* s1, void* z,
                             void* stream) {
     return guarded([&] {

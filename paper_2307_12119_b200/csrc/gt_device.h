@@ -213,6 +213,17 @@ int gtd_lg_split(int m, int* M1, int* M2);
 /* row-phase output layout: 1 = real DCT rows At [rows][n + 1] (n <= 8192, one-pass row kernels;
  * the column phase reads columns c0.. of every row), 0 = packed row-pair spectra Z [pairs][m] */
 int gtd_lg_row_layout(const gtd_lg* g);
+/* Low-mode Anderson mixing on this rank's rows [rows][hy] of the row buffer (die rows row0 ..):
+ * project -> coef[256] (partial: [gtd_lg_lowmode_partial_blocks(rows)][256] scratch), all-reduce
+ * coef over the ranks, mix (state: gtd_lg_lowmode_state_bytes(), depth <= 4) -> corr[256], apply. */
+size_t gtd_lg_lowmode_state_bytes(void);
+int gtd_lg_lowmode_partial_blocks(int rows);
+int gtd_lg_lowmode_init(void* state, cudaStream_t st);
+int gtd_lg_lowmode_project(const gtd_lg* g, const void* y, int hy, int rows, int row0, double* partial, double* coef,
+                           cudaStream_t st);
+int gtd_lg_lowmode_mix(void* state, const double* coef, int depth, double res_prev, double* corr, cudaStream_t st);
+int gtd_lg_lowmode_apply(const gtd_lg* g, void* y, int hy, int rows, int row0, const double* corr, cudaStream_t st);
+
 /* applied rows [2 pairs][n] -> Z [pairs][m] (mirrored rows' spectra, two rows per line) */
 int gtd_lg_rows_fwd(const gtd_lg* g, const double* app, int pairs, void* S1, void* Z, cudaStream_t st);
 /* Z (all pairs) -> Y [n][hc] = rows [0,n) of IFFT_col(fk . FFT_col(mirror(A))) for columns c0..c0+hc.

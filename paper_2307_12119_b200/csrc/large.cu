@@ -32,6 +32,7 @@
 #include "fft_tile.cuh"
 #include "gt_device.h"
 #include "kirchhoff.cuh"
+#include "lowmode.cuh"
 
 namespace gtb {
 namespace {
@@ -563,6 +564,87 @@ lg_pass(Op op, const double2* __restrict__ twm_g, int M, int groups, int nlines)
     }
 }
 
+// ------------------------------------------------ low-mode Anderson mixing on the row buffer
+// The large-grid twin of fixed_point.cu's fp_lowmode (method and state: lowmode.cuh), split in
+// three launches so that a multi-GPU driver (slab.py) can all-reduce the 256 coefficients
+// between the projection of its row slab and the mixing step: every rank then takes the same
+// step. Y: this rank's rows [rows][hy] of the row buffer (die rows row0 ..), columns q < LMK.
+constexpr int LM_ROWS = 64;  // die rows per CTA of the projection / application kernels
+
+__device__ __forceinline__ double lm_cos(int p, int x, int n) { return cospi(double(p) * (2.0 * x + 1.0) / (2.0 * n)); }
+
+__global__ void __launch_bounds__(LMN)
+lg_lowmode_project(const double2* __restrict__ Y, int hy, int rows, int row0, int n, const double2* __restrict__ hs,
+                   double* __restrict__ partial) {
+    const int tid = threadIdx.x, p = tid / LMK, q = tid % LMK;
+    const int x0 = blockIdx.x * LM_ROWS;
+    const double2 hq = hs[q];
+    double acc = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < LM_ROWS; ++t) {
+        const int x = x0 + t;
+        if (x < rows) {
+            const double2 y = Y[static_cast<size_t>(x) * hy + q];
+            acc += (hq.x * y.x - hq.y * y.y) * lm_cos(p, row0 + x, n);  // Re(hs_q Y[x][q]) cos(pi p (X + 1/2) / n)
+        }
+    }
+    partial[static_cast<size_t>(blockIdx.x) * LMN + tid] = acc;
+}
+
+// coef[p][q] = (sum over the CTAs' partial sums, in order) / (M^2 eps_q n eps_p)
+__global__ void __launch_bounds__(LMN) lg_lowmode_reduce(const double* __restrict__ partial, int nblocks, int n,
+                                                         double* __restrict__ coef) {
+    const int tid = threadIdx.x, p = tid / LMK, q = tid % LMK;
+    double acc = 0.0;
+    for (int b = 0; b < nblocks; ++b) acc += partial[static_cast<size_t>(b) * LMN + tid];
+    const double M = 2.0 * n;
+    coef[tid] = acc / (M * M * (q == 0 ? 1.0 : 0.5) * double(n) * (p == 0 ? 1.0 : 0.5));
+}
+
+__global__ void __launch_bounds__(LMN) lg_lowmode_init(LMState* st) {
+    const int tid = threadIdx.x;
+    st->xlow[tid] = 0.0;
+    if (tid == 0) {
+        st->calls = 0;
+        st->nd = 0;
+        st->have_x = 1;  // cold start: x_0 = 0
+        st->have_prev = 0;
+        st->rprev = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(LMN) lg_lowmode_mix(LMState* st, const double* __restrict__ coef, int depth,
+                                                      double res_prev, double* __restrict__ corr) {
+    bool applied = false;
+    corr[threadIdx.x] = lowmode_mix(*st, coef[threadIdx.x], res_prev, depth, threadIdx.x, &applied);
+}
+
+// Y[x][q] += conj(hs_q) M^2 eps_q sum_p corr_pq cos(pi p (X + 1/2) / n)
+__global__ void __launch_bounds__(LMN)
+lg_lowmode_apply(double2* __restrict__ Y, int hy, int rows, int row0, int n, const double2* __restrict__ hs,
+                 const double* __restrict__ corr) {
+    __shared__ double s_corr[LMN];
+    const int tid = threadIdx.x, rg = tid / LMK, q = tid % LMK;
+    s_corr[tid] = corr[tid];
+    __syncthreads();
+    double cq[LMK];
+#pragma unroll
+    for (int pp = 0; pp < LMK; ++pp) cq[pp] = s_corr[pp * LMK + q];
+    const double2 hq = hs[q];
+    const double M = 2.0 * n, sc = M * M * (q == 0 ? 1.0 : 0.5);
+    const int x1 = min(rows, (blockIdx.x + 1) * LM_ROWS);
+    for (int x = blockIdx.x * LM_ROWS + rg; x < x1; x += LMK) {
+        double v = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < LMK; ++pp) v += cq[pp] * lm_cos(pp, row0 + x, n);
+        v *= sc;
+        double2 y = Y[static_cast<size_t>(x) * hy + q];
+        y.x += v * hq.x;  // conj(hs_q) v
+        y.y -= v * hq.y;
+        Y[static_cast<size_t>(x) * hy + q] = y;
+    }
+}
+
 template <typename T, int N>
 size_t lg_smem() {
     return sizeof(cplx<T>) * (N * lg_pitch<T, N>() + N);
@@ -951,6 +1033,35 @@ using namespace gtb;
 extern "C" {
 
 int gtd_lg_row_layout(const gtd_lg* g) { return dct_rows(g) ? 1 : 0; }
+
+size_t gtd_lg_lowmode_state_bytes(void) { return sizeof(LMState); }
+int gtd_lg_lowmode_partial_blocks(int rows) { return (rows + LM_ROWS - 1) / LM_ROWS; }
+int gtd_lg_lowmode_init(void* state, cudaStream_t st) {
+    lg_lowmode_init<<<1, LMN, 0, st>>>(static_cast<LMState*>(state));
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_lg_lowmode_project(const gtd_lg* g, const void* y, int hy, int rows, int row0, double* partial, double* coef,
+                           cudaStream_t st) {
+    if (!g->hs || g->n < LMK) return static_cast<int>(cudaErrorInvalidValue);
+    const int nb = (rows + LM_ROWS - 1) / LM_ROWS;
+    lg_lowmode_project<<<nb, LMN, 0, st>>>(static_cast<const double2*>(y), hy, rows, row0, g->n,
+                                           static_cast<const double2*>(g->hs), partial);
+    lg_lowmode_reduce<<<1, LMN, 0, st>>>(partial, nb, g->n, coef);
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_lg_lowmode_mix(void* state, const double* coef, int depth, double res_prev, double* corr, cudaStream_t st) {
+    if (depth < 1 || depth > LMD) return static_cast<int>(cudaErrorInvalidValue);
+    lg_lowmode_mix<<<1, LMN, 0, st>>>(static_cast<LMState*>(state), coef, depth, res_prev, corr);
+    return static_cast<int>(cudaGetLastError());
+}
+int gtd_lg_lowmode_apply(const gtd_lg* g, void* y, int hy, int rows, int row0, const double* corr, cudaStream_t st) {
+    if (!g->hs || g->n < LMK) return static_cast<int>(cudaErrorInvalidValue);
+    const int nb = (rows + LM_ROWS - 1) / LM_ROWS;
+    lg_lowmode_apply<<<nb, LMN, 0, st>>>(static_cast<double2*>(y), hy, rows, row0, g->n,
+                                         static_cast<const double2*>(g->hs), corr);
+    return static_cast<int>(cudaGetLastError());
+}
+
 
 int gtd_lg_split(int m, int* M1, int* M2) {
     int lg = 0;

@@ -106,6 +106,29 @@ class GpuLargeOps:
         self._check(self.L.gt_large_cols_peer(self.dg._d, self._p(z_table), world, pairs_per_rank, c0, hc,
                                               self._p(c1), self._p(c2), self._p(y_table), hy, C.c_void_p(stream)))
 
+    # low-mode Anderson mixing on the row buffer (gt_large_lowmode_*: no host synchronisation)
+    def lowmode_alloc(self, rows, dev):
+        import torch
+        nb = self.L.gt_large_lowmode_partial_blocks(rows)
+        state = torch.zeros(self.L.gt_large_lowmode_state_bytes(), dtype=torch.uint8, device=dev)
+        return (state, torch.empty((nb, 256), dtype=torch.float64, device=dev),
+                torch.zeros(256, dtype=torch.float64, device=dev), torch.zeros(256, dtype=torch.float64, device=dev))
+
+    def lowmode_init(self, state, stream):
+        self._check(self.L.gt_large_lowmode_init(self._p(state), C.c_void_p(stream)))
+
+    def lowmode_project(self, y, hy, rows, row0, partial, coef, stream):
+        self._check(self.L.gt_large_lowmode_project(self.dg._d, self._p(y), hy, rows, row0, self._p(partial),
+                                                    self._p(coef), C.c_void_p(stream)))
+
+    def lowmode_mix(self, state, coef, depth, res_prev, corr, stream):
+        self._check(self.L.gt_large_lowmode_mix(self._p(state), self._p(coef), depth, float(res_prev),
+                                                self._p(corr), C.c_void_p(stream)))
+
+    def lowmode_apply(self, y, hy, rows, row0, corr, stream):
+        self._check(self.L.gt_large_lowmode_apply(self.dg._d, self._p(y), hy, rows, row0, self._p(corr),
+                                                  C.c_void_p(stream)))
+
     def rows_inv(self, y, hy, pairs, s1, t, app, p, l0, opts, res_bits, status, stream, q=None, g=None,
                  omega=0.0, gamma=1.0):
         if q is None:
@@ -206,10 +229,19 @@ class _LowMode:
     added back to the same 16 columns. The 256-dimensional least squares runs on the host."""
     K = 16
 
-    def __init__(self, depth, n, rows, row0, dev, world):
+    def __init__(self, depth, n, rows, row0, dev, world, ops=None, stream=0):
         import numpy as np
         import torch
         self.depth, self.n, self.world = depth, n, world
+        self.rows, self.row0, self.stream = rows, row0, stream
+        # device kernels when the ops provide them (GpuLargeOps); the torch / numpy
+        # restatement below serves the CPU stand-in ops of the gloo tests
+        self.ops = ops if (ops is not None and hasattr(ops, "lowmode_project") and dev.type == "cuda") else None
+        if self.ops is not None:
+            self.state, self.partial, self.coef, self.corr = self.ops.lowmode_alloc(rows, dev)
+            self.ops.lowmode_init(self.state, stream)
+            self.rprev_seen = 0.0
+            return
         K, m = self.K, 2 * n
         q = torch.arange(K, device=dev, dtype=torch.float64)
         x = torch.arange(row0, row0 + rows, device=dev, dtype=torch.float64)
@@ -272,7 +304,22 @@ class _LowMode:
 
     def step(self, y, res_prev):
         """y: this rank's row buffer [rows][hy] complex128, corrected in place."""
+        import math
         import torch.distributed as dist
+        if self.ops is not None:
+            hy = y.stride(0)
+            self.ops.lowmode_project(y, hy, self.rows, self.row0, self.partial, self.coef, self.stream)
+            if self.world > 1:
+                if dist.get_backend() == "nccl":
+                    dist.all_reduce(self.coef)
+                else:  # gloo (tests): through the host
+                    c = self.coef.cpu()
+                    dist.all_reduce(c)
+                    self.coef.copy_(c)
+            rp = res_prev if math.isfinite(res_prev) else 0.0
+            self.ops.lowmode_mix(self.state, self.coef, self.depth, rp, self.corr, self.stream)
+            self.ops.lowmode_apply(y, hy, self.rows, self.row0, self.corr, self.stream)
+            return
         a = self.project(y)
         if self.world > 1:
             if dist.get_backend() != "nccl":
@@ -413,7 +460,8 @@ def solve_slab(ops, n: int, p_local, v_local, opts, rank: int = 0, world: int = 
 
     it, res, st = 0, float("inf"), 0
     lm_depth = -int(getattr(opts, "accel", 0) or 0)
-    lowmode = _LowMode(min(lm_depth, 4), n, rows, rank * rows, dev, world) if lm_depth > 0 and n >= _LowMode.K else None
+    lowmode = (_LowMode(min(lm_depth, 4), n, rows, rank * rows, dev, world, ops=ops, stream=stream)
+               if lm_depth > 0 and n >= _LowMode.K else None)
     try:
         for it in range(1, opts.max_iters + 1):
             ops.rows_fwd(S.app, P, S.s1, S.z, stream)
