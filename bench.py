@@ -581,7 +581,9 @@ def run_cfg3(args, dev, ws, rank):
     stream = torch.cuda.Stream(dev)
 
     def once(nsteps):
-        o = dg.trace_opts(dt=1e-5, steps=nsteps, window=min(k, nsteps), law=0, beta=0.017,
+        # the warm-up uses the timed run's window too: the power ring ((k + 2) maps per trace,
+        # tens of GB) is then allocated before the timed region, not inside it
+        o = dg.trace_opts(dt=1e-5, steps=nsteps, window=k, law=0, beta=0.017,
                           out_stride=min(stride, nsteps))
         dg.trace_batch_device(blk.data_ptr(), n * n, sch.data_ptr(), nblk, leak0.data_ptr(), n * n, B, o,
                               out.data_ptr(), mx.data_ptr(), stream.cuda_stream)
